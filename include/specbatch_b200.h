@@ -1,0 +1,219 @@
+/*
+ * specbatch_b200.h -- C-ABI of the B200-native batched speculative-decoding engine.
+ *
+ * The reference (arXiv 2310.18813, package `specbatch`) is pure Python and has
+ * no FFI; the drop-in boundary it defines is the per-step oracle/run_batch
+ * surface (pkg/src/specbatch/engine.py:100-106, 155-221).  Every entry point
+ * below replaces one piece of that step on the GPU and is cited against the
+ * reference symbol whose semantics it implements:
+ *
+ *   sb_decoder_forward   <- the model evaluations hidden behind DraftOracle.step
+ *                           (engine.py:100-106; TokenLevel.target_token /
+ *                           draft_tokens engine.py:135-145): draft step (K1) and
+ *                           target verify forward (K2 GEMMs + K3 attention)
+ *   sb_select_tokens     <- greedy argmax / sampling of the next token
+ *                           (TokenLevel.draft_tokens engine.py:138-145)
+ *   sb_accept            <- verify() LCP (engine.py:74-86) + decode_step's
+ *                           advanced = min(accepted+1, remaining) (engine.py:167);
+ *                           stochastic min(1,p/q) mode (PAPER.md:43 refs) (K4)
+ *   sb_kv_commit         <- state.produced += advanced; tokens.extend
+ *                           (engine.py:168-172) + in-place KV rollback (K5)
+ *   sb_kv_compact        <- (new) slab compaction when sequences retire (K5)
+ *   sb_prepare_*         <- per-iteration input staging (no reference analogue;
+ *                           keeps every iteration graph-replayable)
+ *
+ * Conventions: every call is asynchronous on `stream`, graph-capturable, does
+ * not allocate, takes caller-owned device buffers and returns 0 on success or
+ * a cudaError_t / SB_E* code.  No torch types cross this boundary.
+ */
+#ifndef SPECBATCH_B200_H
+#define SPECBATCH_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SB_ABI_VERSION 1
+
+/* status codes beyond cudaError_t (which are < 1000) */
+#define SB_OK 0
+#define SB_EINVAL 1001      /* bad shape / argument (maps to ValueError) */
+#define SB_EWORKSPACE 1002  /* workspace too small */
+#define SB_EUNSUPPORTED 1003
+
+/* dtypes */
+#define SB_BF16 0
+#define SB_F32 1
+
+/* logits selection for sb_decoder_forward */
+#define SB_LOGITS_ALL 0   /* one logits row per input token                */
+#define SB_LOGITS_LAST 1  /* one row per sequence (its last query token)   */
+#define SB_LOGITS_NONE 2  /* prefill: KV only                              */
+
+/* acceptance modes for sb_accept */
+#define SB_ACCEPT_GREEDY 0     /* LCP of draft vs target argmax               */
+#define SB_ACCEPT_STOCHASTIC 1 /* u*q(d) < p(d); residual resample            */
+#define SB_ACCEPT_INJECTED 2   /* l = min(l_inj, k): TraceSampler law on device */
+
+/* token selection modes for sb_select_tokens */
+#define SB_SELECT_ARGMAX 0
+#define SB_SELECT_SAMPLE 1
+
+/*
+ * Llama-style decoder weights.  Arrays of per-layer DEVICE pointers are host
+ * arrays (read by the launcher).  Layouts (row-major, K contiguous):
+ *   embed      [vocab, hidden]
+ *   w_qkv[l]   [(n_heads + 2*n_kv_heads)*head_dim, hidden]  rows: Q | K | V
+ *   w_o[l]     [hidden, n_heads*head_dim]
+ *   w_gu[l]    [2*ffn, hidden]  rows interleaved g0,u0,g1,u1,...
+ *   w_down[l]  [hidden, ffn]
+ *   lm_head    [vocab, hidden]
+ *   norms      [hidden] in `dtype`
+ *   rope_cos/rope_sin [max_pos, head_dim/2] fp32 (host-computed table)
+ */
+typedef struct sb_decoder {
+  int32_t n_layers, hidden, n_heads, n_kv_heads, head_dim, ffn, vocab;
+  int32_t dtype;   /* SB_BF16 | SB_F32 */
+  int32_t max_pos; /* rows of the rope table */
+  float rms_eps;
+  const void* embed;
+  const void* final_norm;
+  const void* lm_head;
+  const void* const* attn_norm;
+  const void* const* w_qkv;
+  const void* const* w_o;
+  const void* const* mlp_norm;
+  const void* const* w_gu;
+  const void* const* w_down;
+  const float* rope_cos;
+  const float* rope_sin;
+} sb_decoder_t;
+
+/* KV cache: k/v base pointers of layout [n_layers][slots][n_kv_heads][ctx_max][head_dim]. */
+typedef struct sb_kvcache {
+  void* k;
+  void* v;
+  int32_t slots, ctx_max;
+} sb_kvcache_t;
+
+/* Workspace bytes sb_decoder_forward needs for n_tokens query tokens. */
+size_t sb_decoder_workspace_bytes(const sb_decoder_t* m, int32_t n_tokens);
+
+/*
+ * One forward of a uniform-q_len batch: n_seq sequences x q_len tokens
+ * (token t = s*q_len + j).  tok_slot[s] is the KV slot of sequence s;
+ * tok_pos[t] the absolute position (-1 = padding: no KV write, masked).
+ * Query at position p attends keys [0, p] of its slot (causal inside the
+ * speculative window).  logits fp32: [n_tok or n_seq, vocab].
+ */
+int sb_decoder_forward(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* tok_ids,
+                       const int32_t* tok_slot, const int32_t* tok_pos, int32_t n_seq, int32_t q_len,
+                       float* logits, int32_t logits_mode, void* workspace, size_t ws_bytes,
+                       void* stream);
+
+/*
+ * Next-token selection over logits rows [rows, vocab] (fp32).
+ *   ARGMAX: ties -> lowest index (np.argmax); probs_out optional.
+ *   SAMPLE: probs_out[r*probs_stride + v] = softmax(logits[r]) (fp32), token =
+ *           canonical inverse CDF at u[r*u_stride] (see sb_accept).
+ * Token r is written to out_tok[r*out_stride] (if non-NULL), next_ids[r], and
+ * next_pos[r] = base_pos[r] + pos_offset (staging the next draft step).
+ * Reference: TokenLevel.draft_tokens (engine.py:138-145) -- here the draft is
+ * a real model and the token is its argmax / sample.
+ */
+int sb_select_tokens(const float* logits, int32_t rows, int32_t vocab, int32_t mode, const float* u,
+                     int32_t u_stride, float* probs_out, int64_t probs_stride, int32_t* out_tok,
+                     int32_t out_stride, int32_t* next_ids, int32_t* next_pos, const int32_t* base_pos,
+                     int32_t pos_offset, void* stream);
+
+/* Row softmax: probs[r] = softmax(logits[r]) (fp32, max-subtracted); in place allowed. */
+int sb_softmax_rows(const float* logits, int32_t rows, int32_t vocab, float* probs, void* stream);
+
+/* Row argmax (ties -> lowest index). */
+int sb_argmax_rows(const float* logits, int32_t rows, int32_t vocab, int32_t* out, void* stream);
+
+/*
+ * Acceptance (K4) for b sequences at speculation length k (>= 0).
+ *   target_tok [b, k+1]      target argmax per verify position (GREEDY / INJECTED)
+ *   p_probs    [b, k+1, V]   target probabilities (STOCHASTIC)
+ *   q_probs    [b, k, V]     draft probabilities (STOCHASTIC)
+ *   draft_tok  row s at draft_tok + s*draft_stride, k entries
+ *   u_acc[s*u_stride + j], u_res[s*u_stride]  uniforms in [0,1) (STOCHASTIC)
+ *   l_inj [b]                injected accepted lengths (INJECTED)
+ *   produced/target_len [b]  remaining = target_len - produced (<= 0: finished, masked)
+ * GREEDY:     l = LCP(draft, target_tok[:k])          (verify, engine.py:74-86)
+ * INJECTED:   l = min(l_inj, k)                        (TraceSampler, engine.py:109-118)
+ * STOCHASTIC: accept d_j iff fp32(u_acc_j * q_j(d_j)) < p_j(d_j); on the first
+ *             rejection resample from max(0, p_l - q_l), else the bonus from p_k.
+ *             Inverse CDF: 256-entry chunks summed sequentially in fp64, chunk
+ *             prefix sequential, first index whose running sum exceeds u*total.
+ * Outputs: accepted_len[b]; advanced[b] = min(l+1, remaining) or 0 if finished
+ *          (engine.py:167); out_tok[b, k+1] = d_1..d_l, next, then -1 padding.
+ */
+int sb_accept(int32_t mode, int32_t b, int32_t k, int32_t vocab, const int32_t* target_tok,
+              const float* p_probs, const float* q_probs, const int32_t* draft_tok, int32_t draft_stride,
+              const float* u_acc, const float* u_res, int32_t u_stride, const int32_t* l_inj,
+              const int32_t* produced, const int32_t* target_len, int32_t* accepted_len, int32_t* advanced,
+              int32_t* out_tok, void* stream);
+
+/*
+ * Commit (K5): append out_tok[s, :advanced] to tokens[s, tok_cap] at n_tok[s];
+ * n_tok += advanced; produced += advanced (engine.py:168-172).  The target
+ * KV valid length is n_tok - 1 and the draft re-feeds the last two committed
+ * tokens each iteration, so the rejected suffix is rolled back in place: its
+ * KV rows are simply overwritten by the next iteration (no copy).
+ * finish_iter[s] (init -1) <- 1-based iteration at which s finished;
+ * acc_log[iter*b + s] <- accepted_len (-1 once finished) while iter < acc_log_cap;
+ * live_count <- #unfinished; iter += 1.
+ */
+int sb_kv_commit(int32_t b, int32_t k, const int32_t* advanced, const int32_t* accepted_len,
+                 const int32_t* out_tok, int32_t* tokens, int32_t tok_cap, int32_t* n_tok, int32_t* produced,
+                 const int32_t* target_len, int32_t* finish_iter, int32_t* iter, int32_t* live_count,
+                 int32_t* acc_log, int32_t acc_log_cap, void* stream);
+
+/*
+ * Stage one iteration from committed state (n = n_tok[s]):
+ *   d1_ids/d1_pos [b, 2] = (tokens[n-2], n-2), (tokens[n-1], n-1); pos -1 if n < 2
+ *   v_ids[s*(k+1)] = tokens[n-1]; v_pos[s, j] = n-1+j (j = 0..k)
+ *   d_last_pos[s] = n-1 (base for sb_select_tokens' next_pos)
+ *   uniforms[s*n_u + i] = sb_uniform_host(seed, iter, s*64 + i)   (n_u <= 64)
+ *   l_inj[s] = inj_samples[mix(seed ^ 0x5DEECE66D, iter, s) % inj_count]
+ * Any output pointer may be NULL (skipped).
+ */
+int sb_prepare_iteration(int32_t b, int32_t k, const int32_t* tokens, int32_t tok_cap, const int32_t* n_tok,
+                         int32_t* d1_ids, int32_t* d1_pos, int32_t* v_ids, int32_t* v_pos,
+                         int32_t* d_last_pos, uint64_t seed, const int32_t* iter, float* uniforms,
+                         int32_t n_u, const int32_t* inj_samples, int32_t inj_count, int32_t* l_inj,
+                         void* stream);
+
+/* Compaction (K5): copy KV slabs src_slot[i] -> dst_slot[i] for positions [0, len[i]). */
+int sb_kv_compact(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* src_slot,
+                  const int32_t* dst_slot, const int32_t* len, int32_t n, void* stream);
+
+/*
+ * GEMM entry used by tests/benches: Y[M,N] = X[M,K] W[N,K]^T, fp32 accumulate.
+ * epi: 0 store dtype, 1 store fp32, 2 fp32 residual +=, 3 silu(gate)*up on
+ * interleaved (gate, up) rows -> [M, N/2].  backend: 0 auto, 1 SIMT (FFMA),
+ * 2 tcgen05 (bf16 only; SB_EUNSUPPORTED otherwise).  The workspace must be
+ * zero-initialised once (stream-K tile counters self-reset).
+ */
+int sb_gemm(int32_t dtype, const void* x, const void* w, void* y, int32_t M, int32_t N, int32_t K,
+            int32_t epi, int32_t backend, void* workspace, size_t ws_bytes, void* stream);
+size_t sb_gemm_workspace_bytes(int32_t M, int32_t N, int32_t K);
+
+/* The counter RNG shared with the oracle: u = (mix(seed, stream, ctr) >> 40) * 2^-24. */
+float sb_uniform_host(uint64_t seed, uint64_t stream_id, uint64_t counter);
+
+/* One-time host setup (kernel attributes, TMA encoder); call before any graph capture. */
+int sb_init(void);
+int sb_version(void);
+const char* sb_build_info(void);
+int sb_last_kernel_count(void); /* kernels launched by the last sb_decoder_forward */
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SPECBATCH_B200_H */

@@ -1,0 +1,211 @@
+"""CPU reference of the draft/target decoders and of speculative decoding with
+them -- TEST INFRASTRUCTURE ONLY (tests/, smoke(), bench.py cpu_baseline).
+
+The reference package has no transformer; BASELINE.json asks for
+parity "against the reference CPU implementation on identical random-init
+weights".  This module is that CPU implementation, written independently of
+the product code: plain PyTorch on the CPU, one sequence at a time, fp32 or
+fp64, with an optional bf16-rounding emulation that rounds exactly where the
+GPU numerics contract (paper_2310_18813_b200/csrc/layer_kernels.cu header)
+rounds.  Speculative decoding follows the reference semantics:
+LCP verify (engine.py:74-86), advance = min(l+1, remaining) (engine.py:167),
+formed batch held until all finish (engine.py:186-188), s=0 plain decoding
+(engine.py:158-160).
+
+Parity status: the reference pins only integer semantics; logits parity is
+"unpinned by the reference" and is anchored here on (i) the
+closed-form identity spec-greedy == plain greedy, and (ii) this oracle.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import torch
+
+from . import spec_ref
+
+
+def rope_tables(max_pos: int, head_dim: int, theta: float = 10000.0):
+    half = head_dim // 2
+    inv = theta ** (-(np.arange(half, dtype=np.float64) * 2.0) / head_dim)
+    ang = np.arange(max_pos, dtype=np.float64)[:, None] * inv[None, :]
+    return torch.from_numpy(np.cos(ang).astype(np.float32)), torch.from_numpy(np.sin(ang).astype(np.float32))
+
+
+def init_masters(cfg, seed: int, std: float = 0.02, round_to=torch.bfloat16):
+    """Independent regeneration of the seeded host init (same draw order as the
+    engine's Decoder(init="host")): embed, per layer q,k,v,o,gate,up,down, lm_head."""
+    gen = torch.Generator(device="cpu").manual_seed(seed)
+    rn = lambda *shape: torch.randn(*shape, generator=gen, dtype=torch.float32) * std
+    h = cfg.hidden
+    hd = h // cfg.n_heads
+    qd, kd = cfg.n_heads * hd, cfg.n_kv_heads * hd
+    r = (lambda t: t.to(round_to).float()) if round_to is not None else (lambda t: t)
+    out = {"embed": r(rn(cfg.vocab, h)), "layers": []}
+    for _ in range(cfg.n_layers):
+        lay = {"wq": rn(qd, h), "wk": rn(kd, h), "wv": rn(kd, h), "wo": rn(h, qd), "wg": rn(cfg.ffn, h),
+               "wu": rn(cfg.ffn, h), "wd": rn(h, cfg.ffn)}
+        out["layers"].append({k: r(v) for k, v in lay.items()})
+    out["lm_head"] = r(rn(cfg.vocab, h))
+    return out
+
+
+class LlamaRef:
+    """Llama-style decoder on the CPU with a per-sequence KV cache.
+
+    dtype: torch.float32 or torch.float64 compute.  bf16_emulation rounds
+    to bf16 where the GPU rounds (norm outputs, qkv, rotated q/k, attention
+    output, silu*up, final norm); the residual stream stays in `dtype`.
+    """
+
+    def __init__(self, masters: dict, n_heads: int, n_kv_heads: int, eps: float, max_pos: int = 4096,
+                 theta: float = 10000.0, dtype=torch.float64, bf16_emulation: bool = False, n_layers=None):
+        self.dt = dtype
+        self.emb = masters["embed"].to(dtype)
+        self.head = masters["lm_head"].to(dtype)
+        lays = masters["layers"] if n_layers is None else masters["layers"][:n_layers]
+        self.layers = [{k: v.to(dtype) for k, v in lay.items()} for lay in lays]
+        self.h = self.emb.shape[1]
+        self.nq, self.nkv = n_heads, n_kv_heads
+        self.hd = self.h // n_heads
+        self.eps = eps
+        cos, sin = rope_tables(max_pos, self.hd, theta)
+        self.cos, self.sin = cos.to(dtype), sin.to(dtype)
+        self.bf16 = bf16_emulation
+
+    def _r(self, x):
+        return x.to(torch.bfloat16).to(self.dt) if self.bf16 else x
+
+    def _norm(self, x):
+        ms = (x.float() * x.float()).mean(-1, keepdim=True) if self.dt == torch.float32 else (x * x).mean(-1, keepdim=True)
+        return self._r(x * torch.rsqrt(ms.to(self.dt) + self.eps))
+
+    def _rope(self, x, pos):  # x [T, heads, hd]
+        half = self.hd // 2
+        c = self.cos[pos][:, None, :]
+        s = self.sin[pos][:, None, :]
+        a, b = x[..., :half], x[..., half:]
+        return self._r(torch.cat([a * c - b * s, b * c + a * s], -1))
+
+    def new_cache(self):
+        return [{"k": None, "v": None} for _ in self.layers]
+
+    @torch.no_grad()
+    def forward(self, ids, pos, cache):
+        """ids/pos: lists (one sequence, positions contiguous and >= cache length
+        of valid entries).  The cache keeps keys by absolute position; entries
+        at positions >= pos[0] are overwritten (in-place rollback)."""
+        ids_t = torch.as_tensor(ids, dtype=torch.long)
+        pos_t = torch.as_tensor(pos, dtype=torch.long)
+        x = self.emb[ids_t].clone()
+        T = len(ids)
+        scale = 1.0 / math.sqrt(self.hd)
+        p0 = int(pos[0])
+        for lay, c in zip(self.layers, cache):
+            xn = self._norm(x)
+            q = self._r(xn @ lay["wq"].T).view(T, self.nq, self.hd)
+            kk = self._r(xn @ lay["wk"].T).view(T, self.nkv, self.hd)
+            vv = self._r(xn @ lay["wv"].T).view(T, self.nkv, self.hd)
+            q = self._rope(q, pos_t)
+            kk = self._rope(kk, pos_t)
+            keep_k = c["k"][:p0] if c["k"] is not None else kk[:0]
+            keep_v = c["v"][:p0] if c["v"] is not None else vv[:0]
+            c["k"] = torch.cat([keep_k, kk], 0)
+            c["v"] = torch.cat([keep_v, vv], 0)
+            K, Vv = c["k"], c["v"]
+            rep = self.nq // self.nkv
+            Kh = K.repeat_interleave(rep, dim=1)  # [S, nq, hd]
+            Vh = Vv.repeat_interleave(rep, dim=1)
+            qs = q * (torch.tensor(scale, dtype=torch.float32).to(self.dt))
+            att = torch.einsum("tnd,snd->nts", qs, Kh)
+            S = K.shape[0]
+            mask = torch.arange(S)[None, :] > pos_t[:, None]
+            att = att.masked_fill(mask[None], float("-inf"))
+            att = torch.softmax(att, -1)
+            o = self._r(torch.einsum("nts,snd->tnd", att, Vh).reshape(T, self.nq * self.hd))
+            x = x + o @ lay["wo"].T
+            xn = self._norm(x)
+            g = xn @ lay["wg"].T
+            u = xn @ lay["wu"].T
+            a = self._r(torch.nn.functional.silu(g) * u)
+            x = x + a @ lay["wd"].T
+        return (self._norm(x) @ self.head.T).to(torch.float64).numpy()
+
+
+def greedy_decode(model: LlamaRef, prompt, n: int):
+    """Plain greedy decoding: the ground truth every speculative run must equal
+    (greedy_reference, engine.py:224-227).  Returns (tokens, top2 gaps)."""
+    cache = model.new_cache()
+    P = len(prompt)
+    toks = list(int(t) for t in prompt)
+    logits = model.forward(toks, list(range(P)), cache)[-1]
+    out, gaps = [], []
+    for i in range(n):
+        srt = np.sort(logits)
+        gaps.append(float(srt[-1] - srt[-2]))
+        t = int(np.argmax(logits))
+        out.append(t)
+        if i + 1 < n:
+            toks.append(t)
+            logits = model.forward([t], [len(toks) - 1], cache)[-1]
+    return out, gaps
+
+
+def spec_generate(target: LlamaRef, draft: LlamaRef, prompts, target_lens, k: int, mode: str = "greedy",
+                  seed: int = 0, inj_samples=None):
+    """Batched speculative decoding on the CPU with the engine's protocol:
+    draft step 1 re-feeds the last two committed tokens, verify feeds
+    (x_{n-1}, d_1..d_k), KV rolled back by position.  Uniforms / injected
+    lengths come from the same counter RNG as the GPU (spec_ref.uniforms).
+    Returns (tokens per sequence, accepted-length log [iters][b])."""
+    b = len(prompts)
+    P = len(prompts[0])
+    tc = [target.new_cache() for _ in range(b)]
+    dc = [draft.new_cache() for _ in range(b)] if draft is not None else None
+    toks = [list(map(int, p)) for p in prompts]
+    for s in range(b):
+        if P >= 2:
+            target.forward(toks[s][:P - 1], list(range(P - 1)), tc[s])
+            if draft is not None:
+                draft.forward(toks[s][:P - 1], list(range(P - 1)), dc[s])
+    produced = np.zeros(b, np.int64)
+    tl = np.asarray(target_lens)
+    log = []
+    it = 0
+    while np.any(produced < tl):
+        u = spec_ref.uniforms(seed, it, b)
+        l_inj = spec_ref.injected_lengths(seed, it, b, inj_samples) if mode == "injected" else None
+        drafts = np.zeros((b, k), np.int32)
+        q = np.zeros((b, k, target.emb.shape[0]), np.float32) if mode == "stochastic" else None
+        p = np.zeros((b, k + 1, target.emb.shape[0]), np.float32) if mode == "stochastic" else None
+        t_tok = np.zeros((b, k + 1), np.int32)
+        for s in range(b):
+            n = len(toks[s])
+            if k > 0:
+                lg = draft.forward(toks[s][n - 2:n] if n >= 2 else toks[s][n - 1:n],
+                                   [n - 2, n - 1] if n >= 2 else [n - 1], dc[s])[-1]
+                for j in range(1, k + 1):
+                    if j > 1:
+                        lg = draft.forward([int(drafts[s, j - 2])], [n - 1 + j - 1], dc[s])[-1]
+                    if mode == "stochastic":
+                        qq = spec_ref.softmax_rows(lg.astype(np.float32)[None])[0]
+                        q[s, j - 1] = qq
+                        drafts[s, j - 1] = spec_ref.inverse_cdf(qq, u[s, j - 1])
+                    else:
+                        drafts[s, j - 1] = int(np.argmax(lg))
+            vin = [toks[s][n - 1]] + [int(x) for x in drafts[s]]
+            tl_logits = target.forward(vin, list(range(n - 1, n + k)), tc[s])
+            if mode == "stochastic":
+                p[s] = spec_ref.softmax_rows(tl_logits.astype(np.float32))
+            t_tok[s] = np.argmax(tl_logits, -1)
+        acc, adv, out = spec_ref.accept_batch(mode, k, drafts, produced, tl, target_tok=t_tok, p=p, q=q,
+                                              u_acc=u[:, k:2 * k], u_res=u[:, 2 * k], l_inj=l_inj)
+        log.append([int(a) if produced[s] < tl[s] else -1 for s, a in enumerate(acc)])
+        for s in range(b):
+            if adv[s] > 0:
+                toks[s].extend(int(t) for t in out[s, :adv[s]])
+                produced[s] += adv[s]
+        it += 1
+    return [t[P:] for t in toks], log

@@ -1,0 +1,86 @@
+// Shared device helpers for the specbatch_b200 kernels (sm_100a).
+#pragma once
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "specbatch_b200.h"
+
+#define SB_CHECK_LAUNCH()                              \
+  do {                                                 \
+    cudaError_t e_ = cudaGetLastError();               \
+    if (e_ != cudaSuccess) return (int)e_;             \
+  } while (0)
+
+#define SB_TRY(expr)                \
+  do {                              \
+    int rc_ = (expr);               \
+    if (rc_ != 0) return rc_;       \
+  } while (0)
+
+namespace sb {
+
+extern thread_local int g_kernel_count;  // launches issued by the current forward
+
+__device__ __forceinline__ float to_f32(float x) { return x; }
+__device__ __forceinline__ float to_f32(__nv_bfloat16 x) { return __bfloat162float(x); }
+template <typename T> __device__ __forceinline__ T from_f32(float x);
+template <> __device__ __forceinline__ float from_f32<float>(float x) { return x; }
+template <> __device__ __forceinline__ __nv_bfloat16 from_f32<__nv_bfloat16>(float x) { return __float2bfloat16_rn(x); }
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// (value, index) argmax with ties -> lowest index; NaN never wins.
+struct ArgMax {
+  float v;
+  int i;
+};
+__device__ __forceinline__ ArgMax argmax_merge(ArgMax a, ArgMax b) {
+  if (b.v > a.v || (b.v == a.v && b.i < a.i)) return b;
+  return a;
+}
+__device__ __forceinline__ ArgMax warp_argmax(ArgMax a) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    ArgMax b{__shfl_xor_sync(0xffffffffu, a.v, o), __shfl_xor_sync(0xffffffffu, a.i, o)};
+    a = argmax_merge(a, b);
+  }
+  return a;
+}
+
+// splitmix-style mix shared with the reference's `_mix` (engine.py:89-97) and
+// with oracle/spec_ref.py: the counter RNG of the engine.
+__host__ __device__ __forceinline__ uint64_t mix3(uint64_t a, uint64_t b, uint64_t c) {
+  uint64_t x = a * 0x9E3779B97F4A7C15ull + b * 0xBF58476D1CE4E5B9ull + c * 0x94D049BB133111EBull;
+  x ^= x >> 30;
+  x *= 0xBF58476D1CE4E5B9ull;
+  x ^= x >> 27;
+  x *= 0x94D049BB133111EBull;
+  x ^= x >> 31;
+  return x;
+}
+__host__ __device__ __forceinline__ float u01(uint64_t seed, uint64_t stream, uint64_t ctr) {
+  return (float)(mix3(seed, stream, ctr) >> 40) * (1.0f / 16777216.0f);
+}
+
+// Canonical inverse-CDF chunking shared with the oracle: chunk sums in fp64,
+// sequential within a chunk, sequential over chunks.
+constexpr int kCdfChunk = 256;
+
+inline int grid_for(long n, int per_block, int cap = 148 * 16) {
+  long g = (n + per_block - 1) / per_block;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+}  // namespace sb

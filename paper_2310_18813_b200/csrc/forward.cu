@@ -1,0 +1,154 @@
+// Native forward driver of a Llama-style decoder: the draft step (K1) and the
+// target verification forward (K2 GEMMs + K3 attention) of one speculative
+// iteration.  Host C++ walks the layers and launches the kernels on the
+// caller's stream; no allocation, so a whole iteration can be captured into
+// one CUDA graph per (b, k) by the host engine.
+#include <cstdio>
+#include <cstring>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace sb {
+
+static inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+struct FwdWorkspace {
+  float* resid;
+  void* xn;
+  void* qkv;
+  void* qr;
+  void* attn;
+  void* act;
+  void* last;
+  void* gemm_ws;
+  size_t gemm_ws_bytes;
+};
+
+static size_t carve(const sb_decoder_t* m, int T, char* base, FwdWorkspace* w) {
+  const size_t es = m->dtype == SB_BF16 ? 2 : 4;
+  const int qkv_n = (m->n_heads + 2 * m->n_kv_heads) * m->head_dim;
+  const int qd = m->n_heads * m->head_dim;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    char* p = base ? base + off : nullptr;
+    off += align_up(bytes);
+    return (void*)p;
+  };
+  FwdWorkspace tmp;
+  FwdWorkspace* o = w ? w : &tmp;
+  o->resid = (float*)take((size_t)T * m->hidden * 4);
+  o->xn = take((size_t)T * m->hidden * es);
+  o->qkv = take((size_t)T * qkv_n * es);
+  o->qr = take((size_t)T * qd * es);
+  o->attn = take((size_t)T * qd * es);
+  o->act = take((size_t)T * m->ffn * es);
+  o->last = take((size_t)T * m->hidden * es);
+  int maxN = m->vocab;
+  if (2 * m->ffn > maxN) maxN = 2 * m->ffn;
+  if (qkv_n > maxN) maxN = qkv_n;
+  int maxK = m->hidden > m->ffn ? m->hidden : m->ffn;
+  if (qd > maxK) maxK = qd;
+  o->gemm_ws_bytes = gemm_workspace_bytes(T, maxN, maxK);
+  o->gemm_ws = take(o->gemm_ws_bytes);
+  return off;
+}
+
+static int g_last_count = 0;
+
+static int forward_impl(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* ids, const int32_t* slot,
+                        const int32_t* pos, int n_seq, int q_len, float* logits, int logits_mode, void* ws,
+                        size_t ws_bytes, cudaStream_t st) {
+  const int T = n_seq * q_len;
+  if (T <= 0 || !m || !kv) return SB_EINVAL;
+  if ((m->head_dim != 128 && m->head_dim != 64) || m->n_heads % m->n_kv_heads) return SB_EUNSUPPORTED;
+  FwdWorkspace w;
+  size_t need = carve(m, T, (char*)ws, &w);
+  if (need > ws_bytes) return SB_EWORKSPACE;
+  const int dt = m->dtype;
+  const size_t es = dt == SB_BF16 ? 2 : 4;
+  const int nq = m->n_heads, nkv = m->n_kv_heads, hd = m->head_dim, H = m->hidden;
+  const int qkv_n = (nq + 2 * nkv) * hd;
+  const size_t layer_kv = (size_t)kv->slots * nkv * kv->ctx_max * hd * es;
+
+  SB_TRY(launch_embed(dt, m->embed, ids, pos, w.resid, T, H, m->vocab, st));
+  for (int l = 0; l < m->n_layers; ++l) {
+    char* kc = (char*)kv->k + l * layer_kv;
+    char* vc = (char*)kv->v + l * layer_kv;
+    SB_TRY(launch_rmsnorm(dt, w.resid, m->attn_norm[l], w.xn, T, H, m->rms_eps, 1, 0, st));
+    GemmArgs g{dt, w.xn, m->w_qkv[l], w.qkv, T, qkv_n, H, H, EPI_STORE, w.gemm_ws, w.gemm_ws_bytes};
+    SB_TRY(gemm(g, GEMM_AUTO, st));
+    SB_TRY(launch_rope_append(dt, w.qkv, w.qr, kc, vc, slot, pos, m->rope_cos, m->rope_sin, T, q_len, nq, nkv, hd,
+                              kv->ctx_max, m->max_pos, st));
+    SB_TRY(launch_attention(dt, w.qr, kc, vc, w.attn, slot, pos, n_seq, q_len, nq, nkv, hd, kv->ctx_max, st));
+    g = GemmArgs{dt, w.attn, m->w_o[l], w.resid, T, H, nq * hd, nq * hd, EPI_RESID_ADD, w.gemm_ws, w.gemm_ws_bytes};
+    SB_TRY(gemm(g, GEMM_AUTO, st));
+    SB_TRY(launch_rmsnorm(dt, w.resid, m->mlp_norm[l], w.xn, T, H, m->rms_eps, 1, 0, st));
+    g = GemmArgs{dt, w.xn, m->w_gu[l], w.act, T, 2 * m->ffn, H, H, EPI_SILU_MUL, w.gemm_ws, w.gemm_ws_bytes};
+    SB_TRY(gemm(g, GEMM_AUTO, st));
+    g = GemmArgs{dt, w.act, m->w_down[l], w.resid, T, H, m->ffn, m->ffn, EPI_RESID_ADD, w.gemm_ws, w.gemm_ws_bytes};
+    SB_TRY(gemm(g, GEMM_AUTO, st));
+  }
+  if (logits_mode == SB_LOGITS_NONE) return 0;
+  int rows = logits_mode == SB_LOGITS_LAST ? n_seq : T;
+  int step = logits_mode == SB_LOGITS_LAST ? q_len : 1;
+  int off = logits_mode == SB_LOGITS_LAST ? q_len - 1 : 0;
+  SB_TRY(launch_rmsnorm(dt, w.resid, m->final_norm, w.last, rows, H, m->rms_eps, step, off, st));
+  GemmArgs g{dt, w.last, m->lm_head, logits, rows, m->vocab, H, H, EPI_STORE_F32, w.gemm_ws, w.gemm_ws_bytes};
+  SB_TRY(gemm(g, GEMM_AUTO, st));
+  return 0;
+}
+
+}  // namespace sb
+
+using namespace sb;
+
+extern "C" {
+
+size_t sb_decoder_workspace_bytes(const sb_decoder_t* m, int32_t n_tokens) {
+  if (!m || n_tokens <= 0) return 0;
+  return carve(m, n_tokens, nullptr, nullptr);
+}
+
+int sb_decoder_forward(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* tok_ids, const int32_t* tok_slot,
+                       const int32_t* tok_pos, int32_t n_seq, int32_t q_len, float* logits, int32_t logits_mode,
+                       void* workspace, size_t ws_bytes, void* stream) {
+  g_kernel_count = 0;
+  int rc = forward_impl(m, kv, tok_ids, tok_slot, tok_pos, n_seq, q_len, logits, logits_mode, workspace, ws_bytes,
+                        (cudaStream_t)stream);
+  g_last_count = g_kernel_count;
+  return rc;
+}
+
+int sb_gemm(int32_t dtype, const void* x, const void* w, void* y, int32_t M, int32_t N, int32_t K, int32_t epi,
+            int32_t backend, void* workspace, size_t ws_bytes, void* stream) {
+  if (epi < 0 || epi > 3) return SB_EINVAL;
+  GemmArgs g{dtype, x, w, y, M, N, K, K, epi, workspace, ws_bytes};
+  return gemm(g, backend, (cudaStream_t)stream);
+}
+
+size_t sb_gemm_workspace_bytes(int32_t M, int32_t N, int32_t K) { return gemm_workspace_bytes(M, N, K); }
+
+int sb_kv_compact(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* src_slot, const int32_t* dst_slot,
+                  const int32_t* len, int32_t n, void* stream) {
+  if (!m || !kv || n < 0) return SB_EINVAL;
+  return launch_kv_compact(m->dtype, kv->k, kv->v, src_slot, dst_slot, len, n, m->n_layers, kv->slots,
+                           m->n_kv_heads, kv->ctx_max, m->head_dim, (cudaStream_t)stream);
+}
+
+int sb_init(void) {
+  // one-time host setup outside any stream capture: kernel attributes and the
+  // driver's tensor-map encoder (TMA descriptors are built per GEMM call)
+  return gemm_tc_init();
+}
+
+int sb_version(void) { return SB_ABI_VERSION; }
+
+const char* sb_build_info(void) {
+  return "specbatch_b200 abi=" "1" " arch=sm_100a kernels=embed,rmsnorm,rope_append,attention,gemm_simt,gemm_tcgen05,"
+         "argmax,softmax,select,accept,commit,prepare,kv_compact";
+}
+
+int sb_last_kernel_count(void) { return g_last_count; }
+
+}  // extern "C"

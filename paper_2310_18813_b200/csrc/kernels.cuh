@@ -1,0 +1,49 @@
+// Internal launcher declarations (host side).  Each returns 0 or an error code.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace sb {
+
+// GEMM epilogues: Y[M,N] = X[M,K] . W[N,K]^T  (fp32 accumulate)
+enum GemmEpi : int {
+  EPI_STORE = 0,      // y (dtype) [M, N]
+  EPI_STORE_F32 = 1,  // y fp32 [M, N]
+  EPI_RESID_ADD = 2,  // resid fp32 [M, N] += acc
+  EPI_SILU_MUL = 3,   // rows interleaved (gate, up): y (dtype) [M, N/2] = silu(g) * u
+};
+
+enum GemmBackend : int { GEMM_AUTO = 0, GEMM_SIMT = 1, GEMM_TC = 2 };
+
+struct GemmArgs {
+  int dtype;
+  const void* x;  // [M, K] dtype, row stride ldx (elements)
+  const void* w;  // [N, K] dtype
+  void* y;
+  int M, N, K, ldx;
+  int epi;
+  void* workspace;  // split-K partials / tile counters
+  size_t ws_bytes;
+};
+
+int gemm(const GemmArgs& a, int backend, cudaStream_t st);
+size_t gemm_workspace_bytes(int M, int N, int K);
+int gemm_simt(const GemmArgs& a, cudaStream_t st);
+int gemm_tc(const GemmArgs& a, cudaStream_t st);  // tcgen05 (bf16 only); SB_EUNSUPPORTED otherwise
+bool gemm_tc_supported(const GemmArgs& a);
+int gemm_tc_init();
+
+int launch_embed(int dtype, const void* table, const int32_t* ids, const int32_t* pos, float* h, int n_tok,
+                 int hidden, int vocab, cudaStream_t st);
+int launch_rmsnorm(int dtype, const float* x, const void* g, void* y, int rows, int hidden, float eps, int row_step,
+                   int row_off, cudaStream_t st);
+int launch_rope_append(int dtype, const void* qkv, void* q_out, void* kc, void* vc, const int32_t* tok_slot,
+                       const int32_t* tok_pos, const float* cosT, const float* sinT, int n_tok, int q_len, int nq,
+                       int nkv, int hd, int ctx_max, int max_pos, cudaStream_t st);
+int launch_attention(int dtype, const void* q, const void* kc, const void* vc, void* out, const int32_t* tok_slot,
+                     const int32_t* tok_pos, int n_seq, int q_len, int nq, int nkv, int hd, int ctx_max,
+                     cudaStream_t st);
+int launch_kv_compact(int dtype, void* k, void* v, const int32_t* src, const int32_t* dst, const int32_t* len, int n,
+                      int layers, int slots, int nkv, int ctx_max, int hd, cudaStream_t st);
+
+}  // namespace sb

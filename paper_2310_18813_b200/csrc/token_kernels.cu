@@ -1,0 +1,372 @@
+// Token-level kernels of one speculative iteration:
+//   argmax / softmax rows, draft token selection (K1 tail), acceptance (K4),
+//   commit + in-place KV rollback (K5), iteration staging + counter RNG.
+//
+// Semantics follow the reference engine (pkg/src/specbatch/engine.py):
+//   verify()        = longest common prefix                     (engine.py:74-86)
+//   decode_step()   advanced = min(accepted + 1, remaining)      (engine.py:167)
+//                   tokens appended = the verifier's stream      (engine.py:168-171)
+//   run_batch()     formed batch held, finished rows masked      (engine.py:186-188)
+//   TraceSampler    l = min(trace[I], s), I uniform              (engine.py:109-118)
+// The stochastic mode is standard speculative sampling (Leviathan/Chen, cited
+// by PAPER.md:43): accept d_j iff u_j * q_j(d_j) < p_j(d_j) (fp32 product),
+// else resample from max(0, p_j - q_j); if all k accepted, sample the bonus
+// from p_k.  Sampling is a canonical inverse CDF (chunk sums of kCdfChunk
+// entries, each chunk summed sequentially in fp64, chunks prefix-summed
+// sequentially) so oracle/spec_ref.py reproduces every draw bit-for-bit.
+#include <climits>
+
+#include "common.cuh"
+
+namespace sb {
+
+// -------------------------------------------------------------- row reductions
+__device__ ArgMax block_argmax_row(const float* __restrict__ row, int V) {
+  ArgMax best{-INFINITY, INT_MAX};
+  for (int v = threadIdx.x; v < V; v += blockDim.x) {
+    float x = row[v];
+    if (x > best.v || (x == best.v && v < best.i)) best = ArgMax{x, v};
+  }
+  best = warp_argmax(best);
+  __shared__ float sv[32];
+  __shared__ int si[32];
+  int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  if (lane == 0) {
+    sv[w] = best.v;
+    si[w] = best.i;
+  }
+  __syncthreads();
+  if (w == 0) {
+    ArgMax a = lane < nw ? ArgMax{sv[lane], si[lane]} : ArgMax{-INFINITY, INT_MAX};
+    a = warp_argmax(a);
+    if (lane == 0) {
+      sv[0] = a.v;
+      si[0] = a.i;
+    }
+  }
+  __syncthreads();
+  ArgMax r{sv[0], si[0]};
+  __syncthreads();
+  return r;
+}
+
+__device__ float block_reduce(float v, bool is_max) {
+  __shared__ float red[32];
+  int w = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  v = is_max ? warp_max(v) : warp_sum(v);
+  if (lane == 0) red[w] = v;
+  __syncthreads();
+  if (w == 0) {
+    float a = lane < nw ? red[lane] : (is_max ? -INFINITY : 0.f);
+    a = is_max ? warp_max(a) : warp_sum(a);
+    if (lane == 0) red[0] = a;
+  }
+  __syncthreads();
+  float r = red[0];
+  __syncthreads();
+  return r;
+}
+
+// probs[v] = exp(x[v] - max) / sum  (fp32); in-place allowed
+__device__ void block_softmax_row(const float* x, float* p, int V) {
+  float m = -INFINITY;
+  for (int v = threadIdx.x; v < V; v += blockDim.x) m = fmaxf(m, x[v]);
+  m = block_reduce(m, true);
+  float s = 0.f;
+  for (int v = threadIdx.x; v < V; v += blockDim.x) s += expf(x[v] - m);
+  s = block_reduce(s, false);
+  float inv = 1.f / s;
+  __syncthreads();
+  for (int v = threadIdx.x; v < V; v += blockDim.x) p[v] = expf(x[v] - m) * inv;
+  __syncthreads();
+}
+
+// Canonical inverse CDF over weights w[v] = f(v) (non-negative fp32).
+// Mode 0: w = a[v].  Mode 1: w = max(a[v] - b[v], 0).  Returns the index.
+__device__ int block_inverse_cdf(const float* a, const float* b, int mode, int V, float u) {
+  __shared__ double csum[512];
+  __shared__ int pick;
+  const int nch = (V + kCdfChunk - 1) / kCdfChunk;
+  for (int c = threadIdx.x; c < nch; c += blockDim.x) {
+    double s = 0.0;
+    int v1 = min(V, (c + 1) * kCdfChunk);
+    for (int v = c * kCdfChunk; v < v1; ++v) {
+      float w = mode ? fmaxf(a[v] - b[v], 0.f) : a[v];
+      s += (double)w;
+    }
+    csum[c] = s;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double total = 0.0;
+    for (int c = 0; c < nch; ++c) total += csum[c];
+    int res = -1;
+    if (total > 0.0) {
+      double target = (double)u * total;
+      double cum = 0.0;
+      int chosen = -1;
+      double before = 0.0;
+      for (int c = 0; c < nch; ++c) {
+        double nxt = cum + csum[c];
+        if (nxt > target) {
+          chosen = c;
+          before = cum;
+          break;
+        }
+        cum = nxt;
+      }
+      if (chosen < 0) {  // rounding: take the last chunk with mass
+        for (int c = nch - 1; c >= 0; --c)
+          if (csum[c] > 0.0) {
+            chosen = c;
+            break;
+          }
+        before = 0.0;
+        for (int c = 0; c < chosen; ++c) before += csum[c];
+        target = before + csum[chosen];  // forces the last massive entry
+      }
+      double local = 0.0;
+      int last_pos = -1;
+      int v1 = min(V, (chosen + 1) * kCdfChunk);
+      for (int v = chosen * kCdfChunk; v < v1; ++v) {
+        float w = mode ? fmaxf(a[v] - b[v], 0.f) : a[v];
+        if (w > 0.f) last_pos = v;
+        local += (double)w;
+        if (before + local > target) {
+          res = v;
+          break;
+        }
+      }
+      if (res < 0) res = last_pos;
+    }
+    pick = res;
+  }
+  __syncthreads();
+  int r = pick;
+  __syncthreads();
+  return r;
+}
+
+__global__ void argmax_rows_kernel(const float* __restrict__ logits, int V, int32_t* __restrict__ out) {
+  ArgMax a = block_argmax_row(logits + (size_t)blockIdx.x * V, V);
+  if (threadIdx.x == 0) out[blockIdx.x] = a.i;
+}
+
+__global__ void softmax_rows_kernel(const float* logits, int V, float* probs) {
+  block_softmax_row(logits + (size_t)blockIdx.x * V, probs + (size_t)blockIdx.x * V, V);
+}
+
+__global__ void select_kernel(const float* logits, int V, int mode, const float* __restrict__ u, int u_stride,
+                              float* probs, long long probs_stride, int32_t* out_tok, int out_stride,
+                              int32_t* next_ids, int32_t* next_pos, const int32_t* base_pos, int pos_offset) {
+  int r = blockIdx.x;
+  const float* row = logits + (size_t)r * V;
+  int tok;
+  if (mode == SB_SELECT_ARGMAX) {
+    tok = block_argmax_row(row, V).i;
+    if (probs) block_softmax_row(row, probs + (size_t)r * probs_stride, V);
+  } else {
+    float* p = probs + (size_t)r * probs_stride;
+    block_softmax_row(row, p, V);
+    tok = block_inverse_cdf(p, nullptr, 0, V, u[(size_t)r * u_stride]);
+  }
+  if (threadIdx.x == 0) {
+    if (out_tok) out_tok[(size_t)r * out_stride] = tok;
+    if (next_ids) next_ids[r] = tok;
+    if (next_pos) next_pos[r] = base_pos[r] + pos_offset;
+  }
+}
+
+// ------------------------------------------------------------------ accept (K4)
+__global__ void accept_kernel(int mode, int k, int V, const int32_t* __restrict__ target_tok,
+                              const float* __restrict__ p_probs, const float* __restrict__ q_probs,
+                              const int32_t* __restrict__ draft_tok, int draft_stride, const float* __restrict__ u_acc,
+                              const float* __restrict__ u_res, int u_stride, const int32_t* __restrict__ l_inj,
+                              const int32_t* __restrict__ produced, const int32_t* __restrict__ target_len,
+                              int32_t* accepted_len, int32_t* advanced, int32_t* out_tok) {
+  const int s = blockIdx.x;
+  const int32_t* d = draft_tok + (size_t)s * draft_stride;
+  __shared__ int sh_l;
+  int l = 0, next = 0;
+  if (mode == SB_ACCEPT_GREEDY || mode == SB_ACCEPT_INJECTED) {
+    const int32_t* t = target_tok + (size_t)s * (k + 1);
+    if (mode == SB_ACCEPT_GREEDY) {
+      while (l < k && d[l] == t[l]) ++l;
+    } else {
+      l = min(max(l_inj[s], 0), k);
+    }
+    next = t[l];
+  } else {
+    if (threadIdx.x == 0) {
+      int j = 0;
+      for (; j < k; ++j) {
+        int tok = d[j];
+        float pj = p_probs[((size_t)s * (k + 1) + j) * V + tok];
+        float qj = q_probs[((size_t)s * k + j) * V + tok];
+        float uq = u_acc[(size_t)s * u_stride + j] * qj;
+        if (!(uq < pj)) break;
+      }
+      sh_l = j;
+    }
+    __syncthreads();
+    l = sh_l;
+    const float* p = p_probs + ((size_t)s * (k + 1) + l) * V;
+    float u = u_res[(size_t)s * u_stride];
+    if (l < k) {
+      const float* q = q_probs + ((size_t)s * k + l) * V;
+      next = block_inverse_cdf(p, q, 1, V, u);
+      if (next < 0) next = block_inverse_cdf(p, nullptr, 0, V, u);
+    } else {
+      next = block_inverse_cdf(p, nullptr, 0, V, u);
+    }
+  }
+  if (threadIdx.x == 0) {
+    int rem = target_len[s] - produced[s];
+    int adv = rem <= 0 ? 0 : min(l + 1, rem);
+    accepted_len[s] = l;
+    advanced[s] = adv;
+    int32_t* o = out_tok + (size_t)s * (k + 1);
+    for (int j = 0; j < l; ++j) o[j] = d[j];
+    o[l] = next;
+    for (int j = l + 1; j <= k; ++j) o[j] = -1;
+  }
+}
+
+// ------------------------------------------------------------------ commit (K5)
+__global__ void commit_kernel(int b, int k, const int32_t* __restrict__ advanced,
+                              const int32_t* __restrict__ accepted_len, const int32_t* __restrict__ out_tok,
+                              int32_t* tokens, int cap, int32_t* n_tok, int32_t* produced,
+                              const int32_t* __restrict__ target_len, int32_t* finish_iter, int32_t* iter,
+                              int32_t* live_count, int32_t* acc_log, int acc_log_cap) {
+  __shared__ int live;
+  if (threadIdx.x == 0) live = 0;
+  __syncthreads();
+  const int it = *iter;
+  for (int s = threadIdx.x; s < b; s += blockDim.x) {
+    int adv = advanced[s];
+    bool was_live = produced[s] < target_len[s];
+    if (adv > 0) {
+      int n = n_tok[s];
+      for (int i = 0; i < adv && n + i < cap; ++i) tokens[(size_t)s * cap + n + i] = out_tok[(size_t)s * (k + 1) + i];
+      n_tok[s] = n + adv;  // target KV valid length = n_tok - 1: the rejected suffix is rolled back in place
+      produced[s] += adv;
+    }
+    bool live_now = produced[s] < target_len[s];
+    if (was_live && !live_now && finish_iter[s] < 0) finish_iter[s] = it + 1;
+    if (acc_log && it < acc_log_cap) acc_log[(size_t)it * b + s] = was_live ? accepted_len[s] : -1;
+    if (live_now) atomicAdd(&live, 1);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    *live_count = live;
+    *iter = it + 1;
+  }
+}
+
+// ------------------------------------------------------------------ staging
+__global__ void prepare_kernel(int b, int k, const int32_t* __restrict__ tokens, int cap,
+                               const int32_t* __restrict__ n_tok, int32_t* d1_ids, int32_t* d1_pos, int32_t* v_ids,
+                               int32_t* v_pos, int32_t* d_last_pos, uint64_t seed, const int32_t* __restrict__ iter,
+                               float* uniforms, int n_u, const int32_t* __restrict__ inj, int inj_count,
+                               int32_t* l_inj) {
+  const uint64_t it = (uint64_t)(*iter);
+  for (int s = threadIdx.x; s < b; s += blockDim.x) {
+    int n = n_tok[s];
+    const int32_t* row = tokens + (size_t)s * cap;
+    if (d1_ids) {
+      d1_ids[2 * s + 0] = n >= 2 ? row[n - 2] : 0;
+      d1_pos[2 * s + 0] = n >= 2 ? n - 2 : -1;
+      d1_ids[2 * s + 1] = row[n - 1];
+      d1_pos[2 * s + 1] = n - 1;
+    }
+    v_ids[(size_t)s * (k + 1)] = row[n - 1];
+    for (int j = 0; j <= k; ++j) v_pos[(size_t)s * (k + 1) + j] = n - 1 + j;
+    if (d_last_pos) d_last_pos[s] = n - 1;
+    if (l_inj && inj_count > 0) l_inj[s] = inj[mix3(seed ^ 0x5DEECE66Dull, it, (uint64_t)s) % (uint64_t)inj_count];
+  }
+  if (uniforms) {
+    for (int e = threadIdx.x; e < b * n_u; e += blockDim.x) {
+      int s = e / n_u, i = e % n_u;
+      uniforms[e] = u01(seed, it, (uint64_t)s * 64 + i);
+    }
+  }
+}
+
+}  // namespace sb
+
+using namespace sb;
+
+extern "C" {
+
+int sb_argmax_rows(const float* logits, int32_t rows, int32_t vocab, int32_t* out, void* stream) {
+  if (rows <= 0) return 0;
+  argmax_rows_kernel<<<rows, 256, 0, (cudaStream_t)stream>>>(logits, vocab, out);
+  SB_CHECK_LAUNCH();
+  return 0;
+}
+
+int sb_softmax_rows(const float* logits, int32_t rows, int32_t vocab, float* probs, void* stream) {
+  if (rows <= 0) return 0;
+  softmax_rows_kernel<<<rows, 256, 0, (cudaStream_t)stream>>>(logits, vocab, probs);
+  SB_CHECK_LAUNCH();
+  return 0;
+}
+
+int sb_select_tokens(const float* logits, int32_t rows, int32_t vocab, int32_t mode, const float* u, int32_t u_stride,
+                     float* probs_out, int64_t probs_stride, int32_t* out_tok, int32_t out_stride, int32_t* next_ids,
+                     int32_t* next_pos, const int32_t* base_pos, int32_t pos_offset, void* stream) {
+  if (rows <= 0) return 0;
+  if (mode == SB_SELECT_SAMPLE && (probs_out == nullptr || u == nullptr)) return SB_EINVAL;
+  if (next_pos && !base_pos) return SB_EINVAL;
+  if ((vocab + kCdfChunk - 1) / kCdfChunk > 512) return SB_EUNSUPPORTED;
+  select_kernel<<<rows, 256, 0, (cudaStream_t)stream>>>(logits, vocab, mode, u, u_stride, probs_out, probs_stride,
+                                                        out_tok, out_stride, next_ids, next_pos, base_pos, pos_offset);
+  SB_CHECK_LAUNCH();
+  return 0;
+}
+
+int sb_accept(int32_t mode, int32_t b, int32_t k, int32_t vocab, const int32_t* target_tok, const float* p_probs,
+              const float* q_probs, const int32_t* draft_tok, int32_t draft_stride, const float* u_acc,
+              const float* u_res, int32_t u_stride, const int32_t* l_inj, const int32_t* produced,
+              const int32_t* target_len, int32_t* accepted_len, int32_t* advanced, int32_t* out_tok, void* stream) {
+  if (b <= 0 || k < 0) return SB_EINVAL;
+  if (mode == SB_ACCEPT_STOCHASTIC && (!p_probs || (k > 0 && (!q_probs || !u_acc)) || !u_res)) return SB_EINVAL;
+  if ((mode == SB_ACCEPT_GREEDY || mode == SB_ACCEPT_INJECTED) && !target_tok) return SB_EINVAL;
+  if (mode == SB_ACCEPT_INJECTED && !l_inj) return SB_EINVAL;
+  if (mode < 0 || mode > 2) return SB_EINVAL;
+  if ((vocab + kCdfChunk - 1) / kCdfChunk > 512) return SB_EUNSUPPORTED;
+  accept_kernel<<<b, 256, 0, (cudaStream_t)stream>>>(mode, k, vocab, target_tok, p_probs, q_probs, draft_tok,
+                                                     draft_stride, u_acc, u_res, u_stride, l_inj, produced,
+                                                     target_len, accepted_len, advanced, out_tok);
+  SB_CHECK_LAUNCH();
+  return 0;
+}
+
+int sb_kv_commit(int32_t b, int32_t k, const int32_t* advanced, const int32_t* accepted_len, const int32_t* out_tok,
+                 int32_t* tokens, int32_t tok_cap, int32_t* n_tok, int32_t* produced, const int32_t* target_len,
+                 int32_t* finish_iter, int32_t* iter, int32_t* live_count, int32_t* acc_log, int32_t acc_log_cap,
+                 void* stream) {
+  if (b <= 0 || k < 0) return SB_EINVAL;
+  commit_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(b, k, advanced, accepted_len, out_tok, tokens, tok_cap, n_tok,
+                                                     produced, target_len, finish_iter, iter, live_count, acc_log,
+                                                     acc_log_cap);
+  SB_CHECK_LAUNCH();
+  return 0;
+}
+
+int sb_prepare_iteration(int32_t b, int32_t k, const int32_t* tokens, int32_t tok_cap, const int32_t* n_tok,
+                         int32_t* d1_ids, int32_t* d1_pos, int32_t* v_ids, int32_t* v_pos, int32_t* d_last_pos,
+                         uint64_t seed, const int32_t* iter, float* uniforms, int32_t n_u,
+                         const int32_t* inj_samples, int32_t inj_count, int32_t* l_inj, void* stream) {
+  if (b <= 0 || k < 0 || n_u > 64) return SB_EINVAL;
+  if ((d1_ids == nullptr) != (d1_pos == nullptr)) return SB_EINVAL;
+  prepare_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(b, k, tokens, tok_cap, n_tok, d1_ids, d1_pos, v_ids, v_pos,
+                                                      d_last_pos, seed, iter, uniforms, n_u, inj_samples, inj_count,
+                                                      l_inj);
+  SB_CHECK_LAUNCH();
+  return 0;
+}
+
+float sb_uniform_host(uint64_t seed, uint64_t stream_id, uint64_t counter) { return u01(seed, stream_id, counter); }
+
+}  // extern "C"

@@ -1,0 +1,229 @@
+"""Draft / target decoder pair: shapes, seeded random-init weights in the
+B200 layout, KV-cache slabs, and the native forward call.
+
+The reference has no neural network (its "draft/target pair" is a
+hash-defined toy, ``TokenLevel`` engine.py:121-152); BASELINE.json's configs
+name real shapes, so this module builds those shapes with random weights
+(there is no network for checkpoints).  Weight layout in HBM, per layer:
+
+  w_qkv  [(nq + 2 nkv) hd, h]   Q | K | V rows          (one TMA stream)
+  w_o    [h, nq hd]
+  w_gu   [2 ffn, h]             gate/up rows interleaved g0,u0,g1,u1,...
+                                (the tcgen05 epilogue pairs adjacent TMEM
+                                lanes with one shuffle to emit silu(g)*u)
+  w_down [h, ffn]
+KV cache: [L][slots][nkv][ctx_max][hd] per K and V (one contiguous slab per
+(layer, slot, head) -> the attention kernel streams it linearly).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass, replace
+
+import numpy as np
+import torch
+
+from . import _native as N
+
+__all__ = ["DecoderConfig", "Decoder", "KVCache", "CONFIGS", "rope_table", "tiny_pair"]
+
+
+@dataclass(frozen=True)
+class DecoderConfig:
+    name: str
+    hidden: int
+    n_layers: int
+    n_heads: int
+    n_kv_heads: int
+    ffn: int
+    vocab: int = 32000
+    rms_eps: float = 1e-5
+    rope_theta: float = 10000.0
+
+    @property
+    def head_dim(self) -> int:
+        return self.hidden // self.n_heads
+
+    @property
+    def qkv_rows(self) -> int:
+        return (self.n_heads + 2 * self.n_kv_heads) * self.head_dim
+
+    def n_params(self, tied: bool = False) -> int:
+        h, L = self.hidden, self.n_layers
+        per = h * self.qkv_rows + h * self.n_heads * self.head_dim + 3 * h * self.ffn + 2 * h
+        return self.vocab * h * (1 if tied else 2) + L * per + h
+
+    def streamed_bytes_per_forward(self, dtype_bytes: int = 2) -> int:
+        """Weight bytes one forward streams from HBM (embedding is a gather,
+        excluded; lm_head and final norm included) -- SURVEY §8(d)."""
+        h, L = self.hidden, self.n_layers
+        per = h * self.qkv_rows + h * self.n_heads * self.head_dim + 3 * h * self.ffn + 2 * h
+        return (L * per + h + self.vocab * h) * dtype_bytes
+
+    def kv_bytes_per_token(self, dtype_bytes: int = 2) -> int:
+        return 2 * self.n_layers * self.n_kv_heads * self.head_dim * dtype_bytes
+
+
+CONFIGS = {
+    # BASELINE config 3 / 5 target and drafts (public model shapes; random init)
+    "llama-2-7b": DecoderConfig("llama-2-7b", 4096, 32, 32, 32, 11008, rms_eps=1e-5),
+    "llama-68m": DecoderConfig("llama-68m", 768, 2, 12, 12, 3072, rms_eps=1e-6),
+    "llama-160m": DecoderConfig("llama-160m", 768, 12, 12, 12, 3072, rms_eps=1e-6),
+    "llama-2-70b": DecoderConfig("llama-2-70b", 8192, 80, 64, 8, 28672, rms_eps=1e-5),
+    # BASELINE config 1: the small CPU-runnable pair
+    "tiny-target": DecoderConfig("tiny-target", 512, 4, 8, 8, 1376, rms_eps=1e-5),
+}
+
+
+def rope_table(max_pos: int, head_dim: int, theta: float) -> tuple[np.ndarray, np.ndarray]:
+    """cos/sin [max_pos, head_dim/2] fp32, computed in fp64 on the host so the
+    GPU and the CPU oracle rotate with identical constants."""
+    half = head_dim // 2
+    inv = theta ** (-(np.arange(half, dtype=np.float64) * 2.0) / head_dim)
+    ang = np.arange(max_pos, dtype=np.float64)[:, None] * inv[None, :]
+    return np.cos(ang).astype(np.float32), np.sin(ang).astype(np.float32)
+
+
+def _randn(shape, gen, device, std):
+    return torch.randn(*shape, generator=gen, device=device, dtype=torch.float32) * std
+
+
+class Decoder:
+    """Seeded random-init Llama-style decoder resident on the GPU.
+
+    init="host": fp32 masters drawn on the CPU with ``torch.Generator(seed)`` in
+    a fixed order (embed, per layer q,k,v,o,gate,up,down, lm_head) -- the CPU
+    oracle reproduces them exactly (used by the parity tests).
+    init="device": drawn on the GPU (7B/70B sizes; no CPU copy).
+    ``share_from``/``share_layers`` build a self-speculative draft that reuses
+    the target's embedding, lm_head and first layers (config 1's pair).
+    """
+
+    def __init__(self, cfg: DecoderConfig, dtype: str = "bf16", device="cuda", seed: int = 0,
+                 init: str = "host", max_pos: int = 4096, std: float = 0.02,
+                 share_from: "Decoder | None" = None, share_layers: int | None = None):
+        if dtype not in ("bf16", "fp32"):
+            raise ValueError(f"dtype must be bf16 or fp32, got {dtype!r}")
+        self.cfg = cfg
+        self.dtype_name = dtype
+        self.tdtype = torch.bfloat16 if dtype == "bf16" else torch.float32
+        self.sb_dtype = N.SB_BF16 if dtype == "bf16" else N.SB_F32
+        self.device = torch.device(device)
+        self.max_pos = max_pos
+        self.seed = seed
+        h, L = cfg.hidden, cfg.n_layers
+        if share_from is not None:
+            n_share = share_layers if share_layers is not None else L
+            base = share_from
+            self.embed, self.lm_head, self.final_norm = base.embed, base.lm_head, base.final_norm
+            self.layers = base.layers[:n_share]
+            self.masters = None if base.masters is None else {
+                "embed": base.masters["embed"], "lm_head": base.masters["lm_head"],
+                "layers": base.masters["layers"][:n_share],
+            }
+            self.cfg = replace(cfg, n_layers=n_share, name=f"{base.cfg.name}[:{n_share}]")
+        else:
+            gen_dev = "cpu" if init == "host" else self.device
+            gen = torch.Generator(device=gen_dev).manual_seed(seed)
+            keep = init == "host"
+            masters = {"layers": []} if keep else None
+
+            def mk(shape):
+                w = _randn(shape, gen, gen_dev, std)
+                return w
+
+            emb = mk((cfg.vocab, h))
+            if keep:
+                masters["embed"] = emb.to(self.tdtype).float()
+            self.embed = emb.to(device=self.device, dtype=self.tdtype)
+            del emb
+            self.layers = []
+            qd = cfg.n_heads * cfg.head_dim
+            kd = cfg.n_kv_heads * cfg.head_dim
+            for _ in range(L):
+                wq, wk, wv = mk((qd, h)), mk((kd, h)), mk((kd, h))
+                wo = mk((h, qd))
+                wg, wu = mk((cfg.ffn, h)), mk((cfg.ffn, h))
+                wd = mk((h, cfg.ffn))
+                lay = {
+                    "attn_norm": torch.ones(h, device=self.device, dtype=self.tdtype),
+                    "mlp_norm": torch.ones(h, device=self.device, dtype=self.tdtype),
+                    "w_qkv": torch.cat([wq, wk, wv], 0).to(device=self.device, dtype=self.tdtype),
+                    "w_o": wo.to(device=self.device, dtype=self.tdtype),
+                    "w_gu": torch.stack([wg, wu], 1).reshape(2 * cfg.ffn, h).to(device=self.device, dtype=self.tdtype),
+                    "w_down": wd.to(device=self.device, dtype=self.tdtype),
+                }
+                if keep:
+                    r = lambda t: t.to(self.tdtype).float()
+                    masters["layers"].append({"wq": r(wq), "wk": r(wk), "wv": r(wv), "wo": r(wo), "wg": r(wg),
+                                              "wu": r(wu), "wd": r(wd)})
+                self.layers.append(lay)
+                del wq, wk, wv, wo, wg, wu, wd
+            head = mk((cfg.vocab, h))
+            if keep:
+                masters["lm_head"] = head.to(self.tdtype).float()
+            self.lm_head = head.to(device=self.device, dtype=self.tdtype)
+            del head
+            self.final_norm = torch.ones(h, device=self.device, dtype=self.tdtype)
+            self.masters = masters
+        cos, sin = rope_table(max_pos, self.cfg.head_dim, self.cfg.rope_theta)
+        self.rope_cos = torch.from_numpy(cos).to(self.device)
+        self.rope_sin = torch.from_numpy(sin).to(self.device)
+        self._build_struct()
+
+    # ---------------------------------------------------------------- C struct
+    def _build_struct(self):
+        cfg = self.cfg
+        L = cfg.n_layers
+        arr = lambda key: (C.c_void_p * L)(*[lay[key].data_ptr() for lay in self.layers])
+        self._arrays = {k: arr(k) for k in ("attn_norm", "w_qkv", "w_o", "mlp_norm", "w_gu", "w_down")}
+        s = N.SbDecoder()
+        s.n_layers, s.hidden, s.n_heads, s.n_kv_heads = L, cfg.hidden, cfg.n_heads, cfg.n_kv_heads
+        s.head_dim, s.ffn, s.vocab, s.dtype, s.max_pos = cfg.head_dim, cfg.ffn, cfg.vocab, self.sb_dtype, self.max_pos
+        s.rms_eps = cfg.rms_eps
+        s.embed, s.final_norm, s.lm_head = self.embed.data_ptr(), self.final_norm.data_ptr(), self.lm_head.data_ptr()
+        for k, a in self._arrays.items():
+            setattr(s, k, C.cast(a, C.POINTER(C.c_void_p)))
+        s.rope_cos, s.rope_sin = self.rope_cos.data_ptr(), self.rope_sin.data_ptr()
+        self.struct = s
+
+    def workspace_bytes(self, n_tokens: int) -> int:
+        return int(N.load().sb_decoder_workspace_bytes(C.byref(self.struct), n_tokens))
+
+    def new_kv(self, slots: int, ctx_max: int) -> "KVCache":
+        return KVCache(self, slots, ctx_max)
+
+    def forward(self, kv: "KVCache", ids, slots, pos, n_seq: int, q_len: int, logits, logits_mode: int,
+                workspace, stream=None):
+        """Launch one forward on ``stream`` (default: torch's current stream)."""
+        st = torch.cuda.current_stream(self.device).cuda_stream if stream is None else stream
+        N.call("sb_decoder_forward", C.byref(self.struct), C.byref(kv.struct), N.ptr(ids), N.ptr(slots),
+               N.ptr(pos), n_seq, q_len, N.ptr(logits), logits_mode, N.ptr(workspace), workspace.numel(), st)
+
+    def weight_bytes(self) -> int:
+        return self.cfg.streamed_bytes_per_forward(2 if self.dtype_name == "bf16" else 4)
+
+
+class KVCache:
+    """K/V slabs [L][slots][nkv][ctx_max][hd] in the decoder's dtype."""
+
+    def __init__(self, dec: Decoder, slots: int, ctx_max: int):
+        cfg = dec.cfg
+        shape = (cfg.n_layers, slots, cfg.n_kv_heads, ctx_max, cfg.head_dim)
+        self.k = torch.zeros(shape, device=dec.device, dtype=dec.tdtype)
+        self.v = torch.zeros(shape, device=dec.device, dtype=dec.tdtype)
+        self.slots, self.ctx_max = slots, ctx_max
+        s = N.SbKVCache()
+        s.k, s.v, s.slots, s.ctx_max = self.k.data_ptr(), self.v.data_ptr(), slots, ctx_max
+        self.struct = s
+
+
+def tiny_pair(dtype: str = "fp32", device="cuda", seed: int = 0, max_pos: int = 1024, draft_layers: int = 1):
+    """Config 1 pair: tiny Llama target (h=512, L=4) and a self-speculative draft
+    made of the target's first layer + shared embedding / lm_head."""
+    tgt = Decoder(CONFIGS["tiny-target"], dtype=dtype, device=device, seed=seed, init="host", max_pos=max_pos)
+    drf = Decoder(CONFIGS["tiny-target"], dtype=dtype, device=device, share_from=tgt, share_layers=draft_layers,
+                  max_pos=max_pos)
+    return tgt, drf

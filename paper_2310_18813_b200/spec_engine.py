@@ -1,0 +1,385 @@
+"""SpecEngine: batched speculative decoding on one B200.
+
+``SpecEngine(target, draft).generate(batch, k)`` is the GPU implementation of
+the reference's ``run_batch`` hot loop (engine.py:176-221): every iteration is
+
+  prepare -> draft step 1 (2 tokens/seq) -> draft steps 2..k (1 token/seq)
+          -> target verify over b(k+1) tokens -> argmax | softmax
+          -> accept (K4) -> commit + in-place KV rollback (K5)
+
+all on one stream and captured into ONE CUDA graph per (b, k, mode); state
+(tokens, lengths, iteration counter) lives on the device so graph replays are
+self-advancing.  The host only replays graphs and, every few iterations,
+reads a 4-byte live count (pinned, async) to stop.  The formed batch is held
+until every sequence finishes, finished rows are masked (engine.py:186-188).
+
+Acceptance modes:
+  greedy      -- LCP of draft tokens and target argmax (engine.py:74-86)
+  stochastic  -- speculative sampling with the engine's counter RNG
+  injected    -- real draft + verify work, accepted length drawn on device
+                 from an AcceptanceTrace (TraceSampler law, engine.py:109-118);
+                 used for throughput runs on random weights, where real
+                 acceptance is ~0.  Always labelled.
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .acceptance import AcceptanceTrace
+from .decoder import Decoder, KVCache
+from .engine import BatchResult, SequenceState
+
+__all__ = ["SpecEngine", "IterationStats"]
+
+_MODES = {"greedy": N.ACCEPT_GREEDY, "stochastic": N.ACCEPT_STOCHASTIC, "injected": N.ACCEPT_INJECTED}
+_NU = 64  # uniforms per sequence slot per iteration
+
+
+@dataclass
+class IterationStats:
+    prefill_ms: float = 0.0
+    decode_ms: float = 0.0
+    iterations: int = 0
+    syncs: int = 0
+    accepted: np.ndarray | None = None  # [iters, b], -1 after finishing
+    finish_iter: np.ndarray | None = None
+    kernels_per_iteration: int = 0
+    graph: bool = True
+    extra: dict = field(default_factory=dict)
+
+
+class SpecEngine:
+    def __init__(self, target: Decoder, draft: Decoder | None, *, mode: str = "greedy",
+                 acceptance: AcceptanceTrace | None = None, max_batch: int = 8, max_k: int = 8,
+                 prompt_len: int = 128, max_new: int = 128, seed: int = 0, use_graphs: bool = True,
+                 prompt_fn=None, prefill_chunk_tokens: int = 4096):
+        if mode not in _MODES:
+            raise ValueError(f"mode must be one of {sorted(_MODES)}, got {mode!r}")
+        if mode == "injected" and acceptance is None:
+            raise ValueError("injected mode needs an AcceptanceTrace")
+        if draft is not None and draft.cfg.vocab != target.cfg.vocab:
+            raise ValueError("draft and target must share a vocabulary")
+        if draft is not None and draft.sb_dtype != target.sb_dtype:
+            raise ValueError("draft and target must share a dtype")
+        N.load()
+        N.init_device()
+        self.target, self.draft = target, draft
+        self.mode = mode
+        self.mode_id = _MODES[mode]
+        self.acceptance = acceptance
+        self.max_batch, self.max_k = max_batch, max_k if draft is not None else 0
+        self.prompt_len, self.max_new = prompt_len, max_new
+        self.seed = seed
+        self.use_graphs = use_graphs
+        self.prompt_fn = prompt_fn or self._default_prompt
+        self.dev = target.device
+        V = target.cfg.vocab
+        self.V = V
+        B, K = max_batch, self.max_k
+        self.cap = prompt_len + max_new + K + 2
+        self.ctx_max = self.cap + 1
+        if self.ctx_max > target.max_pos or (draft is not None and self.ctx_max > draft.max_pos):
+            raise ValueError("rope table shorter than prompt_len + max_new + k")
+        i32 = dict(device=self.dev, dtype=torch.int32)
+        f32 = dict(device=self.dev, dtype=torch.float32)
+        self.kv_t = target.new_kv(B, self.ctx_max)
+        self.kv_d = draft.new_kv(B, self.ctx_max) if draft is not None else None
+        self.slots = torch.arange(B, **i32)
+        self.tokens = torch.zeros(B, self.cap, **i32)
+        self.n_tok = torch.zeros(B, **i32)
+        self.produced = torch.zeros(B, **i32)
+        self.target_len = torch.zeros(B, **i32)
+        self.finish_iter = torch.full((B,), -1, **i32)
+        self.iter = torch.zeros(1, **i32)
+        self.live = torch.zeros(1, **i32)
+        self.d1_ids = torch.zeros(B * 2, **i32)
+        self.d1_pos = torch.zeros(B * 2, **i32)
+        self.ds_ids = torch.zeros(B, **i32)
+        self.ds_pos = torch.zeros(B, **i32)
+        self.d_base = torch.zeros(B, **i32)
+        self.v_ids = torch.zeros(B * (K + 1), **i32)
+        self.v_pos = torch.zeros(B * (K + 1), **i32)
+        self.uniforms = torch.zeros(B * _NU, **f32)
+        self.l_inj = torch.zeros(B, **i32)
+        samples = acceptance.samples if acceptance is not None else (0,)
+        self.inj_samples = torch.tensor(list(samples), **i32)
+        self.d_logits = torch.zeros(B, V, **f32) if draft is not None else None
+        self.q_probs = torch.zeros(max(1, B * K), V, **f32) if (draft is not None and mode == "stochastic") else None
+        self.t_logits = torch.zeros(B * (K + 1), V, **f32)
+        self.t_tok = torch.zeros(B * (K + 1), **i32)
+        self.accepted = torch.zeros(B, **i32)
+        self.advanced = torch.zeros(B, **i32)
+        self.out_tok = torch.zeros(B * (K + 1), **i32)
+        self.log_cap = max_new + 4
+        self.acc_log = torch.full((self.log_cap, B), -1, **i32)
+        # prefill staging
+        self.pf_chunk = max(1, prefill_chunk_tokens // max(1, prompt_len - 1))
+        pf_tok = self.pf_chunk * max(1, prompt_len - 1)
+        self.pf_ids = torch.zeros(pf_tok, **i32)
+        self.pf_pos = torch.zeros(pf_tok, **i32)
+        ws = max(target.workspace_bytes(B * (K + 1)), target.workspace_bytes(pf_tok))
+        if draft is not None:
+            ws = max(ws, draft.workspace_bytes(2 * B), draft.workspace_bytes(pf_tok))
+        self.workspace = torch.zeros(ws, device=self.dev, dtype=torch.uint8)
+        self.live_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
+        self.stream = torch.cuda.Stream(device=self.dev)
+        self.graphs: dict[tuple[int, int], torch.cuda.CUDAGraph] = {}
+        self._iter_kernels: dict[tuple[int, int], int] = {}
+        self.stats = IterationStats()
+
+    # ------------------------------------------------------------- prompts
+    def _default_prompt(self, request_id: int) -> np.ndarray:
+        rng = np.random.default_rng([self.seed, int(request_id)])
+        return rng.integers(0, self.V, size=self.prompt_len, dtype=np.int64).astype(np.int32)
+
+    # ------------------------------------------------------------- one iteration
+    def _iteration(self, b: int, k: int) -> None:
+        st = torch.cuda.current_stream(self.dev).cuda_stream
+        lib = N.load()
+        launches = 4  # prepare, argmax|softmax, accept, commit
+        V = self.V
+        mode = self.mode_id
+        sample = mode == N.ACCEPT_STOCHASTIC
+        use_draft = k > 0 and self.draft is not None
+        N.call("sb_prepare_iteration", b, k, N.ptr(self.tokens), self.cap, N.ptr(self.n_tok),
+               N.ptr(self.d1_ids) if use_draft else None, N.ptr(self.d1_pos) if use_draft else None,
+               N.ptr(self.v_ids), N.ptr(self.v_pos), N.ptr(self.d_base), self.seed, N.ptr(self.iter),
+               N.ptr(self.uniforms), _NU, N.ptr(self.inj_samples), self.inj_samples.numel(),
+               N.ptr(self.l_inj), st)
+        if use_draft:
+            sel = N.SELECT_SAMPLE if sample else N.SELECT_ARGMAX
+            u_base = self.uniforms.data_ptr()
+            for j in range(1, k + 1):
+                if j == 1:
+                    ids, pos, q = self.d1_ids, self.d1_pos, 2
+                else:
+                    ids, pos, q = self.ds_ids, self.ds_pos, 1
+                self.draft.forward(self.kv_d, ids, self.slots, pos, b, q, self.d_logits, N.LOGITS_LAST,
+                                   self.workspace, st)
+                launches += lib.sb_last_kernel_count() + 1
+                probs = None
+                if sample:
+                    probs = self.q_probs.data_ptr() + (j - 1) * V * 4
+                N.call("sb_select_tokens", N.ptr(self.d_logits), b, V, sel, u_base + (j - 1) * 4, _NU,
+                       probs, k * V, self.v_ids.data_ptr() + j * 4, k + 1, N.ptr(self.ds_ids),
+                       N.ptr(self.ds_pos), N.ptr(self.d_base), j, st)
+        T = b * (k + 1)
+        self.target.forward(self.kv_t, self.v_ids, self.slots, self.v_pos, b, k + 1, self.t_logits, N.LOGITS_ALL,
+                            self.workspace, st)
+        launches += lib.sb_last_kernel_count()
+        self._iter_kernels[(b, k)] = launches
+        if sample:
+            N.call("sb_softmax_rows", N.ptr(self.t_logits), T, V, N.ptr(self.t_logits), st)
+        else:
+            N.call("sb_argmax_rows", N.ptr(self.t_logits), T, V, N.ptr(self.t_tok), st)
+        u_base = self.uniforms.data_ptr()
+        N.call("sb_accept", mode, b, k, V, N.ptr(self.t_tok), N.ptr(self.t_logits),
+               N.ptr(self.q_probs) if sample and k > 0 else None, self.v_ids.data_ptr() + 4, k + 1,
+               u_base + k * 4, u_base + 2 * k * 4, _NU, N.ptr(self.l_inj), N.ptr(self.produced),
+               N.ptr(self.target_len), N.ptr(self.accepted), N.ptr(self.advanced), N.ptr(self.out_tok), st)
+        N.call("sb_kv_commit", b, k, N.ptr(self.advanced), N.ptr(self.accepted), N.ptr(self.out_tok),
+               N.ptr(self.tokens), self.cap, N.ptr(self.n_tok), N.ptr(self.produced), N.ptr(self.target_len),
+               N.ptr(self.finish_iter), N.ptr(self.iter), N.ptr(self.live), N.ptr(self.acc_log), self.log_cap, st)
+
+    def kernels_per_iteration(self, b: int, k: int) -> int:
+        """Native kernel launches in one (b, k) iteration, as counted while it was
+        last issued (forward driver count + one per token-level kernel)."""
+        return self._iter_kernels.get((b, k), 0)
+
+    def _graph(self, b: int, k: int):
+        key = (b, k)
+        g = self.graphs.get(key)
+        if g is None:
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(self.stream):
+                torch.cuda.synchronize(self.dev)
+                with torch.cuda.graph(g, stream=self.stream):
+                    self._iteration(b, k)
+            self.graphs[key] = g
+        return g
+
+    # ------------------------------------------------------------- batch lifecycle
+    def _load_batch(self, states: list[SequenceState], prompts) -> None:
+        b = len(states)
+        P = self.prompt_len
+        toks = np.zeros((b, self.cap), dtype=np.int32)
+        for i, st in enumerate(states):
+            pr = prompts[i] if prompts is not None else self.prompt_fn(st.request_id)
+            pr = np.asarray(pr, dtype=np.int32).reshape(-1)
+            if pr.size != P:
+                raise ValueError(f"prompt of request {st.request_id} has {pr.size} tokens, engine expects {P}")
+            toks[i, :P] = pr
+        self.tokens[:b].copy_(torch.from_numpy(toks), non_blocking=False)
+        self.n_tok[:b].fill_(P)
+        self.produced[:b].zero_()
+        self.target_len[:b].copy_(torch.tensor([st.target_len for st in states], dtype=torch.int32))
+        self.finish_iter.fill_(-1)
+        self.iter.zero_()
+        self.acc_log.fill_(-1)
+        self._prompts_host = toks
+
+    def _prefill(self, b: int) -> None:
+        P = self.prompt_len
+        if P < 2:
+            return
+        q = P - 1
+        for s0 in range(0, b, self.pf_chunk):
+            nb = min(self.pf_chunk, b - s0)
+            ids = torch.from_numpy(self._prompts_host[s0:s0 + nb, :q].reshape(-1).copy())
+            self.pf_ids[: nb * q].copy_(ids)
+            self.pf_pos[: nb * q].copy_(torch.arange(q, dtype=torch.int32).repeat(nb))
+            slots = self.slots[s0:]
+            self.target.forward(self.kv_t, self.pf_ids, slots, self.pf_pos, nb, q, None, N.LOGITS_NONE,
+                                self.workspace)
+            if self.draft is not None:
+                self.draft.forward(self.kv_d, self.pf_ids, slots, self.pf_pos, nb, q, None, N.LOGITS_NONE,
+                                   self.workspace)
+
+    def generate(self, states: list[SequenceState], k: int, rng=None, prompts=None) -> BatchResult:
+        """Run a formed batch to completion at speculation length k.
+
+        ``total_time`` / ``per_sequence_finish`` are CUDA-event milliseconds of
+        the decode phase (prefill excluded, as in the reference's cost model,
+        SPEC.md:141; reported in ``self.stats.prefill_ms``).  Each state's
+        ``tokens`` receives its generated stream and ``produced`` its length.
+        """
+        if not states:
+            raise ValueError("empty batch")
+        for st in states:
+            if st.produced != 0:
+                raise ValueError(f"sequence {st.request_id} is not fresh (produced={st.produced})")
+            if st.target_len > self.max_new:
+                raise ValueError(f"target_len {st.target_len} exceeds engine max_new {self.max_new}")
+        if k < 0:
+            raise ValueError(f"s must be >= 0, got {k}")
+        b = len(states)
+        if b > self.max_batch:
+            raise ValueError(f"batch {b} exceeds engine max_batch {self.max_batch}")
+        if k > self.max_k:
+            if self.draft is None:
+                raise ValueError("speculation needs a draft model (k > 0)")
+            raise ValueError(f"k={k} exceeds engine max_k {self.max_k}")
+        with torch.cuda.stream(self.stream):
+            self._load_batch(states, prompts)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            self._prefill(b)
+            e1.record()
+            graph = self._graph(b, k) if self.use_graphs else None
+            ev = [torch.cuda.Event(enable_timing=True)]
+            ev[0].record()
+            remaining = max(st.target_len for st in states)
+            syncs = 0
+            while True:
+                n_launch = max(1, math.ceil(remaining / (k + 1)))
+                for _ in range(n_launch):
+                    if graph is not None:
+                        graph.replay()
+                    else:
+                        self._iteration(b, k)
+                    e = torch.cuda.Event(enable_timing=True)
+                    e.record()
+                    ev.append(e)
+                self.live_host.copy_(self.live, non_blocking=True)
+                self.stream.synchronize()
+                syncs += 1
+                if int(self.live_host[0]) == 0:
+                    break
+                rem = (self.target_len[:b] - self.produced[:b]).max().item()
+                remaining = max(1, int(rem))
+                if len(ev) > 4 * self.max_new + 8:
+                    raise RuntimeError("speculative loop failed to terminate")
+            torch.cuda.synchronize(self.dev)
+        iters = len(ev) - 1
+        fin = self.finish_iter[:b].cpu().numpy()
+        toks = self.tokens[:b].cpu().numpy()
+        produced = self.produced[:b].cpu().numpy()
+        P = self.prompt_len
+        finish = {}
+        for i, st in enumerate(states):
+            st.tokens = [int(t) for t in toks[i, P:P + int(produced[i])]]
+            st.produced = int(produced[i])
+            fi = int(fin[i])
+            finish[st.request_id] = ev[0].elapsed_time(ev[fi]) if fi > 0 else 0.0
+        total = ev[0].elapsed_time(ev[-1])
+        self.stats = IterationStats(
+            prefill_ms=e0.elapsed_time(e1), decode_ms=total, iterations=iters, syncs=syncs,
+            accepted=self.acc_log[: min(iters, self.log_cap), :b].cpu().numpy(), finish_iter=fin,
+            kernels_per_iteration=self.kernels_per_iteration(b, k), graph=graph is not None,
+        )
+        return BatchResult(batch_size=b, spec_len=k, total_time=total, steps=iters,
+                           tokens_generated=sum(st.target_len for st in states), per_sequence_finish=finish)
+
+    # reference-compatible per-sequence hook (DraftOracle protocol) ----------
+    def step(self, state, s, rng):  # pragma: no cover - batched engine
+        raise NotImplementedError("SpecEngine is a batched oracle: use run_batch/generate")
+
+
+# ---------------------------------------------------------------- timing hooks
+def _timed_graph(fn, reps: int, stream) -> float:
+    """Capture ``fn`` once into a CUDA graph, replay it ``reps`` times and return
+    the mean CUDA-event milliseconds per replay (after one warm replay)."""
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(stream):
+        torch.cuda.synchronize()
+        with torch.cuda.graph(g, stream=stream):
+            fn()
+        g.replay()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            g.replay()
+        e1.record()
+        e1.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def _stage_context(eng: "SpecEngine", b: int, k: int, ctx: int) -> None:
+    """Put b slots at context length ctx with random committed tokens (the KV
+    rows are whatever the cache holds: timing only)."""
+    rng = np.random.default_rng(ctx)
+    eng.tokens[:b].copy_(torch.from_numpy(rng.integers(0, eng.V, size=(b, eng.cap)).astype(np.int32)))
+    eng.n_tok[:b].fill_(ctx)
+    eng.iter.zero_()
+    st = torch.cuda.current_stream(eng.dev).cuda_stream
+    N.call("sb_prepare_iteration", b, k, N.ptr(eng.tokens), eng.cap, N.ptr(eng.n_tok), N.ptr(eng.d1_ids),
+           N.ptr(eng.d1_pos), N.ptr(eng.v_ids), N.ptr(eng.v_pos), N.ptr(eng.d_base), eng.seed, N.ptr(eng.iter),
+           N.ptr(eng.uniforms), _NU, None, 0, None, st)
+    eng.ds_ids[:b].copy_(eng.v_ids.view(-1)[: b * (k + 1): k + 1])
+    eng.ds_pos[:b].copy_(eng.d_base[:b] + 1)
+    torch.cuda.synchronize(eng.dev)
+
+
+def time_verify(self, b: int, k: int, ctx: int = 192, reps: int = 20) -> float:
+    """Mean ms of ONE target verify forward over b(k+1) tokens at context ctx."""
+    _stage_context(self, b, k, ctx)
+    fn = lambda: self.target.forward(self.kv_t, self.v_ids, self.slots, self.v_pos, b, k + 1, self.t_logits,
+                                     N.LOGITS_ALL, self.workspace)
+    return _timed_graph(fn, reps, self.stream)
+
+
+def time_draft_step(self, b: int, ctx: int = 192, reps: int = 20) -> float:
+    """Mean ms of ONE draft decode step (b sequences x 1 token) incl. token selection."""
+    if self.draft is None:
+        return 0.0
+    _stage_context(self, b, 1, ctx)
+
+    def fn():
+        st = torch.cuda.current_stream(self.dev).cuda_stream
+        self.draft.forward(self.kv_d, self.ds_ids, self.slots, self.ds_pos, b, 1, self.d_logits, N.LOGITS_LAST,
+                           self.workspace, st)
+        N.call("sb_select_tokens", N.ptr(self.d_logits), b, self.V, N.SELECT_ARGMAX, None, _NU, None, 0, None, 0,
+               N.ptr(self.ds_ids), None, None, 0, st)
+
+    return _timed_graph(fn, reps, self.stream)
+
+
+SpecEngine.time_verify = time_verify
+SpecEngine.time_draft_step = time_draft_step
