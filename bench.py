@@ -238,11 +238,11 @@ def run_ours(args):
     sweep = {}
     if not args.quick:
         for kk in K_GRID:
-            res = eng.generate(batch(-1), kk)
+            res = eng.generate(batch(90000 + kk), kk)
             sweep[kk] = b * NEW / ((res.total_time + eng.stats.prefill_ms) / 1e3)
     # ---- warmup + timed steps (device time, CUDA events around whole generate incl. prefill)
     for w in range(args.warmup):
-        eng.generate(batch(-2 - w), k)
+        eng.generate(batch(80000 + w), k)
     if world > 1:
         torch.distributed.barrier()
     torch.cuda.synchronize()

@@ -37,13 +37,9 @@ static size_t carve(const sb_decoder_t* m, int T, char* base, FwdWorkspace* w) {
   };
   FwdWorkspace tmp;
   FwdWorkspace* o = w ? w : &tmp;
-  o->resid = (float*)take((size_t)T * m->hidden * 4);
-  o->xn = take((size_t)T * m->hidden * es);
-  o->qkv = take((size_t)T * qkv_n * es);
-  o->qr = take((size_t)T * qd * es);
-  o->attn = take((size_t)T * qd * es);
-  o->act = take((size_t)T * m->ffn * es);
-  o->last = take((size_t)T * m->hidden * es);
+  // The GEMM region comes FIRST: its stream-K tile counters must sit at the
+  // same address for every forward sharing this workspace, whatever T is
+  // (they self-reset; any other placement would land them on dirty memory).
   int maxN = m->vocab;
   if (2 * m->ffn > maxN) maxN = 2 * m->ffn;
   if (qkv_n > maxN) maxN = qkv_n;
@@ -51,6 +47,13 @@ static size_t carve(const sb_decoder_t* m, int T, char* base, FwdWorkspace* w) {
   if (qd > maxK) maxK = qd;
   o->gemm_ws_bytes = gemm_workspace_bytes(T, maxN, maxK);
   o->gemm_ws = take(o->gemm_ws_bytes);
+  o->resid = (float*)take((size_t)T * m->hidden * 4);
+  o->xn = take((size_t)T * m->hidden * es);
+  o->qkv = take((size_t)T * qkv_n * es);
+  o->qr = take((size_t)T * qd * es);
+  o->attn = take((size_t)T * qd * es);
+  o->act = take((size_t)T * m->ffn * es);
+  o->last = take((size_t)T * m->hidden * es);
   return off;
 }
 
@@ -140,6 +143,12 @@ int sb_init(void) {
   // one-time host setup outside any stream capture: kernel attributes and the
   // driver's tensor-map encoder (TMA descriptors are built per GEMM call)
   return gemm_tc_init();
+}
+
+int sb_set_gemm_backend(int32_t backend) {
+  if (backend < 0 || backend > 2) return SB_EINVAL;
+  g_backend_override = backend;
+  return 0;
 }
 
 int sb_version(void) { return SB_ABI_VERSION; }

@@ -99,7 +99,10 @@ int gemm_simt(const GemmArgs& a, cudaStream_t st) {
   return 0;
 }
 
+int g_backend_override = GEMM_AUTO;
+
 int gemm(const GemmArgs& a, int backend, cudaStream_t st) {
+  if (backend == GEMM_AUTO) backend = g_backend_override;
   if (backend == GEMM_SIMT) return gemm_simt(a, st);
   if (backend == GEMM_TC) return gemm_tc(a, st);
   if (a.dtype == SB_BF16 && gemm_tc_supported(a)) return gemm_tc(a, st);

@@ -34,6 +34,11 @@ constexpr int TC_BK = 64;    // k per stage (one 128-byte swizzle row of bf16)
 constexpr int TC_UK = 16;    // k per tcgen05.mma (kind::f16)
 constexpr int TC_THREADS = 192;
 constexpr int TC_MAX_TN = 256;
+// Stream-K tile counters live at the head of the workspace in a FIXED-size
+// region (every GEMM sharing the workspace must agree on where partials start,
+// or one GEMM's partial slots would clobber another's self-resetting counters).
+constexpr int TC_MAX_TILES = 16384;
+constexpr size_t TC_CNT_BYTES = (size_t)TC_MAX_TILES * 4;
 
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -409,7 +414,7 @@ static TcPlan plan(int M, int N, int K) {
   long long g = (long long)num_sms() * q.ctas_per_sm;
   q.grid = (int)(units < g ? units : g);
   q.part_bytes = (size_t)q.grid * 2 * q.tn * TC_BM * 4;
-  q.cnt_bytes = ((size_t)q.n_tiles * 4 + 255) / 256 * 256;
+  q.cnt_bytes = TC_CNT_BYTES;
   return q;
 }
 
@@ -434,17 +439,16 @@ bool gemm_tc_supported(const GemmArgs& a) {
 
 size_t gemm_workspace_bytes(int M, int N, int K) {
   // sized for the simt fallback (none) and the tcgen05 stream-K partials
-  TcPlan q;
-  q.tn = tn_for(M);
-  int n_tiles = ((N + TC_BM - 1) / TC_BM) * ((M + q.tn - 1) / q.tn);
-  size_t grid = 148 * 2;
-  return grid * 2 * q.tn * TC_BM * 4 + ((size_t)n_tiles * 4 + 255) / 256 * 256 + 4096;
+  const int tn = tn_for(M);
+  size_t grid = (size_t)num_sms() * 2;
+  return grid * 2 * tn * TC_BM * 4 + TC_CNT_BYTES + 4096;
 }
 
 int gemm_tc(const GemmArgs& a, cudaStream_t st) {
   if (!gemm_tc_supported(a)) return SB_EUNSUPPORTED;
   if (a.M <= 0 || a.N <= 0 || a.K <= 0) return SB_EINVAL;
   TcPlan q = plan(a.M, a.N, a.K);
+  if (q.n_tiles > TC_MAX_TILES) return SB_EUNSUPPORTED;
   if (q.part_bytes + q.cnt_bytes > a.ws_bytes || !a.workspace) return SB_EWORKSPACE;
   CUtensorMap mw, mx;
   SB_TRY(make_map(&mw, a.w, a.N, a.K, a.K, TC_BM));

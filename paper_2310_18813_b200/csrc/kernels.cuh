@@ -26,6 +26,7 @@ struct GemmArgs {
   size_t ws_bytes;
 };
 
+extern int g_backend_override;  // sb_set_gemm_backend (ablation / tests)
 int gemm(const GemmArgs& a, int backend, cudaStream_t st);
 size_t gemm_workspace_bytes(int M, int N, int K);
 int gemm_simt(const GemmArgs& a, cudaStream_t st);

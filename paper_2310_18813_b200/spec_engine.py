@@ -311,7 +311,7 @@ class SpecEngine:
         total = ev[0].elapsed_time(ev[-1])
         self.stats = IterationStats(
             prefill_ms=e0.elapsed_time(e1), decode_ms=total, iterations=iters, syncs=syncs,
-            accepted=self.acc_log[: min(iters, self.log_cap), :b].cpu().numpy(), finish_iter=fin,
+            accepted=self.acc_log.view(-1)[: min(iters, self.log_cap) * b].view(-1, b).cpu().numpy(), finish_iter=fin,
             kernels_per_iteration=self.kernels_per_iteration(b, k), graph=graph is not None,
         )
         return BatchResult(batch_size=b, spec_len=k, total_time=total, steps=iters,

@@ -276,3 +276,20 @@ def test_kv_commit_masks_finished_and_logs(cuda_dev):
     assert fin.cpu().tolist() == [-1, 2, 5]
     assert it.item() == 5 and live.item() == 1
     assert log.cpu().numpy()[4].tolist() == [2, -1, 0]
+
+
+def test_gemm_sequence_shares_workspace(cuda_dev):
+    """Regression: GEMMs of different tile counts share one workspace (as in a
+    forward); stream-K counters must survive other GEMMs' partial slots."""
+    shapes = [(63, 1536, 512), (63, 512, 512), (63, 2752, 512), (63, 512, 1376), (63, 32000, 512)] * 3
+    ws = torch.zeros(int(N.load().sb_gemm_workspace_bytes(63, 32000, 1376)), device=cuda_dev, dtype=torch.uint8)
+    g = torch.Generator(device=cuda_dev).manual_seed(1)
+    for M, N_, K in shapes:
+        x = (torch.randn(M, K, generator=g, device=cuda_dev) * 0.5).to(torch.bfloat16)
+        w = (torch.randn(N_, K, generator=g, device=cuda_dev) * 0.02).to(torch.bfloat16)
+        y = torch.zeros(M, N_, device=cuda_dev)
+        N.call("sb_gemm", N.SB_BF16, x.data_ptr(), w.data_ptr(), y.data_ptr(), M, N_, K, N.EPI_STORE_F32, N.GEMM_TC,
+               ws.data_ptr(), ws.numel(), _st())
+        ref = x.float() @ w.float().T
+        torch.cuda.synchronize()
+        assert (y - ref).abs().max().item() <= 1e-4 * ref.abs().max().item() + 1e-5, (M, N_, K)
