@@ -211,6 +211,8 @@ float sb_uniform_host(uint64_t seed, uint64_t stream_id, uint64_t counter);
 int sb_init(void);
 /* Force the forward's GEMM backend (0 auto = tcgen05 for bf16, 1 SIMT, 2 tcgen05); for ablations. */
 int sb_set_gemm_backend(int32_t backend);
+/* Programmatic dependent launch for every kernel (default on); 0 disables (ablation). */
+int sb_set_pdl(int32_t enabled);
 int sb_version(void);
 const char* sb_build_info(void);
 int sb_last_kernel_count(void); /* kernels launched by the last sb_decoder_forward */

@@ -53,6 +53,7 @@ class SbKVCache(C.Structure):
 _SIGS = {
     "sb_init": (C.c_int, []),
     "sb_set_gemm_backend": (C.c_int, [_I]),
+    "sb_set_pdl": (C.c_int, [_I]),
     "sb_version": (C.c_int, []),
     "sb_build_info": (C.c_char_p, []),
     "sb_last_kernel_count": (C.c_int, []),

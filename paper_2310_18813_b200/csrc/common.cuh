@@ -21,6 +21,32 @@
 namespace sb {
 
 extern thread_local int g_kernel_count;  // launches issued by the current forward
+extern int g_pdl;                        // launch with programmatic stream serialization (PDL)
+
+// Programmatic dependent launch: every kernel of the engine waits for its
+// predecessor's memory before touching activations, and immediately lets its
+// successor launch (the successor's prologue / weight prefetch overlaps).
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// Launch helper: cudaLaunchKernelEx with the PDL attribute (and optional cluster).
+template <typename... KArgs, typename... Args>
+inline int launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = g_pdl ? 1 : 0;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...);
+  if (e != cudaSuccess) return (int)e;
+  ++g_kernel_count;
+  return 0;
+}
 
 __device__ __forceinline__ float to_f32(float x) { return x; }
 __device__ __forceinline__ float to_f32(__nv_bfloat16 x) { return __bfloat162float(x); }

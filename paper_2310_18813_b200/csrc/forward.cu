@@ -151,6 +151,11 @@ int sb_set_gemm_backend(int32_t backend) {
   return 0;
 }
 
+int sb_set_pdl(int32_t enabled) {
+  g_pdl = enabled ? 1 : 0;
+  return 0;
+}
+
 int sb_version(void) { return SB_ABI_VERSION; }
 
 const char* sb_build_info(void) {

@@ -18,6 +18,8 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const T* __restrict__ X,
                                                         int M, int N, int K, int ldx, int epi) {
   __shared__ float Ws[SBK][SBN + 1];
   __shared__ float Xs[SBK][SBM + 1];
+  griddep_wait();
+  griddep_launch();
   const int tid = threadIdx.x;
   const int tx = tid & 15, ty = tid >> 4;
   const int n_blk = blockIdx.x * SBN, m_blk = blockIdx.y * SBM;
@@ -89,14 +91,10 @@ int gemm_simt(const GemmArgs& a, cudaStream_t st) {
   if (a.epi == EPI_SILU_MUL && (a.N & 1)) return SB_EINVAL;
   dim3 grid((a.N + SBN - 1) / SBN, (a.M + SBM - 1) / SBM);
   if (a.dtype == SB_BF16)
-    gemm_simt_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((const __nv_bfloat16*)a.x, (const __nv_bfloat16*)a.w, a.y,
-                                                          a.M, a.N, a.K, a.ldx, a.epi);
-  else
-    gemm_simt_kernel<float><<<grid, 256, 0, st>>>((const float*)a.x, (const float*)a.w, a.y, a.M, a.N, a.K, a.ldx,
-                                                  a.epi);
-  g_kernel_count++;
-  SB_CHECK_LAUNCH();
-  return 0;
+    return launch_k(gemm_simt_kernel<__nv_bfloat16>, grid, dim3(256), 0, st, (const __nv_bfloat16*)a.x,
+                    (const __nv_bfloat16*)a.w, a.y, a.M, a.N, a.K, a.ldx, a.epi);
+  return launch_k(gemm_simt_kernel<float>, grid, dim3(256), 0, st, (const float*)a.x, (const float*)a.w, a.y, a.M, a.N,
+                  a.K, a.ldx, a.epi);
 }
 
 int g_backend_override = GEMM_AUTO;

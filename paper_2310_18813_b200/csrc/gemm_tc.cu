@@ -7,12 +7,14 @@
 // A operand (128 weight rows = UMMA_M 128), the token tile is the B operand
 // (UMMA_N = M rounded up to 16, <= 256), and the accumulator D[128 x TN] lives
 // in TMEM (lane = weight row, column = token).  The weight stream is the
-// roofline term, so the work is split *stream-K*: the (tile, 64-wide k-block)
-// units are divided evenly over a persistent grid of 148 x {1,2} CTAs, which
-// keeps every SM streaming regardless of how many 128-row tiles a matrix has.
-// A tile split across CTAs is fixed up deterministically: every contributor
-// writes its fp32 partial to its own slot and the last arriving CTA sums the
-// slots in k order (bit-reproducible, independent of arrival order).
+// roofline term, so narrow matrices are split along K across a thread-block
+// CLUSTER of up to 8 CTAs (enough CTAs that every SM streams, at most one
+// resident wave); the cluster reduces its fp32 partial tiles through
+// distributed shared memory in rank order (deterministic, no global scratch,
+// no serial fixup).  Launched with programmatic dependent launch: the
+// producer requests its first ring of WEIGHT tiles before griddepcontrol.wait,
+// so a GEMM's weight stream overlaps the tail of the kernel that produces its
+// activations.
 //
 // Warp roles (192 threads): warp 0 = TMA producer (one elected lane),
 // warp 1 = TMEM allocator + MMA issuer (one elected lane), warps 2..5 =
@@ -34,11 +36,7 @@ constexpr int TC_BK = 64;    // k per stage (one 128-byte swizzle row of bf16)
 constexpr int TC_UK = 16;    // k per tcgen05.mma (kind::f16)
 constexpr int TC_THREADS = 192;
 constexpr int TC_MAX_TN = 256;
-// Stream-K tile counters live at the head of the workspace in a FIXED-size
-// region (every GEMM sharing the workspace must agree on where partials start,
-// or one GEMM's partial slots would clobber another's self-resetting counters).
-constexpr int TC_MAX_TILES = 16384;
-constexpr size_t TC_CNT_BYTES = (size_t)TC_MAX_TILES * 4;
+
 
 // ------------------------------------------------------------------ PTX wrappers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
@@ -113,49 +111,53 @@ __host__ __device__ constexpr uint32_t make_idesc(int tn) {
 
 struct TcParams {
   int M, N, K;
-  int tn;          // UMMA_N (tokens per tile)
-  int n_tiles_n;   // ceil(N / 128)
-  int n_tiles;     // n_tiles_n * m_tiles
-  int kb;          // k-blocks per tile
-  int grid;        // persistent CTAs
+  int tn;         // UMMA_N (tokens per tile)
+  int n_tiles_n;  // ceil(N / 128)
+  int kb;         // 64-wide k-blocks of K
+  int splits;     // K splits == cluster size (1, 2, 4, 8)
   int stages;
   int epi;
   void* y;
-  float* part;     // [grid][2][tn][128] fp32 partial slots
-  int* counters;   // [n_tiles]
 };
-
-// segment = maximal run of one tile's k-blocks inside a CTA's unit range
-struct Seg {
-  int tile, kb0, kb1;
-};
-
-__device__ __forceinline__ long long unit_begin(int c, const TcParams& p) {
-  return (long long)c * ((long long)p.n_tiles * p.kb) / p.grid;
-}
-__device__ __forceinline__ int cta_of_unit(long long u, const TcParams& p) {
-  // smallest c with unit_begin(c+1) > u
-  long long U = (long long)p.n_tiles * p.kb;
-  int c = (int)((u * p.grid) / U);
-  while (c + 1 < p.grid && unit_begin(c + 1, p) <= u) ++c;
-  while (c > 0 && unit_begin(c, p) > u) --c;
-  return c;
-}
 
 __device__ __forceinline__ float silu_f(float g) { return g / (1.f + __expf(-g)); }
 
-// Epilogue of one accumulator column set held by thread `lane_row` (weight row
-// n = n0 + lane_row) for tokens m0 + j.
-__device__ __forceinline__ void epi_store(const TcParams& p, int n, int m, float v, int row_in_warp) {
-  // NOTE: SILU handled by caller (needs a lane shuffle)
-  if (p.epi == EPI_STORE)
-    ((__nv_bfloat16*)p.y)[(size_t)m * p.N + n] = __float2bfloat16_rn(v);
-  else if (p.epi == EPI_STORE_F32)
-    ((float*)p.y)[(size_t)m * p.N + n] = v;
-  else
-    ((float*)p.y)[(size_t)m * p.N + n] += v;
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ float ld_dsmem_f32(uint32_t local_addr, uint32_t peer) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_addr), "r"(peer));
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote) : "memory");
+  return v;
 }
 
+// Output of one (token m, weight row n) element; SILU pairs rows (n, n+1).
+__device__ __forceinline__ void epi_one(const TcParams& p, int m, int n, float v) {
+  if (m >= p.M || n >= p.N) return;
+  size_t o = (size_t)m * p.N + n;
+  if (p.epi == EPI_STORE)
+    ((__nv_bfloat16*)p.y)[o] = __float2bfloat16_rn(v);
+  else if (p.epi == EPI_STORE_F32)
+    ((float*)p.y)[o] = v;
+  else
+    ((float*)p.y)[o] += v;
+}
+__device__ __forceinline__ void epi_pair(const TcParams& p, int m, int n, float g, float u) {
+  if (m >= p.M || n >= p.N) return;
+  ((__nv_bfloat16*)p.y)[(size_t)m * (p.N / 2) + n / 2] = __float2bfloat16_rn(silu_f(g) * u);
+}
+
+// grid = (n_tiles_n * splits, m_tiles), cluster = (splits, 1, 1): the `splits`
+// CTAs of a cluster share one 128 x tn output tile and split its K range.
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x, TcParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -165,15 +167,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const uint32_t b_bytes = tn * TC_BK * 2;
   const uint32_t stage_bytes = a_bytes + b_bytes;
   uint8_t* stage_base = smem;
-  uint64_t* full = (uint64_t*)(smem + p.stages * stage_bytes);
+  const uint32_t ring_bytes = p.stages * stage_bytes;
+  const uint32_t red_bytes = (uint32_t)tn * TC_BM * 4;
+  uint64_t* full = (uint64_t*)(smem + (ring_bytes > red_bytes ? ring_bytes : red_bytes));
   uint64_t* empty = full + p.stages;
   uint64_t* tmem_full = empty + p.stages;
-  uint64_t* tmem_empty = tmem_full + 1;
-  uint32_t* tmem_slot = (uint32_t*)(tmem_empty + 1);
-  int* flag = (int*)(tmem_slot + 1);
+  uint32_t* tmem_slot = (uint32_t*)(tmem_full + 1);
+  float* red = (float*)smem;  // split-K partial tile [tn][128] (reuses the drained stage ring)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int c = blockIdx.x;
+  const int split = p.splits > 1 ? (int)cluster_rank() : 0;
+  const int tile_n = blockIdx.x / p.splits;
+  const int n0 = tile_n * TC_BM;
+  const int m0 = blockIdx.y * tn;
+  const int kb0 = (int)((long long)split * p.kb / p.splits);
+  const int kb1 = (int)((long long)(split + 1) * p.kb / p.splits);
+  const int nkb = kb1 - kb0;
   uint32_t tmem_cols = 32;
   while ((int)tmem_cols < tn) tmem_cols <<= 1;
 
@@ -183,7 +192,6 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(tmem_full, 1);
-    mbar_init(tmem_empty, 128);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
@@ -198,143 +206,118 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  const long long u_begin = unit_begin(c, p), u_end = unit_begin(c + 1, p);
-
   if (warp == 0) {
     if (lane == 0) {
-      // ---------------- TMA producer
-      int stage = 0;
-      uint32_t phase = 0;
-      for (long long u = u_begin; u < u_end;) {
-        int tile = (int)(u / p.kb);
-        int kb0 = (int)(u - (long long)tile * p.kb);
-        int kb1 = (int)min((long long)p.kb, u_end - (long long)tile * p.kb);
-        int n0 = (tile % p.n_tiles_n) * TC_BM;
-        int m0 = (tile / p.n_tiles_n) * tn;
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&empty[stage], phase ^ 1);
-          uint8_t* sa = stage_base + stage * stage_bytes;
-          mbar_expect_tx(&full[stage], stage_bytes);
-          tma_load_2d(sa, &map_w, &full[stage], kb * TC_BK, n0);
-          tma_load_2d(sa + a_bytes, &map_x, &full[stage], kb * TC_BK, m0);
-          if (++stage == p.stages) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-        u = (long long)tile * p.kb + kb1;
+      // ---------------- TMA producer.  Weights never depend on the previous
+      // kernel, so the first ring of weight tiles is requested BEFORE the
+      // programmatic-dependency wait: under PDL the weight stream of this GEMM
+      // overlaps the tail of the kernel that produces its activations.
+      const int pre = nkb < p.stages ? nkb : p.stages;
+      for (int i = 0; i < pre; ++i) {
+        uint8_t* sa = stage_base + i * stage_bytes;
+        mbar_expect_tx(&full[i], stage_bytes);
+        tma_load_2d(sa, &map_w, &full[i], (kb0 + i) * TC_BK, n0);
       }
+      griddep_wait();
+      for (int i = 0; i < pre; ++i)
+        tma_load_2d(stage_base + i * stage_bytes + a_bytes, &map_x, &full[i], (kb0 + i) * TC_BK, m0);
+      int stage = pre % p.stages;
+      uint32_t phase = (pre == p.stages) ? 1u : 0u;
+      for (int i = pre; i < nkb; ++i) {
+        mbar_wait(&empty[stage], phase ^ 1);
+        uint8_t* sa = stage_base + stage * stage_bytes;
+        mbar_expect_tx(&full[stage], stage_bytes);
+        tma_load_2d(sa, &map_w, &full[stage], (kb0 + i) * TC_BK, n0);
+        tma_load_2d(sa + a_bytes, &map_x, &full[stage], (kb0 + i) * TC_BK, m0);
+        if (++stage == p.stages) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+      griddep_launch();
     }
   } else if (warp == 1) {
     if (lane == 0) {
-      // ---------------- MMA issuer
+      // ---------------- MMA issuer (single thread)
       const uint32_t idesc = make_idesc(tn);
       int stage = 0;
       uint32_t phase = 0;
-      int seg = 0;
-      for (long long u = u_begin; u < u_end; ++seg) {
-        int tile = (int)(u / p.kb);
-        int kb0 = (int)(u - (long long)tile * p.kb);
-        int kb1 = (int)min((long long)p.kb, u_end - (long long)tile * p.kb);
-        mbar_wait(tmem_empty, (seg & 1) ^ 1);
+      for (int i = 0; i < nkb; ++i) {
+        mbar_wait(&full[stage], phase);
         tc_fence_after();
-        for (int kb = kb0; kb < kb1; ++kb) {
-          mbar_wait(&full[stage], phase);
-          tc_fence_after();
-          uint32_t sa = smem_u32(stage_base + stage * stage_bytes);
-          uint32_t sb = sa + a_bytes;
+        uint32_t sa = smem_u32(stage_base + stage * stage_bytes);
+        uint32_t sb = sa + a_bytes;
 #pragma unroll
-          for (int kk = 0; kk < TC_BK / TC_UK; ++kk) {
-            uint64_t ad = sw128_desc(sa + kk * TC_UK * 2);
-            uint64_t bd = sw128_desc(sb + kk * TC_UK * 2);
-            tc_mma(tmem, ad, bd, idesc, (kb > kb0 || kk > 0) ? 1u : 0u);
-          }
-          tc_commit(&empty[stage]);
-          if (++stage == p.stages) {
-            stage = 0;
-            phase ^= 1;
-          }
+        for (int kk = 0; kk < TC_BK / TC_UK; ++kk)
+          tc_mma(tmem, sw128_desc(sa + kk * TC_UK * 2), sw128_desc(sb + kk * TC_UK * 2), idesc,
+                 (i > 0 || kk > 0) ? 1u : 0u);
+        tc_commit(&empty[stage]);
+        if (++stage == p.stages) {
+          stage = 0;
+          phase ^= 1;
         }
-        tc_commit(tmem_full);
-        u = (long long)tile * p.kb + kb1;
       }
+      tc_commit(tmem_full);
     }
   } else {
-    // ---------------- epilogue warps (128 threads)
-    const int quad = warp & 3;            // TMEM lane quadrant this warp may access
-    const int row = quad * 32 + lane;     // weight row within the tile
+    // ---------------- epilogue warps: TMEM -> registers -> (DSMEM reduce) -> global
+    griddep_wait();
+    const int quad = warp & 3;
+    const int row = quad * 32 + lane;  // weight row within the tile (= TMEM lane)
     const uint32_t lane_addr = tmem + ((uint32_t)(quad * 32) << 16);
-    const int first_tile = (int)(u_begin / p.kb);
-    int seg = 0;
-    for (long long u = u_begin; u < u_end; ++seg) {
-      int tile = (int)(u / p.kb);
-      int kb0 = (int)(u - (long long)tile * p.kb);
-      int kb1 = (int)min((long long)p.kb, u_end - (long long)tile * p.kb);
-      const bool whole = (kb0 == 0 && kb1 == p.kb);
-      const int n0 = (tile % p.n_tiles_n) * TC_BM;
-      const int m0 = (tile / p.n_tiles_n) * tn;
-      const int n = n0 + row;
-      mbar_wait(tmem_full, seg & 1);
-      tc_fence_after();
-      float* slot = nullptr;
-      if (!whole) slot = p.part + ((size_t)c * 2 + (tile == first_tile ? 0 : 1)) * (size_t)tn * TC_BM;
-      for (int j0 = 0; j0 < tn; j0 += 16) {
-        float v[16];
-        tmem_ld16(lane_addr + j0, v);
-        if (!whole) {
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+    for (int j0 = 0; j0 < tn; j0 += 16) {
+      float v[16];
+      tmem_ld16(lane_addr + j0, v);
+      if (p.splits > 1) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) slot[(size_t)(j0 + j) * TC_BM + row] = v[j];
-        } else {
+        for (int j = 0; j < 16; ++j) red[(j0 + j) * TC_BM + row] = v[j];
+      } else if (p.epi == EPI_SILU_MUL) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            int m = m0 + j0 + j;
-            if (p.epi == EPI_SILU_MUL) {
-              float other = __shfl_xor_sync(0xffffffffu, v[j], 1);
-              if (!(lane & 1) && m < p.M && n + 1 < p.N)
-                ((__nv_bfloat16*)p.y)[(size_t)m * (p.N / 2) + n / 2] = __float2bfloat16_rn(silu_f(v[j]) * other);
-            } else if (m < p.M && n < p.N) {
-              epi_store(p, n, m, v[j], lane);
-            }
-          }
+        for (int j = 0; j < 16; ++j) {
+          float other = __shfl_xor_sync(0xffffffffu, v[j], 1);
+          if (!(lane & 1)) epi_pair(p, m0 + j0 + j, n0 + row, v[j], other);
         }
+      } else {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) epi_one(p, m0 + j0 + j, n0 + row, v[j]);
       }
-      tc_fence_before();
-      mbar_arrive(tmem_empty);
-      if (!whole) {
-        // stream-K fixup: publish the partial, last contributor reduces in k order
-        __threadfence();
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        const long long tu0 = (long long)tile * p.kb, tu1 = tu0 + p.kb - 1;
-        const int c_first = cta_of_unit(tu0, p), c_last = cta_of_unit(tu1, p);
-        if (threadIdx.x == 64) {
-          int old = atomicAdd(&p.counters[tile], 1);
-          *flag = (old == c_last - c_first);
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-        if (*flag) {
-          __threadfence();
-          for (int j = 0; j < tn; ++j) {
-            int m = m0 + j;
-            float acc = 0.f;
-            for (int cc = c_first; cc <= c_last; ++cc) {
-              int first_of_cc = (int)(unit_begin(cc, p) / p.kb);
-              const float* sl = p.part + ((size_t)cc * 2 + (tile == first_of_cc ? 0 : 1)) * (size_t)tn * TC_BM;
-              acc += __ldcg(&sl[(size_t)j * TC_BM + row]);
-            }
-            if (p.epi == EPI_SILU_MUL) {
-              float other = __shfl_xor_sync(0xffffffffu, acc, 1);
-              if (!(lane & 1) && m < p.M && n + 1 < p.N)
-                ((__nv_bfloat16*)p.y)[(size_t)m * (p.N / 2) + n / 2] = __float2bfloat16_rn(silu_f(acc) * other);
-            } else if (m < p.M && n < p.N) {
-              epi_store(p, n, m, acc, lane);
-            }
-          }
-          if (threadIdx.x == 64) p.counters[tile] = 0;  // self-cleaning for the next launch / graph replay
-        }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
-      }
-      u = (long long)tile * p.kb + kb1;
     }
+    tc_fence_before();
+  }
+  __syncwarp();
+  if (p.splits > 1) {
+    // deterministic split-K reduction through distributed shared memory:
+    // CTA `split` owns rows [split*R, (split+1)*R) of the tile and sums the
+    // cluster's partials in rank order 0..splits-1.
+    cluster_sync_all();
+    if (warp >= 2) {
+      const int R = TC_BM / p.splits;
+      const int et = threadIdx.x - 64;
+      const int r_base = split * R;
+      const uint32_t red_addr = smem_u32(red);
+      if (p.epi == EPI_SILU_MUL) {
+        const int pairs = R / 2;
+        for (int it = et; it < pairs * tn; it += 128) {
+          int r = r_base + 2 * (it % pairs), j = it / pairs;
+          float g = 0.f, u = 0.f;
+          for (int q = 0; q < p.splits; ++q) {
+            g += ld_dsmem_f32(red_addr + (uint32_t)((j * TC_BM + r) * 4), q);
+            u += ld_dsmem_f32(red_addr + (uint32_t)((j * TC_BM + r + 1) * 4), q);
+          }
+          epi_pair(p, m0 + j, n0 + r, g, u);
+        }
+      } else {
+        for (int it = et; it < R * tn; it += 128) {
+          int r = r_base + it % R, j = it / R;
+          float a = 0.f;
+          for (int q = 0; q < p.splits; ++q) a += ld_dsmem_f32(red_addr + (uint32_t)((j * TC_BM + r) * 4), q);
+          epi_one(p, m0 + j, n0 + r, a);
+        }
+      }
+    }
+    cluster_sync_all();
   }
   tc_fence_before();
   __syncthreads();
@@ -391,30 +374,37 @@ static int tn_for(int M) {
   return t < 16 ? 16 : (t > TC_MAX_TN ? TC_MAX_TN : t);
 }
 
+int g_pdl = 1;  // programmatic dependent launch for every forward kernel (sb_set_pdl)
+
 struct TcPlan {
-  int tn, n_tiles_n, m_tiles, n_tiles, kb, grid, stages, ctas_per_sm;
-  size_t smem, part_bytes, cnt_bytes;
+  int tn, n_tiles_n, m_tiles, kb, splits, stages, ctas_per_sm;
+  size_t smem;
 };
 
+// Split-K policy for the HBM-bound regime: enough CTAs that every SM streams
+// weights (>= one per SM), at most one resident wave, >= 2 k-blocks per CTA,
+// cluster size <= 8 (portable).
 static TcPlan plan(int M, int N, int K) {
   TcPlan q;
   q.tn = tn_for(M);
   q.n_tiles_n = (N + TC_BM - 1) / TC_BM;
   q.m_tiles = (M + q.tn - 1) / q.tn;
-  q.n_tiles = q.n_tiles_n * q.m_tiles;
   q.kb = (K + TC_BK - 1) / TC_BK;
   q.ctas_per_sm = q.tn >= 128 ? 1 : 2;
+  const int sms = num_sms();
+  const int slots = sms * q.ctas_per_sm;
+  const int tiles = q.n_tiles_n * q.m_tiles;
+  q.splits = 1;
+  while (q.splits < 8 && tiles * q.splits < sms && tiles * q.splits * 2 <= slots && q.kb / (q.splits * 2) >= 2)
+    q.splits *= 2;
   size_t budget = q.ctas_per_sm == 2 ? 108 * 1024 : 200 * 1024;
   size_t stage = (size_t)(TC_BM + q.tn) * TC_BK * 2;
   q.stages = (int)((budget - 1024 - 256) / stage);
   if (q.stages > 8) q.stages = 8;
   if (q.stages < 2) q.stages = 2;
-  q.smem = 1024 + (size_t)q.stages * stage + 256;
-  long long units = (long long)q.n_tiles * q.kb;
-  long long g = (long long)num_sms() * q.ctas_per_sm;
-  q.grid = (int)(units < g ? units : g);
-  q.part_bytes = (size_t)q.grid * 2 * q.tn * TC_BM * 4;
-  q.cnt_bytes = TC_CNT_BYTES;
+  size_t ring = (size_t)q.stages * stage;
+  size_t red = (size_t)q.tn * TC_BM * 4;  // split-K partial tile reuses the ring
+  q.smem = 1024 + (ring > red ? ring : red) + 256;
   return q;
 }
 
@@ -437,19 +427,13 @@ bool gemm_tc_supported(const GemmArgs& a) {
   return get_encode() != nullptr;
 }
 
-size_t gemm_workspace_bytes(int M, int N, int K) {
-  // sized for the simt fallback (none) and the tcgen05 stream-K partials
-  const int tn = tn_for(M);
-  size_t grid = (size_t)num_sms() * 2;
-  return grid * 2 * tn * TC_BM * 4 + TC_CNT_BYTES + 4096;
-}
+size_t gemm_workspace_bytes(int, int, int) { return 0; }  // split-K reduces in DSMEM: no global scratch
 
 int gemm_tc(const GemmArgs& a, cudaStream_t st) {
   if (!gemm_tc_supported(a)) return SB_EUNSUPPORTED;
   if (a.M <= 0 || a.N <= 0 || a.K <= 0) return SB_EINVAL;
+  SB_TRY(gemm_tc_init());
   TcPlan q = plan(a.M, a.N, a.K);
-  if (q.n_tiles > TC_MAX_TILES) return SB_EUNSUPPORTED;
-  if (q.part_bytes + q.cnt_bytes > a.ws_bytes || !a.workspace) return SB_EWORKSPACE;
   CUtensorMap mw, mx;
   SB_TRY(make_map(&mw, a.w, a.N, a.K, a.K, TC_BM));
   SB_TRY(make_map(&mx, a.x, a.M, a.K, a.ldx, q.tn));
@@ -459,18 +443,33 @@ int gemm_tc(const GemmArgs& a, cudaStream_t st) {
   p.K = a.K;
   p.tn = q.tn;
   p.n_tiles_n = q.n_tiles_n;
-  p.n_tiles = q.n_tiles;
   p.kb = q.kb;
-  p.grid = q.grid;
+  p.splits = q.splits;
   p.stages = q.stages;
   p.epi = a.epi;
   p.y = a.y;
-  p.counters = (int*)a.workspace;
-  p.part = (float*)((char*)a.workspace + q.cnt_bytes);
-  SB_TRY(gemm_tc_init());
-  gemm_tc_kernel<<<q.grid, TC_THREADS, q.smem, st>>>(mw, mx, p);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(q.n_tiles_n * q.splits, q.m_tiles, 1);
+  cfg.blockDim = dim3(TC_THREADS, 1, 1);
+  cfg.dynamicSmemBytes = q.smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  at[na].id = cudaLaunchAttributeClusterDimension;
+  at[na].val.clusterDim.x = q.splits;
+  at[na].val.clusterDim.y = 1;
+  at[na].val.clusterDim.z = 1;
+  ++na;
+  if (g_pdl) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc_kernel, mw, mx, p);
+  if (e != cudaSuccess) return (int)e;
   g_kernel_count++;
-  SB_CHECK_LAUNCH();
   return 0;
 }
 

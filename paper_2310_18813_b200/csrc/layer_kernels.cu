@@ -6,7 +6,7 @@
 //   residual stream fp32; GEMM inputs rounded to the model dtype after each
 //   norm / activation; RoPE applied in fp32 from a host-built fp32 cos/sin
 //   table then rounded; attention scores/softmax/accumulation in fp32 with a
-//   fixed key order (32-key tiles, ascending) so a query's output does not
+//   fixed key order (64-key tiles, ascending) so a query's output does not
 //   depend on how many other queries share the launch (batch invariance:
 //   spec == greedy exactly in fp32 mode).
 #include "common.cuh"
@@ -20,6 +20,8 @@ thread_local int g_kernel_count = 0;
 template <typename T>
 __global__ void embed_kernel(const T* __restrict__ table, const int32_t* __restrict__ ids,
                              const int32_t* __restrict__ pos, float* __restrict__ h, int hidden, int vocab) {
+  griddep_wait();
+  griddep_launch();
   int t = blockIdx.x;
   int id = ids[t];
   bool pad = pos != nullptr && pos[t] < 0;
@@ -33,53 +35,64 @@ int launch_embed(int dtype, const void* table, const int32_t* ids, const int32_t
                  int hidden, int vocab, cudaStream_t st) {
   if (n_tok <= 0) return 0;
   if (dtype == SB_BF16)
-    embed_kernel<__nv_bfloat16><<<n_tok, 256, 0, st>>>((const __nv_bfloat16*)table, ids, pos, h, hidden, vocab);
-  else
-    embed_kernel<float><<<n_tok, 256, 0, st>>>((const float*)table, ids, pos, h, hidden, vocab);
-  g_kernel_count++;
-  SB_CHECK_LAUNCH();
-  return 0;
+    return launch_k(embed_kernel<__nv_bfloat16>, dim3(n_tok), dim3(256), 0, st, (const __nv_bfloat16*)table, ids, pos,
+                    h, hidden, vocab);
+  return launch_k(embed_kernel<float>, dim3(n_tok), dim3(256), 0, st, (const float*)table, ids, pos, h, hidden, vocab);
 }
 
 // ---------------------------------------------------------------- RMSNorm
-// y[r] = dtype(x[src_row(r)] * rsqrt(mean(x^2) + eps) * g); src_row(r) = r*row_step + row_off
+// y[r] = dtype(x[src_row(r)] * rsqrt(mean(x^2) + eps) * g); src_row(r) = r*row_step + row_off.
+// One CTA per row, the row held in registers as float4 (hidden <= 8192).
 template <typename T>
 __global__ void __launch_bounds__(256) rmsnorm_kernel(const float* __restrict__ x, const T* __restrict__ g,
                                                       T* __restrict__ y, int hidden, float eps, int row_step,
                                                       int row_off) {
-  int r = blockIdx.x;
-  const float* xr = x + (size_t)(r * row_step + row_off) * hidden;
+  griddep_wait();
+  griddep_launch();
+  const int r = blockIdx.x;
+  const float4* xr = reinterpret_cast<const float4*>(x + (size_t)(r * row_step + row_off) * hidden);
+  const int n4 = hidden >> 2;
+  float4 v[8];
   float ss = 0.f;
-  for (int i = threadIdx.x; i < hidden; i += blockDim.x) {
-    float v = xr[i];
-    ss += v * v;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    int i = threadIdx.x + c * 256;
+    if (i < n4) {
+      v[c] = xr[i];
+      ss += v[c].x * v[c].x + v[c].y * v[c].y + v[c].z * v[c].z + v[c].w * v[c].w;
+    }
   }
   __shared__ float red[8];
   ss = warp_sum(ss);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
   __syncthreads();
-  if (threadIdx.x < 32) {
-    float v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.f;
-    v = warp_sum(v);
-    if (threadIdx.x == 0) red[0] = v;
-  }
-  __syncthreads();
-  float inv = rsqrtf(red[0] / (float)hidden + eps);
+  float tot = 0.f;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) tot += red[w];
+  const float inv = rsqrtf(tot / (float)hidden + eps);
   T* yr = y + (size_t)r * hidden;
-  for (int i = threadIdx.x; i < hidden; i += blockDim.x) yr[i] = from_f32<T>(xr[i] * inv * to_f32(g[i]));
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    int i = threadIdx.x + c * 256;
+    if (i < n4) {
+      int e = i * 4;
+      yr[e + 0] = from_f32<T>(v[c].x * inv * to_f32(g[e + 0]));
+      yr[e + 1] = from_f32<T>(v[c].y * inv * to_f32(g[e + 1]));
+      yr[e + 2] = from_f32<T>(v[c].z * inv * to_f32(g[e + 2]));
+      yr[e + 3] = from_f32<T>(v[c].w * inv * to_f32(g[e + 3]));
+    }
+  }
 }
 
 int launch_rmsnorm(int dtype, const float* x, const void* g, void* y, int rows, int hidden, float eps, int row_step,
                    int row_off, cudaStream_t st) {
   if (rows <= 0) return 0;
+  if (hidden % 4 || hidden > 8192) return SB_EUNSUPPORTED;
   if (dtype == SB_BF16)
-    rmsnorm_kernel<__nv_bfloat16><<<rows, 256, 0, st>>>(x, (const __nv_bfloat16*)g, (__nv_bfloat16*)y, hidden, eps,
-                                                        row_step, row_off);
-  else
-    rmsnorm_kernel<float><<<rows, 256, 0, st>>>(x, (const float*)g, (float*)y, hidden, eps, row_step, row_off);
-  g_kernel_count++;
-  SB_CHECK_LAUNCH();
-  return 0;
+    return launch_k(rmsnorm_kernel<__nv_bfloat16>, dim3(rows), dim3(256), 0, st, x, (const __nv_bfloat16*)g,
+                    (__nv_bfloat16*)y, hidden, eps, row_step, row_off);
+  return launch_k(rmsnorm_kernel<float>, dim3(rows), dim3(256), 0, st, x, (const float*)g, (float*)y, hidden, eps,
+                  row_step, row_off);
 }
 
 // ---------------------------------------------------------------- RoPE + KV append
@@ -93,6 +106,8 @@ __global__ void rope_append_kernel(const T* __restrict__ qkv, T* __restrict__ q_
                                    const int32_t* __restrict__ tok_pos, const float* __restrict__ cosT,
                                    const float* __restrict__ sinT, int q_len, int nq, int nkv, int hd,
                                    int ctx_max, int max_pos) {
+  griddep_wait();
+  griddep_launch();
   int t = blockIdx.x;
   int slot = tok_slot[t / q_len];
   int p = tok_pos[t];
@@ -101,7 +116,6 @@ __global__ void rope_append_kernel(const T* __restrict__ qkv, T* __restrict__ q_
   int pc = p < 0 ? 0 : (p >= max_pos ? max_pos - 1 : p);
   const float* cr = cosT + (size_t)pc * half;
   const float* sr = sinT + (size_t)pc * half;
-  // q heads
   for (int e = threadIdx.x; e < nq * half; e += blockDim.x) {
     int h = e / half, i = e % half;
     const T* src = row + h * hd;
@@ -132,162 +146,194 @@ int launch_rope_append(int dtype, const void* qkv, void* q_out, void* kc, void* 
                        int nkv, int hd, int ctx_max, int max_pos, cudaStream_t st) {
   if (n_tok <= 0) return 0;
   if (dtype == SB_BF16)
-    rope_append_kernel<__nv_bfloat16><<<n_tok, 256, 0, st>>>(
-        (const __nv_bfloat16*)qkv, (__nv_bfloat16*)q_out, (__nv_bfloat16*)kc, (__nv_bfloat16*)vc, tok_slot, tok_pos,
-        cosT, sinT, q_len, nq, nkv, hd, ctx_max, max_pos);
-  else
-    rope_append_kernel<float><<<n_tok, 256, 0, st>>>((const float*)qkv, (float*)q_out, (float*)kc, (float*)vc,
-                                                     tok_slot, tok_pos, cosT, sinT, q_len, nq, nkv, hd, ctx_max,
-                                                     max_pos);
-  g_kernel_count++;
-  SB_CHECK_LAUNCH();
-  return 0;
+    return launch_k(rope_append_kernel<__nv_bfloat16>, dim3(n_tok), dim3(256), 0, st, (const __nv_bfloat16*)qkv,
+                    (__nv_bfloat16*)q_out, (__nv_bfloat16*)kc, (__nv_bfloat16*)vc, tok_slot, tok_pos, cosT, sinT,
+                    q_len, nq, nkv, hd, ctx_max, max_pos);
+  return launch_k(rope_append_kernel<float>, dim3(n_tok), dim3(256), 0, st, (const float*)qkv, (float*)q_out,
+                  (float*)kc, (float*)vc, tok_slot, tok_pos, cosT, sinT, q_len, nq, nkv, hd, ctx_max, max_pos);
 }
 
 // ---------------------------------------------------------------- attention (K3)
-// One CTA per (q head, sequence, query group of kQG).  Keys of the slot are
-// streamed in 32-key tiles (coalesced loads into padded smem); each
-// query j at absolute position p_j sees keys [0, p_j] (causal inside the
-// speculative window).  Online softmax in fp32 with a fixed key order
-// (32-key tiles, ascending).
-constexpr int kAttnKT = 32;   // keys per tile (one per lane)
-constexpr int kAttnQG = 16;   // queries per CTA
+// One CTA per (q head, sequence, group of QG queries); 128 threads.  Keys of
+// the slot stream through shared memory in 64-key tiles (16-byte vector loads;
+// row stride padded to 136 elements so 16-byte smem reads are conflict-free).
+// Query j at absolute position p_j sees keys [0, p_j]: the causal mask inside
+// the speculative window.  Online softmax in fp32 with a fixed key order
+// (64-key tiles, ascending) -> a query's output is independent of how many
+// other queries share the launch (batch invariance, spec == greedy in fp32).
+constexpr int kAttnKT = 64;
 
-// HD threads per CTA (thread d owns output dim d); HD/32 warps share the
-// score / softmax work.  Supported head dims: 64, 128.
-template <typename T, int HD>
-__global__ void __launch_bounds__(HD) attention_kernel(const T* __restrict__ q, const T* __restrict__ kc,
+template <typename T> struct AttnVec;  // elements per 16-byte vector
+template <> struct AttnVec<__nv_bfloat16> { static constexpr int n = 8; };
+template <> struct AttnVec<float> { static constexpr int n = 4; };
+
+template <typename T, int HD, int QG>
+__global__ void __launch_bounds__(128) attention_kernel(const T* __restrict__ q, const T* __restrict__ kc,
                                                         const T* __restrict__ vc, T* __restrict__ out,
                                                         const int32_t* __restrict__ tok_slot,
                                                         const int32_t* __restrict__ tok_pos, int q_len, int nq,
                                                         int nkv, int ctx_max, float scale) {
-  constexpr int NW = HD / 32;
-  constexpr int KP = HD + 1;  // padded row (floats) -> conflict-free column reads
-  __shared__ float Ks[kAttnKT][KP];
-  __shared__ float Vs[kAttnKT][HD];
-  __shared__ float Qs[kAttnQG][HD];
-  __shared__ float S[kAttnQG][kAttnKT];
-  __shared__ float m_run[kAttnQG], l_run[kAttnQG], corr[kAttnQG];
+  constexpr int VE = AttnVec<T>::n;           // elements per 16B
+  constexpr int KS = HD + 16 / (int)sizeof(T) * 1;  // padded row stride (elements): +16 bytes
+  __shared__ __align__(16) T Ks[kAttnKT][KS];
+  __shared__ __align__(16) T Vs[kAttnKT][HD];
+  __shared__ float Qs[QG][HD];
+  __shared__ float S[QG][kAttnKT];
+  __shared__ float m_run[QG], l_run[QG], corr[QG];
+  __shared__ int qpos[QG];
+  griddep_wait();
+  griddep_launch();
 
   const int head = blockIdx.x, seq = blockIdx.y, qg = blockIdx.z;
   const int kvh = head / (nq / nkv);
   const int slot = tok_slot[seq];
   const int tid = threadIdx.x;
-  const int j0 = qg * kAttnQG;
-  const int nqg = min(kAttnQG, q_len - j0);
+  const int j0 = qg * QG;
+  const int nqg = min(QG, q_len - j0);
   if (nqg <= 0) return;
 
-  int maxp = -1;
-  for (int j = 0; j < nqg; ++j) maxp = max(maxp, tok_pos[seq * q_len + j0 + j]);
-
-  for (int e = tid; e < kAttnQG * HD; e += HD) {
+  if (tid < QG) {
+    qpos[tid] = tid < nqg ? tok_pos[seq * q_len + j0 + tid] : -1;
+    m_run[tid] = -INFINITY;
+    l_run[tid] = 0.f;
+  }
+  for (int e = tid; e < QG * HD; e += 128) {
     int j = e / HD, d = e % HD;
     float v = 0.f;
     if (j < nqg) v = to_f32(q[((size_t)(seq * q_len + j0 + j) * nq + head) * HD + d]) * scale;
     Qs[j][d] = v;
   }
-  if (tid < kAttnQG) {
-    m_run[tid] = -INFINITY;
-    l_run[tid] = 0.f;
-  }
-  float acc[kAttnQG];
+  __syncthreads();
+  int maxp = -1;
 #pragma unroll
-  for (int j = 0; j < kAttnQG; ++j) acc[j] = 0.f;
+  for (int j = 0; j < QG; ++j) maxp = max(maxp, qpos[j]);
+
+  constexpr int DPT = (HD + 127) / 128;  // output dims per thread
+  float acc[QG][DPT];
+#pragma unroll
+  for (int j = 0; j < QG; ++j)
+#pragma unroll
+    for (int c = 0; c < DPT; ++c) acc[j][c] = 0.f;
 
   const T* kbase = kc + ((size_t)slot * nkv + kvh) * ctx_max * HD;
   const T* vbase = vc + ((size_t)slot * nkv + kvh) * ctx_max * HD;
   const int n_keys = maxp + 1;
-  __syncthreads();
+  constexpr int VPR = HD / VE;  // vectors per row
 
   for (int k0 = 0; k0 < n_keys; k0 += kAttnKT) {
     const int nk = min(kAttnKT, n_keys - k0);
-    for (int e = tid; e < kAttnKT * HD; e += HD) {
-      int r = e / HD, d = e % HD;
-      float kv = 0.f, vv = 0.f;
+    for (int e = tid; e < kAttnKT * VPR; e += 128) {
+      int r = e / VPR, c = (e % VPR) * VE;
+      uint4 kv = make_uint4(0, 0, 0, 0), vv = make_uint4(0, 0, 0, 0);
       if (r < nk) {
-        kv = to_f32(kbase[(size_t)(k0 + r) * HD + d]);
-        vv = to_f32(vbase[(size_t)(k0 + r) * HD + d]);
+        kv = *reinterpret_cast<const uint4*>(kbase + (size_t)(k0 + r) * HD + c);
+        vv = *reinterpret_cast<const uint4*>(vbase + (size_t)(k0 + r) * HD + c);
       }
-      Ks[r][d] = kv;
-      Vs[r][d] = vv;
+      *reinterpret_cast<uint4*>(&Ks[r][c]) = kv;
+      *reinterpret_cast<uint4*>(&Vs[r][c]) = vv;
     }
     __syncthreads();
-    // scores: thread handles key r = lane for queries j = warp, warp+4, ...
+    // scores: thread -> key r = tid % 64, queries j = tid/64 + 2i
     {
-      int r = tid & (kAttnKT - 1);
-      for (int j = tid >> 5; j < kAttnQG; j += NW) {
-        float s = -INFINITY;
-        if (j < nqg) {
-          int pj = tok_pos[seq * q_len + j0 + j];
-          if (r < nk && k0 + r <= pj) {
-            float a = 0.f;
-#pragma unroll 16
-            for (int d = 0; d < HD; ++d) a = fmaf(Qs[j][d], Ks[r][d], a);
-            s = a;
-          }
+      const int r = tid & (kAttnKT - 1);
+      const int jb = tid >> 6;
+      float sc[QG];
+#pragma unroll
+      for (int j = 0; j < QG; ++j) sc[j] = 0.f;
+#pragma unroll 4
+      for (int c = 0; c < HD; c += VE) {
+        uint4 raw = *reinterpret_cast<const uint4*>(&Ks[r][c]);
+        const T* kv = reinterpret_cast<const T*>(&raw);
+#pragma unroll
+        for (int e = 0; e < VE; ++e) {
+          float kf = to_f32(kv[e]);
+#pragma unroll
+          for (int j = 0; j < QG; ++j)
+            if ((j & 1) == jb) sc[j] = fmaf(Qs[j][c + e], kf, sc[j]);
         }
-        S[j][r] = s;
       }
+#pragma unroll
+      for (int j = 0; j < QG; ++j)
+        if ((j & 1) == jb) S[j][r] = (r < nk && k0 + r <= qpos[j]) ? sc[j] : -INFINITY;
     }
     __syncthreads();
-    // online softmax update: warp w handles queries w, w+4, ...
+    // online softmax: warp w handles queries w, w+4, ...
     {
-      int w = tid >> 5, lane = tid & 31;
-      for (int j = w; j < kAttnQG; j += NW) {
-        float a = S[j][lane];
-        float mt = warp_max(a);
+      const int w = tid >> 5, lane = tid & 31;
+      for (int j = w; j < QG; j += 4) {
+        float a = S[j][lane], b = S[j][lane + 32];
+        float mt = warp_max(fmaxf(a, b));
         float mo = m_run[j];
         float mn = fmaxf(mo, mt);
         float ea = (mn == -INFINITY) ? 0.f : __expf(a - mn);
+        float eb = (mn == -INFINITY) ? 0.f : __expf(b - mn);
         S[j][lane] = ea;
-        float sum = warp_sum(ea);
+        S[j][lane + 32] = eb;
+        float sum = warp_sum(ea + eb);
         if (lane == 0) {
-          float c = (mo == -INFINITY) ? 0.f : __expf(mo - mn);
-          corr[j] = c;
-          l_run[j] = l_run[j] * c + sum;
+          float cf = (mo == -INFINITY) ? 0.f : __expf(mo - mn);
+          corr[j] = cf;
+          l_run[j] = l_run[j] * cf + sum;
           m_run[j] = mn;
         }
       }
     }
     __syncthreads();
-    // P.V: thread owns output dim d = tid for all queries
-    {
-      int d = tid;
 #pragma unroll
-      for (int j = 0; j < kAttnQG; ++j) acc[j] *= corr[j];
-      for (int r = 0; r < nk; ++r) {
-        float vv = Vs[r][d];
+    for (int j = 0; j < QG; ++j)
 #pragma unroll
-        for (int j = 0; j < kAttnQG; ++j) acc[j] = fmaf(S[j][r], vv, acc[j]);
+      for (int c = 0; c < DPT; ++c) acc[j][c] *= corr[j];
+    for (int r = 0; r < nk; ++r) {
+#pragma unroll
+      for (int c = 0; c < DPT; ++c) {
+        int d = tid + c * 128;
+        if (d < HD) {
+          float vv = to_f32(Vs[r][d]);
+#pragma unroll
+          for (int j = 0; j < QG; ++j) acc[j][c] = fmaf(S[j][r], vv, acc[j][c]);
+        }
       }
     }
     __syncthreads();
   }
   for (int j = 0; j < nqg; ++j) {
     float l = l_run[j];
-    float o = l > 0.f ? acc[j] / l : 0.f;
-    out[((size_t)(seq * q_len + j0 + j) * nq + head) * HD + tid] = from_f32<T>(o);
+#pragma unroll
+    for (int c = 0; c < DPT; ++c) {
+      int d = tid + c * 128;
+      if (d < HD) out[((size_t)(seq * q_len + j0 + j) * nq + head) * HD + d] = from_f32<T>(l > 0.f ? acc[j][c] / l : 0.f);
+    }
   }
+}
+
+template <typename T, int HD>
+static int attn_dispatch(int q_len, dim3 grid_xy, const void* q, const void* kc, const void* vc, void* out,
+                         const int32_t* slot, const int32_t* pos, int nq, int nkv, int ctx, float scale,
+                         cudaStream_t st) {
+#define SB_ATTN(QG)                                                                                          \
+  return launch_k(attention_kernel<T, HD, QG>, dim3(grid_xy.x, grid_xy.y, (q_len + QG - 1) / QG), dim3(128), 0, st, \
+                  (const T*)q, (const T*)kc, (const T*)vc, (T*)out, slot, pos, q_len, nq, nkv, ctx, scale)
+  if (q_len <= 1) SB_ATTN(1);
+  if (q_len <= 2) SB_ATTN(2);
+  if (q_len <= 4) SB_ATTN(4);
+  if (q_len <= 8) SB_ATTN(8);
+  SB_ATTN(16);
+#undef SB_ATTN
 }
 
 int launch_attention(int dtype, const void* q, const void* kc, const void* vc, void* out, const int32_t* tok_slot,
                      const int32_t* tok_pos, int n_seq, int q_len, int nq, int nkv, int hd, int ctx_max,
                      cudaStream_t st) {
   if ((hd != 64 && hd != 128) || nq % nkv != 0) return SB_EUNSUPPORTED;
-  dim3 grid(nq, n_seq, (q_len + kAttnQG - 1) / kAttnQG);
+  dim3 g(nq, n_seq, 1);
   float scale = 1.0f / sqrtf((float)hd);
-#define SB_ATTN(T, HD)                                                                                        \
-  attention_kernel<T, HD><<<grid, HD, 0, st>>>((const T*)q, (const T*)kc, (const T*)vc, (T*)out, tok_slot, tok_pos, \
-                                               q_len, nq, nkv, ctx_max, scale)
-  if (dtype == SB_BF16) {
-    if (hd == 128) SB_ATTN(__nv_bfloat16, 128); else SB_ATTN(__nv_bfloat16, 64);
-  } else {
-    if (hd == 128) SB_ATTN(float, 128); else SB_ATTN(float, 64);
-  }
-#undef SB_ATTN
-  g_kernel_count++;
-  SB_CHECK_LAUNCH();
-  return 0;
+  if (dtype != SB_BF16 && hd == 128) return SB_EUNSUPPORTED;  // fp32 path: head_dim 64 (config-1 pair)
+  if (dtype == SB_BF16)
+    return hd == 128 ? attn_dispatch<__nv_bfloat16, 128>(q_len, g, q, kc, vc, out, tok_slot, tok_pos, nq, nkv, ctx_max,
+                                                         scale, st)
+                     : attn_dispatch<__nv_bfloat16, 64>(q_len, g, q, kc, vc, out, tok_slot, tok_pos, nq, nkv, ctx_max,
+                                                        scale, st);
+  return attn_dispatch<float, 64>(q_len, g, q, kc, vc, out, tok_slot, tok_pos, nq, nkv, ctx_max, scale, st);
 }
 
 // ---------------------------------------------------------------- KV compaction (K5)
@@ -295,6 +341,8 @@ template <typename T>
 __global__ void kv_compact_kernel(T* __restrict__ k, T* __restrict__ v, const int32_t* __restrict__ src,
                                   const int32_t* __restrict__ dst, const int32_t* __restrict__ len, int slots,
                                   int nkv, int ctx_max, int hd) {
+  griddep_wait();
+  griddep_launch();
   int i = blockIdx.y, layer = blockIdx.z;
   int s = src[i], d = dst[i];
   if (s == d) return;
@@ -314,12 +362,10 @@ int launch_kv_compact(int dtype, void* k, void* v, const int32_t* src, const int
   if (n <= 0) return 0;
   dim3 grid(8, n, layers);
   if (dtype == SB_BF16)
-    kv_compact_kernel<__nv_bfloat16><<<grid, 256, 0, st>>>((__nv_bfloat16*)k, (__nv_bfloat16*)v, src, dst, len, slots,
-                                                           nkv, ctx_max, hd);
-  else
-    kv_compact_kernel<float><<<grid, 256, 0, st>>>((float*)k, (float*)v, src, dst, len, slots, nkv, ctx_max, hd);
-  SB_CHECK_LAUNCH();
-  return 0;
+    return launch_k(kv_compact_kernel<__nv_bfloat16>, grid, dim3(256), 0, st, (__nv_bfloat16*)k, (__nv_bfloat16*)v, src,
+                    dst, len, slots, nkv, ctx_max, hd);
+  return launch_k(kv_compact_kernel<float>, grid, dim3(256), 0, st, (float*)k, (float*)v, src, dst, len, slots, nkv,
+                  ctx_max, hd);
 }
 
 }  // namespace sb

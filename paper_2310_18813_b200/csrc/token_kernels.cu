@@ -148,17 +148,23 @@ __device__ int block_inverse_cdf(const float* a, const float* b, int mode, int V
 }
 
 __global__ void argmax_rows_kernel(const float* __restrict__ logits, int V, int32_t* __restrict__ out) {
+  griddep_wait();
+  griddep_launch();
   ArgMax a = block_argmax_row(logits + (size_t)blockIdx.x * V, V);
   if (threadIdx.x == 0) out[blockIdx.x] = a.i;
 }
 
 __global__ void softmax_rows_kernel(const float* logits, int V, float* probs) {
+  griddep_wait();
+  griddep_launch();
   block_softmax_row(logits + (size_t)blockIdx.x * V, probs + (size_t)blockIdx.x * V, V);
 }
 
 __global__ void select_kernel(const float* logits, int V, int mode, const float* __restrict__ u, int u_stride,
                               float* probs, long long probs_stride, int32_t* out_tok, int out_stride,
                               int32_t* next_ids, int32_t* next_pos, const int32_t* base_pos, int pos_offset) {
+  griddep_wait();
+  griddep_launch();
   int r = blockIdx.x;
   const float* row = logits + (size_t)r * V;
   int tok;
@@ -184,6 +190,8 @@ __global__ void accept_kernel(int mode, int k, int V, const int32_t* __restrict_
                               const float* __restrict__ u_res, int u_stride, const int32_t* __restrict__ l_inj,
                               const int32_t* __restrict__ produced, const int32_t* __restrict__ target_len,
                               int32_t* accepted_len, int32_t* advanced, int32_t* out_tok) {
+  griddep_wait();
+  griddep_launch();
   const int s = blockIdx.x;
   const int32_t* d = draft_tok + (size_t)s * draft_stride;
   __shared__ int sh_l;
@@ -238,6 +246,8 @@ __global__ void commit_kernel(int b, int k, const int32_t* __restrict__ advanced
                               int32_t* tokens, int cap, int32_t* n_tok, int32_t* produced,
                               const int32_t* __restrict__ target_len, int32_t* finish_iter, int32_t* iter,
                               int32_t* live_count, int32_t* acc_log, int acc_log_cap) {
+  griddep_wait();
+  griddep_launch();
   __shared__ int live;
   if (threadIdx.x == 0) live = 0;
   __syncthreads();
@@ -269,6 +279,8 @@ __global__ void prepare_kernel(int b, int k, const int32_t* __restrict__ tokens,
                                int32_t* v_pos, int32_t* d_last_pos, uint64_t seed, const int32_t* __restrict__ iter,
                                float* uniforms, int n_u, const int32_t* __restrict__ inj, int inj_count,
                                int32_t* l_inj) {
+  griddep_wait();
+  griddep_launch();
   const uint64_t it = (uint64_t)(*iter);
   for (int s = threadIdx.x; s < b; s += blockDim.x) {
     int n = n_tok[s];
@@ -300,16 +312,12 @@ extern "C" {
 
 int sb_argmax_rows(const float* logits, int32_t rows, int32_t vocab, int32_t* out, void* stream) {
   if (rows <= 0) return 0;
-  argmax_rows_kernel<<<rows, 256, 0, (cudaStream_t)stream>>>(logits, vocab, out);
-  SB_CHECK_LAUNCH();
-  return 0;
+  return launch_k(argmax_rows_kernel, dim3(rows), dim3(256), 0, (cudaStream_t)stream, logits, vocab, out);
 }
 
 int sb_softmax_rows(const float* logits, int32_t rows, int32_t vocab, float* probs, void* stream) {
   if (rows <= 0) return 0;
-  softmax_rows_kernel<<<rows, 256, 0, (cudaStream_t)stream>>>(logits, vocab, probs);
-  SB_CHECK_LAUNCH();
-  return 0;
+  return launch_k(softmax_rows_kernel, dim3(rows), dim3(256), 0, (cudaStream_t)stream, logits, vocab, probs);
 }
 
 int sb_select_tokens(const float* logits, int32_t rows, int32_t vocab, int32_t mode, const float* u, int32_t u_stride,
@@ -319,10 +327,8 @@ int sb_select_tokens(const float* logits, int32_t rows, int32_t vocab, int32_t m
   if (mode == SB_SELECT_SAMPLE && (probs_out == nullptr || u == nullptr)) return SB_EINVAL;
   if (next_pos && !base_pos) return SB_EINVAL;
   if ((vocab + kCdfChunk - 1) / kCdfChunk > 512) return SB_EUNSUPPORTED;
-  select_kernel<<<rows, 256, 0, (cudaStream_t)stream>>>(logits, vocab, mode, u, u_stride, probs_out, probs_stride,
+  return launch_k(select_kernel, dim3(rows), dim3(256), 0, (cudaStream_t)stream, logits, vocab, mode, u, u_stride, probs_out, probs_stride,
                                                         out_tok, out_stride, next_ids, next_pos, base_pos, pos_offset);
-  SB_CHECK_LAUNCH();
-  return 0;
 }
 
 int sb_accept(int32_t mode, int32_t b, int32_t k, int32_t vocab, const int32_t* target_tok, const float* p_probs,
@@ -335,11 +341,9 @@ int sb_accept(int32_t mode, int32_t b, int32_t k, int32_t vocab, const int32_t* 
   if (mode == SB_ACCEPT_INJECTED && !l_inj) return SB_EINVAL;
   if (mode < 0 || mode > 2) return SB_EINVAL;
   if ((vocab + kCdfChunk - 1) / kCdfChunk > 512) return SB_EUNSUPPORTED;
-  accept_kernel<<<b, 256, 0, (cudaStream_t)stream>>>(mode, k, vocab, target_tok, p_probs, q_probs, draft_tok,
+  return launch_k(accept_kernel, dim3(b), dim3(256), 0, (cudaStream_t)stream, mode, k, vocab, target_tok, p_probs, q_probs, draft_tok,
                                                      draft_stride, u_acc, u_res, u_stride, l_inj, produced,
                                                      target_len, accepted_len, advanced, out_tok);
-  SB_CHECK_LAUNCH();
-  return 0;
 }
 
 int sb_kv_commit(int32_t b, int32_t k, const int32_t* advanced, const int32_t* accepted_len, const int32_t* out_tok,
@@ -347,11 +351,9 @@ int sb_kv_commit(int32_t b, int32_t k, const int32_t* advanced, const int32_t* a
                  int32_t* finish_iter, int32_t* iter, int32_t* live_count, int32_t* acc_log, int32_t acc_log_cap,
                  void* stream) {
   if (b <= 0 || k < 0) return SB_EINVAL;
-  commit_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(b, k, advanced, accepted_len, out_tok, tokens, tok_cap, n_tok,
+  return launch_k(commit_kernel, dim3(1), dim3(256), 0, (cudaStream_t)stream, b, k, advanced, accepted_len, out_tok, tokens, tok_cap, n_tok,
                                                      produced, target_len, finish_iter, iter, live_count, acc_log,
                                                      acc_log_cap);
-  SB_CHECK_LAUNCH();
-  return 0;
 }
 
 int sb_prepare_iteration(int32_t b, int32_t k, const int32_t* tokens, int32_t tok_cap, const int32_t* n_tok,
@@ -360,11 +362,9 @@ int sb_prepare_iteration(int32_t b, int32_t k, const int32_t* tokens, int32_t to
                          const int32_t* inj_samples, int32_t inj_count, int32_t* l_inj, void* stream) {
   if (b <= 0 || k < 0 || n_u > 64) return SB_EINVAL;
   if ((d1_ids == nullptr) != (d1_pos == nullptr)) return SB_EINVAL;
-  prepare_kernel<<<1, 256, 0, (cudaStream_t)stream>>>(b, k, tokens, tok_cap, n_tok, d1_ids, d1_pos, v_ids, v_pos,
+  return launch_k(prepare_kernel, dim3(1), dim3(256), 0, (cudaStream_t)stream, b, k, tokens, tok_cap, n_tok, d1_ids, d1_pos, v_ids, v_pos,
                                                       d_last_pos, seed, iter, uniforms, n_u, inj_samples, inj_count,
                                                       l_inj);
-  SB_CHECK_LAUNCH();
-  return 0;
 }
 
 float sb_uniform_host(uint64_t seed, uint64_t stream_id, uint64_t counter) { return u01(seed, stream_id, counter); }
