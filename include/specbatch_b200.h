@@ -213,6 +213,15 @@ int sb_init(void);
 int sb_set_gemm_backend(int32_t backend);
 /* Programmatic dependent launch for every kernel (default on); 0 disables (ablation). */
 int sb_set_pdl(int32_t enabled);
+/* Diagnostics: eager forward with an event after every kernel; per-stage summed ms as "tag=ms;..." in buf. */
+int sb_profile_forward(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* tok_ids,
+                       const int32_t* tok_slot, const int32_t* tok_pos, int32_t n_seq, int32_t q_len,
+                       float* logits, int32_t logits_mode, void* workspace, size_t ws_bytes, void* stream,
+                       char* buf, int32_t buf_len);
+/* Attention implementation: 0 fused RoPE+append+cluster split-KV (default), 1 separate kernels. */
+int sb_set_attention_impl(int32_t impl);
+/* tcgen05 GEMM tuning overrides (0 = automatic): CTAs per SM (1|2), max pipeline stages, K splits. */
+int sb_gemm_tune(int32_t ctas_per_sm, int32_t max_stages, int32_t splits);
 int sb_version(void);
 const char* sb_build_info(void);
 int sb_last_kernel_count(void); /* kernels launched by the last sb_decoder_forward */

@@ -5,6 +5,8 @@
 // one CUDA graph per (b, k) by the host engine.
 #include <cstdio>
 #include <cstring>
+#include <string>
+#include <vector>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -58,6 +60,23 @@ static size_t carve(const sb_decoder_t* m, int T, char* base, FwdWorkspace* w) {
 }
 
 static int g_last_count = 0;
+// event profiling (sb_profile_forward): an event after every kernel of the forward
+static bool g_prof = false;
+static std::vector<cudaEvent_t> g_prof_ev;
+static std::vector<std::string> g_prof_tag;
+static size_t g_prof_n = 0;
+static void prof_mark(const char* tag, cudaStream_t st) {
+  if (!g_prof) return;
+  if (g_prof_n == g_prof_ev.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    g_prof_ev.push_back(e);
+    g_prof_tag.emplace_back();
+  }
+  g_prof_tag[g_prof_n] = tag;
+  cudaEventRecord(g_prof_ev[g_prof_n++], st);
+}
+static int g_attn_impl = 0;  // 0 fused rope+append+cluster attention, 1 separate kernels (sb_set_attention_impl)
 
 static int forward_impl(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* ids, const int32_t* slot,
                         const int32_t* pos, int n_seq, int q_len, float* logits, int logits_mode, void* ws,
@@ -74,31 +93,49 @@ static int forward_impl(const sb_decoder_t* m, const sb_kvcache_t* kv, const int
   const int qkv_n = (nq + 2 * nkv) * hd;
   const size_t layer_kv = (size_t)kv->slots * nkv * kv->ctx_max * hd * es;
 
+  prof_mark("start", st);
   SB_TRY(launch_embed(dt, m->embed, ids, pos, w.resid, T, H, m->vocab, st));
+  prof_mark("embed", st);
   for (int l = 0; l < m->n_layers; ++l) {
     char* kc = (char*)kv->k + l * layer_kv;
     char* vc = (char*)kv->v + l * layer_kv;
     SB_TRY(launch_rmsnorm(dt, w.resid, m->attn_norm[l], w.xn, T, H, m->rms_eps, 1, 0, st));
+    prof_mark("norm1", st);
     GemmArgs g{dt, w.xn, m->w_qkv[l], w.qkv, T, qkv_n, H, H, EPI_STORE, w.gemm_ws, w.gemm_ws_bytes};
     SB_TRY(gemm(g, GEMM_AUTO, st));
-    SB_TRY(launch_rope_append(dt, w.qkv, w.qr, kc, vc, slot, pos, m->rope_cos, m->rope_sin, T, q_len, nq, nkv, hd,
-                              kv->ctx_max, m->max_pos, st));
-    SB_TRY(launch_attention(dt, w.qr, kc, vc, w.attn, slot, pos, n_seq, q_len, nq, nkv, hd, kv->ctx_max, st));
+    prof_mark("qkv", st);
+    int rc_fa = SB_EUNSUPPORTED;
+    if (g_attn_impl == 0)
+      rc_fa = launch_fused_attention(dt, w.qkv, kc, vc, w.attn, slot, pos, m->rope_cos, m->rope_sin, n_seq, q_len, nq,
+                                     nkv, hd, kv->ctx_max, m->max_pos, st);
+    if (rc_fa != 0 && rc_fa != SB_EUNSUPPORTED) return rc_fa;
+    if (rc_fa == SB_EUNSUPPORTED) {  // prefill-sized query blocks / wide GQA: rope+append then attention
+      SB_TRY(launch_rope_append(dt, w.qkv, w.qr, kc, vc, slot, pos, m->rope_cos, m->rope_sin, T, q_len, nq, nkv, hd,
+                                kv->ctx_max, m->max_pos, st));
+      SB_TRY(launch_attention(dt, w.qr, kc, vc, w.attn, slot, pos, n_seq, q_len, nq, nkv, hd, kv->ctx_max, st));
+    }
+    prof_mark("attn", st);
     g = GemmArgs{dt, w.attn, m->w_o[l], w.resid, T, H, nq * hd, nq * hd, EPI_RESID_ADD, w.gemm_ws, w.gemm_ws_bytes};
     SB_TRY(gemm(g, GEMM_AUTO, st));
+    prof_mark("o", st);
     SB_TRY(launch_rmsnorm(dt, w.resid, m->mlp_norm[l], w.xn, T, H, m->rms_eps, 1, 0, st));
+    prof_mark("norm2", st);
     g = GemmArgs{dt, w.xn, m->w_gu[l], w.act, T, 2 * m->ffn, H, H, EPI_SILU_MUL, w.gemm_ws, w.gemm_ws_bytes};
     SB_TRY(gemm(g, GEMM_AUTO, st));
+    prof_mark("gu", st);
     g = GemmArgs{dt, w.act, m->w_down[l], w.resid, T, H, m->ffn, m->ffn, EPI_RESID_ADD, w.gemm_ws, w.gemm_ws_bytes};
     SB_TRY(gemm(g, GEMM_AUTO, st));
+    prof_mark("down", st);
   }
   if (logits_mode == SB_LOGITS_NONE) return 0;
   int rows = logits_mode == SB_LOGITS_LAST ? n_seq : T;
   int step = logits_mode == SB_LOGITS_LAST ? q_len : 1;
   int off = logits_mode == SB_LOGITS_LAST ? q_len - 1 : 0;
   SB_TRY(launch_rmsnorm(dt, w.resid, m->final_norm, w.last, rows, H, m->rms_eps, step, off, st));
+  prof_mark("norm_f", st);
   GemmArgs g{dt, w.last, m->lm_head, logits, rows, m->vocab, H, H, EPI_STORE_F32, w.gemm_ws, w.gemm_ws_bytes};
   SB_TRY(gemm(g, GEMM_AUTO, st));
+  prof_mark("lm_head", st);
   return 0;
 }
 
@@ -149,6 +186,50 @@ int sb_set_gemm_backend(int32_t backend) {
   if (backend < 0 || backend > 2) return SB_EINVAL;
   g_backend_override = backend;
   return 0;
+}
+
+// Eager forward with an event after every kernel; writes per-tag summed
+// milliseconds as "tag=ms;..." into buf (warm timings of the real launch
+// sequence; events break PDL overlap, so the sum exceeds the graph time).
+int sb_profile_forward(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* tok_ids, const int32_t* tok_slot,
+                       const int32_t* tok_pos, int32_t n_seq, int32_t q_len, float* logits, int32_t logits_mode,
+                       void* workspace, size_t ws_bytes, void* stream, char* buf, int32_t buf_len) {
+  g_prof = true;
+  g_prof_n = 0;
+  int rc = forward_impl(m, kv, tok_ids, tok_slot, tok_pos, n_seq, q_len, logits, logits_mode, workspace, ws_bytes,
+                        (cudaStream_t)stream);
+  g_prof = false;
+  if (rc) return rc;
+  cudaStreamSynchronize((cudaStream_t)stream);
+  std::vector<std::pair<std::string, float>> acc;
+  for (size_t i = 1; i < g_prof_n; ++i) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, g_prof_ev[i - 1], g_prof_ev[i]);
+    bool found = false;
+    for (auto& pr : acc)
+      if (pr.first == g_prof_tag[i]) {
+        pr.second += ms;
+        found = true;
+      }
+    if (!found) acc.emplace_back(g_prof_tag[i], ms);
+  }
+  std::string s;
+  for (auto& pr : acc) s += pr.first + "=" + std::to_string(pr.second) + ";";
+  if ((int)s.size() + 1 > buf_len) return SB_EINVAL;
+  memcpy(buf, s.c_str(), s.size() + 1);
+  return 0;
+}
+
+int sb_set_attention_impl(int32_t impl) {
+  if (impl < 0 || impl > 1) return SB_EINVAL;
+  g_attn_impl = impl;
+  return 0;
+}
+
+int sb_gemm_tune(int32_t ctas_per_sm, int32_t max_stages, int32_t splits) {
+  if (ctas_per_sm < 0 || ctas_per_sm > 2 || max_stages < 0 || max_stages > 16 || splits < 0 || splits > 8)
+    return SB_EINVAL;
+  return gemm_tc_tune(ctas_per_sm, max_stages, splits);
 }
 
 int sb_set_pdl(int32_t enabled) {

@@ -375,6 +375,8 @@ static int tn_for(int M) {
 }
 
 int g_pdl = 1;  // programmatic dependent launch for every forward kernel (sb_set_pdl)
+// tuning overrides (sb_gemm_tune): 0 = automatic
+static int g_tune_cps = 0, g_tune_stages = 0, g_tune_splits = 0;
 
 struct TcPlan {
   int tn, n_tiles_n, m_tiles, kb, splits, stages, ctas_per_sm;
@@ -390,22 +392,30 @@ static TcPlan plan(int M, int N, int K) {
   q.n_tiles_n = (N + TC_BM - 1) / TC_BM;
   q.m_tiles = (M + q.tn - 1) / q.tn;
   q.kb = (K + TC_BK - 1) / TC_BK;
-  q.ctas_per_sm = q.tn >= 128 ? 1 : 2;
+  q.ctas_per_sm = g_tune_cps ? g_tune_cps : (q.tn >= 128 ? 1 : 2);
   const int sms = num_sms();
   const int slots = sms * q.ctas_per_sm;
   const int tiles = q.n_tiles_n * q.m_tiles;
   q.splits = 1;
   while (q.splits < 8 && tiles * q.splits < sms && tiles * q.splits * 2 <= slots && q.kb / (q.splits * 2) >= 2)
     q.splits *= 2;
+  if (g_tune_splits) q.splits = g_tune_splits;
   size_t budget = q.ctas_per_sm == 2 ? 108 * 1024 : 200 * 1024;
   size_t stage = (size_t)(TC_BM + q.tn) * TC_BK * 2;
   q.stages = (int)((budget - 1024 - 256) / stage);
-  if (q.stages > 8) q.stages = 8;
+  if (q.stages > (g_tune_stages ? g_tune_stages : 12)) q.stages = g_tune_stages ? g_tune_stages : 12;
   if (q.stages < 2) q.stages = 2;
   size_t ring = (size_t)q.stages * stage;
   size_t red = (size_t)q.tn * TC_BM * 4;  // split-K partial tile reuses the ring
   q.smem = 1024 + (ring > red ? ring : red) + 256;
   return q;
+}
+
+int gemm_tc_tune(int cps, int stages, int splits) {
+  g_tune_cps = cps;
+  g_tune_stages = stages;
+  g_tune_splits = splits;
+  return 0;
 }
 
 int gemm_tc_init() {

@@ -33,6 +33,7 @@ int gemm_simt(const GemmArgs& a, cudaStream_t st);
 int gemm_tc(const GemmArgs& a, cudaStream_t st);  // tcgen05 (bf16 only); SB_EUNSUPPORTED otherwise
 bool gemm_tc_supported(const GemmArgs& a);
 int gemm_tc_init();
+int gemm_tc_tune(int cps, int stages, int splits);
 
 int launch_embed(int dtype, const void* table, const int32_t* ids, const int32_t* pos, float* h, int n_tok,
                  int hidden, int vocab, cudaStream_t st);
@@ -44,6 +45,9 @@ int launch_rope_append(int dtype, const void* qkv, void* q_out, void* kc, void* 
 int launch_attention(int dtype, const void* q, const void* kc, const void* vc, void* out, const int32_t* tok_slot,
                      const int32_t* tok_pos, int n_seq, int q_len, int nq, int nkv, int hd, int ctx_max,
                      cudaStream_t st);
+int launch_fused_attention(int dtype, const void* qkv, void* kc, void* vc, void* out, const int32_t* tok_slot,
+                           const int32_t* tok_pos, const float* cosT, const float* sinT, int n_seq, int q_len, int nq,
+                           int nkv, int hd, int ctx_max, int max_pos, cudaStream_t st);
 int launch_kv_compact(int dtype, void* k, void* v, const int32_t* src, const int32_t* dst, const int32_t* len, int n,
                       int layers, int slots, int nkv, int ctx_max, int hd, cudaStream_t st);
 
