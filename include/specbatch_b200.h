@@ -218,7 +218,7 @@ int sb_profile_forward(const sb_decoder_t* m, const sb_kvcache_t* kv, const int3
                        const int32_t* tok_slot, const int32_t* tok_pos, int32_t n_seq, int32_t q_len,
                        float* logits, int32_t logits_mode, void* workspace, size_t ws_bytes, void* stream,
                        char* buf, int32_t buf_len);
-/* Attention implementation: 0 fused RoPE+append+cluster split-KV (default), 1 separate kernels. */
+/* Attention implementation: 0 tensor-core flash decoding with fused RoPE+append (bf16 default), 1 separate kernels. */
 int sb_set_attention_impl(int32_t impl);
 /* tcgen05 GEMM tuning overrides (0 = automatic): CTAs per SM (1|2), max pipeline stages, K splits. */
 int sb_gemm_tune(int32_t ctas_per_sm, int32_t max_stages, int32_t splits);

@@ -76,7 +76,9 @@ static void prof_mark(const char* tag, cudaStream_t st) {
   g_prof_tag[g_prof_n] = tag;
   cudaEventRecord(g_prof_ev[g_prof_n++], st);
 }
-static int g_attn_impl = 0;  // 0 fused rope+append+cluster attention, 1 separate kernels (sb_set_attention_impl)
+// 0: tensor-core flash decoding (bf16, <= 16 queries per kv head) else separate kernels;
+// 1: always separate rope/append + attention kernels (sb_set_attention_impl)
+static int g_attn_impl = 0;
 
 static int forward_impl(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* ids, const int32_t* slot,
                         const int32_t* pos, int n_seq, int q_len, float* logits, int logits_mode, void* ws,
@@ -105,9 +107,9 @@ static int forward_impl(const sb_decoder_t* m, const sb_kvcache_t* kv, const int
     SB_TRY(gemm(g, GEMM_AUTO, st));
     prof_mark("qkv", st);
     int rc_fa = SB_EUNSUPPORTED;
-    if (g_attn_impl == 0)
-      rc_fa = launch_fused_attention(dt, w.qkv, kc, vc, w.attn, slot, pos, m->rope_cos, m->rope_sin, n_seq, q_len, nq,
-                                     nkv, hd, kv->ctx_max, m->max_pos, st);
+    if (g_attn_impl == 0 && dt == SB_BF16)
+      rc_fa = launch_attention_tc(w.qkv, kc, vc, w.attn, slot, pos, m->rope_cos, m->rope_sin, n_seq, q_len, nq, nkv,
+                                  hd, kv->ctx_max, m->max_pos, st);
     if (rc_fa != 0 && rc_fa != SB_EUNSUPPORTED) return rc_fa;
     if (rc_fa == SB_EUNSUPPORTED) {  // prefill-sized query blocks / wide GQA: rope+append then attention
       SB_TRY(launch_rope_append(dt, w.qkv, w.qr, kc, vc, slot, pos, m->rope_cos, m->rope_sin, T, q_len, nq, nkv, hd,

@@ -45,9 +45,9 @@ int launch_rope_append(int dtype, const void* qkv, void* q_out, void* kc, void* 
 int launch_attention(int dtype, const void* q, const void* kc, const void* vc, void* out, const int32_t* tok_slot,
                      const int32_t* tok_pos, int n_seq, int q_len, int nq, int nkv, int hd, int ctx_max,
                      cudaStream_t st);
-int launch_fused_attention(int dtype, const void* qkv, void* kc, void* vc, void* out, const int32_t* tok_slot,
-                           const int32_t* tok_pos, const float* cosT, const float* sinT, int n_seq, int q_len, int nq,
-                           int nkv, int hd, int ctx_max, int max_pos, cudaStream_t st);
+int launch_attention_tc(const void* qkv, void* kc, void* vc, void* out, const int32_t* tok_slot, const int32_t* tok_pos,
+                        const float* cosT, const float* sinT, int n_seq, int q_len, int nq, int nkv, int hd,
+                        int ctx_max, int max_pos, cudaStream_t st);
 int launch_kv_compact(int dtype, void* k, void* v, const int32_t* src, const int32_t* dst, const int32_t* len, int n,
                       int layers, int slots, int nkv, int ctx_max, int hd, cudaStream_t st);
 

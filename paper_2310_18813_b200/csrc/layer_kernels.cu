@@ -336,6 +336,332 @@ int launch_attention(int dtype, const void* q, const void* kc, const void* vc, v
   return attn_dispatch<float, 64>(q_len, g, q, kc, vc, out, tok_slot, tok_pos, nq, nkv, ctx_max, scale, st);
 }
 
+// ---------------------------------------------------------------- tensor-core flash decoding (bf16)
+// CTA = (kv head, sequence): all q heads of the kv group x all window tokens
+// (<= 16 queries) form ONE 16-row MMA tile.  4 warps; warp w owns keys
+// [16w, 16w+16) of every 64-key tile (split over keys, combined at the end in
+// warp order -> deterministic).  S = Q K^T and O += P V with
+// mma.sync.m16n8k16 (bf16 in, fp32 accumulate; P is fed from the S
+// accumulators without a smem round trip).  KV tiles stream through a 3-stage
+// cp.async ring; padded 272-byte rows make every ldmatrix conflict-free.  The
+// prologue rotates Q (RoPE, rounded to bf16) and appends this forward's
+// rotated K / V rows to the cache (this CTA is the only reader of its slab).
+constexpr int kTcKT = 64;
+constexpr int kTcStages = 3;
+
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(gmem)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+__device__ __forceinline__ void ldsm_x4(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void ldsm_x4_t(uint32_t addr, uint32_t& r0, uint32_t& r1, uint32_t& r2, uint32_t& r3) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0,%1,%2,%3}, [%4];"
+               : "=r"(r0), "=r"(r1), "=r"(r2), "=r"(r3)
+               : "r"(addr));
+}
+__device__ __forceinline__ void mma_bf16(float (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2, uint32_t a3, uint32_t b0,
+                                         uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+      "{%0,%1,%2,%3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ uint32_t pack_bf16(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+template <int HD>
+struct TcAttnSmem {
+  static constexpr int RS = HD + 8;                             // padded row (elements)
+  static constexpr size_t tile = (size_t)kTcKT * RS * 2;        // one K or V tile
+  static constexpr size_t stage = 2 * tile;
+  static constexpr size_t q = (size_t)16 * RS * 2;
+  static constexpr size_t comb = (size_t)4 * 16 * HD * 4 + 4 * 16 * 2 * 4;  // warp partials (aliases the ring)
+  static constexpr size_t ring = kTcStages * stage;
+  static constexpr size_t bytes = q + (ring > comb ? ring : comb);
+};
+
+template <int HD>
+__global__ void __launch_bounds__(128) attention_tc_kernel(
+    const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc,
+    __nv_bfloat16* __restrict__ out, const int32_t* __restrict__ tok_slot, const int32_t* __restrict__ tok_pos,
+    const float* __restrict__ cosT, const float* __restrict__ sinT, int q_len, int nq, int nkv, int ctx_max,
+    int max_pos, float scale) {
+  using SM = TcAttnSmem<HD>;
+  constexpr int RS = SM::RS, HALF = HD / 2, KSTEP = HD / 16, NT = HD / 8;
+  extern __shared__ __align__(128) uint8_t tsm[];
+  __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(tsm);
+  uint8_t* ring = tsm + SM::q;
+  __shared__ int qpos[16], qtok[16], qhead[16];
+  griddep_wait();
+  griddep_launch();
+
+  const int kvh = blockIdx.x, seq = blockIdx.y;
+  const int group = nq / nkv;
+  const int nQ = group * q_len;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int slot = tok_slot[seq];
+  const int row_w = (nq + 2 * nkv) * HD;
+  const __nv_bfloat16* seq_rows = qkv + (size_t)seq * q_len * row_w;
+  __nv_bfloat16* kslab = kc + ((size_t)slot * nkv + kvh) * ctx_max * HD;
+  __nv_bfloat16* vslab = vc + ((size_t)slot * nkv + kvh) * ctx_max * HD;
+
+  if (tid < 16) {
+    int t = tid / group;
+    qtok[tid] = tid < nQ ? t : 0;
+    qhead[tid] = kvh * group + tid % group;
+    qpos[tid] = tid < nQ ? tok_pos[seq * q_len + t] : -1;
+  }
+  __syncthreads();
+  for (int e = tid; e < 16 * HALF; e += 128) {
+    int j = e / HALF, i = e % HALF;
+    __nv_bfloat16 a = __float2bfloat16_rn(0.f), b = a;
+    if (j < nQ) {
+      int p = qpos[j];
+      int pc = p < 0 ? 0 : (p >= max_pos ? max_pos - 1 : p);
+      const __nv_bfloat16* src = seq_rows + (size_t)qtok[j] * row_w + qhead[j] * HD;
+      float x0 = __bfloat162float(src[i]), x1 = __bfloat162float(src[i + HALF]);
+      float c = cosT[(size_t)pc * HALF + i], sn = sinT[(size_t)pc * HALF + i];
+      a = __float2bfloat16_rn(x0 * c - x1 * sn);
+      b = __float2bfloat16_rn(x1 * c + x0 * sn);
+    }
+    Qs[j * RS + i] = a;
+    Qs[j * RS + i + HALF] = b;
+  }
+  for (int e = tid; e < q_len * HALF; e += 128) {
+    int t = e / HALF, i = e % HALF;
+    int p = tok_pos[seq * q_len + t];
+    if (p < 0) continue;
+    int pc = p >= max_pos ? max_pos - 1 : p;
+    const __nv_bfloat16* src = seq_rows + (size_t)t * row_w + (nq + kvh) * HD;
+    float x0 = __bfloat162float(src[i]), x1 = __bfloat162float(src[i + HALF]);
+    float c = cosT[(size_t)pc * HALF + i], sn = sinT[(size_t)pc * HALF + i];
+    kslab[(size_t)p * HD + i] = __float2bfloat16_rn(x0 * c - x1 * sn);
+    kslab[(size_t)p * HD + i + HALF] = __float2bfloat16_rn(x1 * c + x0 * sn);
+    const __nv_bfloat16* vsrc = seq_rows + (size_t)t * row_w + (nq + nkv + kvh) * HD;
+    vslab[(size_t)p * HD + i] = vsrc[i];
+    vslab[(size_t)p * HD + i + HALF] = vsrc[i + HALF];
+  }
+  __threadfence_block();
+  __syncthreads();
+
+  int maxp = -1;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) maxp = max(maxp, qpos[j]);
+  const int n_keys = maxp + 1;
+  const int n_tiles = (n_keys + kTcKT - 1) / kTcKT;
+
+  auto issue = [&](int tile) {
+    if (tile < n_tiles) {
+      uint8_t* st = ring + (tile % kTcStages) * SM::stage;
+      __nv_bfloat16* Kd = reinterpret_cast<__nv_bfloat16*>(st);
+      __nv_bfloat16* Vd = reinterpret_cast<__nv_bfloat16*>(st + SM::tile);
+      const int k0 = tile * kTcKT;
+      constexpr int CPR = HD / 8;  // 16-byte chunks per row
+      for (int e = tid; e < kTcKT * CPR; e += 128) {
+        int r = e / CPR, c = (e % CPR) * 8;
+        int key = k0 + r;
+        if (key < n_keys) {
+          cp_async16(Kd + r * RS + c, kslab + (size_t)key * HD + c);
+          cp_async16(Vd + r * RS + c, vslab + (size_t)key * HD + c);
+        } else {  // rows past the context: zeros (P is 0 there, and 0 * stale NaN would poison P.V)
+          *reinterpret_cast<uint4*>(Kd + r * RS + c) = make_uint4(0, 0, 0, 0);
+          *reinterpret_cast<uint4*>(Vd + r * RS + c) = make_uint4(0, 0, 0, 0);
+        }
+      }
+    }
+    cp_async_commit();  // always commit (possibly empty) to keep group counting uniform
+  };
+#pragma unroll
+  for (int i = 0; i < kTcStages - 1; ++i) issue(i);
+
+  // Q fragments (A operand), loaded once
+  const uint32_t qs_base = (uint32_t)__cvta_generic_to_shared(Qs);
+  uint32_t qa[KSTEP][4];
+  {
+    const int mi = lane >> 3, ri = lane & 7;
+    const int row = ri + (mi & 1) * 8;
+#pragma unroll
+    for (int ks = 0; ks < KSTEP; ++ks) {
+      int col = ks * 16 + (mi >> 1) * 8;
+      ldsm_x4(qs_base + (uint32_t)(row * RS + col) * 2, qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3]);
+    }
+  }
+  const int g = lane >> 2, t4 = lane & 3;
+  const int pos_lo = qpos[g], pos_hi = qpos[g + 8];
+  float o[NT][4];
+#pragma unroll
+  for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+  float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;
+
+  for (int tile = 0; tile < n_tiles; ++tile) {
+    issue(tile + kTcStages - 1);
+    cp_async_wait<kTcStages - 1>();
+    __syncthreads();
+    const uint8_t* st = ring + (tile % kTcStages) * SM::stage;
+    const uint32_t kb = (uint32_t)__cvta_generic_to_shared(st);
+    const uint32_t vb = kb + (uint32_t)SM::tile;
+    const int kw = warp * 16;  // this warp's 16 keys within the tile
+    // S = Q K^T for keys kw..kw+15 (two n8 tiles)
+    float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
+    {
+      const int mi = lane >> 3, ri = lane & 7;
+      const int key = kw + ri + (mi >> 1) * 8;
+#pragma unroll
+      for (int ks = 0; ks < KSTEP; ++ks) {
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4(kb + (uint32_t)(key * RS + ks * 16 + (mi & 1) * 8) * 2, b0, b1, b2, b3);
+        mma_bf16(s0, qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b0, b1);
+        mma_bf16(s1, qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b2, b3);
+      }
+    }
+    // mask + scale, online softmax (rows g and g+8)
+    const int kbase = tile * kTcKT + kw + 2 * t4;
+    float v[8] = {s0[0], s0[1], s1[0], s1[1], s0[2], s0[3], s1[2], s1[3]};
+    const int kidx[4] = {kbase, kbase + 1, kbase + 8, kbase + 9};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      v[i] = (kidx[i] <= pos_lo) ? v[i] * scale : -INFINITY;
+      v[4 + i] = (kidx[i] <= pos_hi) ? v[4 + i] * scale : -INFINITY;
+    }
+    float mx_lo = fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
+    float mx_hi = fmaxf(fmaxf(v[4], v[5]), fmaxf(v[6], v[7]));
+    mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 1));
+    mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 2));
+    mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 1));
+    mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 2));
+    const float mn_lo = fmaxf(m_lo, mx_lo), mn_hi = fmaxf(m_hi, mx_hi);
+    const float c_lo = (m_lo == -INFINITY) ? 0.f : __expf(m_lo - mn_lo);
+    const float c_hi = (m_hi == -INFINITY) ? 0.f : __expf(m_hi - mn_hi);
+    float p[8], sum_lo = 0.f, sum_hi = 0.f;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      p[i] = (mn_lo == -INFINITY) ? 0.f : __expf(v[i] - mn_lo);
+      p[4 + i] = (mn_hi == -INFINITY) ? 0.f : __expf(v[4 + i] - mn_hi);
+      sum_lo += p[i];
+      sum_hi += p[4 + i];
+    }
+    sum_lo += __shfl_xor_sync(0xffffffffu, sum_lo, 1);
+    sum_lo += __shfl_xor_sync(0xffffffffu, sum_lo, 2);
+    sum_hi += __shfl_xor_sync(0xffffffffu, sum_hi, 1);
+    sum_hi += __shfl_xor_sync(0xffffffffu, sum_hi, 2);
+    l_lo = l_lo * c_lo + sum_lo;
+    l_hi = l_hi * c_hi + sum_hi;
+    m_lo = mn_lo;
+    m_hi = mn_hi;
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      o[n][0] *= c_lo;
+      o[n][1] *= c_lo;
+      o[n][2] *= c_hi;
+      o[n][3] *= c_hi;
+    }
+    // P (A operand, k = the warp's 16 keys) straight from the S accumulators
+    const uint32_t pa0 = pack_bf16(p[0], p[1]), pa1 = pack_bf16(p[4], p[5]);
+    const uint32_t pa2 = pack_bf16(p[2], p[3]), pa3 = pack_bf16(p[6], p[7]);
+    {
+      const int mi = lane >> 3, ri = lane & 7;
+      const int key = kw + ri + (mi & 1) * 8;
+#pragma unroll
+      for (int n = 0; n < NT; n += 2) {
+        uint32_t b0, b1, b2, b3;
+        ldsm_x4_t(vb + (uint32_t)(key * RS + n * 8 + (mi >> 1) * 8) * 2, b0, b1, b2, b3);
+        mma_bf16(o[n], pa0, pa1, pa2, pa3, b0, b1);
+        mma_bf16(o[n + 1], pa0, pa1, pa2, pa3, b2, b3);
+      }
+    }
+    __syncthreads();  // this stage may be overwritten by the next issue
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+  // combine the 4 warps in order (smem partials alias the drained ring)
+  float* comb = reinterpret_cast<float*>(ring);
+  float* cm = comb + 4 * 16 * HD;
+  float* cl = cm + 4 * 16;
+#pragma unroll
+  for (int n = 0; n < NT; ++n) {
+    int d = n * 8 + 2 * t4;
+    comb[(warp * 16 + g) * HD + d] = o[n][0];
+    comb[(warp * 16 + g) * HD + d + 1] = o[n][1];
+    comb[(warp * 16 + g + 8) * HD + d] = o[n][2];
+    comb[(warp * 16 + g + 8) * HD + d + 1] = o[n][3];
+  }
+  if (t4 == 0) {
+    cm[warp * 16 + g] = m_lo;
+    cm[warp * 16 + g + 8] = m_hi;
+    cl[warp * 16 + g] = l_lo;
+    cl[warp * 16 + g + 8] = l_hi;
+  }
+  __syncthreads();
+  for (int e = tid; e < nQ * HD; e += 128) {
+    int j = e / HD, d = e % HD;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) M = fmaxf(M, cm[w * 16 + j]);
+    float L = 0.f, acc = 0.f;
+#pragma unroll
+    for (int w = 0; w < 4; ++w) {
+      float mw = cm[w * 16 + j];
+      float f = (mw == -INFINITY) ? 0.f : __expf(mw - M);
+      L += cl[w * 16 + j] * f;
+      acc += comb[(w * 16 + j) * HD + d] * f;
+    }
+    out[((size_t)(seq * q_len + qtok[j]) * nq + qhead[j]) * HD + d] = __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
+  }
+}
+
+int launch_attention_tc(const void* qkv, void* kc, void* vc, void* out, const int32_t* tok_slot, const int32_t* tok_pos,
+                        const float* cosT, const float* sinT, int n_seq, int q_len, int nq, int nkv, int hd,
+                        int ctx_max, int max_pos, cudaStream_t st) {
+  if ((hd != 64 && hd != 128) || nq % nkv != 0 || (nq / nkv) * q_len > 16) return SB_EUNSUPPORTED;
+  const float scale = 1.0f / sqrtf((float)hd);
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(nkv, n_seq, 1);
+  cfg.blockDim = dim3(128);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = g_pdl ? 1 : 0;
+  cudaError_t e;
+  if (hd == 128) {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(attention_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)TcAttnSmem<128>::bytes);
+      attr = true;
+    }
+    cfg.dynamicSmemBytes = TcAttnSmem<128>::bytes;
+    e = cudaLaunchKernelEx(&cfg, attention_tc_kernel<128>, (const __nv_bfloat16*)qkv, (__nv_bfloat16*)kc,
+                           (__nv_bfloat16*)vc, (__nv_bfloat16*)out, tok_slot, tok_pos, cosT, sinT, q_len, nq, nkv,
+                           ctx_max, max_pos, scale);
+  } else {
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(attention_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)TcAttnSmem<64>::bytes);
+      attr = true;
+    }
+    cfg.dynamicSmemBytes = TcAttnSmem<64>::bytes;
+    e = cudaLaunchKernelEx(&cfg, attention_tc_kernel<64>, (const __nv_bfloat16*)qkv, (__nv_bfloat16*)kc,
+                           (__nv_bfloat16*)vc, (__nv_bfloat16*)out, tok_slot, tok_pos, cosT, sinT, q_len, nq, nkv,
+                           ctx_max, max_pos, scale);
+  }
+  if (e != cudaSuccess) return (int)e;
+  ++g_kernel_count;
+  return 0;
+}
+
 // ---------------------------------------------------------------- KV compaction (K5)
 template <typename T>
 __global__ void kv_compact_kernel(T* __restrict__ k, T* __restrict__ v, const int32_t* __restrict__ src,
