@@ -112,10 +112,13 @@ def verify_bytes(cfg, b, k, ctx_avg):
 
 
 # ============================================================== reference arm (CPU)
-def cpu_sample(b, k, iters=2, threads=None, layers=None):
-    """The CPU oracle (oracle/model_ref.py, fp32, all host threads) running the
-    same speculative iteration: draft k steps + verify b(k+1) tokens of the
-    7B/68M pair, on a bounded sample.  Returns (tokens/s, description, cores)."""
+def cpu_sample(b, k, iters=1, threads=None, layers=None):
+    """The CPU oracle (oracle/model_ref.py forward_batch, fp32, all host
+    threads) running the same speculative iteration -- draft k steps + verify
+    b(k+1) tokens of the full 7B/68M pair, batched over the b sequences -- on a
+    bounded sample (`iters` iterations after an untimed prefill).  Weights are a
+    tiled random block (timing only; CPU parity is tested on the tiny pair).
+    Returns (tokens/s, description, cores)."""
     import torch
 
     from oracle import model_ref, spec_ref
@@ -126,57 +129,65 @@ def cpu_sample(b, k, iters=2, threads=None, layers=None):
     torch.set_num_threads(threads)
     tc, dc = CONFIGS[TARGET], CONFIGS[DRAFT]
     L = tc.n_layers if layers is None else layers
+    block = torch.empty(1 << 20).uniform_(-0.035, 0.035, generator=torch.Generator().manual_seed(0))
 
-    def masters(cfg, n_layers, seed):
-        g = torch.Generator().manual_seed(seed)
+    def mk(*shape):
+        n = int(np.prod(shape))
+        reps = (n + block.numel() - 1) // block.numel()
+        return block.repeat(reps)[:n].view(*shape).clone()
+
+    def masters(cfg, n_layers):
         h, hd = cfg.hidden, cfg.head_dim
-        mk = lambda *s: torch.empty(*s).uniform_(-0.035, 0.035, generator=g)
         return {"embed": mk(cfg.vocab, h), "lm_head": mk(cfg.vocab, h),
                 "layers": [{"wq": mk(cfg.n_heads * hd, h), "wk": mk(cfg.n_kv_heads * hd, h),
                             "wv": mk(cfg.n_kv_heads * hd, h), "wo": mk(h, cfg.n_heads * hd), "wg": mk(cfg.ffn, h),
                             "wu": mk(cfg.ffn, h), "wd": mk(h, cfg.ffn)} for _ in range(n_layers)]}
 
     t_init = time.perf_counter()
-    tgt = model_ref.LlamaRef(masters(tc, L, 0), tc.n_heads, tc.n_kv_heads, tc.rms_eps, max_pos=P + NEW + 16,
+    tgt = model_ref.LlamaRef(masters(tc, L), tc.n_heads, tc.n_kv_heads, tc.rms_eps, max_pos=P + NEW + 16,
                              dtype=torch.float32)
-    drf = model_ref.LlamaRef(masters(dc, dc.n_layers, 1), dc.n_heads, dc.n_kv_heads, dc.rms_eps,
+    drf = model_ref.LlamaRef(masters(dc, dc.n_layers), dc.n_heads, dc.n_kv_heads, dc.rms_eps,
                              max_pos=P + NEW + 16, dtype=torch.float32)
-    t_init = time.perf_counter() - t_init
-    trace = example_trace()
     rng = np.random.default_rng(0)
-    prompts = [rng.integers(0, tc.vocab, P) for _ in range(b)]
+    prompts = [list(map(int, rng.integers(0, tc.vocab, P))) for _ in range(b)]
     tcache = [tgt.new_cache() for _ in range(b)]
     dcache = [drf.new_cache() for _ in range(b)]
-    for s in range(b):  # prefill (untimed)
-        tgt.forward(list(prompts[s][:P - 1]), list(range(P - 1)), tcache[s])
-        drf.forward(list(prompts[s][:P - 1]), list(range(P - 1)), dcache[s])
-    toks = [list(map(int, p)) for p in prompts]
+    pre = [p[:P - 1] for p in prompts]
+    ppos = [list(range(P - 1))] * b
+    model_ref.forward_batch(tgt, pre, ppos, tcache)
+    model_ref.forward_batch(drf, pre, ppos, dcache)
+    t_init = time.perf_counter() - t_init
+    trace = example_trace()
+    toks = [list(p) for p in prompts]
     gen = 0
     t0 = time.perf_counter()
     for it in range(iters):
         l_inj = np.minimum(spec_ref.injected_lengths(0, it, b, trace.samples), k)
-        for s in range(b):
-            n = len(toks[s])
-            drafts = []
-            lg = drf.forward(toks[s][n - 2:n], [n - 2, n - 1], dcache[s])[-1]
+        ns = [len(t) for t in toks]
+        drafts = [[] for _ in range(b)]
+        if k > 0:
+            lg = model_ref.forward_batch(drf, [t[n - 2:n] for t, n in zip(toks, ns)], [[n - 2, n - 1] for n in ns],
+                                         dcache)[:, -1]
             for j in range(1, k + 1):
                 if j > 1:
-                    lg = drf.forward([drafts[-1]], [n - 2 + j], dcache[s])[-1]
-                drafts.append(int(np.argmax(lg)))
-            tl = tgt.forward([toks[s][n - 1]] + drafts, list(range(n - 1, n + k)), tcache[s])
-            tt = np.argmax(tl, -1)
+                    lg = model_ref.forward_batch(drf, [[d[-1]] for d in drafts], [[n - 2 + j] for n in ns],
+                                                 dcache)[:, -1]
+                for s in range(b):
+                    drafts[s].append(int(np.argmax(lg[s])))
+        tl = model_ref.forward_batch(tgt, [[t[n - 1]] + d for t, n, d in zip(toks, ns, drafts)],
+                                     [list(range(n - 1, n + k)) for n in ns], tcache)
+        for s in range(b):
             l = int(l_inj[s])
-            new = drafts[:l] + [int(tt[l])]
+            new = drafts[s][:l] + [int(np.argmax(tl[s, l]))]
             toks[s].extend(new)
             gen += len(new)
     dt = time.perf_counter() - t0
-    scale = tc.n_layers / L
-    # layers beyond the sample are charged at the measured per-layer rate
-    tps = gen / (dt * scale) if scale != 1 else gen / dt
-    desc = (f"{iters} speculative iterations (b={b}, k={k}, injected example_trace acceptance) of the fp32 CPU "
-            f"oracle pair {TARGET}+{DRAFT}" + (f", {L}/{tc.n_layers} target layers timed and scaled" if scale != 1
-                                              else "") + f"; init {t_init:.1f}s untimed")
-    return tps, desc, threads
+    desc = (f"{iters} speculative iteration(s) (b={b}, k={k}, injected example_trace acceptance, prompt {P}) of the "
+            f"fp32 CPU oracle pair {TARGET}+{DRAFT} batched over sequences ({L}/{tc.n_layers} target layers"
+            f"{'' if L == tc.n_layers else ', time scaled by layer count'}); weight init + prefill {t_init:.1f}s untimed")
+    if L != tc.n_layers:
+        dt *= tc.n_layers / L
+    return gen / dt, desc, threads
 
 
 def run_reference(args):
@@ -184,12 +195,9 @@ def run_reference(args):
     if rank != 0:
         return
     k = args.k if args.k >= 0 else 3
-    layers = int(os.environ.get("SB_CPU_LAYERS", "4"))
-    vals = []
-    for _ in range(max(1, args.steps)):
-        tps, desc, cores = cpu_sample(args.batch, k, iters=1, layers=layers)
-        vals.append(tps)
-    v = float(np.median(vals))
+    layers = int(os.environ.get("SB_CPU_LAYERS", "8")) or None
+    tps, desc, cores = cpu_sample(args.batch, k, iters=max(1, min(args.steps, 3)), layers=layers)
+    v = float(tps)
     line = {"metric": "generated tokens/s (batched speculative decoding)", "value": v, "unit": "tokens/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
             "impl": "reference", "dtype": "f32", "data": "synthetic",
@@ -290,7 +298,7 @@ def run_ours(args):
     cpu = None
     if rank == 0 and world == 1 and os.environ.get("SB_SKIP_CPU", "0") != "1":
         try:
-            layers = int(os.environ.get("SB_CPU_LAYERS", "4"))
+            layers = int(os.environ.get("SB_CPU_LAYERS", "8")) or None
             tps, desc, cores = cpu_sample(b, k, iters=1, layers=layers)
             cpu = {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": desc}
         except Exception as exc:  # pragma: no cover

@@ -209,3 +209,45 @@ def spec_generate(target: LlamaRef, draft: LlamaRef, prompts, target_lens, k: in
                 produced[s] += adv[s]
         it += 1
     return [t[P:] for t in toks], log
+
+
+@torch.no_grad()
+def forward_batch(model: LlamaRef, ids, pos, caches):
+    """Batched CPU forward (CPU-baseline timing): b sequences x q tokens share
+    every weight read (one matmul per projection over all b*q rows); attention
+    and KV caches stay per sequence.  Same math as LlamaRef.forward."""
+    b = len(ids)
+    q = len(ids[0])
+    flat = torch.as_tensor([t for row in ids for t in row], dtype=torch.long)
+    pos_t = [torch.as_tensor(p, dtype=torch.long) for p in pos]
+    x = model.emb[flat].clone()
+    T = b * q
+    scale = 1.0 / math.sqrt(model.hd)
+    for li, lay in enumerate(model.layers):
+        xn = model._norm(x)
+        Q = model._r(xn @ lay["wq"].T).view(b, q, model.nq, model.hd)
+        K = model._r(xn @ lay["wk"].T).view(b, q, model.nkv, model.hd)
+        Vv = model._r(xn @ lay["wv"].T).view(b, q, model.nkv, model.hd)
+        outs = []
+        for s in range(b):
+            c = caches[s][li]
+            qs = model._rope(Q[s], pos_t[s])
+            ks = model._rope(K[s], pos_t[s])
+            p0 = int(pos[s][0])
+            keep_k = c["k"][:p0] if c["k"] is not None else ks[:0]
+            keep_v = c["v"][:p0] if c["v"] is not None else Vv[s][:0]
+            c["k"] = torch.cat([keep_k, ks], 0)
+            c["v"] = torch.cat([keep_v, Vv[s]], 0)
+            rep = model.nq // model.nkv
+            Kh = c["k"].repeat_interleave(rep, dim=1)
+            Vh = c["v"].repeat_interleave(rep, dim=1)
+            att = torch.einsum("tnd,snd->nts", qs * scale, Kh)
+            mask = torch.arange(Kh.shape[0])[None, :] > pos_t[s][:, None]
+            att = torch.softmax(att.masked_fill(mask[None], float("-inf")), -1)
+            outs.append(torch.einsum("nts,snd->tnd", att, Vh).reshape(q, model.nq * model.hd))
+        o = model._r(torch.cat(outs, 0))
+        x = x + o @ lay["wo"].T
+        xn = model._norm(x)
+        a = model._r(torch.nn.functional.silu(xn @ lay["wg"].T) * (xn @ lay["wu"].T))
+        x = x + a @ lay["wd"].T
+    return (model._norm(x) @ model.head.T).view(b, q, -1).numpy()
