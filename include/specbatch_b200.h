@@ -115,6 +115,27 @@ int sb_decoder_forward(const sb_decoder_t* m, const sb_kvcache_t* kv, const int3
                        void* stream);
 
 /*
+ * Greedy token sink: when passed to sb_decoder_forward_ex, the argmax of every
+ * logits row (ties -> lowest index) is computed inside the lm_head GEMM
+ * epilogue (per-128-row partials + one-warp finalize) and written to
+ * out_tok[r*out_stride], next_ids[r], next_pos[r] = base_pos[r] + pos_offset
+ * (each pointer optional).  logits may then be NULL (not materialised).
+ */
+typedef struct sb_token_sink {
+  int32_t* out_tok;
+  int32_t out_stride;
+  int32_t* next_ids;
+  int32_t* next_pos;
+  const int32_t* base_pos;
+  int32_t pos_offset;
+} sb_token_sink_t;
+
+int sb_decoder_forward_ex(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* tok_ids,
+                          const int32_t* tok_slot, const int32_t* tok_pos, int32_t n_seq, int32_t q_len,
+                          float* logits, int32_t logits_mode, const sb_token_sink_t* sink, void* workspace,
+                          size_t ws_bytes, void* stream);
+
+/*
  * Next-token selection over logits rows [rows, vocab] (fp32).
  *   ARGMAX: ties -> lowest index (np.argmax); probs_out optional.
  *   SAMPLE: probs_out[r*probs_stride + v] = softmax(logits[r]) (fp32), token =

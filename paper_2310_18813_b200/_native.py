@@ -43,6 +43,13 @@ class SbDecoder(C.Structure):
     ]
 
 
+class SbTokenSink(C.Structure):
+    """Mirror of ``sb_token_sink_t`` (greedy argmax fused into the lm_head epilogue)."""
+
+    _fields_ = [("out_tok", _P), ("out_stride", _I), ("next_ids", _P), ("next_pos", _P), ("base_pos", _P),
+                ("pos_offset", _I)]
+
+
 class SbKVCache(C.Structure):
     """Mirror of ``sb_kvcache_t``."""
 
@@ -64,6 +71,8 @@ _SIGS = {
     "sb_decoder_workspace_bytes": (C.c_size_t, [C.POINTER(SbDecoder), _I]),
     "sb_decoder_forward": (C.c_int, [C.POINTER(SbDecoder), C.POINTER(SbKVCache), _P, _P, _P, _I, _I, _P, _I, _P,
                                      C.c_size_t, _P]),
+    "sb_decoder_forward_ex": (C.c_int, [C.POINTER(SbDecoder), C.POINTER(SbKVCache), _P, _P, _P, _I, _I, _P, _I,
+                                        C.POINTER(SbTokenSink), _P, C.c_size_t, _P]),
     "sb_select_tokens": (C.c_int, [_P, _I, _I, _I, _P, _I, _P, C.c_int64, _P, _I, _P, _P, _P, _I, _P]),
     "sb_softmax_rows": (C.c_int, [_P, _I, _I, _P, _P]),
     "sb_argmax_rows": (C.c_int, [_P, _I, _I, _P, _P]),

@@ -23,6 +23,8 @@ struct FwdWorkspace {
   void* attn;
   void* act;
   void* last;
+  float* amax_val;
+  int* amax_idx;
   void* gemm_ws;
   size_t gemm_ws_bytes;
 };
@@ -56,6 +58,9 @@ static size_t carve(const sb_decoder_t* m, int T, char* base, FwdWorkspace* w) {
   o->attn = take((size_t)T * qd * es);
   o->act = take((size_t)T * m->ffn * es);
   o->last = take((size_t)T * m->hidden * es);
+  const size_t vt = (size_t)((m->vocab + 127) / 128) * T;
+  o->amax_val = (float*)take(vt * 4);
+  o->amax_idx = (int*)take(vt * 4);
   return off;
 }
 
@@ -81,8 +86,8 @@ static void prof_mark(const char* tag, cudaStream_t st) {
 static int g_attn_impl = 0;
 
 static int forward_impl(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* ids, const int32_t* slot,
-                        const int32_t* pos, int n_seq, int q_len, float* logits, int logits_mode, void* ws,
-                        size_t ws_bytes, cudaStream_t st) {
+                        const int32_t* pos, int n_seq, int q_len, float* logits, int logits_mode,
+                        const sb_token_sink_t* sink, void* ws, size_t ws_bytes, cudaStream_t st) {
   const int T = n_seq * q_len;
   if (T <= 0 || !m || !kv) return SB_EINVAL;
   if ((m->head_dim != 128 && m->head_dim != 64) || m->n_heads % m->n_kv_heads) return SB_EUNSUPPORTED;
@@ -135,9 +140,32 @@ static int forward_impl(const sb_decoder_t* m, const sb_kvcache_t* kv, const int
   int off = logits_mode == SB_LOGITS_LAST ? q_len - 1 : 0;
   SB_TRY(launch_rmsnorm(dt, w.resid, m->final_norm, w.last, rows, H, m->rms_eps, step, off, st));
   prof_mark("norm_f", st);
-  GemmArgs g{dt, w.last, m->lm_head, logits, rows, m->vocab, H, H, EPI_STORE_F32, w.gemm_ws, w.gemm_ws_bytes};
+  if (sink == nullptr) {
+    if (!logits) return SB_EINVAL;
+    GemmArgs g{dt, w.last, m->lm_head, logits, rows, m->vocab, H, H, EPI_STORE_F32, w.gemm_ws, w.gemm_ws_bytes};
+    SB_TRY(gemm(g, GEMM_AUTO, st));
+    prof_mark("lm_head", st);
+    return 0;
+  }
+  // greedy token selection fused into the lm_head epilogue (bf16 / tcgen05); logits optional
+  GemmArgs g{dt, w.last, m->lm_head, logits, rows, m->vocab, H, H, EPI_ARGMAX, w.gemm_ws, w.gemm_ws_bytes,
+             w.amax_val, w.amax_idx};
+  int rc = (g_backend_override != GEMM_SIMT && dt == SB_BF16 && gemm_tc_supported(g)) ? gemm_tc(g, st) : SB_EUNSUPPORTED;
+  if (rc == 0) {
+    prof_mark("lm_head", st);
+    SB_TRY(launch_argmax_partials(w.amax_val, w.amax_idx, (m->vocab + 127) / 128, rows, sink->out_tok,
+                                  sink->out_stride, sink->next_ids, sink->next_pos, sink->base_pos, sink->pos_offset, st));
+    prof_mark("argmax", st);
+    return 0;
+  }
+  if (rc != SB_EUNSUPPORTED) return rc;
+  if (!logits) return SB_EINVAL;  // fp32 / SIMT path needs the logits buffer
+  g.epi = EPI_STORE_F32;
   SB_TRY(gemm(g, GEMM_AUTO, st));
   prof_mark("lm_head", st);
+  SB_TRY(launch_select_argmax(logits, rows, m->vocab, sink->out_tok, sink->out_stride, sink->next_ids,
+                              sink->next_pos, sink->base_pos, sink->pos_offset, st));
+  prof_mark("argmax", st);
   return 0;
 }
 
@@ -156,8 +184,19 @@ int sb_decoder_forward(const sb_decoder_t* m, const sb_kvcache_t* kv, const int3
                        const int32_t* tok_pos, int32_t n_seq, int32_t q_len, float* logits, int32_t logits_mode,
                        void* workspace, size_t ws_bytes, void* stream) {
   g_kernel_count = 0;
-  int rc = forward_impl(m, kv, tok_ids, tok_slot, tok_pos, n_seq, q_len, logits, logits_mode, workspace, ws_bytes,
-                        (cudaStream_t)stream);
+  int rc = forward_impl(m, kv, tok_ids, tok_slot, tok_pos, n_seq, q_len, logits, logits_mode, nullptr, workspace,
+                        ws_bytes, (cudaStream_t)stream);
+  g_last_count = g_kernel_count;
+  return rc;
+}
+
+int sb_decoder_forward_ex(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* tok_ids, const int32_t* tok_slot,
+                          const int32_t* tok_pos, int32_t n_seq, int32_t q_len, float* logits, int32_t logits_mode,
+                          const sb_token_sink_t* sink, void* workspace, size_t ws_bytes, void* stream) {
+  g_kernel_count = 0;
+  if (sink && logits_mode == SB_LOGITS_NONE) return SB_EINVAL;
+  int rc = forward_impl(m, kv, tok_ids, tok_slot, tok_pos, n_seq, q_len, logits, logits_mode, sink, workspace,
+                        ws_bytes, (cudaStream_t)stream);
   g_last_count = g_kernel_count;
   return rc;
 }
@@ -166,6 +205,7 @@ int sb_gemm(int32_t dtype, const void* x, const void* w, void* y, int32_t M, int
             int32_t backend, void* workspace, size_t ws_bytes, void* stream) {
   if (epi < 0 || epi > 3) return SB_EINVAL;
   GemmArgs g{dtype, x, w, y, M, N, K, K, epi, workspace, ws_bytes};
+  if (epi == EPI_ARGMAX) return SB_EINVAL;  // use sb_decoder_forward_ex's token sink
   return gemm(g, backend, (cudaStream_t)stream);
 }
 
@@ -198,8 +238,8 @@ int sb_profile_forward(const sb_decoder_t* m, const sb_kvcache_t* kv, const int3
                        void* workspace, size_t ws_bytes, void* stream, char* buf, int32_t buf_len) {
   g_prof = true;
   g_prof_n = 0;
-  int rc = forward_impl(m, kv, tok_ids, tok_slot, tok_pos, n_seq, q_len, logits, logits_mode, workspace, ws_bytes,
-                        (cudaStream_t)stream);
+  int rc = forward_impl(m, kv, tok_ids, tok_slot, tok_pos, n_seq, q_len, logits, logits_mode, nullptr, workspace,
+                        ws_bytes, (cudaStream_t)stream);
   g_prof = false;
   if (rc) return rc;
   cudaStreamSynchronize((cudaStream_t)stream);

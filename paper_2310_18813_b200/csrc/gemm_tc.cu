@@ -23,6 +23,7 @@
 // ring; tcgen05.commit releases a stage back to the producer.
 #include <cuda.h>
 
+#include <climits>
 #include <cstdio>
 #include <mutex>
 
@@ -118,6 +119,8 @@ struct TcParams {
   int stages;
   int epi;
   void* y;
+  float* aux_val;  // EPI_ARGMAX partials [n_tiles_n][M]
+  int* aux_idx;
 };
 
 __device__ __forceinline__ float silu_f(float g) { return g / (1.f + __expf(-g)); }
@@ -273,6 +276,21 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       if (p.splits > 1) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) red[(j0 + j) * TC_BM + row] = v[j];
+      } else if (p.epi == EPI_ARGMAX) {
+        // per token: warp argmax over its 32 rows (ties -> lowest row), staged per quadrant
+        float* qv = red;                                  // [4][tn] values
+        int* qi = reinterpret_cast<int*>(red + 4 * tn);   // [4][tn] indices
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int m = m0 + j0 + j, n = n0 + row;
+          float val = (n < p.N) ? v[j] : -INFINITY;
+          if (p.y && m < p.M && n < p.N) ((float*)p.y)[(size_t)m * p.N + n] = v[j];
+          ArgMax a = warp_argmax(ArgMax{val, n < p.N ? n : INT_MAX});
+          if (lane == 0) {
+            qv[quad * tn + j0 + j] = a.v;
+            qi[quad * tn + j0 + j] = a.i;
+          }
+        }
       } else if (p.epi == EPI_SILU_MUL) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
@@ -282,6 +300,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       } else {
 #pragma unroll
         for (int j = 0; j < 16; ++j) epi_one(p, m0 + j0 + j, n0 + row, v[j]);
+      }
+    }
+    if (p.epi == EPI_ARGMAX) {
+      asm volatile("bar.sync 1, 128;" ::: "memory");
+      const int et = threadIdx.x - 64;
+      const float* qv = red;
+      const int* qi = reinterpret_cast<const int*>(red + 4 * tn);
+      for (int j = et; j < tn; j += 128) {
+        ArgMax a{qv[j], qi[j]};
+#pragma unroll
+        for (int q = 1; q < 4; ++q) a = argmax_merge(a, ArgMax{qv[q * tn + j], qi[q * tn + j]});
+        const int m = m0 + j;
+        if (m < p.M) {
+          p.aux_val[(size_t)tile_n * p.M + m] = a.v;
+          p.aux_idx[(size_t)tile_n * p.M + m] = a.i;
+        }
       }
     }
     tc_fence_before();
@@ -386,7 +420,7 @@ struct TcPlan {
 // Split-K policy for the HBM-bound regime: enough CTAs that every SM streams
 // weights (>= one per SM), at most one resident wave, >= 2 k-blocks per CTA,
 // cluster size <= 8 (portable).
-static TcPlan plan(int M, int N, int K) {
+static TcPlan plan(int M, int N, int K, int epi) {
   TcPlan q;
   q.tn = tn_for(M);
   q.n_tiles_n = (N + TC_BM - 1) / TC_BM;
@@ -400,6 +434,7 @@ static TcPlan plan(int M, int N, int K) {
   while (q.splits < 8 && tiles * q.splits < sms && tiles * q.splits * 2 <= slots && q.kb / (q.splits * 2) >= 2)
     q.splits *= 2;
   if (g_tune_splits) q.splits = g_tune_splits;
+  if (epi == EPI_ARGMAX) q.splits = 1;  // the fused argmax reads whole tiles straight from TMEM
   size_t budget = q.ctas_per_sm == 2 ? 108 * 1024 : 200 * 1024;
   size_t stage = (size_t)(TC_BM + q.tn) * TC_BK * 2;
   q.stages = (int)((budget - 1024 - 256) / stage);
@@ -443,7 +478,7 @@ int gemm_tc(const GemmArgs& a, cudaStream_t st) {
   if (!gemm_tc_supported(a)) return SB_EUNSUPPORTED;
   if (a.M <= 0 || a.N <= 0 || a.K <= 0) return SB_EINVAL;
   SB_TRY(gemm_tc_init());
-  TcPlan q = plan(a.M, a.N, a.K);
+  TcPlan q = plan(a.M, a.N, a.K, a.epi);
   CUtensorMap mw, mx;
   SB_TRY(make_map(&mw, a.w, a.N, a.K, a.K, TC_BM));
   SB_TRY(make_map(&mx, a.x, a.M, a.K, a.ldx, q.tn));
@@ -458,6 +493,9 @@ int gemm_tc(const GemmArgs& a, cudaStream_t st) {
   p.stages = q.stages;
   p.epi = a.epi;
   p.y = a.y;
+  p.aux_val = a.aux_val;
+  p.aux_idx = a.aux_idx;
+  if (a.epi == EPI_ARGMAX && (!a.aux_val || !a.aux_idx)) return SB_EINVAL;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(q.n_tiles_n * q.splits, q.m_tiles, 1);
   cfg.blockDim = dim3(TC_THREADS, 1, 1);

@@ -11,6 +11,7 @@ enum GemmEpi : int {
   EPI_STORE_F32 = 1,  // y fp32 [M, N]
   EPI_RESID_ADD = 2,  // resid fp32 [M, N] += acc
   EPI_SILU_MUL = 3,   // rows interleaved (gate, up): y (dtype) [M, N/2] = silu(g) * u
+  EPI_ARGMAX = 4,     // optional fp32 y [M, N] + per-128-row-tile argmax partials (aux_val/aux_idx [N/128][M])
 };
 
 enum GemmBackend : int { GEMM_AUTO = 0, GEMM_SIMT = 1, GEMM_TC = 2 };
@@ -24,6 +25,8 @@ struct GemmArgs {
   int epi;
   void* workspace;  // split-K partials / tile counters
   size_t ws_bytes;
+  float* aux_val = nullptr;  // EPI_ARGMAX partials
+  int* aux_idx = nullptr;
 };
 
 extern int g_backend_override;  // sb_set_gemm_backend (ablation / tests)
@@ -48,6 +51,11 @@ int launch_attention(int dtype, const void* q, const void* kc, const void* vc, v
 int launch_attention_tc(const void* qkv, void* kc, void* vc, void* out, const int32_t* tok_slot, const int32_t* tok_pos,
                         const float* cosT, const float* sinT, int n_seq, int q_len, int nq, int nkv, int hd,
                         int ctx_max, int max_pos, cudaStream_t st);
+int launch_argmax_partials(const float* val, const int* idx, int n_tiles, int rows, int32_t* out_tok, int out_stride,
+                           int32_t* next_ids, int32_t* next_pos, const int32_t* base_pos, int pos_offset,
+                           cudaStream_t st);
+int launch_select_argmax(const float* logits, int rows, int vocab, int32_t* out_tok, int out_stride, int32_t* next_ids,
+                         int32_t* next_pos, const int32_t* base_pos, int pos_offset, cudaStream_t st);
 int launch_kv_compact(int dtype, void* k, void* v, const int32_t* src, const int32_t* dst, const int32_t* len, int n,
                       int layers, int slots, int nkv, int ctx_max, int hd, cudaStream_t st);
 

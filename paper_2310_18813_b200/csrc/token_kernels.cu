@@ -17,6 +17,7 @@
 #include <climits>
 
 #include "common.cuh"
+#include "kernels.cuh"
 
 namespace sb {
 
@@ -181,6 +182,40 @@ __global__ void select_kernel(const float* logits, int V, int mode, const float*
     if (next_ids) next_ids[r] = tok;
     if (next_pos) next_pos[r] = base_pos[r] + pos_offset;
   }
+}
+
+// Finalize of the lm_head-fused argmax: one warp per row merges the per-tile
+// (value, index) partials (ties -> lowest index, identical to a full argmax).
+__global__ void argmax_partials_kernel(const float* __restrict__ val, const int* __restrict__ idx, int n_tiles, int rows,
+                                       int32_t* out_tok, int out_stride, int32_t* next_ids, int32_t* next_pos,
+                                       const int32_t* base_pos, int pos_offset) {
+  griddep_wait();
+  griddep_launch();
+  const int r = blockIdx.x, lane = threadIdx.x;
+  ArgMax a{-INFINITY, INT_MAX};
+  for (int t = lane; t < n_tiles; t += 32) a = argmax_merge(a, ArgMax{val[(size_t)t * rows + r], idx[(size_t)t * rows + r]});
+  a = warp_argmax(a);
+  if (lane == 0) {
+    if (out_tok) out_tok[(size_t)r * out_stride] = a.i;
+    if (next_ids) next_ids[r] = a.i;
+    if (next_pos) next_pos[r] = base_pos[r] + pos_offset;
+  }
+}
+
+int launch_argmax_partials(const float* val, const int* idx, int n_tiles, int rows, int32_t* out_tok, int out_stride,
+                           int32_t* next_ids, int32_t* next_pos, const int32_t* base_pos, int pos_offset,
+                           cudaStream_t st) {
+  if (rows <= 0) return 0;
+  return launch_k(argmax_partials_kernel, dim3(rows), dim3(32), 0, st, val, idx, n_tiles, rows, out_tok, out_stride,
+                  next_ids, next_pos, base_pos, pos_offset);
+}
+
+int launch_select_argmax(const float* logits, int rows, int vocab, int32_t* out_tok, int out_stride, int32_t* next_ids,
+                         int32_t* next_pos, const int32_t* base_pos, int pos_offset, cudaStream_t st) {
+  if (rows <= 0) return 0;
+  return launch_k(select_kernel, dim3(rows), dim3(256), 0, st, logits, vocab, (int)SB_SELECT_ARGMAX,
+                  (const float*)nullptr, 0, (float*)nullptr, 0LL, out_tok, out_stride, next_ids, next_pos, base_pos,
+                  pos_offset);
 }
 
 // ------------------------------------------------------------------ accept (K4)

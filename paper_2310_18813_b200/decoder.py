@@ -202,6 +202,15 @@ class Decoder:
         N.call("sb_decoder_forward", C.byref(self.struct), C.byref(kv.struct), N.ptr(ids), N.ptr(slots),
                N.ptr(pos), n_seq, q_len, N.ptr(logits), logits_mode, N.ptr(workspace), workspace.numel(), st)
 
+    def forward_greedy(self, kv: "KVCache", ids, slots, pos, n_seq: int, q_len: int, logits, logits_mode: int,
+                       workspace, sink: "N.SbTokenSink", stream=None):
+        """Forward whose lm_head epilogue emits the greedy token of every row into
+        ``sink`` (logits may be None on the bf16 / tcgen05 path)."""
+        st = torch.cuda.current_stream(self.device).cuda_stream if stream is None else stream
+        N.call("sb_decoder_forward_ex", C.byref(self.struct), C.byref(kv.struct), N.ptr(ids), N.ptr(slots),
+               N.ptr(pos), n_seq, q_len, N.ptr(logits), logits_mode, C.byref(sink), N.ptr(workspace),
+               workspace.numel(), st)
+
     def weight_bytes(self) -> int:
         return self.cfg.streamed_bytes_per_forward(2 if self.dtype_name == "bf16" else 4)
 

@@ -132,6 +132,7 @@ class SpecEngine:
         self.stream = torch.cuda.Stream(device=self.dev)
         self.graphs: dict[tuple[int, int], torch.cuda.CUDAGraph] = {}
         self._iter_kernels: dict[tuple[int, int], int] = {}
+        self._sinks: list = []  # keep ctypes sink structs alive while graphs reference their contents
         self.stats = IterationStats()
 
     # ------------------------------------------------------------- prompts
@@ -143,7 +144,7 @@ class SpecEngine:
     def _iteration(self, b: int, k: int) -> None:
         st = torch.cuda.current_stream(self.dev).cuda_stream
         lib = N.load()
-        launches = 4  # prepare, argmax|softmax, accept, commit
+        launches = 3  # prepare, accept, commit (+ softmax in stochastic mode)
         V = self.V
         mode = self.mode_id
         sample = mode == N.ACCEPT_STOCHASTIC
@@ -153,6 +154,8 @@ class SpecEngine:
                N.ptr(self.v_ids), N.ptr(self.v_pos), N.ptr(self.d_base), self.seed, N.ptr(self.iter),
                N.ptr(self.uniforms), _NU, N.ptr(self.inj_samples), self.inj_samples.numel(),
                N.ptr(self.l_inj), st)
+        greedy_draft = not sample
+        need_logits = self.target.sb_dtype != N.SB_BF16  # the fp32 path selects from materialised logits
         if use_draft:
             sel = N.SELECT_SAMPLE if sample else N.SELECT_ARGMAX
             u_base = self.uniforms.data_ptr()
@@ -161,24 +164,37 @@ class SpecEngine:
                     ids, pos, q = self.d1_ids, self.d1_pos, 2
                 else:
                     ids, pos, q = self.ds_ids, self.ds_pos, 1
+                if greedy_draft:
+                    sink = N.SbTokenSink(self.v_ids.data_ptr() + j * 4, k + 1, self.ds_ids.data_ptr(),
+                                         self.ds_pos.data_ptr(), self.d_base.data_ptr(), j)
+                    self._sinks.append(sink)
+                    self.draft.forward_greedy(self.kv_d, ids, self.slots, pos, b, q,
+                                              self.d_logits if need_logits else None, N.LOGITS_LAST,
+                                              self.workspace, sink, st)
+                    launches += lib.sb_last_kernel_count()
+                    continue
                 self.draft.forward(self.kv_d, ids, self.slots, pos, b, q, self.d_logits, N.LOGITS_LAST,
                                    self.workspace, st)
                 launches += lib.sb_last_kernel_count() + 1
-                probs = None
-                if sample:
-                    probs = self.q_probs.data_ptr() + (j - 1) * V * 4
+                probs = self.q_probs.data_ptr() + (j - 1) * V * 4
                 N.call("sb_select_tokens", N.ptr(self.d_logits), b, V, sel, u_base + (j - 1) * 4, _NU,
                        probs, k * V, self.v_ids.data_ptr() + j * 4, k + 1, N.ptr(self.ds_ids),
                        N.ptr(self.ds_pos), N.ptr(self.d_base), j, st)
         T = b * (k + 1)
-        self.target.forward(self.kv_t, self.v_ids, self.slots, self.v_pos, b, k + 1, self.t_logits, N.LOGITS_ALL,
-                            self.workspace, st)
-        launches += lib.sb_last_kernel_count()
-        self._iter_kernels[(b, k)] = launches
         if sample:
+            self.target.forward(self.kv_t, self.v_ids, self.slots, self.v_pos, b, k + 1, self.t_logits,
+                                N.LOGITS_ALL, self.workspace, st)
+            launches += lib.sb_last_kernel_count()
             N.call("sb_softmax_rows", N.ptr(self.t_logits), T, V, N.ptr(self.t_logits), st)
+            launches += 1
         else:
-            N.call("sb_argmax_rows", N.ptr(self.t_logits), T, V, N.ptr(self.t_tok), st)
+            sink = N.SbTokenSink(self.t_tok.data_ptr(), 1, None, None, None, 0)
+            self._sinks.append(sink)
+            self.target.forward_greedy(self.kv_t, self.v_ids, self.slots, self.v_pos, b, k + 1,
+                                       self.t_logits if need_logits else None, N.LOGITS_ALL, self.workspace, sink,
+                                       st)
+            launches += lib.sb_last_kernel_count()
+        self._iter_kernels[(b, k)] = launches
         u_base = self.uniforms.data_ptr()
         N.call("sb_accept", mode, b, k, V, N.ptr(self.t_tok), N.ptr(self.t_logits),
                N.ptr(self.q_probs) if sample and k > 0 else None, self.v_ids.data_ptr() + 4, k + 1,
@@ -371,12 +387,13 @@ def time_draft_step(self, b: int, ctx: int = 192, reps: int = 20) -> float:
         return 0.0
     _stage_context(self, b, 1, ctx)
 
+    sink = N.SbTokenSink(None, 0, self.ds_ids.data_ptr(), None, None, 0)
+    need_logits = self.draft.sb_dtype != N.SB_BF16
+
     def fn():
         st = torch.cuda.current_stream(self.dev).cuda_stream
-        self.draft.forward(self.kv_d, self.ds_ids, self.slots, self.ds_pos, b, 1, self.d_logits, N.LOGITS_LAST,
-                           self.workspace, st)
-        N.call("sb_select_tokens", N.ptr(self.d_logits), b, self.V, N.SELECT_ARGMAX, None, _NU, None, 0, None, 0,
-               N.ptr(self.ds_ids), None, None, 0, st)
+        self.draft.forward_greedy(self.kv_d, self.ds_ids, self.slots, self.ds_pos, b, 1,
+                                  self.d_logits if need_logits else None, N.LOGITS_LAST, self.workspace, sink, st)
 
     return _timed_graph(fn, reps, self.stream)
 

@@ -293,3 +293,32 @@ def test_gemm_sequence_shares_workspace(cuda_dev):
         ref = x.float() @ w.float().T
         torch.cuda.synchronize()
         assert (y - ref).abs().max().item() <= 1e-4 * ref.abs().max().item() + 1e-5, (M, N_, K)
+
+
+@pytest.mark.parametrize("M", [1, 8, 32, 72])
+def test_fused_lm_head_argmax_matches_full_argmax(cuda_dev, M):
+    """The greedy token sink (argmax in the lm_head tcgen05 epilogue) equals a
+    full argmax over the logits the same GEMM produces, ties -> lowest index."""
+    from paper_2310_18813_b200.decoder import CONFIGS, Decoder
+    import ctypes as C
+
+    tgt = Decoder(CONFIGS["tiny-target"], dtype="bf16", device=cuda_dev, seed=5, init="host", max_pos=256)
+    kv = tgt.new_kv(M, 64)
+    ws = torch.zeros(tgt.workspace_bytes(M), device=cuda_dev, dtype=torch.uint8)
+    ids = torch.randint(0, 32000, (M,), device=cuda_dev, dtype=torch.int32)
+    slots = torch.arange(M, dtype=torch.int32, device=cuda_dev)
+    pos = torch.zeros(M, dtype=torch.int32, device=cuda_dev)
+    logits = torch.zeros(M, 32000, device=cuda_dev)
+    tgt.forward(kv, ids, slots, pos, M, 1, logits, N.LOGITS_ALL, ws)
+    tok = torch.full((M,), -1, dtype=torch.int32, device=cuda_dev)
+    logits2 = torch.zeros_like(logits)
+    sink = N.SbTokenSink(tok.data_ptr(), 1, None, None, None, 0)
+    tgt.forward_greedy(kv, ids, slots, pos, M, 1, logits2, N.LOGITS_ALL, ws, sink)
+    torch.cuda.synchronize()
+    assert torch.equal(logits, logits2)
+    assert np.array_equal(tok.cpu().numpy(), spec_ref.argmax_rows(logits.cpu().numpy()))
+    tok2 = torch.full((M,), -1, dtype=torch.int32, device=cuda_dev)
+    sink2 = N.SbTokenSink(tok2.data_ptr(), 1, None, None, None, 0)
+    tgt.forward_greedy(kv, ids, slots, pos, M, 1, None, N.LOGITS_ALL, ws, sink2)  # logits not materialised
+    torch.cuda.synchronize()
+    assert torch.equal(tok, tok2)
