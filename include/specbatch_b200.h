@@ -234,6 +234,8 @@ int sb_init(void);
 int sb_set_gemm_backend(int32_t backend);
 /* Programmatic dependent launch for every kernel (default on); 0 disables (ablation). */
 int sb_set_pdl(int32_t enabled);
+/* RMSNorm fused into the GEMM epilogues on the bf16 path (default on); 0 = separate norm kernels. */
+int sb_set_fuse_norm(int32_t enabled);
 /* Diagnostics: eager forward with an event after every kernel; per-stage summed ms as "tag=ms;..." in buf. */
 int sb_profile_forward(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* tok_ids,
                        const int32_t* tok_slot, const int32_t* tok_pos, int32_t n_seq, int32_t q_len,

@@ -56,8 +56,12 @@ class LlamaRef:
     """Llama-style decoder on the CPU with a per-sequence KV cache.
 
     dtype: torch.float32 or torch.float64 compute.  bf16_emulation rounds
-    to bf16 where the GPU rounds (norm outputs, qkv, rotated q/k, attention
-    output, silu*up, final norm); the residual stream stays in `dtype`.
+    to bf16 where the GPU rounds (GEMM inputs, qkv, rotated q/k, attention
+    output, silu*up); the residual stream stays in `dtype`.  With
+    bf16_emulation the RMSNorm follows the GPU's fused contract: the GEMM
+    input is the bf16-rounded RAW residual and 1/rms scales the GEMM output
+    (norm gains are 1 / folded into the weights); in fp32/fp64 the two
+    orders are the same math.
     """
 
     def __init__(self, masters: dict, n_heads: int, n_kv_heads: int, eps: float, max_pos: int = 4096,
@@ -82,6 +86,13 @@ class LlamaRef:
         ms = (x.float() * x.float()).mean(-1, keepdim=True) if self.dt == torch.float32 else (x * x).mean(-1, keepdim=True)
         return self._r(x * torch.rsqrt(ms.to(self.dt) + self.eps))
 
+    def _nm(self, x, W):
+        """rmsnorm(x) @ W^T under the numerics contract."""
+        if self.bf16:
+            inv = torch.rsqrt((x * x).mean(-1, keepdim=True) + self.eps)
+            return (self._r(x) @ W.T) * inv
+        return self._norm(x) @ W.T
+
     def _rope(self, x, pos):  # x [T, heads, hd]
         half = self.hd // 2
         c = self.cos[pos][:, None, :]
@@ -104,10 +115,9 @@ class LlamaRef:
         scale = 1.0 / math.sqrt(self.hd)
         p0 = int(pos[0])
         for lay, c in zip(self.layers, cache):
-            xn = self._norm(x)
-            q = self._r(xn @ lay["wq"].T).view(T, self.nq, self.hd)
-            kk = self._r(xn @ lay["wk"].T).view(T, self.nkv, self.hd)
-            vv = self._r(xn @ lay["wv"].T).view(T, self.nkv, self.hd)
+            q = self._r(self._nm(x, lay["wq"])).view(T, self.nq, self.hd)
+            kk = self._r(self._nm(x, lay["wk"])).view(T, self.nkv, self.hd)
+            vv = self._r(self._nm(x, lay["wv"])).view(T, self.nkv, self.hd)
             q = self._rope(q, pos_t)
             kk = self._rope(kk, pos_t)
             keep_k = c["k"][:p0] if c["k"] is not None else kk[:0]
@@ -126,12 +136,11 @@ class LlamaRef:
             att = torch.softmax(att, -1)
             o = self._r(torch.einsum("nts,snd->tnd", att, Vh).reshape(T, self.nq * self.hd))
             x = x + o @ lay["wo"].T
-            xn = self._norm(x)
-            g = xn @ lay["wg"].T
-            u = xn @ lay["wu"].T
+            g = self._nm(x, lay["wg"])
+            u = self._nm(x, lay["wu"])
             a = self._r(torch.nn.functional.silu(g) * u)
             x = x + a @ lay["wd"].T
-        return (self._norm(x) @ self.head.T).to(torch.float64).numpy()
+        return self._nm(x, self.head).to(torch.float64).numpy()
 
 
 def greedy_decode(model: LlamaRef, prompt, n: int):
@@ -224,10 +233,9 @@ def forward_batch(model: LlamaRef, ids, pos, caches):
     T = b * q
     scale = 1.0 / math.sqrt(model.hd)
     for li, lay in enumerate(model.layers):
-        xn = model._norm(x)
-        Q = model._r(xn @ lay["wq"].T).view(b, q, model.nq, model.hd)
-        K = model._r(xn @ lay["wk"].T).view(b, q, model.nkv, model.hd)
-        Vv = model._r(xn @ lay["wv"].T).view(b, q, model.nkv, model.hd)
+        Q = model._r(model._nm(x, lay["wq"])).view(b, q, model.nq, model.hd)
+        K = model._r(model._nm(x, lay["wk"])).view(b, q, model.nkv, model.hd)
+        Vv = model._r(model._nm(x, lay["wv"])).view(b, q, model.nkv, model.hd)
         outs = []
         for s in range(b):
             c = caches[s][li]
@@ -247,7 +255,6 @@ def forward_batch(model: LlamaRef, ids, pos, caches):
             outs.append(torch.einsum("nts,snd->tnd", att, Vh).reshape(q, model.nq * model.hd))
         o = model._r(torch.cat(outs, 0))
         x = x + o @ lay["wo"].T
-        xn = model._norm(x)
-        a = model._r(torch.nn.functional.silu(xn @ lay["wg"].T) * (xn @ lay["wu"].T))
+        a = model._r(torch.nn.functional.silu(model._nm(x, lay["wg"])) * model._nm(x, lay["wu"]))
         x = x + a @ lay["wd"].T
-    return (model._norm(x) @ model.head.T).view(b, q, -1).numpy()
+    return model._nm(x, model.head).view(b, q, -1).numpy()

@@ -61,6 +61,7 @@ _SIGS = {
     "sb_init": (C.c_int, []),
     "sb_set_gemm_backend": (C.c_int, [_I]),
     "sb_set_pdl": (C.c_int, [_I]),
+    "sb_set_fuse_norm": (C.c_int, [_I]),
     "sb_set_attention_impl": (C.c_int, [_I]),
     "sb_gemm_tune": (C.c_int, [_I, _I, _I]),
     "sb_profile_forward": (C.c_int, [C.POINTER(SbDecoder), C.POINTER(SbKVCache), _P, _P, _P, _I, _I, _P, _I, _P,

@@ -25,6 +25,8 @@ struct FwdWorkspace {
   void* last;
   float* amax_val;
   int* amax_idx;
+  void* xb;       // bf16 copy of the residual (fused-RMSNorm GEMM input)
+  float* npart;   // sum-of-squares partials [P_max][T]
   void* gemm_ws;
   size_t gemm_ws_bytes;
 };
@@ -61,6 +63,8 @@ static size_t carve(const sb_decoder_t* m, int T, char* base, FwdWorkspace* w) {
   const size_t vt = (size_t)((m->vocab + 127) / 128) * T;
   o->amax_val = (float*)take(vt * 4);
   o->amax_idx = (int*)take(vt * 4);
+  o->xb = take((size_t)T * m->hidden * 2);
+  o->npart = (float*)take((size_t)((m->hidden + 127) / 128) * 8 * T * 4);
   return off;
 }
 
@@ -85,6 +89,119 @@ static void prof_mark(const char* tag, cudaStream_t st) {
 // 1: always separate rope/append + attention kernels (sb_set_attention_impl)
 static int g_attn_impl = 0;
 
+static int g_fuse_norm = 1;  // RMSNorm fused into the GEMMs (bf16 / tcgen05 path), sb_set_fuse_norm
+
+// lm_head + optional greedy sink; g already carries X (and fused-norm scaling)
+static int lm_head(const sb_decoder_t* m, GemmArgs g, float* logits, const sb_token_sink_t* sink,
+                   const FwdWorkspace& w, int rows, cudaStream_t st) {
+  if (sink == nullptr) {
+    if (!logits) return SB_EINVAL;
+    g.epi = EPI_STORE_F32;
+    g.y = logits;
+    SB_TRY(gemm(g, GEMM_AUTO, st));
+    prof_mark("lm_head", st);
+    return 0;
+  }
+  g.epi = EPI_ARGMAX;
+  g.y = logits;
+  g.aux_val = w.amax_val;
+  g.aux_idx = w.amax_idx;
+  int rc = (g_backend_override != GEMM_SIMT && m->dtype == SB_BF16 && gemm_tc_supported(g)) ? gemm_tc(g, st)
+                                                                                             : SB_EUNSUPPORTED;
+  if (rc == 0) {
+    prof_mark("lm_head", st);
+    SB_TRY(launch_argmax_partials(w.amax_val, w.amax_idx, (m->vocab + 127) / 128, rows, sink->out_tok,
+                                  sink->out_stride, sink->next_ids, sink->next_pos, sink->base_pos, sink->pos_offset, st));
+    prof_mark("argmax", st);
+    return 0;
+  }
+  if (rc != SB_EUNSUPPORTED) return rc;
+  if (!logits || g.ns_part) return SB_EINVAL;  // fp32 / SIMT path needs the logits buffer
+  g.epi = EPI_STORE_F32;
+  SB_TRY(gemm(g, GEMM_AUTO, st));
+  prof_mark("lm_head", st);
+  SB_TRY(launch_select_argmax(logits, rows, m->vocab, sink->out_tok, sink->out_stride, sink->next_ids,
+                              sink->next_pos, sink->base_pos, sink->pos_offset, st));
+  prof_mark("argmax", st);
+  return 0;
+}
+
+// bf16 forward with RMSNorm fused into the GEMMs: residual-producing GEMMs
+// (embedding, o_proj, down_proj) emit a bf16 copy of the new residual and
+// per-tile sum-of-squares partials; the consuming GEMMs (qkv, gate/up,
+// lm_head) read that copy and scale each token by 1/rms in their epilogue.
+// Norm gains are folded into the consumer weights by the host (ones here).
+static int forward_fused_norm(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* ids, const int32_t* slot,
+                              const int32_t* pos, int n_seq, int q_len, float* logits, int logits_mode,
+                              const sb_token_sink_t* sink, const FwdWorkspace& w, cudaStream_t st) {
+  const int T = n_seq * q_len;
+  const int nq = m->n_heads, nkv = m->n_kv_heads, hd = m->head_dim, H = m->hidden;
+  const int qkv_n = (nq + 2 * nkv) * hd;
+  const size_t layer_kv = (size_t)kv->slots * nkv * kv->ctx_max * hd * 2;
+  const float inv_h = 1.0f / (float)H;
+  SB_TRY(launch_embed_norm(m->embed, ids, pos, w.resid, w.xb, w.npart, T, H, m->vocab, st));
+  prof_mark("embed", st);
+  int P = 1;
+  for (int l = 0; l < m->n_layers; ++l) {
+    char* kc = (char*)kv->k + l * layer_kv;
+    char* vc = (char*)kv->v + l * layer_kv;
+    GemmArgs g{SB_BF16, w.xb, m->w_qkv[l], w.qkv, T, qkv_n, H, H, EPI_STORE, w.gemm_ws, w.gemm_ws_bytes};
+    g.ns_part = w.npart;
+    g.ns_P = P;
+    g.ns_stride = T;
+    g.ns_eps = m->rms_eps;
+    g.ns_inv_h = inv_h;
+    SB_TRY(gemm_tc(g, st));
+    prof_mark("qkv", st);
+    int rc_fa = g_attn_impl == 0 ? launch_attention_tc(w.qkv, kc, vc, w.attn, slot, pos, m->rope_cos, m->rope_sin,
+                                                        n_seq, q_len, nq, nkv, hd, kv->ctx_max, m->max_pos, st)
+                                  : SB_EUNSUPPORTED;
+    if (rc_fa != 0 && rc_fa != SB_EUNSUPPORTED) return rc_fa;
+    if (rc_fa == SB_EUNSUPPORTED) {
+      SB_TRY(launch_rope_append(SB_BF16, w.qkv, w.qr, kc, vc, slot, pos, m->rope_cos, m->rope_sin, T, q_len, nq, nkv,
+                                hd, kv->ctx_max, m->max_pos, st));
+      SB_TRY(launch_attention(SB_BF16, w.qr, kc, vc, w.attn, slot, pos, n_seq, q_len, nq, nkv, hd, kv->ctx_max, st));
+    }
+    prof_mark("attn", st);
+    GemmArgs o{SB_BF16, w.attn, m->w_o[l], w.resid, T, H, nq * hd, nq * hd, EPI_RESID_ADD, w.gemm_ws,
+               w.gemm_ws_bytes};
+    o.out_part = w.npart;
+    o.out_xb = w.xb;
+    SB_TRY(gemm_tc(o, st));
+    P = gemm_tc_norm_partials(o);
+    prof_mark("o", st);
+    GemmArgs gu{SB_BF16, w.xb, m->w_gu[l], w.act, T, 2 * m->ffn, H, H, EPI_SILU_MUL, w.gemm_ws, w.gemm_ws_bytes};
+    gu.ns_part = w.npart;
+    gu.ns_P = P;
+    gu.ns_stride = T;
+    gu.ns_eps = m->rms_eps;
+    gu.ns_inv_h = inv_h;
+    SB_TRY(gemm_tc(gu, st));
+    prof_mark("gu", st);
+    GemmArgs dn{SB_BF16, w.act, m->w_down[l], w.resid, T, H, m->ffn, m->ffn, EPI_RESID_ADD, w.gemm_ws,
+                w.gemm_ws_bytes};
+    dn.out_part = w.npart;
+    dn.out_xb = w.xb;
+    SB_TRY(gemm_tc(dn, st));
+    P = gemm_tc_norm_partials(dn);
+    prof_mark("down", st);
+  }
+  if (logits_mode == SB_LOGITS_NONE) return 0;
+  const bool last = logits_mode == SB_LOGITS_LAST;
+  const int rows = last ? n_seq : T;
+  const int step = last ? q_len : 1, off = last ? q_len - 1 : 0;
+  GemmArgs g{SB_BF16, (const char*)w.xb + (size_t)off * H * 2, m->lm_head, logits, rows, m->vocab, H, step * H,
+             EPI_STORE_F32, w.gemm_ws, w.gemm_ws_bytes};
+  g.ns_part = w.npart;
+  g.ns_P = P;
+  g.ns_stride = T;
+  g.ns_row_step = step;
+  g.ns_row_off = off;
+  g.ns_eps = m->rms_eps;
+  g.ns_inv_h = inv_h;
+  return lm_head(m, g, logits, sink, w, rows, st);
+}
+
 static int forward_impl(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* ids, const int32_t* slot,
                         const int32_t* pos, int n_seq, int q_len, float* logits, int logits_mode,
                         const sb_token_sink_t* sink, void* ws, size_t ws_bytes, cudaStream_t st) {
@@ -101,6 +218,8 @@ static int forward_impl(const sb_decoder_t* m, const sb_kvcache_t* kv, const int
   const size_t layer_kv = (size_t)kv->slots * nkv * kv->ctx_max * hd * es;
 
   prof_mark("start", st);
+  if (g_fuse_norm && dt == SB_BF16 && g_backend_override != GEMM_SIMT)
+    return forward_fused_norm(m, kv, ids, slot, pos, n_seq, q_len, logits, logits_mode, sink, w, st);
   SB_TRY(launch_embed(dt, m->embed, ids, pos, w.resid, T, H, m->vocab, st));
   prof_mark("embed", st);
   for (int l = 0; l < m->n_layers; ++l) {
@@ -140,33 +259,8 @@ static int forward_impl(const sb_decoder_t* m, const sb_kvcache_t* kv, const int
   int off = logits_mode == SB_LOGITS_LAST ? q_len - 1 : 0;
   SB_TRY(launch_rmsnorm(dt, w.resid, m->final_norm, w.last, rows, H, m->rms_eps, step, off, st));
   prof_mark("norm_f", st);
-  if (sink == nullptr) {
-    if (!logits) return SB_EINVAL;
-    GemmArgs g{dt, w.last, m->lm_head, logits, rows, m->vocab, H, H, EPI_STORE_F32, w.gemm_ws, w.gemm_ws_bytes};
-    SB_TRY(gemm(g, GEMM_AUTO, st));
-    prof_mark("lm_head", st);
-    return 0;
-  }
-  // greedy token selection fused into the lm_head epilogue (bf16 / tcgen05); logits optional
-  GemmArgs g{dt, w.last, m->lm_head, logits, rows, m->vocab, H, H, EPI_ARGMAX, w.gemm_ws, w.gemm_ws_bytes,
-             w.amax_val, w.amax_idx};
-  int rc = (g_backend_override != GEMM_SIMT && dt == SB_BF16 && gemm_tc_supported(g)) ? gemm_tc(g, st) : SB_EUNSUPPORTED;
-  if (rc == 0) {
-    prof_mark("lm_head", st);
-    SB_TRY(launch_argmax_partials(w.amax_val, w.amax_idx, (m->vocab + 127) / 128, rows, sink->out_tok,
-                                  sink->out_stride, sink->next_ids, sink->next_pos, sink->base_pos, sink->pos_offset, st));
-    prof_mark("argmax", st);
-    return 0;
-  }
-  if (rc != SB_EUNSUPPORTED) return rc;
-  if (!logits) return SB_EINVAL;  // fp32 / SIMT path needs the logits buffer
-  g.epi = EPI_STORE_F32;
-  SB_TRY(gemm(g, GEMM_AUTO, st));
-  prof_mark("lm_head", st);
-  SB_TRY(launch_select_argmax(logits, rows, m->vocab, sink->out_tok, sink->out_stride, sink->next_ids,
-                              sink->next_pos, sink->base_pos, sink->pos_offset, st));
-  prof_mark("argmax", st);
-  return 0;
+  GemmArgs g{dt, w.last, m->lm_head, logits, rows, m->vocab, H, H, EPI_STORE_F32, w.gemm_ws, w.gemm_ws_bytes};
+  return lm_head(m, g, logits, sink, w, rows, st);
 }
 
 }  // namespace sb
@@ -272,6 +366,11 @@ int sb_gemm_tune(int32_t ctas_per_sm, int32_t max_stages, int32_t splits) {
   if (ctas_per_sm < 0 || ctas_per_sm > 2 || max_stages < 0 || max_stages > 16 || splits < 0 || splits > 8)
     return SB_EINVAL;
   return gemm_tc_tune(ctas_per_sm, max_stages, splits);
+}
+
+int sb_set_fuse_norm(int32_t enabled) {
+  g_fuse_norm = enabled ? 1 : 0;
+  return 0;
 }
 
 int sb_set_pdl(int32_t enabled) {

@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const T* __restrict__ X,
 
 int gemm_simt(const GemmArgs& a, cudaStream_t st) {
   if (a.M <= 0 || a.N <= 0 || a.K <= 0) return SB_EINVAL;
-  if (a.epi == EPI_ARGMAX) return SB_EUNSUPPORTED;
+  if (a.epi == EPI_ARGMAX || a.ns_part || a.out_part) return SB_EUNSUPPORTED;
   if (a.epi == EPI_SILU_MUL && (a.N & 1)) return SB_EINVAL;
   dim3 grid((a.N + SBN - 1) / SBN, (a.M + SBM - 1) / SBM);
   if (a.dtype == SB_BF16)

@@ -121,6 +121,15 @@ struct TcParams {
   void* y;
   float* aux_val;  // EPI_ARGMAX partials [n_tiles_n][M]
   int* aux_idx;
+  // fused RMSNorm, consumer side: scale token m by
+  //   rsqrt(sum_p ns_part[p * ns_stride + m * ns_row_step + ns_row_off] * ns_inv_h + ns_eps)
+  const float* ns_part;
+  int ns_P, ns_stride, ns_row_step, ns_row_off;
+  float ns_eps, ns_inv_h;
+  // fused RMSNorm, producer side (EPI_RESID_ADD): xb = bf16(new residual) [M, N];
+  // out_part[(tile_n * splits + split) * M + m] = sum over this CTA's rows of new^2
+  float* out_part;
+  __nv_bfloat16* out_xb;
 };
 
 __device__ __forceinline__ float silu_f(float g) { return g / (1.f + __expf(-g)); }
@@ -143,17 +152,24 @@ __device__ __forceinline__ float ld_dsmem_f32(uint32_t local_addr, uint32_t peer
   return v;
 }
 
-// Output of one (token m, weight row n) element; SILU pairs rows (n, n+1).
-__device__ __forceinline__ void epi_one(const TcParams& p, int m, int n, float v) {
-  if (m >= p.M || n >= p.N) return;
+// Output of one (token m, weight row n) element.  Returns the value the
+// element ends with (the new residual for EPI_RESID_ADD) for norm partials.
+__device__ __forceinline__ float epi_one(const TcParams& p, int m, int n, float v) {
+  if (m >= p.M || n >= p.N) return 0.f;
   size_t o = (size_t)m * p.N + n;
-  if (p.epi == EPI_STORE)
+  if (p.epi == EPI_STORE) {
     ((__nv_bfloat16*)p.y)[o] = __float2bfloat16_rn(v);
-  else if (p.epi == EPI_STORE_F32)
+  } else if (p.epi == EPI_STORE_F32) {
     ((float*)p.y)[o] = v;
-  else
-    ((float*)p.y)[o] += v;
+  } else {
+    float nv = ((float*)p.y)[o] + v;
+    ((float*)p.y)[o] = nv;
+    if (p.out_xb) p.out_xb[o] = __float2bfloat16_rn(nv);
+    return nv;
+  }
+  return v;
 }
+// SILU pairs rows (n, n+1) = (gate, up)
 __device__ __forceinline__ void epi_pair(const TcParams& p, int m, int n, float g, float u) {
   if (m >= p.M || n >= p.N) return;
   ((__nv_bfloat16*)p.y)[(size_t)m * (p.N / 2) + n / 2] = __float2bfloat16_rn(silu_f(g) * u);
@@ -169,14 +185,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const uint32_t a_bytes = TC_BM * TC_BK * 2;
   const uint32_t b_bytes = tn * TC_BK * 2;
   const uint32_t stage_bytes = a_bytes + b_bytes;
-  uint8_t* stage_base = smem;
   const uint32_t ring_bytes = p.stages * stage_bytes;
-  const uint32_t red_bytes = (uint32_t)tn * TC_BM * 4;
-  uint64_t* full = (uint64_t*)(smem + (ring_bytes > red_bytes ? ring_bytes : red_bytes));
+  // scratch (reuses the drained ring): split>1: partial tile [tn][128] + squares [tn][128/splits];
+  // split==1: argmax staging [2][4][tn] + squares [4][tn]
+  const uint32_t scratch_bytes = p.splits > 1 ? (uint32_t)tn * (TC_BM + TC_BM / p.splits) * 4 : (uint32_t)tn * 12 * 4;
+  uint8_t* stage_base = smem;
+  uint64_t* full = (uint64_t*)(smem + (ring_bytes > scratch_bytes ? ring_bytes : scratch_bytes));
   uint64_t* empty = full + p.stages;
   uint64_t* tmem_full = empty + p.stages;
   uint32_t* tmem_slot = (uint32_t*)(tmem_full + 1);
-  float* red = (float*)smem;  // split-K partial tile [tn][128] (reuses the drained stage ring)
+  float* inv_s = (float*)(tmem_slot + 4);  // [tn] per-token 1/rms (fused RMSNorm)
+  float* red = (float*)smem;               // split-K partial tile [tn][128] (reuses the drained ring)
+  float* sq = p.splits > 1 ? red + tn * TC_BM : red + 8 * tn;  // norm squares staging
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int split = p.splits > 1 ? (int)cluster_rank() : 0;
@@ -265,21 +285,43 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   } else {
     // ---------------- epilogue warps: TMEM -> registers -> (DSMEM reduce) -> global
     griddep_wait();
+    const int et = threadIdx.x - 64;
     const int quad = warp & 3;
     const int row = quad * 32 + lane;  // weight row within the tile (= TMEM lane)
     const uint32_t lane_addr = tmem + ((uint32_t)(quad * 32) << 16);
+    // fused RMSNorm (consumer): per-token 1/rms from the producer's partials,
+    // computed while the weights stream (these warps are otherwise idle)
+    if (p.ns_part) {
+      for (int j = et; j < tn; j += 128) {
+        const int m = m0 + j;
+        float s = 0.f;
+        if (m < p.M) {
+          const float* src = p.ns_part + (size_t)m * p.ns_row_step + p.ns_row_off;
+          for (int q = 0; q < p.ns_P; ++q) s += src[(size_t)q * p.ns_stride];
+        }
+        inv_s[j] = rsqrtf(s * p.ns_inv_h + p.ns_eps);
+      }
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+    }
     mbar_wait(tmem_full, 0);
     tc_fence_after();
+    const bool scale = p.ns_part != nullptr;
     for (int j0 = 0; j0 < tn; j0 += 16) {
       float v[16];
       tmem_ld16(lane_addr + j0, v);
       if (p.splits > 1) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) red[(j0 + j) * TC_BM + row] = v[j];
-      } else if (p.epi == EPI_ARGMAX) {
+        continue;
+      }
+      if (scale) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] *= inv_s[j0 + j];
+      }
+      if (p.epi == EPI_ARGMAX) {
         // per token: warp argmax over its 32 rows (ties -> lowest row), staged per quadrant
-        float* qv = red;                                  // [4][tn] values
-        int* qi = reinterpret_cast<int*>(red + 4 * tn);   // [4][tn] indices
+        float* qv = red;
+        int* qi = reinterpret_cast<int*>(red + 4 * tn);
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const int m = m0 + j0 + j, n = n0 + row;
@@ -299,22 +341,30 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
       } else {
 #pragma unroll
-        for (int j = 0; j < 16; ++j) epi_one(p, m0 + j0 + j, n0 + row, v[j]);
+        for (int j = 0; j < 16; ++j) {
+          float nv = epi_one(p, m0 + j0 + j, n0 + row, v[j]);
+          if (p.out_part) {  // per-token sum of squares over the tile's 128 rows (fixed xor tree)
+            float s = warp_sum(nv * nv);
+            if (lane == 0) sq[quad * tn + j0 + j] = s;
+          }
+        }
       }
     }
-    if (p.epi == EPI_ARGMAX) {
+    if (p.splits == 1 && (p.epi == EPI_ARGMAX || p.out_part)) {
       asm volatile("bar.sync 1, 128;" ::: "memory");
-      const int et = threadIdx.x - 64;
-      const float* qv = red;
-      const int* qi = reinterpret_cast<const int*>(red + 4 * tn);
       for (int j = et; j < tn; j += 128) {
-        ArgMax a{qv[j], qi[j]};
-#pragma unroll
-        for (int q = 1; q < 4; ++q) a = argmax_merge(a, ArgMax{qv[q * tn + j], qi[q * tn + j]});
         const int m = m0 + j;
-        if (m < p.M) {
+        if (m >= p.M) continue;
+        if (p.epi == EPI_ARGMAX) {
+          const float* qv = red;
+          const int* qi = reinterpret_cast<const int*>(red + 4 * tn);
+          ArgMax a{qv[j], qi[j]};
+#pragma unroll
+          for (int q = 1; q < 4; ++q) a = argmax_merge(a, ArgMax{qv[q * tn + j], qi[q * tn + j]});
           p.aux_val[(size_t)tile_n * p.M + m] = a.v;
           p.aux_idx[(size_t)tile_n * p.M + m] = a.i;
+        } else {
+          p.out_part[(size_t)tile_n * p.M + m] = ((sq[j] + sq[tn + j]) + sq[2 * tn + j]) + sq[3 * tn + j];
         }
       }
     }
@@ -331,6 +381,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int et = threadIdx.x - 64;
       const int r_base = split * R;
       const uint32_t red_addr = smem_u32(red);
+      const bool scale = p.ns_part != nullptr;
       if (p.epi == EPI_SILU_MUL) {
         const int pairs = R / 2;
         for (int it = et; it < pairs * tn; it += 128) {
@@ -340,14 +391,30 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             g += ld_dsmem_f32(red_addr + (uint32_t)((j * TC_BM + r) * 4), q);
             u += ld_dsmem_f32(red_addr + (uint32_t)((j * TC_BM + r + 1) * 4), q);
           }
+          if (scale) {
+            g *= inv_s[j];
+            u *= inv_s[j];
+          }
           epi_pair(p, m0 + j, n0 + r, g, u);
         }
       } else {
         for (int it = et; it < R * tn; it += 128) {
-          int r = r_base + it % R, j = it / R;
+          int rl = it % R, j = it / R, r = r_base + rl;
           float a = 0.f;
           for (int q = 0; q < p.splits; ++q) a += ld_dsmem_f32(red_addr + (uint32_t)((j * TC_BM + r) * 4), q);
-          epi_one(p, m0 + j, n0 + r, a);
+          if (scale) a *= inv_s[j];
+          float nv = epi_one(p, m0 + j, n0 + r, a);
+          if (p.out_part) sq[j * R + rl] = nv * nv;
+        }
+        if (p.out_part) {
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+          for (int j = et; j < tn; j += 128) {
+            const int m = m0 + j;
+            if (m >= p.M) continue;
+            float s = 0.f;
+            for (int rl = 0; rl < R; ++rl) s += sq[j * R + rl];
+            p.out_part[((size_t)tile_n * p.splits + split) * p.M + m] = s;
+          }
         }
       }
     }
@@ -441,8 +508,8 @@ static TcPlan plan(int M, int N, int K, int epi) {
   if (q.stages > (g_tune_stages ? g_tune_stages : 12)) q.stages = g_tune_stages ? g_tune_stages : 12;
   if (q.stages < 2) q.stages = 2;
   size_t ring = (size_t)q.stages * stage;
-  size_t red = (size_t)q.tn * TC_BM * 4;  // split-K partial tile reuses the ring
-  q.smem = 1024 + (ring > red ? ring : red) + 256;
+  size_t scratch = q.splits > 1 ? (size_t)q.tn * (TC_BM + TC_BM / q.splits) * 4 : (size_t)q.tn * 12 * 4;
+  q.smem = 1024 + (ring > scratch ? ring : scratch) + 256 + 16 + (size_t)q.tn * 4;
   return q;
 }
 
@@ -462,6 +529,11 @@ int gemm_tc_init() {
     get_encode();
   }
   return rc;
+}
+
+int gemm_tc_norm_partials(const GemmArgs& a) {
+  TcPlan q = plan(a.M, a.N, a.K, a.epi);
+  return q.n_tiles_n * q.splits;
 }
 
 bool gemm_tc_supported(const GemmArgs& a) {
@@ -495,6 +567,16 @@ int gemm_tc(const GemmArgs& a, cudaStream_t st) {
   p.y = a.y;
   p.aux_val = a.aux_val;
   p.aux_idx = a.aux_idx;
+  p.ns_part = a.ns_part;
+  p.ns_P = a.ns_P;
+  p.ns_stride = a.ns_stride;
+  p.ns_row_step = a.ns_row_step;
+  p.ns_row_off = a.ns_row_off;
+  p.ns_eps = a.ns_eps;
+  p.ns_inv_h = a.ns_inv_h;
+  p.out_part = a.out_part;
+  p.out_xb = (__nv_bfloat16*)a.out_xb;
+  if (a.out_part && a.epi != EPI_RESID_ADD) return SB_EINVAL;
   if (a.epi == EPI_ARGMAX && (!a.aux_val || !a.aux_idx)) return SB_EINVAL;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(q.n_tiles_n * q.splits, q.m_tiles, 1);

@@ -27,6 +27,14 @@ struct GemmArgs {
   size_t ws_bytes;
   float* aux_val = nullptr;  // EPI_ARGMAX partials
   int* aux_idx = nullptr;
+  // fused RMSNorm consumer (tcgen05 only): scale token m by rsqrt(sum_p ns_part[p*ns_stride +
+  // m*ns_row_step + ns_row_off] * ns_inv_h + ns_eps); X is the raw (bf16) residual, norm gains folded in W
+  const float* ns_part = nullptr;
+  int ns_P = 0, ns_stride = 0, ns_row_step = 1, ns_row_off = 0;
+  float ns_eps = 0.f, ns_inv_h = 0.f;
+  // fused RMSNorm producer (EPI_RESID_ADD): bf16 copy of the new residual + sum-of-squares partials
+  float* out_part = nullptr;
+  void* out_xb = nullptr;
 };
 
 extern int g_backend_override;  // sb_set_gemm_backend (ablation / tests)
@@ -36,10 +44,13 @@ int gemm_simt(const GemmArgs& a, cudaStream_t st);
 int gemm_tc(const GemmArgs& a, cudaStream_t st);  // tcgen05 (bf16 only); SB_EUNSUPPORTED otherwise
 bool gemm_tc_supported(const GemmArgs& a);
 int gemm_tc_init();
+int gemm_tc_norm_partials(const GemmArgs& a);  // rows of out_part this GEMM writes
 int gemm_tc_tune(int cps, int stages, int splits);
 
 int launch_embed(int dtype, const void* table, const int32_t* ids, const int32_t* pos, float* h, int n_tok,
                  int hidden, int vocab, cudaStream_t st);
+int launch_embed_norm(const void* table, const int32_t* ids, const int32_t* pos, float* h, void* xb, float* part,
+                      int n_tok, int hidden, int vocab, cudaStream_t st);
 int launch_rmsnorm(int dtype, const float* x, const void* g, void* y, int rows, int hidden, float eps, int row_step,
                    int row_off, cudaStream_t st);
 int launch_rope_append(int dtype, const void* qkv, void* q_out, void* kc, void* vc, const int32_t* tok_slot,

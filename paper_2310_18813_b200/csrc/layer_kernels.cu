@@ -3,8 +3,10 @@
 // speculative window (K3).  All are HBM/latency-bound.
 //
 // Numerics contract (mirrored by oracle/model_ref.py):
-//   residual stream fp32; GEMM inputs rounded to the model dtype after each
-//   norm / activation; RoPE applied in fp32 from a host-built fp32 cos/sin
+//   residual stream fp32; GEMM inputs rounded to the model dtype; on the bf16
+//   path RMSNorm is fused into the GEMMs (input = bf16 raw residual, output
+//   scaled by 1/rms, gains folded into W), on the fp32 path the normalised
+//   input is materialised (same math); RoPE applied in fp32 from a host-built fp32 cos/sin
 //   table then rounded; attention scores/softmax/accumulation in fp32 with a
 //   fixed key order (64-key tiles, ascending) so a query's output does not
 //   depend on how many other queries share the launch (batch invariance:
@@ -38,6 +40,44 @@ int launch_embed(int dtype, const void* table, const int32_t* ids, const int32_t
     return launch_k(embed_kernel<__nv_bfloat16>, dim3(n_tok), dim3(256), 0, st, (const __nv_bfloat16*)table, ids, pos,
                     h, hidden, vocab);
   return launch_k(embed_kernel<float>, dim3(n_tok), dim3(256), 0, st, (const float*)table, ids, pos, h, hidden, vocab);
+}
+
+// Embedding for the fused-RMSNorm path: fp32 residual, its bf16 copy (the
+// next GEMM's X) and the row's sum of squares (one partial per token).
+__global__ void __launch_bounds__(256) embed_norm_kernel(const __nv_bfloat16* __restrict__ table,
+                                                         const int32_t* __restrict__ ids,
+                                                         const int32_t* __restrict__ pos, float* __restrict__ h,
+                                                         __nv_bfloat16* __restrict__ xb, float* __restrict__ part,
+                                                         int hidden, int vocab) {
+  griddep_wait();
+  griddep_launch();
+  const int t = blockIdx.x;
+  const int id = ids[t];
+  const bool pad = (pos != nullptr && pos[t] < 0) || id < 0 || id >= vocab;
+  const __nv_bfloat16* row = table + (size_t)(pad ? 0 : id) * hidden;
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < hidden; i += blockDim.x) {
+    float v = pad ? 0.f : __bfloat162float(row[i]);
+    h[(size_t)t * hidden + i] = v;
+    xb[(size_t)t * hidden + i] = __float2bfloat16_rn(v);
+    ss += v * v;
+  }
+  __shared__ float red[8];
+  ss = warp_sum(ss);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float tot = 0.f;
+    for (int w = 0; w < 8; ++w) tot += red[w];
+    part[t] = tot;
+  }
+}
+
+int launch_embed_norm(const void* table, const int32_t* ids, const int32_t* pos, float* h, void* xb, float* part,
+                      int n_tok, int hidden, int vocab, cudaStream_t st) {
+  if (n_tok <= 0) return 0;
+  return launch_k(embed_norm_kernel, dim3(n_tok), dim3(256), 0, st, (const __nv_bfloat16*)table, ids, pos, h,
+                  (__nv_bfloat16*)xb, part, hidden, vocab);
 }
 
 // ---------------------------------------------------------------- RMSNorm
