@@ -225,6 +225,7 @@ def run_ours(args):
     from paper_2310_18813_b200.policy import build_lut, lookup
     from paper_2310_18813_b200.presets import example_trace
     from paper_2310_18813_b200.profiler import calibrate
+    from paper_2310_18813_b200.replicas import max_over_ranks
     from paper_2310_18813_b200.spec_engine import SpecEngine
 
     b = args.batch
@@ -269,10 +270,7 @@ def run_ours(args):
         e1.record(eng.stream)
         torch.cuda.synchronize()
     total_ms = e0.elapsed_time(e1)
-    if world > 1:
-        t = torch.tensor([total_ms], device=dev)
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        total_ms = float(t.item())
+    total_ms = max_over_ranks(total_ms, device=dev)
     tokens = world * args.steps * b * NEW
     value = tokens / (total_ms / 1e3)
 
@@ -294,6 +292,12 @@ def run_ours(args):
     vb = verify_bytes(tgt.cfg, b, k, ctx_avg)
     v_ms = eng.time_verify(b, k, ctx=ctx_avg, reps=20)
     achieved = vb / (v_ms / 1e3) / 1e9
+    traffic = None
+    tf_path = ROOT / "profiles" / "verify_traffic.json"
+    if tf_path.exists():
+        tfd = json.loads(tf_path.read_text())
+        if tfd.get("b") == b and tfd.get("k") == k:
+            traffic = tfd["dram_bytes_read_plus_write"]
 
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
@@ -328,7 +332,7 @@ def run_ours(args):
             "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": b * P * 4,
                     "d2h_bytes_per_step": b * eng.cap * 4 + b * 4 * 3},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                         "frac": achieved / hbm, "traffic": None, "kernel": f"verify forward b={b} k={k}",
+                         "frac": achieved / hbm, "traffic": traffic, "kernel": f"verify forward b={b} k={k}",
                          "algorithmic_bytes": vb, "verify_ms": v_ms, "peak_kind": peak_kind,
                          "frac_of_8TBs": achieved / 8000.0},
             "cpu_baseline": cpu,
