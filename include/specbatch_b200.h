@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define SB_ABI_VERSION 1
+#define SB_ABI_VERSION 2
 
 /* status codes beyond cudaError_t (which are < 1000) */
 #define SB_OK 0
@@ -90,6 +90,9 @@ typedef struct sb_decoder {
   const void* const* w_down;
   const float* rope_cos;
   const float* rope_sin;
+  /* bf16 only, optional: device copy of the weight TMA descriptors written by
+     sb_decoder_encode_tmaps (enables the persistent forward; NULL = off) */
+  const void* tmaps;
 } sb_decoder_t;
 
 /* KV cache: k/v base pointers of layout [n_layers][slots][n_kv_heads][ctx_max][head_dim]. */
@@ -98,6 +101,16 @@ typedef struct sb_kvcache {
   void* v;
   int32_t slots, ctx_max;
 } sb_kvcache_t;
+
+/* Bytes of the weight TMA descriptor table (4 per layer + lm_head, 128 B each). */
+size_t sb_decoder_tmaps_bytes(const sb_decoder_t* m);
+/*
+ * Encode the weight TMA descriptors into host memory `host_out`
+ * (sb_decoder_tmaps_bytes).  The caller copies them to 64-byte-aligned device
+ * memory and stores that pointer in m->tmaps: sb_decoder_forward then runs the
+ * persistent single-kernel forward for n_tokens <= 256 (bf16).
+ */
+int sb_decoder_encode_tmaps(const sb_decoder_t* m, void* host_out);
 
 /* Workspace bytes sb_decoder_forward needs for n_tokens query tokens. */
 size_t sb_decoder_workspace_bytes(const sb_decoder_t* m, int32_t n_tokens);
@@ -232,6 +245,8 @@ float sb_uniform_host(uint64_t seed, uint64_t stream_id, uint64_t counter);
 int sb_init(void);
 /* Force the forward's GEMM backend (0 auto = tcgen05 for bf16, 1 SIMT, 2 tcgen05); for ablations. */
 int sb_set_gemm_backend(int32_t backend);
+/* Persistent single-kernel forward when eligible (default on); 0 = per-layer kernels (ablation). */
+int sb_set_persistent(int32_t enabled);
 /* Programmatic dependent launch for every kernel (default on); 0 disables (ablation). */
 int sb_set_pdl(int32_t enabled);
 /* RMSNorm fused into the GEMM epilogues on the bf16 path (default on); 0 = separate norm kernels. */

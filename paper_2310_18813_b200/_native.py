@@ -39,7 +39,7 @@ class SbDecoder(C.Structure):
         ("ffn", _I), ("vocab", _I), ("dtype", _I), ("max_pos", _I), ("rms_eps", C.c_float),
         ("embed", _P), ("final_norm", _P), ("lm_head", _P),
         ("attn_norm", _PP), ("w_qkv", _PP), ("w_o", _PP), ("mlp_norm", _PP), ("w_gu", _PP), ("w_down", _PP),
-        ("rope_cos", _P), ("rope_sin", _P),
+        ("rope_cos", _P), ("rope_sin", _P), ("tmaps", _P),
     ]
 
 
@@ -63,6 +63,9 @@ _SIGS = {
     "sb_set_pdl": (C.c_int, [_I]),
     "sb_set_fuse_norm": (C.c_int, [_I]),
     "sb_set_attention_impl": (C.c_int, [_I]),
+    "sb_set_persistent": (C.c_int, [_I]),
+    "sb_decoder_tmaps_bytes": (C.c_size_t, [C.POINTER(SbDecoder)]),
+    "sb_decoder_encode_tmaps": (C.c_int, [C.POINTER(SbDecoder), _P]),
     "sb_gemm_tune": (C.c_int, [_I, _I, _I]),
     "sb_profile_forward": (C.c_int, [C.POINTER(SbDecoder), C.POINTER(SbKVCache), _P, _P, _P, _I, _I, _P, _I, _P,
                                      C.c_size_t, _P, C.c_char_p, _I]),

@@ -27,6 +27,8 @@ struct FwdWorkspace {
   int* amax_idx;
   void* xb;       // bf16 copy of the residual (fused-RMSNorm GEMM input)
   float* npart;   // sum-of-squares partials [P_max][T]
+  float* pk_scratch;  // persistent forward: stream-K partial tiles
+  unsigned* pk_sync;  // persistent forward: barrier / exit / flag words (zero between launches)
   void* gemm_ws;
   size_t gemm_ws_bytes;
 };
@@ -43,9 +45,11 @@ static size_t carve(const sb_decoder_t* m, int T, char* base, FwdWorkspace* w) {
   };
   FwdWorkspace tmp;
   FwdWorkspace* o = w ? w : &tmp;
-  // The GEMM region comes FIRST: its stream-K tile counters must sit at the
-  // same address for every forward sharing this workspace, whatever T is
-  // (they self-reset; any other placement would land them on dirty memory).
+  // The persistent forward's sync words come FIRST: they must sit at the same
+  // address for every forward sharing this workspace, whatever T is (each
+  // launch leaves them zero; any other placement would land them on dirty memory).
+  o->pk_sync = (unsigned*)take(persistent_sync_bytes());
+  o->pk_scratch = (float*)take(persistent_scratch_bytes(T));
   int maxN = m->vocab;
   if (2 * m->ffn > maxN) maxN = 2 * m->ffn;
   if (qkv_n > maxN) maxN = qkv_n;
@@ -218,6 +222,10 @@ static int forward_impl(const sb_decoder_t* m, const sb_kvcache_t* kv, const int
   const size_t layer_kv = (size_t)kv->slots * nkv * kv->ctx_max * hd * es;
 
   prof_mark("start", st);
+  if (!g_prof && g_backend_override != GEMM_SIMT && persistent_eligible(m, T)) {
+    PkBuffers b{w.resid, w.xb, w.qr, w.attn, w.act, w.npart, w.amax_val, w.amax_idx, w.pk_scratch, w.pk_sync};
+    return persistent_forward(m, kv, ids, slot, pos, n_seq, q_len, logits, logits_mode, sink, b, st);
+  }
   if (g_fuse_norm && dt == SB_BF16 && g_backend_override != GEMM_SIMT)
     return forward_fused_norm(m, kv, ids, slot, pos, n_seq, q_len, logits, logits_mode, sink, w, st);
   SB_TRY(launch_embed(dt, m->embed, ids, pos, w.resid, T, H, m->vocab, st));
@@ -373,6 +381,16 @@ int sb_set_fuse_norm(int32_t enabled) {
   return 0;
 }
 
+int sb_set_persistent(int32_t enabled) { return set_persistent(enabled); }
+
+size_t sb_decoder_tmaps_bytes(const sb_decoder_t* m) { return m ? decoder_tmaps_bytes(m) : 0; }
+
+int sb_decoder_encode_tmaps(const sb_decoder_t* m, void* host_out) {
+  if (!m || !host_out) return SB_EINVAL;
+  SB_TRY(gemm_tc_init());
+  return decoder_encode_tmaps(m, host_out);
+}
+
 int sb_set_pdl(int32_t enabled) {
   g_pdl = enabled ? 1 : 0;
   return 0;
@@ -381,7 +399,7 @@ int sb_set_pdl(int32_t enabled) {
 int sb_version(void) { return SB_ABI_VERSION; }
 
 const char* sb_build_info(void) {
-  return "specbatch_b200 abi=" "1" " arch=sm_100a kernels=embed,rmsnorm,rope_append,attention,gemm_simt,gemm_tcgen05,"
+  return "specbatch_b200 abi=" "2" " arch=sm_100a kernels=persistent_forward,embed,rmsnorm,rope_append,attention,gemm_simt,gemm_tcgen05,"
          "argmax,softmax,select,accept,commit,prepare,kv_compact";
 }
 

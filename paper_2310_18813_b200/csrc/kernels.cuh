@@ -1,7 +1,10 @@
 // Internal launcher declarations (host side).  Each returns 0 or an error code.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
+
+#include "specbatch_b200.h"
 
 namespace sb {
 
@@ -46,6 +49,9 @@ bool gemm_tc_supported(const GemmArgs& a);
 int gemm_tc_init();
 int gemm_tc_norm_partials(const GemmArgs& a);  // rows of out_part this GEMM writes
 int gemm_tc_tune(int cps, int stages, int splits);
+int num_sms();
+// 2-D bf16 tensor map [rows, cols] (row stride ld elements), box TC_BK x box_rows, 128B swizzle.
+int make_map(CUtensorMap* map, const void* base, int rows, int cols, int ld, int box_rows);
 
 int launch_embed(int dtype, const void* table, const int32_t* ids, const int32_t* pos, float* h, int n_tok,
                  int hidden, int vocab, cudaStream_t st);
@@ -69,5 +75,28 @@ int launch_select_argmax(const float* logits, int rows, int vocab, int32_t* out_
                          int32_t* next_pos, const int32_t* base_pos, int pos_offset, cudaStream_t st);
 int launch_kv_compact(int dtype, void* k, void* v, const int32_t* src, const int32_t* dst, const int32_t* len, int n,
                       int layers, int slots, int nkv, int ctx_max, int hd, cudaStream_t st);
+
+// ---- persistent forward (persistent.cu)
+struct PkBuffers {
+  float* resid;
+  void* xb;
+  void* qr;
+  void* attn;
+  void* act;
+  float* npart;
+  float* amax_val;
+  int* amax_idx;
+  float* scratch;
+  unsigned* sync;
+};
+size_t persistent_sync_bytes();
+size_t persistent_scratch_bytes(int T);
+bool persistent_eligible(const sb_decoder_t* m, int T);
+int persistent_forward(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* ids, const int32_t* slot,
+                       const int32_t* pos, int n_seq, int q_len, float* logits, int logits_mode,
+                       const sb_token_sink_t* sink, const PkBuffers& b, cudaStream_t st);
+int set_persistent(int enabled);
+size_t decoder_tmaps_bytes(const sb_decoder_t* m);
+int decoder_encode_tmaps(const sb_decoder_t* m, void* host_out);
 
 }  // namespace sb

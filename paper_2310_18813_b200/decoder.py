@@ -187,6 +187,17 @@ class Decoder:
         for k, a in self._arrays.items():
             setattr(s, k, C.cast(a, C.POINTER(C.c_void_p)))
         s.rope_cos, s.rope_sin = self.rope_cos.data_ptr(), self.rope_sin.data_ptr()
+        s.tmaps = None
+        self.tmaps = None
+        if self.sb_dtype == N.SB_BF16 and self.device.type == "cuda":
+            # weight TMA descriptors, encoded once on the host and kept resident:
+            # they enable the persistent single-kernel forward (csrc/persistent.cu)
+            lib = N.load()
+            nbytes = int(lib.sb_decoder_tmaps_bytes(C.byref(s)))
+            host = (C.c_uint8 * nbytes)()
+            N.call("sb_decoder_encode_tmaps", C.byref(s), C.cast(host, C.c_void_p))
+            self.tmaps = torch.frombuffer(bytearray(host), dtype=torch.uint8).to(self.device)
+            s.tmaps = self.tmaps.data_ptr()
         self.struct = s
 
     def workspace_bytes(self, n_tokens: int) -> int:
