@@ -107,8 +107,9 @@ size_t sb_decoder_tmaps_bytes(const sb_decoder_t* m);
 /*
  * Encode the weight TMA descriptors into host memory `host_out`
  * (sb_decoder_tmaps_bytes).  The caller copies them to 64-byte-aligned device
- * memory and stores that pointer in m->tmaps: sb_decoder_forward then runs the
- * persistent single-kernel forward for n_tokens <= 256 (bf16).
+ * memory and stores that pointer in m->tmaps: with sb_set_persistent(1),
+ * sb_decoder_forward then runs the persistent single-kernel forward for
+ * n_tokens <= 256 (bf16).
  */
 int sb_decoder_encode_tmaps(const sb_decoder_t* m, void* host_out);
 
@@ -245,8 +246,11 @@ float sb_uniform_host(uint64_t seed, uint64_t stream_id, uint64_t counter);
 int sb_init(void);
 /* Force the forward's GEMM backend (0 auto = tcgen05 for bf16, 1 SIMT, 2 tcgen05); for ablations. */
 int sb_set_gemm_backend(int32_t backend);
-/* Persistent single-kernel forward when eligible (default on); 0 = per-layer kernels (ablation). */
+/* Persistent single-kernel forward when eligible (default off: measured slower); 0 = per-layer kernels. */
 int sb_set_persistent(int32_t enabled);
+/* Diagnostics: per (CTA, phase) globaltimer stamps [G][n_phases][4] of the persistent forward
+   (barrier wait start/end, first accumulator ready, phase end); NULL disables. */
+int sb_debug_persistent_trace(void* device_buf);
 /* Programmatic dependent launch for every kernel (default on); 0 disables (ablation). */
 int sb_set_pdl(int32_t enabled);
 /* RMSNorm fused into the GEMM epilogues on the bf16 path (default on); 0 = separate norm kernels. */

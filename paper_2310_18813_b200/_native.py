@@ -64,6 +64,7 @@ _SIGS = {
     "sb_set_fuse_norm": (C.c_int, [_I]),
     "sb_set_attention_impl": (C.c_int, [_I]),
     "sb_set_persistent": (C.c_int, [_I]),
+    "sb_debug_persistent_trace": (C.c_int, [_P]),
     "sb_decoder_tmaps_bytes": (C.c_size_t, [C.POINTER(SbDecoder)]),
     "sb_decoder_encode_tmaps": (C.c_int, [C.POINTER(SbDecoder), _P]),
     "sb_gemm_tune": (C.c_int, [_I, _I, _I]),

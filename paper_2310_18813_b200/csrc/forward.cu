@@ -4,6 +4,7 @@
 // caller's stream; no allocation, so a whole iteration can be captured into
 // one CUDA graph per (b, k) by the host engine.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -224,7 +225,9 @@ static int forward_impl(const sb_decoder_t* m, const sb_kvcache_t* kv, const int
   prof_mark("start", st);
   if (!g_prof && g_backend_override != GEMM_SIMT && persistent_eligible(m, T)) {
     PkBuffers b{w.resid, w.xb, w.qr, w.attn, w.act, w.npart, w.amax_val, w.amax_idx, w.pk_scratch, w.pk_sync};
-    return persistent_forward(m, kv, ids, slot, pos, n_seq, q_len, logits, logits_mode, sink, b, st);
+    int rc = persistent_forward(m, kv, ids, slot, pos, n_seq, q_len, logits, logits_mode, sink, b, st);
+    if (rc && getenv("SB_DEBUG")) fprintf(stderr, "persistent_forward rc=%d T=%d\n", rc, T);
+    return rc;
   }
   if (g_fuse_norm && dt == SB_BF16 && g_backend_override != GEMM_SIMT)
     return forward_fused_norm(m, kv, ids, slot, pos, n_seq, q_len, logits, logits_mode, sink, w, st);
@@ -289,6 +292,9 @@ int sb_decoder_forward(const sb_decoder_t* m, const sb_kvcache_t* kv, const int3
   int rc = forward_impl(m, kv, tok_ids, tok_slot, tok_pos, n_seq, q_len, logits, logits_mode, nullptr, workspace,
                         ws_bytes, (cudaStream_t)stream);
   g_last_count = g_kernel_count;
+  if (rc && getenv("SB_DEBUG"))
+    fprintf(stderr, "sb_decoder_forward rc=%d T=%d eligible=%d\n", rc, n_seq * q_len,
+            (int)persistent_eligible(m, n_seq * q_len));
   return rc;
 }
 
@@ -382,6 +388,8 @@ int sb_set_fuse_norm(int32_t enabled) {
 }
 
 int sb_set_persistent(int32_t enabled) { return set_persistent(enabled); }
+
+int sb_debug_persistent_trace(void* device_buf) { return set_persistent_trace(device_buf); }
 
 size_t sb_decoder_tmaps_bytes(const sb_decoder_t* m) { return m ? decoder_tmaps_bytes(m) : 0; }
 

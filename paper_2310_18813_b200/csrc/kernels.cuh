@@ -96,6 +96,7 @@ int persistent_forward(const sb_decoder_t* m, const sb_kvcache_t* kv, const int3
                        const int32_t* pos, int n_seq, int q_len, float* logits, int logits_mode,
                        const sb_token_sink_t* sink, const PkBuffers& b, cudaStream_t st);
 int set_persistent(int enabled);
+int set_persistent_trace(void* buf);
 size_t decoder_tmaps_bytes(const sb_decoder_t* m);
 int decoder_encode_tmaps(const sb_decoder_t* m, void* host_out);
 

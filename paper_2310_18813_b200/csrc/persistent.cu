@@ -36,6 +36,7 @@
 
 #include <climits>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "common.cuh"
@@ -48,8 +49,6 @@ namespace sb {
 constexpr int PK_THREADS = 224;
 constexpr int PK_MAX_T = 256;
 constexpr int PK_MAX_G = 1024;
-constexpr int PK_ATT_KT = 64;
-constexpr int PK_ATT_STAGES = 2;
 constexpr int PK_STAGE_PAD = 17;  // RoPE staging row stride (floats)
 
 enum : int { PG_QKV = 0, PG_O = 1, PG_GU = 2, PG_DOWN = 3, PG_LM = 4 };
@@ -62,6 +61,8 @@ struct PkGemm {
 struct PkParams {
   int T, n_seq, q_len, H, nq, nkv, hd, ffn, V, L;
   int tn, G, n_phases, stages;
+  int epi_bytes;
+  int l2_ahead;  // units the L2 prefetch cursor runs ahead of the smem ring
   int lm_rows, lm_step, lm_off;
   int want_logits, want_argmax;
   float eps, inv_h, att_scale;
@@ -94,6 +95,7 @@ struct PkParams {
   int32_t* next_pos;
   const int32_t* base_pos;
   int pos_offset;
+  unsigned long long* trace;  // diagnostics: [G][n_phases][8] globaltimer ns (NULL = off)
 };
 
 // ------------------------------------------------------------------ sync helpers
@@ -172,116 +174,192 @@ struct PkSmem {
   uint8_t* epi;   // aliased epilogue region (attention ring / RoPE staging / quadrant partials)
 };
 
-// ------------------------------------------------------------------ attention item
-// One (sequence, kv head, 16-query chunk): S = Q K^T and O += P V with
-// mma.sync m16n8k16 over 64-key tiles (warp w owns keys [16w, 16w+16) of each
-// tile; warps combined in order).  Q is already rotated (qkv epilogue) and the
-// window's K/V rows are already in the cache.
-template <int HD>
-__device__ void attn_item(const PkParams& p, uint8_t* epi, int seq, int kvh, int chunk, int* qpos, int* qtok,
-                          int* qhead) {
-  constexpr int RS = HD + 8, HALF = HD / 2, KSTEP = HD / 16, NT = HD / 8;
-  constexpr size_t TILE = (size_t)PK_ATT_KT * RS * 2;
-  constexpr size_t STAGE = 2 * TILE;
-  __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(epi);
-  uint8_t* ring = epi + (size_t)16 * RS * 2;
-  const int tid = threadIdx.x - 64, warp = tid >> 5, lane = tid & 31;
-  const int group = p.nq / p.nkv;
-  const int nQ = group * p.q_len;
-  const int slot = p.slot[seq];
-  const __nv_bfloat16* kslab = p.kc + ((size_t)slot * p.nkv + kvh) * p.ctx_max * HD;
-  const __nv_bfloat16* vslab = p.vc + ((size_t)slot * p.nkv + kvh) * p.ctx_max * HD;
-  (void)HALF;
-  if (tid < 16) {
-    const int jj = chunk * 16 + tid;
-    const int t = jj / group;
-    const bool ok = jj < nQ;
-    qtok[tid] = ok ? t : 0;
-    qhead[tid] = kvh * group + (ok ? jj % group : 0);
-    qpos[tid] = ok ? p.pos[seq * p.q_len + t] : -1;
-  }
-  epi_sync();
-  const int qd = p.nq * HD;
-  for (int e = tid; e < 16 * (HD / 8); e += 128) {
-    const int j = e / (HD / 8), c = (e % (HD / 8)) * 8;
-    uint4 v = make_uint4(0, 0, 0, 0);
-    if (qpos[j] >= 0)
-      v = __ldcg(reinterpret_cast<const uint4*>(p.qr + (size_t)(seq * p.q_len + qtok[j]) * qd + qhead[j] * HD + c));
-    *reinterpret_cast<uint4*>(Qs + j * RS + c) = v;
-  }
-  epi_sync();
-  int maxp = -1;
-#pragma unroll
-  for (int j = 0; j < 16; ++j) maxp = max(maxp, qpos[j]);
-  const int n_keys = maxp + 1;
-  const int n_tiles = (n_keys + PK_ATT_KT - 1) / PK_ATT_KT;
-
-  auto issue = [&](int tile) {
-    if (tile < n_tiles) {
-      uint8_t* st = ring + (tile % PK_ATT_STAGES) * STAGE;
-      __nv_bfloat16* Kd = reinterpret_cast<__nv_bfloat16*>(st);
-      __nv_bfloat16* Vd = reinterpret_cast<__nv_bfloat16*>(st + TILE);
-      const int k0 = tile * PK_ATT_KT;
-      constexpr int CPR = HD / 8;
-      for (int e = tid; e < PK_ATT_KT * CPR; e += 128) {
-        const int r = e / CPR, c = (e % CPR) * 8;
-        const int key = k0 + r;
-        if (key < n_keys) {
-          cp_async16(Kd + r * RS + c, kslab + (size_t)key * HD + c);
-          cp_async16(Vd + r * RS + c, vslab + (size_t)key * HD + c);
-        } else {
-          *reinterpret_cast<uint4*>(Kd + r * RS + c) = make_uint4(0, 0, 0, 0);
-          *reinterpret_cast<uint4*>(Vd + r * RS + c) = make_uint4(0, 0, 0, 0);
-        }
+// ------------------------------------------------------------------ work order
+// Stream-K segments of CTA range [s, e) in PROCESSING order: the tail of a
+// tile begun by another CTA ("contrib", published first so its owner never
+// waits long), then the head of the tile this CTA owns (fix-up overlaps the
+// MMA of the full tiles that follow), then whole tiles.
+struct SegWalk {
+  int kb, cs, ce, hs, he, fs, fe, k;
+  __device__ __forceinline__ SegWalk(int s, int e, int kb_) : kb(kb_), cs(0), ce(0), hs(0), he(0), fs(0), fe(0), k(0) {
+    if (s >= e) return;
+    int f = s;
+    if (s % kb) {
+      cs = s;
+      ce = min(e, (s / kb + 1) * kb);
+      f = ce;
+    }
+    int fend = e;
+    if (f < e && (e % kb)) {
+      const int t1 = (e - 1) / kb * kb;
+      if (t1 >= f) {
+        hs = t1;
+        he = e;
+        fend = t1;
       }
     }
-    cp_async_commit();
-  };
-#pragma unroll
-  for (int i = 0; i < PK_ATT_STAGES - 1; ++i) issue(i);
-
-  const uint32_t qs_base = (uint32_t)__cvta_generic_to_shared(Qs);
-  uint32_t qa[KSTEP][4];
-  {
-    const int mi = lane >> 3, ri = lane & 7;
-    const int row = ri + (mi & 1) * 8;
-#pragma unroll
-    for (int ks = 0; ks < KSTEP; ++ks) {
-      const int col = ks * 16 + (mi >> 1) * 8;
-      ldsm_x4(qs_base + (uint32_t)(row * RS + col) * 2, qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3]);
+    if (f < fend) {
+      fs = f;
+      fe = fend;
     }
   }
-  const int g = lane >> 2, t4 = lane & 3;
-  const int pos_lo = qpos[g], pos_hi = qpos[g + 8];
-  float o[NT][4];
-#pragma unroll
-  for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
-  float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;
-  const float scale = p.att_scale;
+  // next segment [a, b) of units; false when done
+  __device__ __forceinline__ bool next(int& a, int& b) {
+    if (k == 0) {
+      k = 1;
+      if (ce > cs) {
+        a = cs;
+        b = ce;
+        return true;
+      }
+    }
+    if (k == 1) {
+      k = 2;
+      if (he > hs) {
+        a = hs;
+        b = he;
+        return true;
+      }
+    }
+    if (fs < fe) {
+      a = fs;
+      b = fs + kb;
+      fs = b;
+      return true;
+    }
+    return false;
+  }
+};
 
-  for (int tile = 0; tile < n_tiles; ++tile) {
-    issue(tile + PK_ATT_STAGES - 1);
-    cp_async_wait<PK_ATT_STAGES - 1>();
-    epi_sync();
-    const uint8_t* st = ring + (tile % PK_ATT_STAGES) * STAGE;
-    const uint32_t kb = (uint32_t)__cvta_generic_to_shared(st);
-    const uint32_t vb = kb + (uint32_t)TILE;
-    const int kw = warp * 16;
+// Attention work: item = (sequence, kv head, 16-query chunk); its keys
+// [0, maxpos] stream through the shared TMA ring as "KV units" of UK keys
+// (K and V tiles, 16 KB: UK = 32 at hd 128, 64 at hd 64).
+struct AttnItem {
+  int seq, kvh, chunk, n_units, maxp;
+};
+__device__ __forceinline__ AttnItem attn_item_of(const PkParams& p, int i) {
+  AttnItem it;
+  const int group = p.nq / p.nkv;
+  const int nQ = group * p.q_len;
+  const int n_chunks = (nQ + 15) / 16;
+  it.chunk = i % n_chunks;
+  it.kvh = (i / n_chunks) % p.nkv;
+  it.seq = i / (n_chunks * p.nkv);
+  int mp = -1;
+  const int t0 = (it.chunk * 16) / group, t1 = min(nQ - 1, it.chunk * 16 + 15) / group;
+  for (int t = t0; t <= t1; ++t) mp = max(mp, p.pos[it.seq * p.q_len + t]);
+  it.maxp = mp;
+  const int uk = 4096 / p.hd;
+  it.n_units = (mp + 1 + uk - 1) / uk;
+  return it;
+}
+__device__ __forceinline__ int attn_items(const PkParams& p) {
+  const int group = p.nq / p.nkv;
+  return p.n_seq * p.nkv * ((group * p.q_len + 15) / 16);
+}
+// row of the first key of unit v of an item in the [rows, hd] view of the cache
+__device__ __forceinline__ int kv_row(const PkParams& p, int layer, const AttnItem& it, int v) {
+  const int slot = p.slot[it.seq];
+  return (int)((((size_t)layer * p.kv_slots + slot) * p.nkv + it.kvh) * p.ctx_max) + v * (4096 / p.hd);
+}
+
+// The CTA's ring work sequence (GEMM weight units and attention KV units, in
+// ring order) as a resumable cursor: the weight producer walks it twice, once
+// to fill the smem ring and once, `l2_ahead` units in front, to prefetch into L2.
+struct UnitCursor {
+  int ph, kind, layer, gk, a, b, u, i, v, nu, n_items;
+  SegWalk sw;
+  AttnItem item;
+  __device__ __forceinline__ UnitCursor() : ph(0), kind(-1), layer(0), gk(0), a(0), b(0), u(0), i(0), v(0), nu(0),
+                                            n_items(0), sw(0, 0, 1) {}
+  // next unit; kind_out PH_GEMM (u_out = unit of gemm gk_out) or PH_ATTN (item_out, v_out)
+  __device__ __forceinline__ bool next(const PkParams& p, int c, bool& waited, int& kind_out, int& layer_out,
+                                       int& gk_out, int& u_out, AttnItem& item_out, int& v_out) {
+    while (true) {
+      if (kind == PH_GEMM) {
+        if (u < b) {
+          kind_out = PH_GEMM;
+          layer_out = layer;
+          gk_out = gk;
+          u_out = u++;
+          return true;
+        }
+        if (sw.next(a, b)) {
+          u = a;
+          continue;
+        }
+      } else if (kind == PH_ATTN) {
+        if (v < nu) {
+          kind_out = PH_ATTN;
+          layer_out = layer;
+          item_out = item;
+          v_out = v++;
+          return true;
+        }
+        i += p.G;
+        if (i < n_items) {
+          item = attn_item_of(p, i);
+          nu = item.n_units;
+          v = 0;
+          continue;
+        }
+      }
+      if (++ph >= p.n_phases) return false;
+      kind = phase_kind(p, ph, layer, gk);
+      if (kind == PH_GEMM) {
+        int s, e;
+        unit_range(p.g[gk], c, s, e);
+        sw = SegWalk(s, e, p.g[gk].kb);
+        u = b = 0;
+      } else if (kind == PH_ATTN) {
+        if (!waited) {
+          griddep_wait();  // positions come from the previous kernel
+          waited = true;
+        }
+        n_items = attn_items(p);
+        i = c - p.G;
+        v = nu = 0;
+      } else {
+        kind = -1;
+      }
+    }
+  }
+};
+
+// swizzled (128B) smem address of 16-byte chunk `ch` (0..7) of row r in a
+// [rows][128 B] TMA box; `base` 1024-aligned
+__device__ __forceinline__ uint32_t sw_addr(uint32_t base, int r, int ch) {
+  return base + (uint32_t)(r * 128) + (uint32_t)(((ch ^ (r & 7)) & 7) << 4);
+}
+
+// One warp's share (KW = 2048/HD keys) of one KV unit: S = Q K^T, online
+// softmax, O += P V (mma.sync m16n8k16; Q fragments in registers).
+template <int HD>
+__device__ __forceinline__ void attn_unit(uint32_t kbase, uint32_t vbase, int key0, int kw, const uint32_t (&qa)[HD / 16][4],
+                                          int pos_lo, int pos_hi, float scale, float (&o)[HD / 8][4], float& m_lo,
+                                          float& m_hi, float& l_lo, float& l_hi) {
+  constexpr int KSTEP = HD / 16, NT = HD / 8, UK = 4096 / HD, KW = UK / 2;
+  const int lane = threadIdx.x & 31;
+  const int mi = lane >> 3, ri = lane & 7;
+  const int g = lane >> 2, t4 = lane & 3;
+#pragma unroll
+  for (int sb = 0; sb < KW / 16; ++sb) {
+    const int kl = kw + sb * 16;  // first key (within the unit) of this 16-key block
     float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
     {
-      const int mi = lane >> 3, ri = lane & 7;
-      const int key = kw + ri + (mi >> 1) * 8;
+      const int key = kl + ri + (mi >> 1) * 8;
 #pragma unroll
       for (int ks = 0; ks < KSTEP; ++ks) {
+        const int col = ks * 16 + (mi & 1) * 8;  // element column
         uint32_t b0, b1, b2, b3;
-        ldsm_x4(kb + (uint32_t)(key * RS + ks * 16 + (mi & 1) * 8) * 2, b0, b1, b2, b3);
+        ldsm_x4(sw_addr(kbase + (uint32_t)((col >> 6) * UK * 128), key, (col & 63) >> 3), b0, b1, b2, b3);
         mma_bf16(s0, qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b0, b1);
         mma_bf16(s1, qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b2, b3);
       }
     }
-    const int kbase = tile * PK_ATT_KT + kw + 2 * t4;
+    const int kbase_i = key0 + kl + 2 * t4;
     float v[8] = {s0[0], s0[1], s1[0], s1[1], s0[2], s0[3], s1[2], s1[3]};
-    const int kidx[4] = {kbase, kbase + 1, kbase + 8, kbase + 9};
+    const int kidx[4] = {kbase_i, kbase_i + 1, kbase_i + 8, kbase_i + 9};
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       v[i] = (kidx[i] <= pos_lo) ? v[i] * scale : -INFINITY;
@@ -322,61 +400,127 @@ __device__ void attn_item(const PkParams& p, uint8_t* epi, int seq, int kvh, int
     const uint32_t pa0 = pack_bf16(pr[0], pr[1]), pa1 = pack_bf16(pr[4], pr[5]);
     const uint32_t pa2 = pack_bf16(pr[2], pr[3]), pa3 = pack_bf16(pr[6], pr[7]);
     {
-      const int mi = lane >> 3, ri = lane & 7;
-      const int key = kw + ri + (mi & 1) * 8;
+      const int key = kl + ri + (mi & 1) * 8;
 #pragma unroll
       for (int n = 0; n < NT; n += 2) {
+        const int col = n * 8 + (mi >> 1) * 8;
         uint32_t b0, b1, b2, b3;
-        ldsm_x4_t(vb + (uint32_t)(key * RS + n * 8 + (mi >> 1) * 8) * 2, b0, b1, b2, b3);
+        ldsm_x4_t(sw_addr(vbase + (uint32_t)((col >> 6) * UK * 128), key, (col & 63) >> 3), b0, b1, b2, b3);
         mma_bf16(o[n], pa0, pa1, pa2, pa3, b0, b1);
         mma_bf16(o[n + 1], pa0, pa1, pa2, pa3, b2, b3);
       }
     }
-    epi_sync();
   }
-  cp_async_wait<0>();
-  epi_sync();
-  float* comb = reinterpret_cast<float*>(ring);
+}
+
+// The attention phase of one CTA: its items in order, KV units consumed from
+// the ring by two warp pairs (pair q takes units q, q+2, ...; within a unit
+// each warp takes half the keys), warps combined in order through smem.
+template <int HD>
+__device__ void attn_phase(const PkParams& p, const PkSmem& sm, uint32_t stage_bytes, int S, uint32_t& it, int c,
+                           int* qpos, int* qtok, int* qhead) {
+  constexpr int RS = HD + 8, KSTEP = HD / 16, NT = HD / 8, UK = 4096 / HD, KW = UK / 2;
+  const int tid = threadIdx.x - 64, warp = tid >> 5, lane = tid & 31;
+  const int pair = warp >> 1, wp = warp & 1;
+  __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(sm.epi);
+  float* comb = reinterpret_cast<float*>(sm.epi + (size_t)16 * RS * 2);
   float* cm = comb + 4 * 16 * HD;
   float* cl = cm + 4 * 16;
-#pragma unroll
-  for (int n = 0; n < NT; ++n) {
-    const int d = n * 8 + 2 * t4;
-    comb[(warp * 16 + g) * HD + d] = o[n][0];
-    comb[(warp * 16 + g) * HD + d + 1] = o[n][1];
-    comb[(warp * 16 + g + 8) * HD + d] = o[n][2];
-    comb[(warp * 16 + g + 8) * HD + d + 1] = o[n][3];
-  }
-  if (t4 == 0) {
-    cm[warp * 16 + g] = m_lo;
-    cm[warp * 16 + g + 8] = m_hi;
-    cl[warp * 16 + g] = l_lo;
-    cl[warp * 16 + g + 8] = l_hi;
-  }
-  epi_sync();
-  for (int e = tid; e < 16 * HD; e += 128) {
-    const int j = e / HD, d = e % HD;
-    if (qpos[j] < 0) continue;
-    float M = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) M = fmaxf(M, cm[w * 16 + j]);
-    float L = 0.f, acc = 0.f;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      const float mw = cm[w * 16 + j];
-      const float f = (mw == -INFINITY) ? 0.f : __expf(mw - M);
-      L += cl[w * 16 + j] * f;
-      acc += comb[(w * 16 + j) * HD + d] * f;
+  const int group = p.nq / p.nkv;
+  const int qd = p.nq * HD;
+  const int G = p.G;
+  const int n_items = attn_items(p);
+  for (int i = c; i < n_items; i += G) {
+    const AttnItem item = attn_item_of(p, i);
+    if (tid < 16) {
+      const int jj = item.chunk * 16 + tid;
+      const int t = jj / group;
+      const bool ok = jj < group * p.q_len;
+      qtok[tid] = ok ? t : 0;
+      qhead[tid] = item.kvh * group + (ok ? jj % group : 0);
+      qpos[tid] = ok ? p.pos[item.seq * p.q_len + t] : -1;
     }
-    p.attn[((size_t)(seq * p.q_len + qtok[j]) * p.nq + qhead[j]) * HD + d] = __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
+    epi_sync();
+    for (int e = tid; e < 16 * (HD / 8); e += 128) {
+      const int j = e / (HD / 8), cc = (e % (HD / 8)) * 8;
+      uint4 v = make_uint4(0, 0, 0, 0);
+      if (qpos[j] >= 0)
+        v = __ldcg(reinterpret_cast<const uint4*>(p.qr + (size_t)(item.seq * p.q_len + qtok[j]) * qd + qhead[j] * HD + cc));
+      *reinterpret_cast<uint4*>(Qs + j * RS + cc) = v;
+    }
+    epi_sync();
+    uint32_t qa[KSTEP][4];
+    {
+      const uint32_t qs_base = (uint32_t)__cvta_generic_to_shared(Qs);
+      const int mi = lane >> 3, ri = lane & 7;
+      const int r = ri + (mi & 1) * 8;
+#pragma unroll
+      for (int ks = 0; ks < KSTEP; ++ks)
+        ldsm_x4(qs_base + (uint32_t)(r * RS + ks * 16 + (mi >> 1) * 8) * 2, qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3]);
+    }
+    const int g = lane >> 2, t4 = lane & 3;
+    const int pos_lo = qpos[g], pos_hi = qpos[g + 8];
+    float o[NT][4];
+#pragma unroll
+    for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
+    float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;
+    for (int v0 = 0; v0 < item.n_units; v0 += 2) {
+      const int v = v0 + pair;
+      if (v < item.n_units) {
+        const uint32_t u = it + (uint32_t)v;
+        const int stg = (int)(u % (uint32_t)S);
+        mbar_wait(&sm.full[stg], (u / S) & 1);
+        const uint32_t kb = smem_u32(sm.ring + (size_t)stg * stage_bytes);
+        attn_unit<HD>(kb, kb + 8192, v * UK, wp * KW, qa, pos_lo, pos_hi, p.att_scale, o, m_lo, m_hi, l_lo, l_hi);
+        asm volatile("bar.sync %0, 64;" ::"r"(2 + pair) : "memory");  // both warps of the pair are done with the stage
+        if (wp == 0 && lane == 0) mbar_arrive(&sm.empty[stg]);
+      }
+      // lockstep: a pair may not run a ring's length ahead of the other (the
+      // mbarrier parity of a stage two rounds ahead would alias)
+      epi_sync();
+    }
+    it += (uint32_t)item.n_units;
+#pragma unroll
+    for (int n = 0; n < NT; ++n) {
+      const int d = n * 8 + 2 * t4;
+      comb[(warp * 16 + g) * HD + d] = o[n][0];
+      comb[(warp * 16 + g) * HD + d + 1] = o[n][1];
+      comb[(warp * 16 + g + 8) * HD + d] = o[n][2];
+      comb[(warp * 16 + g + 8) * HD + d + 1] = o[n][3];
+    }
+    if (t4 == 0) {
+      cm[warp * 16 + g] = m_lo;
+      cm[warp * 16 + g + 8] = m_hi;
+      cl[warp * 16 + g] = l_lo;
+      cl[warp * 16 + g + 8] = l_hi;
+    }
+    epi_sync();
+    for (int e = tid; e < 16 * HD; e += 128) {
+      const int j = e / HD, d = e % HD;
+      if (qpos[j] < 0) continue;
+      float M = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) M = fmaxf(M, cm[w * 16 + j]);
+      float L = 0.f, acc = 0.f;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        const float mw = cm[w * 16 + j];
+        const float f = (mw == -INFINITY) ? 0.f : __expf(mw - M);
+        L += cl[w * 16 + j] * f;
+        acc += comb[(w * 16 + j) * HD + d] * f;
+      }
+      p.attn[((size_t)(item.seq * p.q_len + qtok[j]) * p.nq + qhead[j]) * HD + d] =
+          __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
+    }
+    epi_sync();
   }
-  epi_sync();  // the ring / comb region is reused by the next item
 }
 
 // ------------------------------------------------------------------ the kernel
 __global__ void __launch_bounds__(PK_THREADS, 1)
     persistent_forward_kernel(const __grid_constant__ CUtensorMap map_xb, const __grid_constant__ CUtensorMap map_attn,
                               const __grid_constant__ CUtensorMap map_act, const __grid_constant__ CUtensorMap map_lm,
+                              const __grid_constant__ CUtensorMap map_kc, const __grid_constant__ CUtensorMap map_vc,
                               const __grid_constant__ PkParams p) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* base = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -388,12 +532,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1)
   sm.ring = base;
   size_t off = (size_t)S * stage_bytes;
   sm.epi = base + off;
-  const size_t att_bytes = p.hd == 128 ? (size_t)16 * 136 * 2 + (size_t)PK_ATT_STAGES * 2 * PK_ATT_KT * 136 * 2
-                                       : (size_t)16 * 72 * 2 + (size_t)PK_ATT_STAGES * 2 * PK_ATT_KT * 72 * 2;
-  size_t epi_bytes = att_bytes;
-  if ((size_t)128 * PK_STAGE_PAD * 4 > epi_bytes) epi_bytes = (size_t)128 * PK_STAGE_PAD * 4;
-  if ((size_t)8 * tn * 4 > epi_bytes) epi_bytes = (size_t)8 * tn * 4;
-  off += (epi_bytes + 127) & ~(size_t)127;
+  off += p.epi_bytes;
   sm.inv_s = (float*)(base + off);
   off += PK_MAX_T * 4;
   sm.s_pos = (int*)(base + off);
@@ -406,12 +545,16 @@ __global__ void __launch_bounds__(PK_THREADS, 1)
   sm.tempty = sm.tfull + 2;
   sm.tmem_slot = (uint32_t*)(sm.tempty + 2);
   __shared__ int a_qpos[16], a_qtok[16], a_qhead[16];
+  // attention phases finished by this CTA's epilogue warps: the MMA warp skips the
+  // ring slots of KV units and must not run a ring round ahead of their consumers
+  __shared__ int s_attn_done;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint32_t tmem_cols = 32;
   while ((int)tmem_cols < 2 * tn) tmem_cols <<= 1;
 
   if (threadIdx.x == 0) {
+    s_attn_done = 0;
     for (int s = 0; s < S; ++s) {
       mbar_init(&sm.full[s], 2);
       mbar_init(&sm.empty[s], 1);
@@ -434,37 +577,88 @@ __global__ void __launch_bounds__(PK_THREADS, 1)
   unsigned* bar = p.sync;
   unsigned* done = p.sync + 1;
   unsigned* flags = p.sync + 2;
+  const uint32_t kv_unit_bytes = 16384;
 
   if (warp == 0) {
     // ================= weight producer: runs ahead through every GEMM phase
-    // (weights never depend on earlier phases, nor on the previous kernel)
+    // (weights depend neither on earlier phases nor on the previous kernel);
+    // for the KV units of an attention phase it only arrives (the activation
+    // producer loads them), keeping the ring's FIFO order.  A second cursor
+    // `l2_ahead` units in front prefetches weights / KV into L2, so HBM keeps
+    // streaming through phase tails and grid barriers.
     if (lane == 0) {
       uint32_t it = 0;
-      for (int ph = 1; ph < p.n_phases; ++ph) {
-        int layer, gk;
-        if (phase_kind(p, ph, layer, gk) != PH_GEMM) continue;
-        const PkGemm& g = p.g[gk];
-        const CUtensorMap* wm = wmap_of(p, layer, gk);
-        int s, e;
-        unit_range(g, c, s, e);
-        for (int u = s; u < e; ++u, ++it) {
-          const int stg = (int)(it % S);
-          if (it >= (uint32_t)S) mbar_wait(&sm.empty[stg], ((it / S) + 1) & 1);
+      bool waited = false;
+      UnitCursor ld, pf;
+      int kd, ly, gk, u, v;
+      AttnItem item;
+      auto prefetch = [&](int kd_, int ly_, int gk_, int u_, const AttnItem& item_, int v_) {
+        if (kd_ == PH_GEMM) {
+          const PkGemm& g = p.g[gk_];
+          const int tile = u_ / g.kb, kbi = u_ - tile * g.kb;
+          tma_prefetch_2d(wmap_of(p, ly_, gk_), kbi * TC_BK, tile * TC_BM);
+        } else {
+          const int r0 = kv_row(p, ly_, item_, v_);
+          for (int h = 0; h < p.hd / 64; ++h) {
+            tma_prefetch_2d(&map_kc, h * 64, r0);
+            tma_prefetch_2d(&map_vc, h * 64, r0);
+          }
+        }
+      };
+      for (int k = 0; k < p.l2_ahead && pf.next(p, c, waited, kd, ly, gk, u, item, v); ++k)
+        prefetch(kd, ly, gk, u, item, v);
+      while (ld.next(p, c, waited, kd, ly, gk, u, item, v)) {
+        {
+          int kd2, ly2, gk2, u2, v2;
+          AttnItem item2;
+          if (p.l2_ahead > 0 && pf.next(p, c, waited, kd2, ly2, gk2, u2, item2, v2)) prefetch(kd2, ly2, gk2, u2, item2, v2);
+        }
+        const int stg = (int)(it % S);
+        if (it >= (uint32_t)S) mbar_wait(&sm.empty[stg], ((it / S) + 1) & 1);
+        if (kd == PH_ATTN) {
+          mbar_arrive(&sm.full[stg]);
+        } else {
+          const PkGemm& g = p.g[gk];
           mbar_arrive_expect(&sm.full[stg], a_bytes);
           const int tile = u / g.kb, kbi = u - tile * g.kb;
-          tma_load_2d(sm.ring + (size_t)stg * stage_bytes, wm, &sm.full[stg], kbi * TC_BK, tile * TC_BM);
+          tma_load_2d(sm.ring + (size_t)stg * stage_bytes, wmap_of(p, ly, gk), &sm.full[stg], kbi * TC_BK, tile * TC_BM);
         }
+        ++it;
       }
     }
   } else if (warp == 6) {
-    // ================= activation producer: X tiles of phase ph only after the
-    // grid barrier says every CTA finished phases < ph
+    // ================= activation producer: X tiles (and attention KV units)
+    // of phase ph only after the grid barrier says every CTA finished phases < ph
     if (lane == 0) {
       griddep_wait();
       uint32_t it = 0;
       for (int ph = 1; ph < p.n_phases; ++ph) {
         int layer, gk;
-        if (phase_kind(p, ph, layer, gk) != PH_GEMM) continue;
+        const int kind = phase_kind(p, ph, layer, gk);
+        if (kind == PH_ATTN) {
+          const int n_items = attn_items(p);
+          if (c < n_items) {
+            wait_geq(bar, (unsigned)(ph * G));
+            fence_proxy_async();
+          }
+          for (int i = c; i < n_items; i += G) {
+            const AttnItem item = attn_item_of(p, i);
+            for (int v = 0; v < item.n_units; ++v, ++it) {
+              const int stg = (int)(it % S);
+              if (it >= (uint32_t)S) mbar_wait(&sm.empty[stg], ((it / S) + 1) & 1);
+              mbar_arrive_expect(&sm.full[stg], kv_unit_bytes);
+              const int r0 = kv_row(p, layer, item, v);
+              uint8_t* dst = sm.ring + (size_t)stg * stage_bytes;
+              const int uk = 4096 / p.hd;
+              for (int h = 0; h < p.hd / 64; ++h) {
+                tma_load_2d(dst + h * uk * 128, &map_kc, &sm.full[stg], h * 64, r0);
+                tma_load_2d(dst + 8192 + h * uk * 128, &map_vc, &sm.full[stg], h * 64, r0);
+              }
+            }
+          }
+          continue;
+        }
+        if (kind != PH_GEMM) continue;
         const PkGemm& g = p.g[gk];
         const CUtensorMap* xm = gk == PG_O ? &map_attn : (gk == PG_DOWN ? &map_act : (gk == PG_LM ? &map_lm : &map_xb));
         int s, e;
@@ -473,37 +667,53 @@ __global__ void __launch_bounds__(PK_THREADS, 1)
           wait_geq(bar, (unsigned)(ph * G));
           fence_proxy_async();
         }
-        for (int u = s; u < e; ++u, ++it) {
-          const int stg = (int)(it % S);
-          if (it >= (uint32_t)S) mbar_wait(&sm.empty[stg], ((it / S) + 1) & 1);
-          mbar_arrive_expect(&sm.full[stg], b_bytes);
-          const int kbi = u % g.kb;
-          tma_load_2d(sm.ring + (size_t)stg * stage_bytes + a_bytes, xm, &sm.full[stg], kbi * TC_BK, 0);
+        SegWalk sw(s, e, g.kb);
+        int a, b;
+        while (sw.next(a, b)) {
+          for (int u = a; u < b; ++u, ++it) {
+            const int stg = (int)(it % S);
+            if (it >= (uint32_t)S) mbar_wait(&sm.empty[stg], ((it / S) + 1) & 1);
+            mbar_arrive_expect(&sm.full[stg], b_bytes);
+            const int kbi = u % g.kb;
+            tma_load_2d(sm.ring + (size_t)stg * stage_bytes + a_bytes, xm, &sm.full[stg], kbi * TC_BK, 0);
+          }
         }
       }
     }
   } else if (warp == 1) {
-    // ================= MMA issuer
+    // ================= MMA issuer (skips the ring slots of attention KV units)
     if (lane == 0) {
       const uint32_t idesc = make_idesc(tn);
       uint32_t it = 0, seg = 0;
+      int n_attn = 0;
+      bool waited = false;
       for (int ph = 1; ph < p.n_phases; ++ph) {
         int layer, gk;
-        if (phase_kind(p, ph, layer, gk) != PH_GEMM) continue;
+        const int kind = phase_kind(p, ph, layer, gk);
+        if (kind == PH_ATTN) {
+          if (!waited) {
+            griddep_wait();
+            waited = true;
+          }
+          const int n_items = attn_items(p);
+          for (int i = c; i < n_items; i += G) it += (uint32_t)attn_item_of(p, i).n_units;
+          ++n_attn;
+          while (*(volatile int*)&s_attn_done < n_attn) __nanosleep(20);
+          continue;
+        }
+        if (kind != PH_GEMM) continue;
         const PkGemm& g = p.g[gk];
         int s, e;
         unit_range(g, c, s, e);
-        int u = s;
-        while (u < e) {
-          const int tile = u / g.kb;
-          const int seg_end = min(e, (tile + 1) * g.kb);
+        SegWalk sw(s, e, g.kb);
+        int a, b;
+        while (sw.next(a, b)) {
           const int buf = seg & 1;
           const uint32_t use = seg >> 1;
           if (seg >= 2) mbar_wait(&sm.tempty[buf], (use + 1) & 1);
           tc_fence_after();
           const uint32_t d = tmem + (uint32_t)(buf * tn);
-          const int first = u;
-          for (; u < seg_end; ++u, ++it) {
+          for (int u = a; u < b; ++u, ++it) {
             const int stg = (int)(it % S);
             mbar_wait(&sm.full[stg], (it / S) & 1);
             tc_fence_after();
@@ -512,7 +722,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1)
 #pragma unroll
             for (int kk = 0; kk < TC_BK / TC_UK; ++kk)
               tc_mma(d, sw128_desc(sa + kk * TC_UK * 2), sw128_desc(sb + kk * TC_UK * 2), idesc,
-                     (u > first || kk > 0) ? 1u : 0u);
+                     (u > a || kk > 0) ? 1u : 0u);
             tc_commit(&sm.empty[stg]);
           }
           tc_commit(&sm.tfull[buf]);
@@ -529,11 +739,15 @@ __global__ void __launch_bounds__(PK_THREADS, 1)
     const uint32_t lane_addr = tmem + ((uint32_t)(quad * 32) << 16);
     const int T = p.T, H = p.H;
     const int nTH = (H + TC_BM - 1) / TC_BM;  // norm partials written by o / down
-    uint32_t seg = 0;
+    uint32_t seg = 0, it = 0;
     for (int ph = 0; ph < p.n_phases; ++ph) {
       int layer, gk;
       const int kind = phase_kind(p, ph, layer, gk);
+      unsigned long long* tr = p.trace ? p.trace + ((size_t)c * p.n_phases + ph) * 8 : nullptr;
+      if (tr && et == 0) tr[0] = globaltimer();
       if (et == 0) wait_geq(bar, (unsigned)(ph * G));
+      if (tr && et == 0) tr[1] = globaltimer();
+      bool first_seg = true;
       epi_sync();
       if (kind == PH_EMBED) {
         float* red = reinterpret_cast<float*>(sm.epi);
@@ -555,18 +769,12 @@ __global__ void __launch_bounds__(PK_THREADS, 1)
           epi_sync();
         }
       } else if (kind == PH_ATTN) {
-        const int group = p.nq / p.nkv;
-        const int n_chunks = (group * p.q_len + 15) / 16;
-        const int items = p.n_seq * p.nkv * n_chunks;
-        for (int i = c; i < items; i += G) {
-          const int chunk = i % n_chunks;
-          const int kvh = (i / n_chunks) % p.nkv;
-          const int seq = i / (n_chunks * p.nkv);
-          if (p.hd == 128)
-            attn_item<128>(p, sm.epi, seq, kvh, chunk, a_qpos, a_qtok, a_qhead);
-          else
-            attn_item<64>(p, sm.epi, seq, kvh, chunk, a_qpos, a_qtok, a_qhead);
-        }
+        if (p.hd == 128)
+          attn_phase<128>(p, sm, stage_bytes, S, it, c, a_qpos, a_qtok, a_qhead);
+        else
+          attn_phase<64>(p, sm, stage_bytes, S, it, c, a_qpos, a_qtok, a_qhead);
+        epi_sync();
+        if (et == 0) *(volatile int*)&s_attn_done = layer + 1;
       } else if (kind == PH_FINAL) {
         const int nt = p.g[PG_LM].n_tiles;
         const int rows = p.lm_rows;
@@ -590,6 +798,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1)
         const int rows = gk == PG_LM ? p.lm_rows : T;
         int s, e;
         unit_range(g, c, s, e);
+        it += (uint32_t)(e - s);
         if (s < e) {
           if (norm_in) {
             int P_in = nTH;
@@ -604,7 +813,13 @@ __global__ void __launch_bounds__(PK_THREADS, 1)
               float sacc = 0.f;
               if (j < rows) {
                 const float* src = p.npart + (size_t)j * step + roff;
-                for (int q = 0; q < P_in; ++q) sacc += __ldcg(src + (size_t)q * T);
+                for (int q0 = 0; q0 < P_in; q0 += 8) {  // 8 loads in flight, summed in order
+                  float t8[8];
+#pragma unroll
+                  for (int i = 0; i < 8; ++i) t8[i] = q0 + i < P_in ? __ldcg(src + (size_t)(q0 + i) * T) : 0.f;
+#pragma unroll
+                  for (int i = 0; i < 8; ++i) sacc += t8[i];
+                }
               }
               sm.inv_s[j] = rsqrtf(sacc * p.inv_h + p.eps);
             }
@@ -617,12 +832,12 @@ __global__ void __launch_bounds__(PK_THREADS, 1)
           }
           epi_sync();
         }
-        int u = s;
-        while (u < e) {
-          const int tile = u / g.kb;
-          const int a0 = u - tile * g.kb;
-          const int seg_end = min(e, (tile + 1) * g.kb);
-          const int b1 = seg_end - tile * g.kb;
+        SegWalk sw(s, e, g.kb);
+        int a_u, b_u;
+        while (sw.next(a_u, b_u)) {
+          const int tile = a_u / g.kb;
+          const int a0 = a_u - tile * g.kb;
+          const int b1 = b_u - tile * g.kb;
           const bool contrib = a0 > 0;
           const bool owner = a0 == 0 && b1 < g.kb;
           const int buf = seg & 1;
@@ -632,10 +847,16 @@ __global__ void __launch_bounds__(PK_THREADS, 1)
           int c_last = c;
           if (owner) {
             while (c_last + 1 < g.ctas && unit_start(g, c_last + 1) < (tile + 1) * g.kb) ++c_last;
-            if (et == 0)
+            if (et == 0) {
+              if (tr) tr[4] = globaltimer();
               for (int c2 = c + 1; c2 <= c_last; ++c2) wait_geq(&flags[c2], (unsigned)(ph + 1));
+              if (tr) tr[5] = globaltimer();
+            }
           }
           mbar_wait(&sm.tfull[buf], use & 1);
+          if (tr && et == 0 && first_seg) tr[2] = globaltimer();
+          if (tr && et == 0) tr[6] = globaltimer();
+          first_seg = false;
           tc_fence_after();
           if (owner) epi_sync();
           // QKV tile region: 0 = Q, 1 = K, 2 = V (tiles never straddle: checked on the host)
@@ -648,23 +869,45 @@ __global__ void __launch_bounds__(PK_THREADS, 1)
             float v[16];
             tmem_ld16(lane_addr + (uint32_t)(buf * tn + j0), v);
             if (contrib) {
-              float* dst = p.scratch + ((size_t)c * tn + j0) * TC_BM + row;
+              // partial tile, row-major per weight row: [c][row][tn] (float4 stores / loads)
+              float4* dst = reinterpret_cast<float4*>(p.scratch + ((size_t)c * TC_BM + row) * tn + j0);
 #pragma unroll
-              for (int j = 0; j < 16; ++j) dst[(size_t)j * TC_BM] = v[j];
+              for (int q = 0; q < 4; ++q) __stcg(dst + q, make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]));
               continue;
             }
             if (owner) {
-              for (int c2 = c + 1; c2 <= c_last; ++c2) {
-                const float* src = p.scratch + ((size_t)c2 * tn + j0) * TC_BM + row;
+              // contributors in CTA order, up to four partials in flight per batch
+              for (int c0 = c + 1; c0 <= c_last; c0 += 4) {
+                float4 pr[4][4];
 #pragma unroll
-                for (int j = 0; j < 16; ++j) v[j] += __ldcg(src + (size_t)j * TC_BM);
+                for (int w = 0; w < 4; ++w) {
+                  if (c0 + w <= c_last) {
+                    const float4* src =
+                        reinterpret_cast<const float4*>(p.scratch + ((size_t)(c0 + w) * TC_BM + row) * tn + j0);
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) pr[w][q] = __ldcg(src + q);
+                  }
+                }
+#pragma unroll
+                for (int w = 0; w < 4; ++w) {
+                  if (c0 + w <= c_last) {
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                      v[4 * q] += pr[w][q].x;
+                      v[4 * q + 1] += pr[w][q].y;
+                      v[4 * q + 2] += pr[w][q].z;
+                      v[4 * q + 3] += pr[w][q].w;
+                    }
+                  }
+                }
               }
             }
             if (gk == PG_QKV) {
 #pragma unroll
               for (int j = 0; j < 16; ++j) v[j] = bf16r(v[j] * sm.inv_s[j0 + j]);
-              const int d = (n - (region == 0 ? 0 : (region == 1 ? qd : qd + kd))) % p.hd;
-              const int head = (n - (region == 0 ? 0 : (region == 1 ? qd : qd + kd))) / p.hd;
+              const int rbase = region == 0 ? 0 : (region == 1 ? qd : qd + kd);
+              const int d = (n - rbase) % p.hd;
+              const int head = (n - rbase) / p.hd;
               __nv_bfloat16* kv_base = (region == 1 ? p.kc : p.vc) + (size_t)layer * p.layer_kv;
               if (region < 2) {
                 const int half = p.hd >> 1;
@@ -674,15 +917,21 @@ __global__ void __launch_bounds__(PK_THREADS, 1)
                 const bool lo = d < half;
                 const int prow = lo ? row + half : row - half;
                 const int di = lo ? d : d - half;
+                float cs[16], sn[16];
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {  // table loads first, all in flight
+                  const int ps = sm.s_pos[j0 + j];
+                  const int pc = ps < 0 ? 0 : (ps >= p.max_pos ? p.max_pos - 1 : ps);
+                  cs[j] = __ldg(&p.cosT[(size_t)pc * half + di]);
+                  sn[j] = __ldg(&p.sinT[(size_t)pc * half + di]);
+                }
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
                   const int m = j0 + j;
                   if (m >= T || n >= N) continue;
                   const float xp = stage_f[prow * PK_STAGE_PAD + j];
                   const int ps = sm.s_pos[m];
-                  const int pc = ps < 0 ? 0 : (ps >= p.max_pos ? p.max_pos - 1 : ps);
-                  const float cs = p.cosT[(size_t)pc * half + di], sn = p.sinT[(size_t)pc * half + di];
-                  const float r = lo ? v[j] * cs - xp * sn : v[j] * cs + xp * sn;
+                  const float r = lo ? v[j] * cs[j] - xp * sn[j] : v[j] * cs[j] + xp * sn[j];
                   const __nv_bfloat16 ob = __float2bfloat16_rn(r);
                   if (region == 0) {
                     p.qr[(size_t)m * qd + n] = ob;
@@ -712,13 +961,20 @@ __global__ void __launch_bounds__(PK_THREADS, 1)
                   p.act[(size_t)m * (N / 2) + n / 2] = __float2bfloat16_rn(pk_silu(x) * other);
               }
             } else if (gk == PG_O || gk == PG_DOWN) {
+              // all 16 residual loads in flight before any store (one L2 round trip per chunk)
+              float rv[16];
+#pragma unroll
+              for (int j = 0; j < 16; ++j) {
+                const int m = j0 + j;
+                rv[j] = (m < T && n < N) ? __ldcg(&p.resid[(size_t)m * H + n]) : 0.f;
+              }
 #pragma unroll
               for (int j = 0; j < 16; ++j) {
                 const int m = j0 + j;
                 float sq = 0.f;
                 if (m < T && n < N) {
                   const size_t o = (size_t)m * H + n;
-                  const float nv = __ldcg(&p.resid[o]) + v[j];
+                  const float nv = rv[j] + v[j];
                   p.resid[o] = nv;
                   p.xb[o] = __float2bfloat16_rn(nv);
                   sq = nv * nv;
@@ -750,6 +1006,7 @@ __global__ void __launch_bounds__(PK_THREADS, 1)
             if (et == 0) {
               __threadfence();
               st_release_u32(&flags[c], (unsigned)(ph + 1));
+              if (tr) tr[7] = globaltimer();
             }
           } else if (gk == PG_O || gk == PG_DOWN || (gk == PG_LM && p.want_argmax)) {
             epi_sync();
@@ -766,13 +1023,13 @@ __global__ void __launch_bounds__(PK_THREADS, 1)
             }
             epi_sync();
           }
-          u = seg_end;
           ++seg;
         }
       }
       // ---- phase done: publish (fence orders generic writes for other SMs' TMA reads)
       epi_sync();
       if (et == 0) {
+        if (tr) tr[3] = globaltimer();
         __threadfence();
         fence_proxy_async();
         atomicAdd(bar, 1u);
@@ -802,15 +1059,17 @@ __global__ void __launch_bounds__(PK_THREADS, 1)
 }
 
 // ------------------------------------------------------------------ host side
-static int g_persistent = 1;  // sb_set_persistent
+static int g_persistent = 0;  // sb_set_persistent (off by default: see DESIGN.md §4b)
+static unsigned long long* g_pk_trace = nullptr;  // sb_debug_persistent_trace
 
+// epilogue-warp smem region (phases use it one at a time): attention Q tile +
+// 4-warp combine buffer, RoPE pair staging, per-quadrant norm / argmax partials
 static size_t pk_epi_bytes(int hd, int tn) {
-  const int RS = hd + 8;
-  size_t att = (size_t)16 * RS * 2 + (size_t)PK_ATT_STAGES * 2 * PK_ATT_KT * RS * 2;
+  size_t att = (size_t)16 * (hd + 8) * 2 + (size_t)4 * 16 * hd * 4 + 2 * 4 * 16 * 4;
   size_t e = att;
   if ((size_t)128 * PK_STAGE_PAD * 4 > e) e = (size_t)128 * PK_STAGE_PAD * 4;
   if ((size_t)8 * tn * 4 > e) e = (size_t)8 * tn * 4;
-  return (e + 127) & ~(size_t)127;
+  return (e + 1023) & ~(size_t)1023;
 }
 
 static int pk_grid() {
@@ -833,10 +1092,19 @@ bool persistent_eligible(const sb_decoder_t* m, int T) {
   if (m->head_dim != 64 && m->head_dim != 128) return false;
   const int qd = m->n_heads * m->head_dim, kd = m->n_kv_heads * m->head_dim;
   if (qd % TC_BM || kd % TC_BM) return false;
-  if (m->hidden % 64 || m->ffn % 64 || qd % 64) return false;
+  if (m->hidden % 8 || m->ffn % 8) return false;  // 16-byte TMA row strides
   if (m->n_heads % m->n_kv_heads) return false;
   return true;
 }
+
+#define PK_TRY(expr)                                                                           \
+  do {                                                                                         \
+    int rc_ = (expr);                                                                          \
+    if (rc_ != 0) {                                                                            \
+      if (getenv("SB_DEBUG")) fprintf(stderr, "persistent_forward: %s -> %d\n", #expr, rc_); \
+      return rc_;                                                                              \
+    }                                                                                          \
+  } while (0)
 
 int persistent_forward(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* ids, const int32_t* slot,
                        const int32_t* pos, int n_seq, int q_len, float* logits, int logits_mode,
@@ -865,7 +1133,7 @@ int persistent_forward(const sb_decoder_t* m, const sb_kvcache_t* kv, const int3
   p.lm_off = last ? q_len - 1 : 0;
   p.want_argmax = want_lm && sink != nullptr;
   p.want_logits = want_lm && logits != nullptr;
-  if (want_lm && !p.want_argmax && !p.want_logits) return SB_EINVAL;
+  if (want_lm && !p.want_argmax && !p.want_logits) PK_TRY(SB_EINVAL);
   p.n_phases = 1 + 5 * p.L + (want_lm ? 1 : 0) + (p.want_argmax ? 1 : 0);
   p.eps = m->rms_eps;
   p.inv_h = 1.0f / (float)p.H;
@@ -906,6 +1174,7 @@ int persistent_forward(const sb_decoder_t* m, const sb_kvcache_t* kv, const int3
   p.amax_idx = b.amax_idx;
   p.scratch = b.scratch;
   p.sync = b.sync;
+  p.trace = g_pk_trace;
   if (sink) {
     p.out_tok = sink->out_tok;
     p.out_stride = sink->out_stride;
@@ -917,27 +1186,42 @@ int persistent_forward(const sb_decoder_t* m, const sb_kvcache_t* kv, const int3
   }
   // shared memory: ring gets what the epilogue region leaves
   const size_t epi = pk_epi_bytes(p.hd, p.tn);
+  p.epi_bytes = (int)epi;
+  {
+    static int ahead = -1;
+    if (ahead < 0) {
+      const char* env = getenv("SB_PK_L2_AHEAD");
+      ahead = env ? atoi(env) : 0;  // measured: L2 prefetch ahead of the ring slows the stream
+    }
+    p.l2_ahead = ahead;
+  }
   const size_t fixed = 1024 + epi + 3 * PK_MAX_T * 4 + 64 * 8 + 16;
   const size_t budget = 226 * 1024;
   const size_t stage = (size_t)(TC_BM + p.tn) * TC_BK * 2;
   int S = (int)((budget - fixed) / stage);
   if (S > 16) S = 16;
-  if (S < 2) return SB_EUNSUPPORTED;
+  if (S < 2) PK_TRY(SB_EUNSUPPORTED);
   p.stages = S;
   const size_t smem = 1024 + (size_t)S * stage + epi + 3 * PK_MAX_T * 4 + (2 * S + 4) * 8 + 16;
-  static bool attr = false;
-  if (!attr) {
+  static size_t attr_smem = 0;
+  if (smem > attr_smem) {
     cudaError_t e = cudaFuncSetAttribute(persistent_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         227 * 1024);
-    if (e != cudaSuccess) return (int)e;
-    attr = true;
+                                         (int)smem);
+    PK_TRY((int)e);
+    attr_smem = smem;
   }
-  CUtensorMap mx, ma, mc, ml;
-  SB_TRY(make_map(&mx, b.xb, T, p.H, p.H, p.tn));
-  SB_TRY(make_map(&ma, b.attn, T, qd, qd, p.tn));
-  SB_TRY(make_map(&mc, b.act, T, p.ffn, p.ffn, p.tn));
+  CUtensorMap mx, ma, mc, ml, mk, mv;
+  {
+    // KV cache as a 2-D [L*slots*nkv*ctx_max, hd] tensor: attention KV units of 4096/hd keys
+    const int kv_rows = (int)((size_t)p.L * kv->slots * p.nkv * kv->ctx_max);
+    PK_TRY(make_map(&mk, kv->k, kv_rows, p.hd, p.hd, 4096 / p.hd));
+    PK_TRY(make_map(&mv, kv->v, kv_rows, p.hd, p.hd, 4096 / p.hd));
+  }
+  PK_TRY(make_map(&mx, b.xb, T, p.H, p.H, p.tn));
+  PK_TRY(make_map(&ma, b.attn, T, qd, qd, p.tn));
+  PK_TRY(make_map(&mc, b.act, T, p.ffn, p.ffn, p.tn));
   if (want_lm) {
-    SB_TRY(make_map(&ml, (const char*)b.xb + (size_t)p.lm_off * p.H * 2, p.lm_rows, p.H, p.lm_step * p.H, p.tn));
+    PK_TRY(make_map(&ml, (const char*)b.xb + (size_t)p.lm_off * p.H * 2, p.lm_rows, p.H, p.lm_step * p.H, p.tn));
   } else {
     ml = mx;
   }
@@ -951,9 +1235,18 @@ int persistent_forward(const sb_decoder_t* m, const sb_kvcache_t* kv, const int3
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = g_pdl ? 1 : 0;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, persistent_forward_kernel, mx, ma, mc, ml, p);
-  if (e != cudaSuccess) return (int)e;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, persistent_forward_kernel, mx, ma, mc, ml, mk, mv, p);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "specbatch_b200: persistent forward launch failed: %s (T=%d tn=%d stages=%d smem=%zu)\n",
+            cudaGetErrorString(e), T, p.tn, S, smem);
+    return (int)e;
+  }
   ++g_kernel_count;
+  return 0;
+}
+
+int set_persistent_trace(void* buf) {
+  g_pk_trace = (unsigned long long*)buf;
   return 0;
 }
 

@@ -32,7 +32,7 @@ def _run(dec, persistent, ids, pos, slots, b, q, logits_mode, ws, kv, sink=None)
         torch.cuda.synchronize()
         return logits
     finally:
-        lib.sb_set_persistent(1)
+        lib.sb_set_persistent(0)
 
 
 def _case(cfg, cuda_dev, b, P, k, seed=0):
@@ -59,14 +59,16 @@ SHAPES = [
     ("68m", CONFIGS["llama-68m"], 8, 12, 3),
     ("7b-2l", replace(CONFIGS["llama-2-7b"], n_layers=2), 8, 16, 3),
     ("7b-2l-b8k8", replace(CONFIGS["llama-2-7b"], n_layers=2), 8, 20, 8),
+    ("7b-1l-long", replace(CONFIGS["llama-2-7b"], n_layers=1), 2, 100, 4),
+    ("68m-long", CONFIGS["llama-68m"], 2, 110, 3),
 ]
 
 
 @pytest.mark.parametrize("name,cfg,b,P,k", SHAPES, ids=[s[0] for s in SHAPES])
 def test_persistent_matches_layered(cuda_dev, name, cfg, b, P, k):
     dec, slots, ws, (ids1, pos1), (ids2, pos2) = _case(cfg, cuda_dev, b, P, k)
-    kv_a = dec.new_kv(b, 128)
-    kv_b = dec.new_kv(b, 128)
+    kv_a = dec.new_kv(b, 160)
+    kv_b = dec.new_kv(b, 160)
     # prompt (T = b*P) then a speculative window (T = b*(k+1)) on each path
     la1 = _run(dec, False, ids1, pos1, slots, b, P, N.LOGITS_ALL, ws, kv_a)
     lb1 = _run(dec, True, ids1, pos1, slots, b, P, N.LOGITS_ALL, ws, kv_b)
