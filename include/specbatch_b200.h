@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define SB_ABI_VERSION 2
+#define SB_ABI_VERSION 3
 
 /* status codes beyond cudaError_t (which are < 1000) */
 #define SB_OK 0
@@ -61,6 +61,28 @@ extern "C" {
 /* token selection modes for sb_select_tokens */
 #define SB_SELECT_ARGMAX 0
 #define SB_SELECT_SAMPLE 1
+
+/*
+ * Tensor-parallel exchange (BASELINE config 4: a target too large for one GPU,
+ * sharded over 2/4/8 GPUs of one NVLink box).  The forward calls these at its
+ * two exchange points per layer (after the row-parallel o / down projections:
+ * all_reduce_sum of the fp32 partial residual update) and once for the
+ * vocab-parallel lm_head (all_gather of the local logits slice).  Both are
+ * asynchronous on `stream`.  sb_nccl_collectives_init fills one backed by NCCL
+ * over NVLink (graph-capturable); a host may supply its own (tests use
+ * torch.distributed gloo to run TP=2 on one GPU).  Return 0 or an error code.
+ */
+typedef struct sb_collectives {
+  void* ctx;
+  int (*all_reduce_sum)(void* ctx, void* buf, size_t count, int32_t dtype, void* stream);
+  int (*all_gather)(void* ctx, const void* send, void* recv, size_t count_per_rank, int32_t dtype, void* stream);
+  int32_t world, rank;
+} sb_collectives_t;
+
+/* NCCL backend: rank 0 makes the 128-byte id, the host broadcasts it, every rank inits. */
+int sb_nccl_unique_id(void* id_out);
+int sb_nccl_collectives_init(const void* id, int32_t world, int32_t rank, sb_collectives_t* out);
+int sb_nccl_collectives_destroy(sb_collectives_t* c);
 
 /*
  * Llama-style decoder weights.  Arrays of per-layer DEVICE pointers are host
@@ -93,6 +115,11 @@ typedef struct sb_decoder {
   /* bf16 only, optional: device copy of the weight TMA descriptors written by
      sb_decoder_encode_tmaps (enables the persistent forward; NULL = off) */
   const void* tmaps;
+  /* tensor parallelism (NULL = unsharded).  A shard holds n_heads/world q heads,
+     n_kv_heads/world kv heads, ffn/world ffn rows and vocab/world lm_head rows
+     (the fields above are the LOCAL sizes); embedding and norms are replicated.
+     Logits come back full-width [rows, vocab * world] on every rank. */
+  const sb_collectives_t* tp;
 } sb_decoder_t;
 
 /* KV cache: k/v base pointers of layout [n_layers][slots][n_kv_heads][ctx_max][head_dim]. */

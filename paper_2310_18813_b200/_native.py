@@ -31,6 +31,17 @@ _I = C.c_int32
 _PP = C.POINTER(C.c_void_p)
 
 
+_ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int32, C.c_void_p)
+_ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_int32, C.c_void_p)
+
+
+class SbCollectives(C.Structure):
+    """Mirror of ``sb_collectives_t`` (tensor-parallel exchange of a sharded target)."""
+
+    _fields_ = [("ctx", _P), ("all_reduce_sum", _ALLREDUCE_FN), ("all_gather", _ALLGATHER_FN), ("world", _I),
+                ("rank", _I)]
+
+
 class SbDecoder(C.Structure):
     """Mirror of ``sb_decoder_t``."""
 
@@ -39,7 +50,7 @@ class SbDecoder(C.Structure):
         ("ffn", _I), ("vocab", _I), ("dtype", _I), ("max_pos", _I), ("rms_eps", C.c_float),
         ("embed", _P), ("final_norm", _P), ("lm_head", _P),
         ("attn_norm", _PP), ("w_qkv", _PP), ("w_o", _PP), ("mlp_norm", _PP), ("w_gu", _PP), ("w_down", _PP),
-        ("rope_cos", _P), ("rope_sin", _P), ("tmaps", _P),
+        ("rope_cos", _P), ("rope_sin", _P), ("tmaps", _P), ("tp", C.POINTER(SbCollectives)),
     ]
 
 
@@ -64,6 +75,9 @@ _SIGS = {
     "sb_set_fuse_norm": (C.c_int, [_I]),
     "sb_set_attention_impl": (C.c_int, [_I]),
     "sb_set_persistent": (C.c_int, [_I]),
+    "sb_nccl_unique_id": (C.c_int, [_P]),
+    "sb_nccl_collectives_init": (C.c_int, [_P, _I, _I, C.POINTER(SbCollectives)]),
+    "sb_nccl_collectives_destroy": (C.c_int, [C.POINTER(SbCollectives)]),
     "sb_debug_persistent_trace": (C.c_int, [_P]),
     "sb_decoder_tmaps_bytes": (C.c_size_t, [C.POINTER(SbDecoder)]),
     "sb_decoder_encode_tmaps": (C.c_int, [C.POINTER(SbDecoder), _P]),

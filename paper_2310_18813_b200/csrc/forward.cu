@@ -28,6 +28,9 @@ struct FwdWorkspace {
   int* amax_idx;
   void* xb;       // bf16 copy of the residual (fused-RMSNorm GEMM input)
   float* npart;   // sum-of-squares partials [P_max][T]
+  float* tp_part;     // TP: fp32 partial residual update, all-reduced in place [T, H]
+  float* tp_logits;   // TP: local vocab slice of the logits [T, vocab_local]
+  float* tp_gather;   // TP: all-gathered slices [world][T][vocab_local]
   float* pk_scratch;  // persistent forward: stream-K partial tiles
   unsigned* pk_sync;  // persistent forward: barrier / exit / flag words (zero between launches)
   void* gemm_ws;
@@ -70,8 +73,15 @@ static size_t carve(const sb_decoder_t* m, int T, char* base, FwdWorkspace* w) {
   o->amax_idx = (int*)take(vt * 4);
   o->xb = take((size_t)T * m->hidden * 2);
   o->npart = (float*)take((size_t)((m->hidden + 127) / 128) * 8 * T * 4);
+  const int tpw = m->tp ? m->tp->world : 0;
+  o->tp_part = tpw ? (float*)take((size_t)T * m->hidden * 4) : nullptr;
+  o->tp_logits = tpw ? (float*)take((size_t)T * m->vocab * 4) : nullptr;
+  o->tp_gather = tpw ? (float*)take((size_t)tpw * T * m->vocab * 4) : nullptr;
   return off;
 }
+
+// the embedding is replicated: token ids range over the full vocabulary even on a TP shard
+static inline int vocab_full(const sb_decoder_t* m) { return m->vocab * (m->tp ? m->tp->world : 1); }
 
 static int g_last_count = 0;
 // event profiling (sb_profile_forward): an event after every kernel of the forward
@@ -95,6 +105,34 @@ static void prof_mark(const char* tag, cudaStream_t st) {
 static int g_attn_impl = 0;
 
 static int g_fuse_norm = 1;  // RMSNorm fused into the GEMMs (bf16 / tcgen05 path), sb_set_fuse_norm
+
+// TP exchange after a row-parallel projection whose partial went to w.tp_part:
+// all-reduce (sum over ranks), then resid += sum (+ bf16 copy / norm partials)
+static int tp_reduce_add(const sb_decoder_t* m, const FwdWorkspace& w, int T, bool fused, cudaStream_t st) {
+  const sb_collectives_t* c = m->tp;
+  SB_TRY(c->all_reduce_sum(c->ctx, w.tp_part, (size_t)T * m->hidden, SB_F32, st));
+  prof_mark("allreduce", st);
+  return launch_tp_resid_add(w.resid, w.tp_part, fused ? w.xb : nullptr, fused ? w.npart : nullptr, T, m->hidden, st);
+}
+
+// vocab-parallel lm_head: local slice -> all-gather -> full-width logits on
+// every rank (+ greedy sink from the full row)
+static int tp_lm_head(const sb_decoder_t* m, GemmArgs g, float* logits, const sb_token_sink_t* sink,
+                      const FwdWorkspace& w, int rows, cudaStream_t st) {
+  if (!logits) return SB_EINVAL;
+  const sb_collectives_t* c = m->tp;
+  g.epi = EPI_STORE_F32;
+  g.y = w.tp_logits;
+  SB_TRY(gemm(g, GEMM_AUTO, st));
+  prof_mark("lm_head", st);
+  SB_TRY(c->all_gather(c->ctx, w.tp_logits, w.tp_gather, (size_t)rows * m->vocab, SB_F32, st));
+  SB_TRY(launch_unshard_logits(w.tp_gather, logits, c->world, rows, m->vocab, st));
+  if (sink)
+    SB_TRY(launch_select_argmax(logits, rows, m->vocab * c->world, sink->out_tok, sink->out_stride, sink->next_ids,
+                                sink->next_pos, sink->base_pos, sink->pos_offset, st));
+  prof_mark("argmax", st);
+  return 0;
+}
 
 // lm_head + optional greedy sink; g already carries X (and fused-norm scaling)
 static int lm_head(const sb_decoder_t* m, GemmArgs g, float* logits, const sb_token_sink_t* sink,
@@ -144,7 +182,7 @@ static int forward_fused_norm(const sb_decoder_t* m, const sb_kvcache_t* kv, con
   const int qkv_n = (nq + 2 * nkv) * hd;
   const size_t layer_kv = (size_t)kv->slots * nkv * kv->ctx_max * hd * 2;
   const float inv_h = 1.0f / (float)H;
-  SB_TRY(launch_embed_norm(m->embed, ids, pos, w.resid, w.xb, w.npart, T, H, m->vocab, st));
+  SB_TRY(launch_embed_norm(m->embed, ids, pos, w.resid, w.xb, w.npart, T, H, vocab_full(m), st));
   prof_mark("embed", st);
   int P = 1;
   for (int l = 0; l < m->n_layers; ++l) {
@@ -168,13 +206,22 @@ static int forward_fused_norm(const sb_decoder_t* m, const sb_kvcache_t* kv, con
       SB_TRY(launch_attention(SB_BF16, w.qr, kc, vc, w.attn, slot, pos, n_seq, q_len, nq, nkv, hd, kv->ctx_max, st));
     }
     prof_mark("attn", st);
-    GemmArgs o{SB_BF16, w.attn, m->w_o[l], w.resid, T, H, nq * hd, nq * hd, EPI_RESID_ADD, w.gemm_ws,
-               w.gemm_ws_bytes};
-    o.out_part = w.npart;
-    o.out_xb = w.xb;
-    SB_TRY(gemm_tc(o, st));
-    P = gemm_tc_norm_partials(o);
-    prof_mark("o", st);
+    if (m->tp) {  // row-parallel o_proj: partial -> all-reduce -> residual
+      GemmArgs o{SB_BF16, w.attn, m->w_o[l], w.tp_part, T, H, nq * hd, nq * hd, EPI_STORE_F32, w.gemm_ws,
+                 w.gemm_ws_bytes};
+      SB_TRY(gemm_tc(o, st));
+      prof_mark("o", st);
+      SB_TRY(tp_reduce_add(m, w, T, true, st));
+      P = (H + 127) / 128;
+    } else {
+      GemmArgs o{SB_BF16, w.attn, m->w_o[l], w.resid, T, H, nq * hd, nq * hd, EPI_RESID_ADD, w.gemm_ws,
+                 w.gemm_ws_bytes};
+      o.out_part = w.npart;
+      o.out_xb = w.xb;
+      SB_TRY(gemm_tc(o, st));
+      P = gemm_tc_norm_partials(o);
+      prof_mark("o", st);
+    }
     GemmArgs gu{SB_BF16, w.xb, m->w_gu[l], w.act, T, 2 * m->ffn, H, H, EPI_SILU_MUL, w.gemm_ws, w.gemm_ws_bytes};
     gu.ns_part = w.npart;
     gu.ns_P = P;
@@ -183,13 +230,22 @@ static int forward_fused_norm(const sb_decoder_t* m, const sb_kvcache_t* kv, con
     gu.ns_inv_h = inv_h;
     SB_TRY(gemm_tc(gu, st));
     prof_mark("gu", st);
-    GemmArgs dn{SB_BF16, w.act, m->w_down[l], w.resid, T, H, m->ffn, m->ffn, EPI_RESID_ADD, w.gemm_ws,
-                w.gemm_ws_bytes};
-    dn.out_part = w.npart;
-    dn.out_xb = w.xb;
-    SB_TRY(gemm_tc(dn, st));
-    P = gemm_tc_norm_partials(dn);
-    prof_mark("down", st);
+    if (m->tp) {  // row-parallel down_proj
+      GemmArgs dn{SB_BF16, w.act, m->w_down[l], w.tp_part, T, H, m->ffn, m->ffn, EPI_STORE_F32, w.gemm_ws,
+                  w.gemm_ws_bytes};
+      SB_TRY(gemm_tc(dn, st));
+      prof_mark("down", st);
+      SB_TRY(tp_reduce_add(m, w, T, true, st));
+      P = (H + 127) / 128;
+    } else {
+      GemmArgs dn{SB_BF16, w.act, m->w_down[l], w.resid, T, H, m->ffn, m->ffn, EPI_RESID_ADD, w.gemm_ws,
+                  w.gemm_ws_bytes};
+      dn.out_part = w.npart;
+      dn.out_xb = w.xb;
+      SB_TRY(gemm_tc(dn, st));
+      P = gemm_tc_norm_partials(dn);
+      prof_mark("down", st);
+    }
   }
   if (logits_mode == SB_LOGITS_NONE) return 0;
   const bool last = logits_mode == SB_LOGITS_LAST;
@@ -204,6 +260,7 @@ static int forward_fused_norm(const sb_decoder_t* m, const sb_kvcache_t* kv, con
   g.ns_row_off = off;
   g.ns_eps = m->rms_eps;
   g.ns_inv_h = inv_h;
+  if (m->tp) return tp_lm_head(m, g, logits, sink, w, rows, st);
   return lm_head(m, g, logits, sink, w, rows, st);
 }
 
@@ -223,7 +280,8 @@ static int forward_impl(const sb_decoder_t* m, const sb_kvcache_t* kv, const int
   const size_t layer_kv = (size_t)kv->slots * nkv * kv->ctx_max * hd * es;
 
   prof_mark("start", st);
-  if (!g_prof && g_backend_override != GEMM_SIMT && persistent_eligible(m, T)) {
+  if (m->tp && (m->tp->world < 1 || !m->tp->all_reduce_sum || !m->tp->all_gather)) return SB_EINVAL;
+  if (!g_prof && !m->tp && g_backend_override != GEMM_SIMT && persistent_eligible(m, T)) {
     PkBuffers b{w.resid, w.xb, w.qr, w.attn, w.act, w.npart, w.amax_val, w.amax_idx, w.pk_scratch, w.pk_sync};
     int rc = persistent_forward(m, kv, ids, slot, pos, n_seq, q_len, logits, logits_mode, sink, b, st);
     if (rc && getenv("SB_DEBUG")) fprintf(stderr, "persistent_forward rc=%d T=%d\n", rc, T);
@@ -231,7 +289,7 @@ static int forward_impl(const sb_decoder_t* m, const sb_kvcache_t* kv, const int
   }
   if (g_fuse_norm && dt == SB_BF16 && g_backend_override != GEMM_SIMT)
     return forward_fused_norm(m, kv, ids, slot, pos, n_seq, q_len, logits, logits_mode, sink, w, st);
-  SB_TRY(launch_embed(dt, m->embed, ids, pos, w.resid, T, H, m->vocab, st));
+  SB_TRY(launch_embed(dt, m->embed, ids, pos, w.resid, T, H, vocab_full(m), st));
   prof_mark("embed", st);
   for (int l = 0; l < m->n_layers; ++l) {
     char* kc = (char*)kv->k + l * layer_kv;
@@ -252,17 +310,21 @@ static int forward_impl(const sb_decoder_t* m, const sb_kvcache_t* kv, const int
       SB_TRY(launch_attention(dt, w.qr, kc, vc, w.attn, slot, pos, n_seq, q_len, nq, nkv, hd, kv->ctx_max, st));
     }
     prof_mark("attn", st);
-    g = GemmArgs{dt, w.attn, m->w_o[l], w.resid, T, H, nq * hd, nq * hd, EPI_RESID_ADD, w.gemm_ws, w.gemm_ws_bytes};
+    g = GemmArgs{dt, w.attn, m->w_o[l], m->tp ? w.tp_part : w.resid, T, H, nq * hd, nq * hd,
+                 m->tp ? EPI_STORE_F32 : EPI_RESID_ADD, w.gemm_ws, w.gemm_ws_bytes};
     SB_TRY(gemm(g, GEMM_AUTO, st));
     prof_mark("o", st);
+    if (m->tp) SB_TRY(tp_reduce_add(m, w, T, false, st));
     SB_TRY(launch_rmsnorm(dt, w.resid, m->mlp_norm[l], w.xn, T, H, m->rms_eps, 1, 0, st));
     prof_mark("norm2", st);
     g = GemmArgs{dt, w.xn, m->w_gu[l], w.act, T, 2 * m->ffn, H, H, EPI_SILU_MUL, w.gemm_ws, w.gemm_ws_bytes};
     SB_TRY(gemm(g, GEMM_AUTO, st));
     prof_mark("gu", st);
-    g = GemmArgs{dt, w.act, m->w_down[l], w.resid, T, H, m->ffn, m->ffn, EPI_RESID_ADD, w.gemm_ws, w.gemm_ws_bytes};
+    g = GemmArgs{dt, w.act, m->w_down[l], m->tp ? w.tp_part : w.resid, T, H, m->ffn, m->ffn,
+                 m->tp ? EPI_STORE_F32 : EPI_RESID_ADD, w.gemm_ws, w.gemm_ws_bytes};
     SB_TRY(gemm(g, GEMM_AUTO, st));
     prof_mark("down", st);
+    if (m->tp) SB_TRY(tp_reduce_add(m, w, T, false, st));
   }
   if (logits_mode == SB_LOGITS_NONE) return 0;
   int rows = logits_mode == SB_LOGITS_LAST ? n_seq : T;
@@ -271,6 +333,7 @@ static int forward_impl(const sb_decoder_t* m, const sb_kvcache_t* kv, const int
   SB_TRY(launch_rmsnorm(dt, w.resid, m->final_norm, w.last, rows, H, m->rms_eps, step, off, st));
   prof_mark("norm_f", st);
   GemmArgs g{dt, w.last, m->lm_head, logits, rows, m->vocab, H, H, EPI_STORE_F32, w.gemm_ws, w.gemm_ws_bytes};
+  if (m->tp) return tp_lm_head(m, g, logits, sink, w, rows, st);
   return lm_head(m, g, logits, sink, w, rows, st);
 }
 
@@ -407,7 +470,7 @@ int sb_set_pdl(int32_t enabled) {
 int sb_version(void) { return SB_ABI_VERSION; }
 
 const char* sb_build_info(void) {
-  return "specbatch_b200 abi=" "2" " arch=sm_100a kernels=persistent_forward,embed,rmsnorm,rope_append,attention,gemm_simt,gemm_tcgen05,"
+  return "specbatch_b200 abi=" "3" " arch=sm_100a tp=nccl kernels=persistent_forward,tp_resid_add,unshard_logits,embed,rmsnorm,rope_append,attention,gemm_simt,gemm_tcgen05,"
          "argmax,softmax,select,accept,commit,prepare,kv_compact";
 }
 

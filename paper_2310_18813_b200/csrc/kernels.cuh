@@ -76,6 +76,10 @@ int launch_select_argmax(const float* logits, int rows, int vocab, int32_t* out_
 int launch_kv_compact(int dtype, void* k, void* v, const int32_t* src, const int32_t* dst, const int32_t* len, int n,
                       int layers, int slots, int nkv, int ctx_max, int hd, cudaStream_t st);
 
+// ---- tensor-parallel glue (layer_kernels.cu)
+int launch_tp_resid_add(float* resid, const float* part, void* xb, float* npart, int T, int H, cudaStream_t st);
+int launch_unshard_logits(const float* gathered, float* logits, int world, int rows, int vl, cudaStream_t st);
+
 // ---- persistent forward (persistent.cu)
 struct PkBuffers {
   float* resid;

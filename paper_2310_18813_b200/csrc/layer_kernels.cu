@@ -706,3 +706,62 @@ int launch_kv_compact(int dtype, void* k, void* v, const int32_t* src, const int
 }
 
 }  // namespace sb
+
+// ---------------------------------------------------------------- tensor-parallel glue
+namespace sb {
+
+// After the all-reduce of a row-parallel projection: resid += part; on the
+// fused-norm path also the bf16 residual copy and the per-128-column
+// sum-of-squares partials npart[tile][t] the next GEMM's 1/rms reads.
+// grid (T, ceil(H/128)), 128 threads: one element per thread, fixed-order sums.
+__global__ void __launch_bounds__(128) tp_resid_add_kernel(float* __restrict__ resid, const float* __restrict__ part,
+                                                           __nv_bfloat16* __restrict__ xb, float* __restrict__ npart,
+                                                           int T, int H) {
+  griddep_wait();
+  griddep_launch();
+  const int t = blockIdx.x, tile = blockIdx.y;
+  const int col = tile * 128 + threadIdx.x;
+  float nv = 0.f;
+  if (col < H) {
+    const size_t o = (size_t)t * H + col;
+    nv = resid[o] + part[o];
+    resid[o] = nv;
+    if (xb) xb[o] = __float2bfloat16_rn(nv);
+  }
+  if (!npart) return;
+  __shared__ float red[4];
+  const float s = warp_sum(nv * nv);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) npart[(size_t)tile * T + t] = ((red[0] + red[1]) + red[2]) + red[3];
+}
+
+int launch_tp_resid_add(float* resid, const float* part, void* xb, float* npart, int T, int H, cudaStream_t st) {
+  if (T <= 0) return 0;
+  return launch_k(tp_resid_add_kernel, dim3(T, (H + 127) / 128), dim3(128), 0, st, resid, part, (__nv_bfloat16*)xb,
+                  npart, T, H);
+}
+
+// all_gather output [world][rows][Vl] -> logits [rows][world * Vl] (vocab-parallel lm_head)
+__global__ void unshard_logits_kernel(const float4* __restrict__ g, float4* __restrict__ out, int world, int rows,
+                                      int vl4) {
+  griddep_wait();
+  griddep_launch();
+  const long n = (long)world * rows * vl4;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < n; i += (long)gridDim.x * blockDim.x) {
+    const int c = (int)(i % vl4);
+    const long rr = i / vl4;
+    const int r = (int)(rr % rows), w = (int)(rr / rows);
+    out[((long)r * world + w) * vl4 + c] = g[i];
+  }
+}
+
+int launch_unshard_logits(const float* gathered, float* logits, int world, int rows, int vl, cudaStream_t st) {
+  if (rows <= 0) return 0;
+  if (vl % 4) return SB_EUNSUPPORTED;
+  const long n = (long)world * rows * (vl / 4);
+  return launch_k(unshard_logits_kernel, dim3(grid_for(n, 256)), dim3(256), 0, st, (const float4*)gathered,
+                  (float4*)logits, world, rows, vl / 4);
+}
+
+}  // namespace sb

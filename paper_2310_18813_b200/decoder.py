@@ -200,6 +200,16 @@ class Decoder:
             s.tmaps = self.tmaps.data_ptr()
         self.struct = s
 
+    @property
+    def vocab_full(self) -> int:
+        """Full vocabulary (a tensor-parallel shard holds vocab / world lm_head rows)."""
+        return self.cfg.vocab * getattr(self, "world", 1)
+
+    @property
+    def is_tp(self) -> bool:
+        """True for a tensor-parallel shard attached to a collectives group (tp.py)."""
+        return bool(self.struct.tp)
+
     def workspace_bytes(self, n_tokens: int) -> int:
         return int(N.load().sb_decoder_workspace_bytes(C.byref(self.struct), n_tokens))
 

@@ -64,7 +64,7 @@ class SpecEngine:
             raise ValueError(f"mode must be one of {sorted(_MODES)}, got {mode!r}")
         if mode == "injected" and acceptance is None:
             raise ValueError("injected mode needs an AcceptanceTrace")
-        if draft is not None and draft.cfg.vocab != target.cfg.vocab:
+        if draft is not None and draft.vocab_full != target.vocab_full:
             raise ValueError("draft and target must share a vocabulary")
         if draft is not None and draft.sb_dtype != target.sb_dtype:
             raise ValueError("draft and target must share a dtype")
@@ -80,7 +80,7 @@ class SpecEngine:
         self.use_graphs = use_graphs
         self.prompt_fn = prompt_fn or self._default_prompt
         self.dev = target.device
-        V = target.cfg.vocab
+        V = target.vocab_full
         self.V = V
         B, K = max_batch, self.max_k
         self.cap = prompt_len + max_new + K + 2
@@ -155,7 +155,8 @@ class SpecEngine:
                N.ptr(self.uniforms), _NU, N.ptr(self.inj_samples), self.inj_samples.numel(),
                N.ptr(self.l_inj), st)
         greedy_draft = not sample
-        need_logits = self.target.sb_dtype != N.SB_BF16  # the fp32 path selects from materialised logits
+        # the fp32 path and a tensor-parallel target select from materialised (full-width) logits
+        need_logits = self.target.sb_dtype != N.SB_BF16 or self.target.is_tp
         if use_draft:
             sel = N.SELECT_SAMPLE if sample else N.SELECT_ARGMAX
             u_base = self.uniforms.data_ptr()
