@@ -65,7 +65,11 @@ class LlamaRef:
     """
 
     def __init__(self, masters: dict, n_heads: int, n_kv_heads: int, eps: float, max_pos: int = 4096,
-                 theta: float = 10000.0, dtype=torch.float64, bf16_emulation: bool = False, n_layers=None):
+                 theta: float = 10000.0, dtype=torch.float64, bf16_emulation: bool = False, n_layers=None,
+                 head_dim=None, tp_reduce=None, tp_gather=None):
+        """head_dim / tp_reduce / tp_gather describe a tensor-parallel SHARD
+        (local head counts, sliced masters): tp_reduce sums the row-parallel
+        o / down partials over ranks, tp_gather concatenates the vocab slices."""
         self.dt = dtype
         self.emb = masters["embed"].to(dtype)
         self.head = masters["lm_head"].to(dtype)
@@ -73,7 +77,9 @@ class LlamaRef:
         self.layers = [{k: v.to(dtype) for k, v in lay.items()} for lay in lays]
         self.h = self.emb.shape[1]
         self.nq, self.nkv = n_heads, n_kv_heads
-        self.hd = self.h // n_heads
+        self.hd = head_dim or self.h // n_heads
+        self.tp_reduce = tp_reduce or (lambda t: t)
+        self.tp_gather = tp_gather or (lambda t: t)
         self.eps = eps
         cos, sin = rope_tables(max_pos, self.hd, theta)
         self.cos, self.sin = cos.to(dtype), sin.to(dtype)
@@ -135,12 +141,12 @@ class LlamaRef:
             att = att.masked_fill(mask[None], float("-inf"))
             att = torch.softmax(att, -1)
             o = self._r(torch.einsum("nts,snd->tnd", att, Vh).reshape(T, self.nq * self.hd))
-            x = x + o @ lay["wo"].T
+            x = x + self.tp_reduce(o @ lay["wo"].T)
             g = self._nm(x, lay["wg"])
             u = self._nm(x, lay["wu"])
             a = self._r(torch.nn.functional.silu(g) * u)
-            x = x + a @ lay["wd"].T
-        return self._nm(x, self.head).to(torch.float64).numpy()
+            x = x + self.tp_reduce(a @ lay["wd"].T)
+        return self.tp_gather(self._nm(x, self.head)).to(torch.float64).numpy()
 
 
 def greedy_decode(model: LlamaRef, prompt, n: int):
