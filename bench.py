@@ -29,7 +29,12 @@ import numpy as np
 ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
-TARGET, DRAFT = "llama-2-7b", "llama-68m"
+# workload -> (target, draft): "7b" = BASELINE configs[2] (the headline), "70b" =
+# configs[3] (Llama-2-70B; tensor-parallel over the ranks when launched with
+# torchrun --nproc-per-node N, whole model on one B200 at N=1)
+WORKLOADS = {"7b": ("llama-2-7b", "llama-68m"), "70b": ("llama-2-70b", "llama-160m"),
+             "trace": ("llama-2-7b", "llama-68m")}
+TARGET, DRAFT = WORKLOADS["7b"]
 B, P, NEW = 8, 128, 128
 K_GRID = tuple(range(9))
 
@@ -43,6 +48,9 @@ def _args():
     ap.add_argument("--batch", type=int, default=B)
     ap.add_argument("--k", type=int, default=-1, help="fixed k (default: adaptive LUT)")
     ap.add_argument("--quick", action="store_true", help="skip the k sweep")
+    ap.add_argument("--workload", default="7b", choices=sorted(WORKLOADS))
+    ap.add_argument("--trace-scale", type=float, default=0.1,
+                    help="config 5: wall seconds per trace second (0.1 = the 6 x 50 s schedule in 30 s)")
     return ap.parse_args()
 
 
@@ -208,6 +216,69 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+
+# ============================================================== config 5 (serving trace)
+def run_trace(args):
+    """BASELINE configs[4]: a time-varying Poisson trace (the reference's
+    timeline schedule, harness.py:257-265: alternating intense 0.2 s / sparse
+    1.0 s mean gaps, CV 1, 6 x 50 s phases, max_batch 16) replayed in WALL
+    time on the GPU engine (simulator.serve_wallclock), once with the adaptive
+    LUT policy and once per fixed k = 1..8.  Metric: mean request latency
+    (queueing + prefill + decode), lower is better.  The schedule is time
+    compressed by --trace-scale so one policy takes ~30 s."""
+    import torch
+
+    from paper_2310_18813_b200.decoder import CONFIGS, Decoder
+    from paper_2310_18813_b200.policy import AdaptivePolicy, FixedPolicy, build_lut
+    from paper_2310_18813_b200.presets import example_trace
+    from paper_2310_18813_b200.simulator import ServerConfig, serve_wallclock
+    from paper_2310_18813_b200.spec_engine import SpecEngine
+    from paper_2310_18813_b200.traffic import PhaseSchedule, TrafficConfig, gen_phased
+
+    rank, world, local = _dist()
+    if rank != 0:
+        return
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    trace = example_trace()
+    tgt = Decoder(CONFIGS[TARGET], dtype="bf16", device=dev, seed=0, init="device", max_pos=P + NEW + 32)
+    drf = Decoder(CONFIGS[DRAFT], dtype="bf16", device=dev, seed=1, init="device", max_pos=P + NEW + 32)
+    eng = SpecEngine(tgt, drf, mode="injected", acceptance=trace, max_batch=16, max_k=8, prompt_len=P,
+                     max_new=NEW, seed=0)
+    lut = build_lut(None, trace, s_grid=K_GRID, profiled_sizes=(1, 2, 4, 8, 16), mode="measured",
+                    sample_size=1, rng=np.random.default_rng(0), gen_len=NEW, engine=eng)
+    phases = tuple((50.0, TrafficConfig(mean_interval=0.2 if i % 2 == 0 else 1.0, cv=1.0, count=1000))
+                   for i in range(6))
+    workload = gen_phased(PhaseSchedule(phases=phases), np.random.default_rng([0, 6]), gen_len=NEW)
+    policies = [AdaptivePolicy(lut)] + [FixedPolicy(k) for k in range(1, 9)]
+    lat, batches = {}, {}
+    t_cap = time.perf_counter()
+    for bb in range(1, 17):  # capture every (b, k) iteration graph up front: no capture inside a replay
+        for kk in range(1, 9):
+            eng._graph(bb, kk)
+    t_cap = time.perf_counter() - t_cap
+    t_run = time.perf_counter()
+    for pol in policies:
+        rep = serve_wallclock(workload, ServerConfig(policy=pol, max_batch=16), eng, time_scale=args.trace_scale)
+        lat[pol.label] = rep.avg_latency / args.trace_scale  # back to trace seconds
+        sizes = [r.served_batch_size for r in rep.records]
+        batches[pol.label] = round(float(np.mean(sizes)), 2)
+    t_run = time.perf_counter() - t_run
+    fixed = {k: v for k, v in lat.items() if k.startswith("fixed")}
+    best = min(fixed, key=fixed.get)
+    ad = [k for k in lat if k not in fixed][0]
+    line = {"metric": "mean request latency, phased Poisson trace (adaptive k)", "value": lat[ad], "unit": "s",
+            "n_gpus": 1, "higher_is_better": False, "impl": "ours", "dtype": "bf16",
+            "data": "synthetic (random-init weights, injected example_trace acceptance)",
+            "config": {"workload": f"{TARGET} target + {DRAFT} draft, timeline trace 6x50s (0.2/1.0 s gaps, CV 1), "
+                                   f"max_batch 16, N={NEW}, P={P}", "time_scale": args.trace_scale,
+                       "requests": len(workload), "lut": {str(k): v for k, v in lut.entries.items()}},
+            "latency_s_by_policy": {k: round(v, 4) for k, v in lat.items()},
+            "mean_batch_by_policy": batches, "best_fixed": best,
+            "adaptive_vs_best_fixed_latency": lat[ad] / fixed[best], "wall_s": round(t_run, 1),
+            "graph_capture_s": round(t_cap, 1)}
+    print(json.dumps(line), flush=True)
+
 # ============================================================== our arm (GPU)
 def run_ours(args):
     import torch
@@ -230,10 +301,24 @@ def run_ours(args):
 
     b = args.batch
     trace = example_trace()
-    tgt = Decoder(CONFIGS[TARGET], dtype="bf16", device=dev, seed=0, init="device", max_pos=P + NEW + 32)
+    tp = args.workload == "70b" and world > 1  # tensor-parallel target over the ranks (config 4)
+    if tp:
+        from paper_2310_18813_b200.tp import NcclTP, shard_config
+
+        # each rank draws its own shard directly (random init; no full copy anywhere)
+        tgt = Decoder(shard_config(CONFIGS[TARGET], world), dtype="bf16", device=dev, seed=100 + rank,
+                      init="device", max_pos=P + NEW + 32)
+        tgt.world, tgt.rank = world, rank
+        ids = [NcclTP.unique_id() if rank == 0 else None]
+        torch.distributed.broadcast_object_list(ids, src=0)
+        tp_group = NcclTP(world, rank, ids[0])
+        tp_group.attach(tgt)
+    else:
+        tgt = Decoder(CONFIGS[TARGET], dtype="bf16", device=dev, seed=0, init="device", max_pos=P + NEW + 32)
     drf = Decoder(CONFIGS[DRAFT], dtype="bf16", device=dev, seed=1, init="device", max_pos=P + NEW + 32)
+    # replicas: independent request streams per rank; TP: one engine spanning the ranks (same seed)
     eng = SpecEngine(tgt, drf, mode="injected", acceptance=trace, max_batch=max(b, 8), max_k=8, prompt_len=P,
-                     max_new=NEW, seed=rank)
+                     max_new=NEW, seed=0 if tp else rank)
 
     # ---- the paper's profiler on THIS GPU: every (b, k) cell runs the real
     # engine (build_lut mode="measured"); the analytic LUT from a measured
@@ -271,7 +356,8 @@ def run_ours(args):
         torch.cuda.synchronize()
     total_ms = e0.elapsed_time(e1)
     total_ms = max_over_ranks(total_ms, device=dev)
-    tokens = world * args.steps * b * NEW
+    jobs = 1 if tp else world  # TP: the ranks share one batch
+    tokens = jobs * args.steps * b * NEW
     value = tokens / (total_ms / 1e3)
 
     # ---- e2e through the public API (run_batch), pinned H2D prompts + D2H tokens per step
@@ -284,7 +370,7 @@ def run_ours(args):
         res = run_batch(sts, k, None, eng, np.random.default_rng(s), )
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
-    e2e = world * args.steps * b * NEW / e2e_s
+    e2e = jobs * args.steps * b * NEW / e2e_s
 
     # ---- roofline of the verify forward (the north_star's roofline object), timed live
     hbm, tf, peak_kind = _peaks()
@@ -296,14 +382,14 @@ def run_ours(args):
     tf_path = ROOT / "profiles" / "verify_traffic.json"
     if tf_path.exists():
         tfd = json.loads(tf_path.read_text())
-        if tfd.get("b") == b and tfd.get("k") == k:
+        if tfd.get("b") == b and tfd.get("k") == k and str(tfd.get("workload", "")).startswith(TARGET + " "):
             traffic = tfd["dram_bytes_read_plus_write"]
 
     # ---- CPU baseline (rank 0, N=1 only)
     cpu = None
     if rank == 0 and world == 1 and os.environ.get("SB_SKIP_CPU", "0") != "1":
         try:
-            layers = int(os.environ.get("SB_CPU_LAYERS", "8")) or None
+            layers = int(os.environ.get("SB_CPU_LAYERS", "8" if TARGET == "llama-2-7b" else "2")) or None
             tps, desc, cores = cpu_sample(b, k, iters=1, layers=layers)
             cpu = {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": desc}
         except Exception as exc:  # pragma: no cover
@@ -315,15 +401,16 @@ def run_ours(args):
         line = {
             "metric": "generated tokens/s (batched speculative decoding, adaptive k)", "value": value,
             "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong" if tp else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, random prompts)",
             "config": {"workload": f"{TARGET} target + {DRAFT} draft, bf16, b={b}, P={P}, N={NEW}",
                        "k": k, "k_source": "adaptive LUT (profiled on this GPU)" if args.k < 0 else "fixed",
                        "lut": {str(kk): v for kk, v in lut.entries.items()},
                        "lut_analytic_from_measured_calibration": {str(kk): v for kk, v in lut_analytic.entries.items()},
                        "acceptance": "injected: TraceSampler(example_trace()) law on device",
-                       "parallelism": f"replicas x{world}", "l2": "inputs (13.5 GB weights) > L2; no flush"},
-            "decode_tokens_per_s": world * args.steps * b * NEW / (sum(decode_ms) / 1e3) if world == 1 else None,
+                       "parallelism": f"tp{world} (NCCL all-reduce / all-gather)" if tp else f"replicas x{world}",
+                       "l2": "inputs (weights >= 13.5 GB) > L2; no flush"},
+            "decode_tokens_per_s": jobs * args.steps * b * NEW / (sum(decode_ms) / 1e3) if world == 1 else None,
             "k_sweep_decode_tokens_per_s": {str(kk): round(v, 1) for kk, v in sorted(sweep.items())},
             "best_fixed_k": best_fixed,
             "adaptive_vs_best_fixed": (sweep[k] / sweep[best_fixed]) if (sweep and k in sweep) else None,
@@ -345,7 +432,10 @@ def run_ours(args):
 
 if __name__ == "__main__":
     a = _args()
+    TARGET, DRAFT = WORKLOADS[a.workload]
     if a.impl == "reference":
         run_reference(a)
+    elif a.workload == "trace":
+        run_trace(a)
     else:
         run_ours(a)
