@@ -33,7 +33,7 @@ sys.path.insert(0, str(ROOT))
 # configs[3] (Llama-2-70B; tensor-parallel over the ranks when launched with
 # torchrun --nproc-per-node N, whole model on one B200 at N=1)
 WORKLOADS = {"7b": ("llama-2-7b", "llama-68m"), "70b": ("llama-2-70b", "llama-160m"),
-             "trace": ("llama-2-7b", "llama-68m")}
+             "opt": ("opt-6.7b", "opt-125m"), "trace": ("llama-2-7b", "llama-68m")}
 TARGET, DRAFT = WORKLOADS["7b"]
 B, P, NEW = 8, 128, 128
 K_GRID = tuple(range(9))
@@ -151,11 +151,23 @@ def cpu_sample(b, k, iters=1, threads=None, layers=None):
                             "wv": mk(cfg.n_kv_heads * hd, h), "wo": mk(h, cfg.n_heads * hd), "wg": mk(cfg.ffn, h),
                             "wu": mk(cfg.ffn, h), "wd": mk(h, cfg.ffn)} for _ in range(n_layers)]}
 
+    def opt_masters(cfg, n_layers):
+        h, F = cfg.hidden, cfg.ffn
+        lay = lambda: dict(wq=mk(h, h), wk=mk(h, h), wv=mk(h, h), bq=mk(h), bk=mk(h), bv=mk(h), wo=mk(h, h),
+                           bo=mk(h), f1=mk(F, h), b1=mk(F), f2=mk(h, F), b2=mk(h), g1=1 + mk(h), c1=mk(h),
+                           g2=1 + mk(h), c2=mk(h))
+        return {"embed": mk(cfg.vocab, h), "pos": mk(P + NEW + 32, h), "layers": [lay() for _ in range(n_layers)],
+                "gf": 1 + mk(h), "cf": mk(h)}
+
+    def build(cfg, n_layers):
+        if cfg.arch == "opt":
+            return model_ref.OptRef(opt_masters(cfg, n_layers), cfg.n_heads, cfg.rms_eps, dtype=torch.float32)
+        return model_ref.LlamaRef(masters(cfg, n_layers), cfg.n_heads, cfg.n_kv_heads, cfg.rms_eps,
+                                  max_pos=P + NEW + 16, dtype=torch.float32)
+
     t_init = time.perf_counter()
-    tgt = model_ref.LlamaRef(masters(tc, L), tc.n_heads, tc.n_kv_heads, tc.rms_eps, max_pos=P + NEW + 16,
-                             dtype=torch.float32)
-    drf = model_ref.LlamaRef(masters(dc, dc.n_layers), dc.n_heads, dc.n_kv_heads, dc.rms_eps,
-                             max_pos=P + NEW + 16, dtype=torch.float32)
+    tgt = build(tc, L)
+    drf = build(dc, dc.n_layers)
     rng = np.random.default_rng(0)
     prompts = [list(map(int, rng.integers(0, tc.vocab, P))) for _ in range(b)]
     tcache = [tgt.new_cache() for _ in range(b)]

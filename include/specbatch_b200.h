@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define SB_ABI_VERSION 3
+#define SB_ABI_VERSION 4
 
 /* status codes beyond cudaError_t (which are < 1000) */
 #define SB_OK 0
@@ -47,6 +47,10 @@ extern "C" {
 /* dtypes */
 #define SB_BF16 0
 #define SB_F32 1
+
+/* decoder architectures (sb_decoder_t.arch) */
+#define SB_ARCH_LLAMA 0 /* RMSNorm, RoPE, SwiGLU, GQA, untied lm_head (Llama-2, LLaMA-68M/160M) */
+#define SB_ARCH_OPT 1   /* LayerNorm+bias, learned positions (+offset), biased projections, ReLU FFN, tied head */
 
 /* logits selection for sb_decoder_forward */
 #define SB_LOGITS_ALL 0   /* one logits row per input token                */
@@ -120,6 +124,20 @@ typedef struct sb_decoder {
      (the fields above are the LOCAL sizes); embedding and norms are replicated.
      Logits come back full-width [rows, vocab * world] on every rank. */
   const sb_collectives_t* tp;
+  /* SB_ARCH_OPT (BASELINE config 2: OPT-125M / OPT-6.7B).  For OPT, w_gu holds
+     fc1 [ffn, hidden] (no gate) and w_down fc2 [hidden, ffn]; attn_norm /
+     mlp_norm / final_norm are LayerNorm gains with the *_b betas; lm_head may
+     alias embed (tied); the rope tables are identity (cos 1, sin 0). */
+  int32_t arch;
+  int32_t pos_offset;             /* learned position p reads pos_embed row p + pos_offset (OPT: 2) */
+  const void* pos_embed;          /* [max_pos + pos_offset, hidden] */
+  const void* final_norm_b;
+  const void* const* attn_norm_b;
+  const void* const* mlp_norm_b;
+  const void* const* b_qkv;       /* [(n_heads + 2 n_kv_heads) head_dim] */
+  const void* const* b_o;         /* [hidden] */
+  const void* const* b_fc1;       /* [ffn] */
+  const void* const* b_fc2;       /* [hidden] */
 } sb_decoder_t;
 
 /* KV cache: k/v base pointers of layout [n_layers][slots][n_kv_heads][ctx_max][head_dim]. */

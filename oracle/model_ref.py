@@ -149,6 +149,111 @@ class LlamaRef:
         return self.tp_gather(self._nm(x, self.head)).to(torch.float64).numpy()
 
 
+def init_opt_masters(cfg, seed: int, max_pos: int, std: float = 0.02, round_to=torch.bfloat16):
+    """Independent regeneration of the engine's OPT host init (decoder.py
+    Decoder._init_opt draw order)."""
+    gen = torch.Generator(device="cpu").manual_seed(seed)
+    rn = lambda *shape: torch.randn(*shape, generator=gen, dtype=torch.float32) * std
+    r = (lambda t: t.to(round_to).float()) if round_to is not None else (lambda t: t)
+    h = cfg.hidden
+    hd = h // cfg.n_heads
+    qd, kd = cfg.n_heads * hd, cfg.n_kv_heads * hd
+    out = {"embed": r(rn(cfg.vocab, h)), "pos": r(rn(max_pos + cfg.pos_offset, h)), "layers": []}
+    for _ in range(cfg.n_layers):
+        lay = dict(wq=rn(qd, h), wk=rn(kd, h), wv=rn(kd, h), bq=rn(qd), bk=rn(kd), bv=rn(kd), wo=rn(h, qd), bo=rn(h),
+                   f1=rn(cfg.ffn, h), b1=rn(cfg.ffn), f2=rn(h, cfg.ffn), b2=rn(h))
+        lay.update(g1=1.0 + rn(h), c1=rn(h), g2=1.0 + rn(h), c2=rn(h))
+        out["layers"].append({k: r(v) for k, v in lay.items()})
+    out["gf"], out["cf"] = r(1.0 + rn(h)), r(rn(h))
+    return out
+
+
+class OptRef:
+    """OPT decoder on the CPU (BASELINE config 2), restated from the public
+    architecture: pre-LayerNorm blocks, biased q/k/v/o, learned absolute
+    positions at row p + pos_offset, fc1 -> ReLU -> fc2, final LayerNorm,
+    lm_head tied to the token embedding.  bf16_emulation rounds where the GPU
+    rounds: LayerNorm outputs (GEMM inputs), q/k/v after bias, the attention
+    output and relu(fc1); residual stream in `dtype`."""
+
+    def __init__(self, masters: dict, n_heads: int, eps: float, pos_offset: int = 2, dtype=torch.float64,
+                 bf16_emulation: bool = False):
+        self.dt = dtype
+        self.m = {k: (v.to(dtype) if torch.is_tensor(v) else v) for k, v in masters.items() if k != "layers"}
+        self.layers = [{k: v.to(dtype) for k, v in lay.items()} for lay in masters["layers"]]
+        self.h = self.m["embed"].shape[1]
+        self.nq = n_heads
+        self.hd = self.h // n_heads
+        self.eps, self.off, self.bf16 = eps, pos_offset, bf16_emulation
+
+    def _r(self, x):
+        return x.to(torch.bfloat16).to(self.dt) if self.bf16 else x
+
+    def _ln(self, x, g, b):
+        mu = x.mean(-1, keepdim=True)
+        var = ((x - mu) ** 2).mean(-1, keepdim=True)
+        return self._r((x - mu) * torch.rsqrt(var + self.eps) * g + b)
+
+    def new_cache(self):
+        return [{"k": None, "v": None} for _ in self.layers]
+
+    @torch.no_grad()
+    def forward(self, ids, pos, cache):
+        ids_t = torch.as_tensor(ids, dtype=torch.long)
+        pos_t = torch.as_tensor(pos, dtype=torch.long)
+        x = self.m["embed"][ids_t] + self.m["pos"][pos_t + self.off]
+        T, p0 = len(ids), int(pos[0])
+        for lay, c in zip(self.layers, cache):
+            xn = self._ln(x, lay["g1"], lay["c1"])
+            q = self._r(xn @ lay["wq"].T + lay["bq"]).view(T, self.nq, self.hd)
+            kk = self._r(xn @ lay["wk"].T + lay["bk"]).view(T, self.nq, self.hd)
+            vv = self._r(xn @ lay["wv"].T + lay["bv"]).view(T, self.nq, self.hd)
+            keep_k = c["k"][:p0] if c["k"] is not None else kk[:0]
+            keep_v = c["v"][:p0] if c["v"] is not None else vv[:0]
+            c["k"], c["v"] = torch.cat([keep_k, kk], 0), torch.cat([keep_v, vv], 0)
+            att = torch.einsum("tnd,snd->nts", q / math.sqrt(self.hd), c["k"])
+            mask = torch.arange(c["k"].shape[0])[None, :] > pos_t[:, None]
+            att = torch.softmax(att.masked_fill(mask[None], float("-inf")), -1)
+            o = self._r(torch.einsum("nts,snd->tnd", att, c["v"]).reshape(T, self.h))
+            x = x + (o @ lay["wo"].T + lay["bo"])
+            xn = self._ln(x, lay["g2"], lay["c2"])
+            a = self._r(torch.relu(xn @ lay["f1"].T + lay["b1"]))
+            x = x + (a @ lay["f2"].T + lay["b2"])
+        xn = self._ln(x, self.m["gf"], self.m["cf"])
+        return (xn @ self.m["embed"].T).to(torch.float64).numpy()
+
+    @torch.no_grad()
+    def forward_batch(self, ids, pos, caches):
+        """b sequences x q tokens sharing every weight read (CPU-baseline timing);
+        same math as forward."""
+        b, q = len(ids), len(ids[0])
+        flat = torch.as_tensor([t for row in ids for t in row], dtype=torch.long)
+        pflat = torch.as_tensor([p for row in pos for p in row], dtype=torch.long)
+        pos_t = [torch.as_tensor(p, dtype=torch.long) for p in pos]
+        x = self.m["embed"][flat] + self.m["pos"][pflat + self.off]
+        for li, lay in enumerate(self.layers):
+            xn = self._ln(x, lay["g1"], lay["c1"])
+            Q = self._r(xn @ lay["wq"].T + lay["bq"]).view(b, q, self.nq, self.hd)
+            K = self._r(xn @ lay["wk"].T + lay["bk"]).view(b, q, self.nq, self.hd)
+            Vv = self._r(xn @ lay["wv"].T + lay["bv"]).view(b, q, self.nq, self.hd)
+            outs = []
+            for s in range(b):
+                c = caches[s][li]
+                p0 = int(pos[s][0])
+                keep_k = c["k"][:p0] if c["k"] is not None else K[s][:0]
+                keep_v = c["v"][:p0] if c["v"] is not None else Vv[s][:0]
+                c["k"], c["v"] = torch.cat([keep_k, K[s]], 0), torch.cat([keep_v, Vv[s]], 0)
+                att = torch.einsum("tnd,snd->nts", Q[s] / math.sqrt(self.hd), c["k"])
+                mask = torch.arange(c["k"].shape[0])[None, :] > pos_t[s][:, None]
+                att = torch.softmax(att.masked_fill(mask[None], float("-inf")), -1)
+                outs.append(torch.einsum("nts,snd->tnd", att, c["v"]).reshape(q, self.h))
+            x = x + (self._r(torch.cat(outs, 0)) @ lay["wo"].T + lay["bo"])
+            xn = self._ln(x, lay["g2"], lay["c2"])
+            x = x + (self._r(torch.relu(xn @ lay["f1"].T + lay["b1"])) @ lay["f2"].T + lay["b2"])
+        xn = self._ln(x, self.m["gf"], self.m["cf"])
+        return (xn @ self.m["embed"].T).view(b, q, -1).numpy()
+
+
 def greedy_decode(model: LlamaRef, prompt, n: int):
     """Plain greedy decoding: the ground truth every speculative run must equal
     (greedy_reference, engine.py:224-227).  Returns (tokens, top2 gaps)."""
@@ -231,6 +336,8 @@ def forward_batch(model: LlamaRef, ids, pos, caches):
     """Batched CPU forward (CPU-baseline timing): b sequences x q tokens share
     every weight read (one matmul per projection over all b*q rows); attention
     and KV caches stay per sequence.  Same math as LlamaRef.forward."""
+    if isinstance(model, OptRef):
+        return model.forward_batch(ids, pos, caches)
     b = len(ids)
     q = len(ids[0])
     flat = torch.as_tensor([t for row in ids for t in row], dtype=torch.long)

@@ -20,6 +20,7 @@ SB_EWORKSPACE = 1002
 SB_EUNSUPPORTED = 1003
 
 SB_BF16, SB_F32 = 0, 1
+ARCH_LLAMA, ARCH_OPT = 0, 1
 LOGITS_ALL, LOGITS_LAST, LOGITS_NONE = 0, 1, 2
 ACCEPT_GREEDY, ACCEPT_STOCHASTIC, ACCEPT_INJECTED = 0, 1, 2
 SELECT_ARGMAX, SELECT_SAMPLE = 0, 1
@@ -51,6 +52,8 @@ class SbDecoder(C.Structure):
         ("embed", _P), ("final_norm", _P), ("lm_head", _P),
         ("attn_norm", _PP), ("w_qkv", _PP), ("w_o", _PP), ("mlp_norm", _PP), ("w_gu", _PP), ("w_down", _PP),
         ("rope_cos", _P), ("rope_sin", _P), ("tmaps", _P), ("tp", C.POINTER(SbCollectives)),
+        ("arch", _I), ("pos_offset", _I), ("pos_embed", _P), ("final_norm_b", _P), ("attn_norm_b", _PP),
+        ("mlp_norm_b", _PP), ("b_qkv", _PP), ("b_o", _PP), ("b_fc1", _PP), ("b_fc2", _PP),
     ]
 
 

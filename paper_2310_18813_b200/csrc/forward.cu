@@ -264,6 +264,72 @@ static int forward_fused_norm(const sb_decoder_t* m, const sb_kvcache_t* kv, con
   return lm_head(m, g, logits, sink, w, rows, st);
 }
 
+// OPT decoder (BASELINE config 2): pre-LayerNorm blocks with biased
+// projections, learned positions (embedding row p + pos_offset), ReLU FFN
+// (fc1 -> relu -> fc2), final LayerNorm, lm_head tied to the embedding (the
+// host passes the same pointer).  RoPE tables are identity for OPT, so the
+// shared attention kernels apply no rotation.
+static int forward_opt(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* ids, const int32_t* slot,
+                       const int32_t* pos, int n_seq, int q_len, float* logits, int logits_mode,
+                       const sb_token_sink_t* sink, const FwdWorkspace& w, cudaStream_t st) {
+  if (m->tp) return SB_EUNSUPPORTED;  // OPT targets fit one B200 (config 2)
+  if (!m->pos_embed || !m->b_qkv || !m->b_o || !m->b_fc1 || !m->b_fc2 || !m->attn_norm_b || !m->mlp_norm_b ||
+      !m->final_norm_b)
+    return SB_EINVAL;
+  const int T = n_seq * q_len;
+  const int dt = m->dtype;
+  const size_t es = dt == SB_BF16 ? 2 : 4;
+  const int nq = m->n_heads, nkv = m->n_kv_heads, hd = m->head_dim, H = m->hidden;
+  const int qkv_n = (nq + 2 * nkv) * hd;
+  const size_t layer_kv = (size_t)kv->slots * nkv * kv->ctx_max * hd * es;
+  SB_TRY(launch_embed(dt, m->embed, ids, pos, w.resid, T, H, m->vocab, st, m->pos_embed, m->pos_offset));
+  prof_mark("embed", st);
+  for (int l = 0; l < m->n_layers; ++l) {
+    char* kc = (char*)kv->k + l * layer_kv;
+    char* vc = (char*)kv->v + l * layer_kv;
+    SB_TRY(launch_layernorm(dt, w.resid, m->attn_norm[l], m->attn_norm_b[l], w.xn, T, H, m->rms_eps, 1, 0, st));
+    prof_mark("norm1", st);
+    GemmArgs g{dt, w.xn, m->w_qkv[l], w.qkv, T, qkv_n, H, H, EPI_STORE, w.gemm_ws, w.gemm_ws_bytes};
+    g.bias = m->b_qkv[l];
+    SB_TRY(gemm(g, GEMM_AUTO, st));
+    prof_mark("qkv", st);
+    int rc_fa = SB_EUNSUPPORTED;
+    if (g_attn_impl == 0 && dt == SB_BF16)
+      rc_fa = launch_attention_tc(w.qkv, kc, vc, w.attn, slot, pos, m->rope_cos, m->rope_sin, n_seq, q_len, nq, nkv,
+                                  hd, kv->ctx_max, m->max_pos, st);
+    if (rc_fa != 0 && rc_fa != SB_EUNSUPPORTED) return rc_fa;
+    if (rc_fa == SB_EUNSUPPORTED) {
+      SB_TRY(launch_rope_append(dt, w.qkv, w.qr, kc, vc, slot, pos, m->rope_cos, m->rope_sin, T, q_len, nq, nkv, hd,
+                                kv->ctx_max, m->max_pos, st));
+      SB_TRY(launch_attention(dt, w.qr, kc, vc, w.attn, slot, pos, n_seq, q_len, nq, nkv, hd, kv->ctx_max, st));
+    }
+    prof_mark("attn", st);
+    g = GemmArgs{dt, w.attn, m->w_o[l], w.resid, T, H, nq * hd, nq * hd, EPI_RESID_ADD, w.gemm_ws, w.gemm_ws_bytes};
+    g.bias = m->b_o[l];
+    SB_TRY(gemm(g, GEMM_AUTO, st));
+    prof_mark("o", st);
+    SB_TRY(launch_layernorm(dt, w.resid, m->mlp_norm[l], m->mlp_norm_b[l], w.xn, T, H, m->rms_eps, 1, 0, st));
+    prof_mark("norm2", st);
+    g = GemmArgs{dt, w.xn, m->w_gu[l], w.act, T, m->ffn, H, H, EPI_STORE, w.gemm_ws, w.gemm_ws_bytes};
+    g.bias = m->b_fc1[l];
+    g.relu = 1;
+    SB_TRY(gemm(g, GEMM_AUTO, st));
+    prof_mark("fc1", st);
+    g = GemmArgs{dt, w.act, m->w_down[l], w.resid, T, H, m->ffn, m->ffn, EPI_RESID_ADD, w.gemm_ws, w.gemm_ws_bytes};
+    g.bias = m->b_fc2[l];
+    SB_TRY(gemm(g, GEMM_AUTO, st));
+    prof_mark("fc2", st);
+  }
+  if (logits_mode == SB_LOGITS_NONE) return 0;
+  const int rows = logits_mode == SB_LOGITS_LAST ? n_seq : T;
+  const int step = logits_mode == SB_LOGITS_LAST ? q_len : 1;
+  const int off = logits_mode == SB_LOGITS_LAST ? q_len - 1 : 0;
+  SB_TRY(launch_layernorm(dt, w.resid, m->final_norm, m->final_norm_b, w.last, rows, H, m->rms_eps, step, off, st));
+  prof_mark("norm_f", st);
+  GemmArgs g{dt, w.last, m->lm_head, logits, rows, m->vocab, H, H, EPI_STORE_F32, w.gemm_ws, w.gemm_ws_bytes};
+  return lm_head(m, g, logits, sink, w, rows, st);
+}
+
 static int forward_impl(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* ids, const int32_t* slot,
                         const int32_t* pos, int n_seq, int q_len, float* logits, int logits_mode,
                         const sb_token_sink_t* sink, void* ws, size_t ws_bytes, cudaStream_t st) {
@@ -280,6 +346,8 @@ static int forward_impl(const sb_decoder_t* m, const sb_kvcache_t* kv, const int
   const size_t layer_kv = (size_t)kv->slots * nkv * kv->ctx_max * hd * es;
 
   prof_mark("start", st);
+  if (m->arch == SB_ARCH_OPT) return forward_opt(m, kv, ids, slot, pos, n_seq, q_len, logits, logits_mode, sink, w, st);
+  if (m->arch != SB_ARCH_LLAMA) return SB_EINVAL;
   if (m->tp && (m->tp->world < 1 || !m->tp->all_reduce_sum || !m->tp->all_gather)) return SB_EINVAL;
   if (!g_prof && !m->tp && g_backend_override != GEMM_SIMT && persistent_eligible(m, T)) {
     PkBuffers b{w.resid, w.xb, w.qr, w.attn, w.act, w.npart, w.amax_val, w.amax_idx, w.pk_scratch, w.pk_sync};
@@ -470,7 +538,7 @@ int sb_set_pdl(int32_t enabled) {
 int sb_version(void) { return SB_ABI_VERSION; }
 
 const char* sb_build_info(void) {
-  return "specbatch_b200 abi=" "3" " arch=sm_100a tp=nccl kernels=persistent_forward,tp_resid_add,unshard_logits,embed,rmsnorm,rope_append,attention,gemm_simt,gemm_tcgen05,"
+  return "specbatch_b200 abi=" "4" " arch=sm_100a tp=nccl models=llama,opt kernels=persistent_forward,layernorm,tp_resid_add,unshard_logits,embed,rmsnorm,rope_append,attention,gemm_simt,gemm_tcgen05,"
          "argmax,softmax,select,accept,commit,prepare,kv_compact";
 }
 

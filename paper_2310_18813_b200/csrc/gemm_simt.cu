@@ -15,7 +15,8 @@ constexpr int SBN = 64, SBM = 32, SBK = 32;
 
 template <typename T>
 __global__ void __launch_bounds__(256) gemm_simt_kernel(const T* __restrict__ X, const T* __restrict__ W, void* Y,
-                                                        int M, int N, int K, int ldx, int epi) {
+                                                        int M, int N, int K, int ldx, int epi,
+                                                        const T* __restrict__ bias, int relu) {
   __shared__ float Ws[SBK][SBN + 1];
   __shared__ float Xs[SBK][SBM + 1];
   griddep_wait();
@@ -76,12 +77,15 @@ __global__ void __launch_bounds__(256) gemm_simt_kernel(const T* __restrict__ X,
       int n = n0 + i;
       if (n >= N) continue;
       size_t o = (size_t)m * N + n;
+      float v = acc[i][j];
+      if (bias) v += to_f32(bias[n]);
+      if (relu && epi != EPI_RESID_ADD) v = fmaxf(v, 0.f);
       if (epi == EPI_STORE)
-        ((T*)Y)[o] = from_f32<T>(acc[i][j]);
+        ((T*)Y)[o] = from_f32<T>(v);
       else if (epi == EPI_STORE_F32)
-        ((float*)Y)[o] = acc[i][j];
+        ((float*)Y)[o] = v;
       else
-        ((float*)Y)[o] += acc[i][j];
+        ((float*)Y)[o] += v;
     }
   }
 }
@@ -90,12 +94,14 @@ int gemm_simt(const GemmArgs& a, cudaStream_t st) {
   if (a.M <= 0 || a.N <= 0 || a.K <= 0) return SB_EINVAL;
   if (a.epi == EPI_ARGMAX || a.ns_part || a.out_part) return SB_EUNSUPPORTED;
   if (a.epi == EPI_SILU_MUL && (a.N & 1)) return SB_EINVAL;
+  if (a.epi == EPI_SILU_MUL && (a.bias || a.relu)) return SB_EINVAL;
   dim3 grid((a.N + SBN - 1) / SBN, (a.M + SBM - 1) / SBM);
   if (a.dtype == SB_BF16)
     return launch_k(gemm_simt_kernel<__nv_bfloat16>, grid, dim3(256), 0, st, (const __nv_bfloat16*)a.x,
-                    (const __nv_bfloat16*)a.w, a.y, a.M, a.N, a.K, a.ldx, a.epi);
+                    (const __nv_bfloat16*)a.w, a.y, a.M, a.N, a.K, a.ldx, a.epi, (const __nv_bfloat16*)a.bias,
+                    a.relu);
   return launch_k(gemm_simt_kernel<float>, grid, dim3(256), 0, st, (const float*)a.x, (const float*)a.w, a.y, a.M, a.N,
-                  a.K, a.ldx, a.epi);
+                  a.K, a.ldx, a.epi, (const float*)a.bias, a.relu);
 }
 
 int g_backend_override = GEMM_AUTO;

@@ -57,6 +57,8 @@ struct TcParams {
   // out_part[(tile_n * splits + split) * M + m] = sum over this CTA's rows of new^2
   float* out_part;
   __nv_bfloat16* out_xb;
+  const __nv_bfloat16* bias;  // OPT: per-row bias [N] added before the epilogue op
+  int relu;
 };
 
 __device__ __forceinline__ float silu_f(float g) { return g / (1.f + __expf(-g)); }
@@ -67,6 +69,8 @@ __device__ __forceinline__ float silu_f(float g) { return g / (1.f + __expf(-g))
 __device__ __forceinline__ float epi_one(const TcParams& p, int m, int n, float v) {
   if (m >= p.M || n >= p.N) return 0.f;
   size_t o = (size_t)m * p.N + n;
+  if (p.bias) v += __bfloat162float(p.bias[n]);
+  if (p.relu && p.epi != EPI_RESID_ADD) v = fmaxf(v, 0.f);
   if (p.epi == EPI_STORE) {
     ((__nv_bfloat16*)p.y)[o] = __float2bfloat16_rn(v);
   } else if (p.epi == EPI_STORE_F32) {
@@ -486,6 +490,9 @@ int gemm_tc(const GemmArgs& a, cudaStream_t st) {
   p.ns_inv_h = a.ns_inv_h;
   p.out_part = a.out_part;
   p.out_xb = (__nv_bfloat16*)a.out_xb;
+  p.bias = (const __nv_bfloat16*)a.bias;
+  p.relu = a.relu;
+  if ((a.bias || a.relu) && (a.epi == EPI_SILU_MUL || a.epi == EPI_ARGMAX)) return SB_EINVAL;
   if (a.out_part && a.epi != EPI_RESID_ADD) return SB_EINVAL;
   if (a.epi == EPI_ARGMAX && (!a.aux_val || !a.aux_idx)) return SB_EINVAL;
   cudaLaunchConfig_t cfg = {};

@@ -38,6 +38,9 @@ struct GemmArgs {
   // fused RMSNorm producer (EPI_RESID_ADD): bf16 copy of the new residual + sum-of-squares partials
   float* out_part = nullptr;
   void* out_xb = nullptr;
+  // OPT: per-output-row bias (model dtype, [N]) added to the fp32 accumulator, then ReLU (store epilogues)
+  const void* bias = nullptr;
+  int relu = 0;
 };
 
 extern int g_backend_override;  // sb_set_gemm_backend (ablation / tests)
@@ -54,7 +57,9 @@ int num_sms();
 int make_map(CUtensorMap* map, const void* base, int rows, int cols, int ld, int box_rows);
 
 int launch_embed(int dtype, const void* table, const int32_t* ids, const int32_t* pos, float* h, int n_tok,
-                 int hidden, int vocab, cudaStream_t st);
+                 int hidden, int vocab, cudaStream_t st, const void* pos_table = nullptr, int pos_offset = 0);
+int launch_layernorm(int dtype, const float* x, const void* g, const void* b, void* y, int rows, int hidden, float eps,
+                     int row_step, int row_off, cudaStream_t st);
 int launch_embed_norm(const void* table, const int32_t* ids, const int32_t* pos, float* h, void* xb, float* part,
                       int n_tok, int hidden, int vocab, cudaStream_t st);
 int launch_rmsnorm(int dtype, const float* x, const void* g, void* y, int rows, int hidden, float eps, int row_step,

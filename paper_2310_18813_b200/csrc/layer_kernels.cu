@@ -22,7 +22,8 @@ thread_local int g_kernel_count = 0;
 // ---------------------------------------------------------------- embedding
 template <typename T>
 __global__ void embed_kernel(const T* __restrict__ table, const int32_t* __restrict__ ids,
-                             const int32_t* __restrict__ pos, float* __restrict__ h, int hidden, int vocab) {
+                             const int32_t* __restrict__ pos, float* __restrict__ h, int hidden, int vocab,
+                             const T* __restrict__ pos_table, int pos_offset) {
   griddep_wait();
   griddep_launch();
   int t = blockIdx.x;
@@ -30,17 +31,22 @@ __global__ void embed_kernel(const T* __restrict__ table, const int32_t* __restr
   bool pad = pos != nullptr && pos[t] < 0;
   if (id < 0 || id >= vocab) pad = true;
   const T* row = table + (size_t)(pad ? 0 : id) * hidden;
+  // OPT: learned absolute positions, row p + offset (the reference model's offset of 2)
+  const T* prow = (pos_table && !pad) ? pos_table + (size_t)(pos[t] + pos_offset) * hidden : nullptr;
   float* out = h + (size_t)t * hidden;
-  for (int i = threadIdx.x; i < hidden; i += blockDim.x) out[i] = pad ? 0.f : to_f32(row[i]);
+  for (int i = threadIdx.x; i < hidden; i += blockDim.x)
+    out[i] = pad ? 0.f : (prow ? to_f32(row[i]) + to_f32(prow[i]) : to_f32(row[i]));
 }
 
 int launch_embed(int dtype, const void* table, const int32_t* ids, const int32_t* pos, float* h, int n_tok,
-                 int hidden, int vocab, cudaStream_t st) {
+                 int hidden, int vocab, cudaStream_t st, const void* pos_table, int pos_offset) {
   if (n_tok <= 0) return 0;
+  if (pos_table && !pos) return SB_EINVAL;
   if (dtype == SB_BF16)
     return launch_k(embed_kernel<__nv_bfloat16>, dim3(n_tok), dim3(256), 0, st, (const __nv_bfloat16*)table, ids, pos,
-                    h, hidden, vocab);
-  return launch_k(embed_kernel<float>, dim3(n_tok), dim3(256), 0, st, (const float*)table, ids, pos, h, hidden, vocab);
+                    h, hidden, vocab, (const __nv_bfloat16*)pos_table, pos_offset);
+  return launch_k(embed_kernel<float>, dim3(n_tok), dim3(256), 0, st, (const float*)table, ids, pos, h, hidden, vocab,
+                  (const float*)pos_table, pos_offset);
 }
 
 // Embedding for the fused-RMSNorm path: fp32 residual, its bf16 copy (the
@@ -134,6 +140,85 @@ int launch_rmsnorm(int dtype, const float* x, const void* g, void* y, int rows, 
                     (__nv_bfloat16*)y, hidden, eps, row_step, row_off);
   return launch_k(rmsnorm_kernel<float>, dim3(rows), dim3(256), 0, st, x, (const float*)g, (float*)y, hidden, eps,
                   row_step, row_off);
+}
+
+// ---------------------------------------------------------------- LayerNorm (OPT)
+// y[r] = dtype((x - mean) * rsqrt(var + eps) * g + b), two passes over the row
+// held in registers (float4, hidden <= 8192); src_row(r) = r*row_step + row_off.
+template <typename T>
+__global__ void __launch_bounds__(256) layernorm_kernel(const float* __restrict__ x, const T* __restrict__ g,
+                                                        const T* __restrict__ b, T* __restrict__ y, int hidden,
+                                                        float eps, int row_step, int row_off) {
+  griddep_wait();
+  griddep_launch();
+  const int r = blockIdx.x;
+  const float4* xr = reinterpret_cast<const float4*>(x + (size_t)(r * row_step + row_off) * hidden);
+  const int n4 = hidden >> 2;
+  float4 v[8];
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    int i = threadIdx.x + c * 256;
+    if (i < n4) {
+      v[c] = xr[i];
+      s += (v[c].x + v[c].y) + (v[c].z + v[c].w);
+    }
+  }
+  __shared__ float red[8];
+  __shared__ float stat[2];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    stat[0] = t / (float)hidden;
+  }
+  __syncthreads();
+  const float mean = stat[0];
+  float q = 0.f;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    int i = threadIdx.x + c * 256;
+    if (i < n4) {
+      const float a = v[c].x - mean, bb = v[c].y - mean, cc = v[c].z - mean, d = v[c].w - mean;
+      q += (a * a + bb * bb) + (cc * cc + d * d);
+    }
+  }
+  q = warp_sum(q);
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = q;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < 8; ++w) t += red[w];
+    stat[1] = rsqrtf(t / (float)hidden + eps);
+  }
+  __syncthreads();
+  const float inv = stat[1];
+  T* yr = y + (size_t)r * hidden;
+#pragma unroll
+  for (int c = 0; c < 8; ++c) {
+    int i = threadIdx.x + c * 256;
+    if (i < n4) {
+      int e = i * 4;
+      yr[e + 0] = from_f32<T>((v[c].x - mean) * inv * to_f32(g[e + 0]) + to_f32(b[e + 0]));
+      yr[e + 1] = from_f32<T>((v[c].y - mean) * inv * to_f32(g[e + 1]) + to_f32(b[e + 1]));
+      yr[e + 2] = from_f32<T>((v[c].z - mean) * inv * to_f32(g[e + 2]) + to_f32(b[e + 2]));
+      yr[e + 3] = from_f32<T>((v[c].w - mean) * inv * to_f32(g[e + 3]) + to_f32(b[e + 3]));
+    }
+  }
+}
+
+int launch_layernorm(int dtype, const float* x, const void* g, const void* b, void* y, int rows, int hidden, float eps,
+                     int row_step, int row_off, cudaStream_t st) {
+  if (rows <= 0) return 0;
+  if (hidden % 4 || hidden > 8192 || !g || !b) return SB_EUNSUPPORTED;
+  if (dtype == SB_BF16)
+    return launch_k(layernorm_kernel<__nv_bfloat16>, dim3(rows), dim3(256), 0, st, x, (const __nv_bfloat16*)g,
+                    (const __nv_bfloat16*)b, (__nv_bfloat16*)y, hidden, eps, row_step, row_off);
+  return launch_k(layernorm_kernel<float>, dim3(rows), dim3(256), 0, st, x, (const float*)g, (const float*)b,
+                  (float*)y, hidden, eps, row_step, row_off);
 }
 
 // ---------------------------------------------------------------- RoPE + KV append

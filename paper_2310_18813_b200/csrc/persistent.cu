@@ -1088,7 +1088,7 @@ size_t persistent_scratch_bytes(int T) {
 }
 
 bool persistent_eligible(const sb_decoder_t* m, int T) {
-  if (!g_persistent || m->dtype != SB_BF16 || !m->tmaps || T > PK_MAX_T) return false;
+  if (!g_persistent || m->arch != SB_ARCH_LLAMA || m->dtype != SB_BF16 || !m->tmaps || T > PK_MAX_T) return false;
   if (m->head_dim != 64 && m->head_dim != 128) return false;
   const int qd = m->n_heads * m->head_dim, kd = m->n_kv_heads * m->head_dim;
   if (qd % TC_BM || kd % TC_BM) return false;

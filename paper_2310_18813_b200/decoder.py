@@ -41,6 +41,8 @@ class DecoderConfig:
     vocab: int = 32000
     rms_eps: float = 1e-5
     rope_theta: float = 10000.0
+    arch: str = "llama"  # "llama" | "opt" (config 2: LayerNorm+bias, learned positions, ReLU FFN, tied head)
+    pos_offset: int = 2  # OPT: position p reads learned row p + 2
 
     @property
     def head_dim(self) -> int:
@@ -50,17 +52,24 @@ class DecoderConfig:
     def qkv_rows(self) -> int:
         return (self.n_heads + 2 * self.n_kv_heads) * self.head_dim
 
+    def _per_layer(self) -> int:
+        h, qd = self.hidden, self.n_heads * self.head_dim
+        if self.arch == "opt":  # qkv, o, fc1, fc2 + their biases + two LayerNorms (gain, bias)
+            return h * self.qkv_rows + h * qd + 2 * h * self.ffn + self.qkv_rows + h + self.ffn + h + 4 * h
+        return h * self.qkv_rows + h * qd + 3 * h * self.ffn + 2 * h
+
     def n_params(self, tied: bool = False) -> int:
-        h, L = self.hidden, self.n_layers
-        per = h * self.qkv_rows + h * self.n_heads * self.head_dim + 3 * h * self.ffn + 2 * h
-        return self.vocab * h * (1 if tied else 2) + L * per + h
+        h = self.hidden
+        tied = tied or self.arch == "opt"
+        fin = 2 * h if self.arch == "opt" else h
+        return self.vocab * h * (1 if tied else 2) + self.n_layers * self._per_layer() + fin
 
     def streamed_bytes_per_forward(self, dtype_bytes: int = 2) -> int:
         """Weight bytes one forward streams from HBM (embedding is a gather,
-        excluded; lm_head and final norm included) -- SURVEY §8(d)."""
-        h, L = self.hidden, self.n_layers
-        per = h * self.qkv_rows + h * self.n_heads * self.head_dim + 3 * h * self.ffn + 2 * h
-        return (L * per + h + self.vocab * h) * dtype_bytes
+        excluded; lm_head -- tied or not -- and final norm included) -- SURVEY §8(d)."""
+        h = self.hidden
+        fin = 2 * h if self.arch == "opt" else h
+        return (self.n_layers * self._per_layer() + fin + self.vocab * h) * dtype_bytes
 
     def kv_bytes_per_token(self, dtype_bytes: int = 2) -> int:
         return 2 * self.n_layers * self.n_kv_heads * self.head_dim * dtype_bytes
@@ -74,6 +83,10 @@ CONFIGS = {
     "llama-2-70b": DecoderConfig("llama-2-70b", 8192, 80, 64, 8, 28672, rms_eps=1e-5),
     # BASELINE config 1: the small CPU-runnable pair
     "tiny-target": DecoderConfig("tiny-target", 512, 4, 8, 8, 1376, rms_eps=1e-5),
+    # BASELINE config 2: OPT-125M draft / OPT-6.7B target (public shapes; random init)
+    "opt-125m": DecoderConfig("opt-125m", 768, 12, 12, 12, 3072, vocab=50272, rms_eps=1e-5, arch="opt"),
+    "opt-6.7b": DecoderConfig("opt-6.7b", 4096, 32, 32, 32, 16384, vocab=50272, rms_eps=1e-5, arch="opt"),
+    "tiny-opt": DecoderConfig("tiny-opt", 512, 4, 8, 8, 2048, vocab=50272, rms_eps=1e-5, arch="opt"),
 }
 
 
@@ -118,12 +131,17 @@ class Decoder:
             n_share = share_layers if share_layers is not None else L
             base = share_from
             self.embed, self.lm_head, self.final_norm = base.embed, base.lm_head, base.final_norm
+            for extra in ("pos_embed", "final_norm_b"):  # OPT
+                if hasattr(base, extra):
+                    setattr(self, extra, getattr(base, extra))
             self.layers = base.layers[:n_share]
             self.masters = None if base.masters is None else {
-                "embed": base.masters["embed"], "lm_head": base.masters["lm_head"],
+                **{k: v for k, v in base.masters.items() if k != "layers"},
                 "layers": base.masters["layers"][:n_share],
             }
             self.cfg = replace(cfg, n_layers=n_share, name=f"{base.cfg.name}[:{n_share}]")
+        elif cfg.arch == "opt":
+            self._init_opt(cfg, init, seed, std, max_pos)
         else:
             gen_dev = "cpu" if init == "host" else self.device
             gen = torch.Generator(device=gen_dev).manual_seed(seed)
@@ -168,10 +186,55 @@ class Decoder:
             del head
             self.final_norm = torch.ones(h, device=self.device, dtype=self.tdtype)
             self.masters = masters
-        cos, sin = rope_table(max_pos, self.cfg.head_dim, self.cfg.rope_theta)
+        if self.cfg.arch == "opt":  # learned positions: identity rotation tables (cos 1, sin 0)
+            cos = np.ones((max_pos, self.cfg.head_dim // 2), np.float32)
+            sin = np.zeros_like(cos)
+        else:
+            cos, sin = rope_table(max_pos, self.cfg.head_dim, self.cfg.rope_theta)
         self.rope_cos = torch.from_numpy(cos).to(self.device)
         self.rope_sin = torch.from_numpy(sin).to(self.device)
         self._build_struct()
+
+    def _init_opt(self, cfg, init, seed, std, max_pos):
+        """OPT weights, fp32 masters drawn in a fixed order (oracle/model_ref.py
+        init_opt_masters repeats it): embed (= tied lm_head), learned positions
+        [max_pos + offset], per layer wq,wk,wv,bq,bk,bv,wo,bo,fc1,b1,fc2,b2,
+        ln1 gain/bias, ln2 gain/bias (gains 1 + N(0, std)), final gain/bias."""
+        gen_dev = "cpu" if init == "host" else self.device
+        gen = torch.Generator(device=gen_dev).manual_seed(seed)
+        keep = init == "host"
+        h = cfg.hidden
+        qd, kd = cfg.n_heads * cfg.head_dim, cfg.n_kv_heads * cfg.head_dim
+        mk = lambda *shape: _randn(shape, gen, gen_dev, std)
+        dev = lambda t: t.to(device=self.device, dtype=self.tdtype)
+        r = lambda t: t.to(self.tdtype).float()
+        masters = {"layers": []} if keep else None
+        emb, pos = mk(cfg.vocab, h), mk(max_pos + cfg.pos_offset, h)
+        self.embed, self.pos_embed = dev(emb), dev(pos)
+        self.lm_head = self.embed  # tied
+        if keep:
+            masters["embed"], masters["pos"] = r(emb), r(pos)
+        self.layers = []
+        for _ in range(cfg.n_layers):
+            wq, wk, wv = mk(qd, h), mk(kd, h), mk(kd, h)
+            bq, bk, bv = mk(qd), mk(kd), mk(kd)
+            wo, bo = mk(h, qd), mk(h)
+            f1, b1, f2, b2 = mk(cfg.ffn, h), mk(cfg.ffn), mk(h, cfg.ffn), mk(h)
+            g1, c1, g2, c2 = 1.0 + mk(h), mk(h), 1.0 + mk(h), mk(h)
+            self.layers.append({
+                "w_qkv": dev(torch.cat([wq, wk, wv], 0)), "b_qkv": dev(torch.cat([bq, bk, bv], 0)),
+                "w_o": dev(wo), "b_o": dev(bo), "w_gu": dev(f1), "b_fc1": dev(b1), "w_down": dev(f2), "b_fc2": dev(b2),
+                "attn_norm": dev(g1), "attn_norm_b": dev(c1), "mlp_norm": dev(g2), "mlp_norm_b": dev(c2),
+            })
+            if keep:
+                masters["layers"].append({k: r(v) for k, v in dict(
+                    wq=wq, wk=wk, wv=wv, bq=bq, bk=bk, bv=bv, wo=wo, bo=bo, f1=f1, b1=b1, f2=f2, b2=b2,
+                    g1=g1, c1=c1, g2=g2, c2=c2).items()})
+        gf, cf = 1.0 + mk(h), mk(h)
+        self.final_norm, self.final_norm_b = dev(gf), dev(cf)
+        if keep:
+            masters["gf"], masters["cf"] = r(gf), r(cf)
+        self.masters = masters
 
     # ---------------------------------------------------------------- C struct
     def _build_struct(self):
@@ -187,9 +250,16 @@ class Decoder:
         for k, a in self._arrays.items():
             setattr(s, k, C.cast(a, C.POINTER(C.c_void_p)))
         s.rope_cos, s.rope_sin = self.rope_cos.data_ptr(), self.rope_sin.data_ptr()
+        s.arch = N.ARCH_OPT if cfg.arch == "opt" else N.ARCH_LLAMA
+        if cfg.arch == "opt":
+            for k in ("attn_norm_b", "mlp_norm_b", "b_qkv", "b_o", "b_fc1", "b_fc2"):
+                self._arrays[k] = arr(k)
+                setattr(s, k, C.cast(self._arrays[k], C.POINTER(C.c_void_p)))
+            s.pos_offset, s.pos_embed = cfg.pos_offset, self.pos_embed.data_ptr()
+            s.final_norm_b = self.final_norm_b.data_ptr()
         s.tmaps = None
         self.tmaps = None
-        if self.sb_dtype == N.SB_BF16 and self.device.type == "cuda":
+        if self.sb_dtype == N.SB_BF16 and self.device.type == "cuda" and cfg.arch == "llama":
             # weight TMA descriptors, encoded once on the host and kept resident:
             # they enable the persistent single-kernel forward (csrc/persistent.cu)
             lib = N.load()
