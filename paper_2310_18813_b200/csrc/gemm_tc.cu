@@ -42,7 +42,7 @@ struct TcParams {
   int tn;         // UMMA_N (tokens per tile)
   int n_tiles_n;  // ceil(N / 128)
   int kb;         // 64-wide k-blocks of K
-  int splits;     // K splits == cluster size (1, 2, 4, 8)
+  int splits;     // K splits == cluster size (1..8)
   int stages;
   int epi;
   void* y;
@@ -89,6 +89,11 @@ __device__ __forceinline__ void epi_pair(const TcParams& p, int m, int n, float 
   ((__nv_bfloat16*)p.y)[(size_t)m * (p.N / 2) + n / 2] = __float2bfloat16_rn(silu_f(g) * u);
 }
 
+// Rows of the 128-row tile reduced by cluster rank `split` (pairs, so the
+// silu(gate)*up epilogue never straddles two ranks): [2*(split*64/s), 2*((split+1)*64/s)).
+__host__ __device__ __forceinline__ int split_row_lo(int split, int splits) { return 2 * (split * (TC_BM / 2) / splits); }
+__host__ __device__ __forceinline__ int split_rows_max(int splits) { return 2 * ((TC_BM / 2 + splits - 1) / splits); }
+
 // grid = (n_tiles_n * splits, m_tiles), cluster = (splits, 1, 1): the `splits`
 // CTAs of a cluster share one 128 x tn output tile and split its K range.
 __global__ void __launch_bounds__(TC_THREADS, 1)
@@ -100,9 +105,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const uint32_t b_bytes = tn * TC_BK * 2;
   const uint32_t stage_bytes = a_bytes + b_bytes;
   const uint32_t ring_bytes = p.stages * stage_bytes;
-  // scratch (reuses the drained ring): split>1: partial tile [tn][128] + squares [tn][128/splits];
+  // scratch (reuses the drained ring): split>1: partial tile [tn][128] + squares [tn][rows_max];
   // split==1: argmax staging [2][4][tn] + squares [4][tn]
-  const uint32_t scratch_bytes = p.splits > 1 ? (uint32_t)tn * (TC_BM + TC_BM / p.splits) * 4 : (uint32_t)tn * 12 * 4;
+  const uint32_t scratch_bytes = p.splits > 1 ? (uint32_t)tn * (TC_BM + split_rows_max(p.splits)) * 4 : (uint32_t)tn * 12 * 4;
   uint8_t* stage_base = smem;
   uint64_t* full = (uint64_t*)(smem + (ring_bytes > scratch_bytes ? ring_bytes : scratch_bytes));
   uint64_t* empty = full + p.stages;
@@ -291,9 +296,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // cluster's partials in rank order 0..splits-1.
     cluster_sync_all();
     if (warp >= 2) {
-      const int R = TC_BM / p.splits;
+      const int r_base = split_row_lo(split, p.splits);
+      const int R = split_row_lo(split + 1, p.splits) - r_base;
       const int et = threadIdx.x - 64;
-      const int r_base = split * R;
       const uint32_t red_addr = smem_u32(red);
       const bool scale = p.ns_part != nullptr;
       if (p.epi == EPI_SILU_MUL) {
@@ -411,6 +416,9 @@ static TcPlan plan(int M, int N, int K, int epi) {
   const int sms = num_sms();
   const int slots = sms * q.ctas_per_sm;
   const int tiles = q.n_tiles_n * q.m_tiles;
+  // K splits (= cluster size; powers of two: measured, 3-CTA clusters and
+  // multi-wave splits both lost 5-50% on B200): enough CTAs that every SM
+  // streams, at most one resident wave, >= 2 k-blocks per CTA
   q.splits = 1;
   while (q.splits < 8 && tiles * q.splits < sms && tiles * q.splits * 2 <= slots && q.kb / (q.splits * 2) >= 2)
     q.splits *= 2;
@@ -422,7 +430,7 @@ static TcPlan plan(int M, int N, int K, int epi) {
   if (q.stages > (g_tune_stages ? g_tune_stages : 12)) q.stages = g_tune_stages ? g_tune_stages : 12;
   if (q.stages < 2) q.stages = 2;
   size_t ring = (size_t)q.stages * stage;
-  size_t scratch = q.splits > 1 ? (size_t)q.tn * (TC_BM + TC_BM / q.splits) * 4 : (size_t)q.tn * 12 * 4;
+  size_t scratch = q.splits > 1 ? (size_t)q.tn * (TC_BM + split_rows_max(q.splits)) * 4 : (size_t)q.tn * 12 * 4;
   q.smem = 1024 + (ring > scratch ? ring : scratch) + 256 + 16 + (size_t)q.tn * 4;
   return q;
 }

@@ -322,3 +322,30 @@ def test_fused_lm_head_argmax_matches_full_argmax(cuda_dev, M):
     tgt.forward_greedy(kv, ids, slots, pos, M, 1, None, N.LOGITS_ALL, ws, sink2)  # logits not materialised
     torch.cuda.synchronize()
     assert torch.equal(tok, tok2)
+
+
+@pytest.mark.parametrize("splits", [3, 5, 6, 7])
+def test_gemm_uneven_cluster_splits(cuda_dev, splits):
+    """Cluster split-K with split counts that do not divide the 128-row tile
+    (row pairs per rank: uneven ranges): residual + norm partials, silu*up."""
+    lib = N.load()
+    M, N_, K = 20, 2048, 4096
+    g = torch.Generator(device=cuda_dev).manual_seed(splits)
+    x = (torch.randn(M, K, generator=g, device=cuda_dev) * 0.5).to(torch.bfloat16)
+    w = (torch.randn(N_, K, generator=g, device=cuda_dev) * 0.02).to(torch.bfloat16)
+    ref = x.float() @ w.float().T
+    lib.sb_gemm_tune(0, 0, splits)
+    try:
+        base = torch.randn(M, N_, generator=g, device=cuda_dev)
+        y = base.clone()
+        N.call("sb_gemm", N.SB_BF16, x.data_ptr(), w.data_ptr(), y.data_ptr(), M, N_, K, N.EPI_RESID_ADD,
+               N.GEMM_TC, None, 0, _st())
+        ya = torch.zeros(M, N_ // 2, device=cuda_dev, dtype=torch.bfloat16)
+        N.call("sb_gemm", N.SB_BF16, x.data_ptr(), w.data_ptr(), ya.data_ptr(), M, N_, K, N.EPI_SILU_MUL,
+               N.GEMM_TC, None, 0, _st())
+        torch.cuda.synchronize()
+    finally:
+        lib.sb_gemm_tune(0, 0, 0)
+    assert (y - (base + ref)).abs().max().item() < 1e-3
+    want = torch.nn.functional.silu(ref[:, 0::2]) * ref[:, 1::2]
+    assert (ya.float() - want).abs().max().item() <= 1e-2 * want.abs().max().item() + 1e-4
