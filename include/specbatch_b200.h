@@ -309,6 +309,15 @@ int sb_profile_forward(const sb_decoder_t* m, const sb_kvcache_t* kv, const int3
 int sb_set_attention_impl(int32_t impl);
 /* tcgen05 GEMM tuning overrides (0 = automatic): CTAs per SM (1|2), max pipeline stages, K splits. */
 int sb_gemm_tune(int32_t ctas_per_sm, int32_t max_stages, int32_t splits);
+/*
+ * Measure the tcgen05 GEMM configurations (CTAs per SM x K splits) of one
+ * shape Y[M,N] = X[M,K] W[N,K]^T on real bf16 operands (y: fp32 [M,N] scratch)
+ * and use the fastest for every later GEMM of that (token tile, N, K) shape.
+ * Not during graph capture (SB_EINVAL).  Outputs optional.
+ */
+int sb_gemm_autotune(const void* x, const void* w, void* y_f32, int32_t M, int32_t N, int32_t K, void* stream,
+                     int32_t* cps_out, int32_t* splits_out, float* us_out);
+int sb_gemm_autotune_clear(void);
 int sb_version(void);
 const char* sb_build_info(void);
 int sb_last_kernel_count(void); /* kernels launched by the last sb_decoder_forward */

@@ -85,6 +85,8 @@ _SIGS = {
     "sb_decoder_tmaps_bytes": (C.c_size_t, [C.POINTER(SbDecoder)]),
     "sb_decoder_encode_tmaps": (C.c_int, [C.POINTER(SbDecoder), _P]),
     "sb_gemm_tune": (C.c_int, [_I, _I, _I]),
+    "sb_gemm_autotune": (C.c_int, [_P, _P, _P, _I, _I, _I, _P, C.POINTER(_I), C.POINTER(_I), C.POINTER(C.c_float)]),
+    "sb_gemm_autotune_clear": (C.c_int, []),
     "sb_profile_forward": (C.c_int, [C.POINTER(SbDecoder), C.POINTER(SbKVCache), _P, _P, _P, _I, _I, _P, _I, _P,
                                      C.c_size_t, _P, C.c_char_p, _I]),
     "sb_version": (C.c_int, []),

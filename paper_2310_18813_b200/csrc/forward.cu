@@ -513,6 +513,15 @@ int sb_gemm_tune(int32_t ctas_per_sm, int32_t max_stages, int32_t splits) {
   return gemm_tc_tune(ctas_per_sm, max_stages, splits);
 }
 
+int sb_gemm_autotune(const void* x, const void* w, void* y_f32, int32_t M, int32_t N, int32_t K, void* stream,
+                     int32_t* cps_out, int32_t* splits_out, float* us_out) {
+  if (!x || !w || !y_f32 || M <= 0 || N <= 0 || K <= 0) return SB_EINVAL;
+  SB_TRY(gemm_tc_init());
+  return gemm_tc_autotune(x, w, (float*)y_f32, M, N, K, (cudaStream_t)stream, cps_out, splits_out, us_out);
+}
+
+int sb_gemm_autotune_clear(void) { return gemm_tc_autotune_clear(); }
+
 int sb_set_fuse_norm(int32_t enabled) {
   g_fuse_norm = enabled ? 1 : 0;
   return 0;

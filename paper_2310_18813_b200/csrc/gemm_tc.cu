@@ -25,6 +25,7 @@
 
 #include <climits>
 #include <cstdio>
+#include <map>
 #include <mutex>
 
 #include "common.cuh"
@@ -403,6 +404,16 @@ struct TcPlan {
   size_t smem;
 };
 
+// Measured (CTAs per SM, K splits) per GEMM shape (sb_gemm_autotune, run by the
+// host outside graph capture for the token counts an engine will use); the
+// heuristic below is the fallback.
+static std::mutex g_tuned_mu;
+static std::map<unsigned long long, std::pair<int, int>> g_tuned;
+static unsigned long long tune_key(int tn, int m_tiles, int N, int K) {
+  return ((unsigned long long)tn << 48) | ((unsigned long long)m_tiles << 40) | ((unsigned long long)N << 20) |
+         (unsigned long long)K;
+}
+
 // Split-K policy for the HBM-bound regime: enough CTAs that every SM streams
 // weights (>= one per SM), at most one resident wave, >= 2 k-blocks per CTA,
 // cluster size <= 8 (portable).
@@ -413,6 +424,15 @@ static TcPlan plan(int M, int N, int K, int epi) {
   q.m_tiles = (M + q.tn - 1) / q.tn;
   q.kb = (K + TC_BK - 1) / TC_BK;
   q.ctas_per_sm = g_tune_cps ? g_tune_cps : (q.tn >= 128 ? 1 : 2);
+  int tuned_splits = 0;
+  if (!g_tune_cps && !g_tune_splits) {
+    std::lock_guard<std::mutex> lk(g_tuned_mu);
+    auto it = g_tuned.find(tune_key(q.tn, q.m_tiles, N, K));
+    if (it != g_tuned.end()) {
+      q.ctas_per_sm = it->second.first;
+      tuned_splits = it->second.second;
+    }
+  }
   const int sms = num_sms();
   const int slots = sms * q.ctas_per_sm;
   const int tiles = q.n_tiles_n * q.m_tiles;
@@ -422,6 +442,7 @@ static TcPlan plan(int M, int N, int K, int epi) {
   q.splits = 1;
   while (q.splits < 8 && tiles * q.splits < sms && tiles * q.splits * 2 <= slots && q.kb / (q.splits * 2) >= 2)
     q.splits *= 2;
+  if (tuned_splits) q.splits = tuned_splits;
   if (g_tune_splits) q.splits = g_tune_splits;
   if (epi == EPI_ARGMAX) q.splits = 1;  // the fused argmax reads whole tiles straight from TMEM
   size_t budget = q.ctas_per_sm == 2 ? 108 * 1024 : 200 * 1024;
@@ -439,6 +460,69 @@ int gemm_tc_tune(int cps, int stages, int splits) {
   g_tune_cps = cps;
   g_tune_stages = stages;
   g_tune_splits = splits;
+  return 0;
+}
+
+// Time the candidate (CTAs per SM, splits) configurations of one GEMM shape
+// on real operands (EPI_STORE_F32 into y) and remember the fastest.
+int gemm_tc_autotune(const void* x, const void* w, float* y, int M, int N, int K, cudaStream_t st, int* cps_out,
+                     int* splits_out, float* us_out) {
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cs) != cudaSuccess || cs != cudaStreamCaptureStatusNone) return SB_EINVAL;
+  GemmArgs a{SB_BF16, x, w, y, M, N, K, K, EPI_STORE_F32, nullptr, 0};
+  if (!gemm_tc_supported(a)) return SB_EUNSUPPORTED;
+  const int save_cps = g_tune_cps, save_st = g_tune_stages, save_sp = g_tune_splits;
+  const int kb = (K + TC_BK - 1) / TC_BK;
+  const int tn = tn_for(M), m_tiles = (M + tn - 1) / tn;
+  const int tiles = ((N + TC_BM - 1) / TC_BM) * m_tiles;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  float best = 1e30f;
+  int best_cps = 0, best_sp = 0, rc = 0;
+  for (int cps = 1; cps <= 2 && !rc; ++cps) {
+    for (int sp = 1; sp <= 8 && !rc; sp *= 2) {
+      if (sp > 1 && kb / sp < 2) break;
+      if (tiles * sp > 2 * num_sms() * cps) break;  // more than two waves: never the winner
+      g_tune_cps = cps;
+      g_tune_splits = sp;
+      g_tune_stages = 0;
+      rc = gemm_tc(a, st);  // warm
+      if (rc) break;
+      const int reps = 5;
+      cudaEventRecord(e0, st);
+      for (int r = 0; r < reps && !rc; ++r) rc = gemm_tc(a, st);
+      cudaEventRecord(e1, st);
+      cudaEventSynchronize(e1);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      const float us = ms * 1e3f / reps;
+      if (!rc && us < best) {
+        best = us;
+        best_cps = cps;
+        best_sp = sp;
+      }
+    }
+  }
+  g_tune_cps = save_cps;
+  g_tune_stages = save_st;
+  g_tune_splits = save_sp;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  if (rc) return rc;
+  {
+    std::lock_guard<std::mutex> lk(g_tuned_mu);
+    g_tuned[tune_key(tn, m_tiles, N, K)] = {best_cps, best_sp};
+  }
+  if (cps_out) *cps_out = best_cps;
+  if (splits_out) *splits_out = best_sp;
+  if (us_out) *us_out = best;
+  return 0;
+}
+
+int gemm_tc_autotune_clear() {
+  std::lock_guard<std::mutex> lk(g_tuned_mu);
+  g_tuned.clear();
   return 0;
 }
 

@@ -270,6 +270,43 @@ class Decoder:
             s.tmaps = self.tmaps.data_ptr()
         self.struct = s
 
+    def gemm_shapes(self) -> dict:
+        """(N, K, weight tensor) of the GEMMs one forward runs (layer 0 stands for all)."""
+        cfg, lay = self.cfg, self.layers[0] if self.layers else None
+        H, qd = cfg.hidden, cfg.n_heads * cfg.head_dim
+        out = {"lm": (cfg.vocab, H, self.lm_head)}
+        if lay is not None:
+            gu_n = cfg.ffn if cfg.arch == "opt" else 2 * cfg.ffn
+            out.update(qkv=(cfg.qkv_rows, H, lay["w_qkv"]), o=(H, qd, lay["w_o"]), gu=(gu_n, H, lay["w_gu"]),
+                       down=(H, cfg.ffn, lay["w_down"]))
+        return out
+
+    def autotune(self, token_counts, stream=None) -> dict:
+        """Measure the tcgen05 GEMM configuration of every projection for the
+        token tiles `token_counts` will use (sb_gemm_autotune); later forwards --
+        and graphs captured after this -- use the fastest.  bf16 only; returns
+        {(name, tokens): (ctas_per_sm, splits, us)}."""
+        if self.sb_dtype != N.SB_BF16 or self.device.type != "cuda":
+            return {}
+        lib = N.load()
+        st = torch.cuda.current_stream(self.device).cuda_stream if stream is None else stream
+        seen, res = set(), {}
+        for T in sorted(set(int(t) for t in token_counts if t > 0)):
+            tn = min(256, max(16, (T + 15) // 16 * 16))
+            bucket = (tn, (T + tn - 1) // tn)
+            if bucket in seen:
+                continue
+            seen.add(bucket)
+            for name, (n, k, w) in self.gemm_shapes().items():
+                x = torch.randn(T, k, device=self.device, dtype=torch.bfloat16)
+                y = torch.empty(T, n, device=self.device, dtype=torch.float32)
+                cps, sp, us = C.c_int32(), C.c_int32(), C.c_float()
+                N.call("sb_gemm_autotune", x.data_ptr(), w.data_ptr(), y.data_ptr(), T, n, k, st, C.byref(cps),
+                       C.byref(sp), C.byref(us))
+                res[(name, T)] = (cps.value, sp.value, us.value)
+        torch.cuda.synchronize(self.device)
+        return res
+
     @property
     def vocab_full(self) -> int:
         """Full vocabulary (a tensor-parallel shard holds vocab / world lm_head rows)."""

@@ -59,7 +59,7 @@ class SpecEngine:
     def __init__(self, target: Decoder, draft: Decoder | None, *, mode: str = "greedy",
                  acceptance: AcceptanceTrace | None = None, max_batch: int = 8, max_k: int = 8,
                  prompt_len: int = 128, max_new: int = 128, seed: int = 0, use_graphs: bool = True,
-                 prompt_fn=None, prefill_chunk_tokens: int = 4096):
+                 prompt_fn=None, prefill_chunk_tokens: int = 4096, autotune: bool = True):
         if mode not in _MODES:
             raise ValueError(f"mode must be one of {sorted(_MODES)}, got {mode!r}")
         if mode == "injected" and acceptance is None:
@@ -134,6 +134,13 @@ class SpecEngine:
         self._iter_kernels: dict[tuple[int, int], int] = {}
         self._sinks: list = []  # keep ctypes sink structs alive while graphs reference their contents
         self.stats = IterationStats()
+        self.tuning = {}
+        if autotune:
+            # measured GEMM configurations for every token count the target verify
+            # can present (b(k+1) rows, b rows for the lm_head); must precede graph capture
+            Ts = {b * (k + 1) for b in range(1, B + 1) for k in range(K + 1)} | set(range(1, 2 * B + 1))
+            # (the draft keeps the heuristic: its isolated-GEMM winners measured slower in-graph)
+            self.tuning["target"] = target.autotune(Ts)
 
     # ------------------------------------------------------------- prompts
     def _default_prompt(self, request_id: int) -> np.ndarray:

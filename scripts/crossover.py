@@ -20,11 +20,16 @@ drf = Decoder(CONFIGS["llama-68m"], dtype="bf16", device=dev, seed=1, init="devi
 eng = SpecEngine(tgt, drf, mode="injected", acceptance=example_trace(), max_batch=64, max_k=8, prompt_len=128,
                  max_new=128)
 ctx = 192
+if os.environ.get("SB_PERSISTENT") == "1":
+    from paper_2310_18813_b200 import _native as N
+    N.load().sb_set_persistent(1)
 W = cfg.streamed_bytes_per_forward(2)
 params = W / 2
 rows = []
-for b in (1, 2, 4, 8, 16, 32, 64):
-    for k in (1, 3, 8):
+grid_b = [int(x) for x in os.environ.get("XB", "1,2,4,8,16,32,64").split(",")]
+grid_k = [int(x) for x in os.environ.get("XK", "1,3,8").split(",")]
+for b in grid_b:
+    for k in grid_k:
         T = b * (k + 1)
         ms = eng.time_verify(b, k, ctx=ctx, reps=10)
         byts = W + cfg.kv_bytes_per_token(2) * (b * ctx + T) + 4 * cfg.vocab * T + 2 * cfg.hidden * T
