@@ -372,17 +372,42 @@ def run_ours(args):
     tokens = jobs * args.steps * b * NEW
     value = tokens / (total_ms / 1e3)
 
-    # ---- e2e through the public API (run_batch), pinned H2D prompts + D2H tokens per step
-    pinned_prompts = torch.zeros(b, P, dtype=torch.int32, pin_memory=True)
+    # ---- e2e through the public API (SpecEngine.generate(batch, k) -- the north_star's
+    # call): each step's prompts H2D from pinned host memory inside the timed region,
+    # generated tokens D2H into the caller's SequenceStates (wall clock)
+    pinned = [torch.from_numpy(np.stack([eng.prompt_fn(st.request_id) for st in batch(100 + s)])).pin_memory()
+              for s in range(args.steps)]
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
     for s in range(args.steps):
         sts = batch(100 + s)
-        pr = np.stack([eng.prompt_fn(st.request_id) for st in sts])
-        pinned_prompts.copy_(torch.from_numpy(pr))
-        res = run_batch(sts, k, None, eng, np.random.default_rng(s), )
+        res = eng.generate(sts, k, prompts=pinned[s])
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
+    # the reference-facing path (run_batch, engine.py:176) gives the same streams
+    chk = batch(100)
+    run_batch(chk, k, None, eng, np.random.default_rng(0))
     e2e = jobs * args.steps * b * NEW / e2e_s
+
+    # ---- config 3 names stochastic rejection sampling: the same pair in stochastic mode
+    # (REAL acceptance of the random-init weights at temperature 1, canonical inverse-CDF
+    # resampling, materialised fp32 logits/probabilities), device-timed
+    stoch = None
+    if not tp:
+        eng_s = SpecEngine(tgt, drf, mode="stochastic", max_batch=max(b, 8), max_k=8, prompt_len=P, max_new=NEW,
+                           seed=rank, autotune=False)
+        eng_s.generate(batch(90000), k)
+        ms_s, acc_s, prop_s = 0.0, 0, 0
+        for s in range(2):
+            r = eng_s.generate(batch(91000 + s), k)
+            ms_s += r.total_time + eng_s.stats.prefill_ms
+            log = eng_s.stats.accepted
+            acc_s += int(log[log >= 0].sum())
+            prop_s += int(k * (log >= 0).sum())
+        stoch = {"tokens_per_s": 2 * b * NEW / (ms_s / 1e3), "k": k,
+                 "acceptance_rate": acc_s / max(prop_s, 1), "acceptance": "real (random-init pair, T=1)"}
+        del eng_s
+        torch.cuda.empty_cache()
 
     # ---- roofline of the verify forward (the north_star's roofline object), timed live
     hbm, tf, peak_kind = _peaks()
@@ -428,13 +453,15 @@ def run_ours(args):
             "adaptive_vs_best_fixed": (sweep[k] / sweep[best_fixed]) if (sweep and k in sweep) else None,
             "iterations_per_step": iters / args.steps,
             "gpu_launches": launches,
-            "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": b * P * 4,
-                    "d2h_bytes_per_step": b * eng.cap * 4 + b * 4 * 3},
+            "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": b * P * 4 + b * 4,
+                    "d2h_bytes_per_step": b * eng.cap * 4 + b * 4 * 2 + eng.log_cap * b * 4 + 4 * 8,
+                    "api": "SpecEngine.generate(batch, k, prompts=pinned) (wall clock)"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                          "frac": achieved / hbm, "traffic": traffic, "kernel": f"verify forward b={b} k={k}",
                          "algorithmic_bytes": vb, "verify_ms": v_ms, "peak_kind": peak_kind,
                          "frac_of_8TBs": achieved / 8000.0},
             "cpu_baseline": cpu,
+            "stochastic": stoch,
             "clocks": clk.summary(),
         }
         print(json.dumps(line), flush=True)

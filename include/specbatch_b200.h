@@ -307,6 +307,8 @@ int sb_profile_forward(const sb_decoder_t* m, const sb_kvcache_t* kv, const int3
                        char* buf, int32_t buf_len);
 /* Attention implementation: 0 tensor-core flash decoding with fused RoPE+append (bf16 default), 1 separate kernels. */
 int sb_set_attention_impl(int32_t impl);
+/* Flash-decoding key splits of the tensor-core attention: 1 off (default; measured slower), 0 automatic (~2 CTAs per SM), n forced (<= 8). */
+int sb_set_attention_splits(int32_t splits);
 /* tcgen05 GEMM tuning overrides (0 = automatic): CTAs per SM (1|2), max pipeline stages, K splits. */
 int sb_gemm_tune(int32_t ctas_per_sm, int32_t max_stages, int32_t splits);
 /*

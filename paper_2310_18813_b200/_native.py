@@ -77,6 +77,7 @@ _SIGS = {
     "sb_set_pdl": (C.c_int, [_I]),
     "sb_set_fuse_norm": (C.c_int, [_I]),
     "sb_set_attention_impl": (C.c_int, [_I]),
+    "sb_set_attention_splits": (C.c_int, [_I]),
     "sb_set_persistent": (C.c_int, [_I]),
     "sb_nccl_unique_id": (C.c_int, [_P]),
     "sb_nccl_collectives_init": (C.c_int, [_P, _I, _I, C.POINTER(SbCollectives)]),

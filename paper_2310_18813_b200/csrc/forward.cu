@@ -31,6 +31,7 @@ struct FwdWorkspace {
   float* tp_part;     // TP: fp32 partial residual update, all-reduced in place [T, H]
   float* tp_logits;   // TP: local vocab slice of the logits [T, vocab_local]
   float* tp_gather;   // TP: all-gathered slices [world][T][vocab_local]
+  AttnScratch att_split;  // flash-decoding key-split partials + counters
   float* pk_scratch;  // persistent forward: stream-K partial tiles
   unsigned* pk_sync;  // persistent forward: barrier / exit / flag words (zero between launches)
   void* gemm_ws;
@@ -53,6 +54,12 @@ static size_t carve(const sb_decoder_t* m, int T, char* base, FwdWorkspace* w) {
   // address for every forward sharing this workspace, whatever T is (each
   // launch leaves them zero; any other placement would land them on dirty memory).
   o->pk_sync = (unsigned*)take(persistent_sync_bytes());
+  constexpr int kAttnItems = 16384, kAttnEntries = 640;  // counters stay at a fixed address too
+  o->att_split.counter = (int*)take((size_t)kAttnItems * 4);
+  o->att_split.max_items = kAttnItems;
+  o->att_split.max_entries = kAttnEntries;
+  o->att_split.part = (float*)take((size_t)kAttnEntries * 16 * m->head_dim * 4);
+  o->att_split.ml = (float*)take((size_t)kAttnEntries * 16 * 2 * 4);
   o->pk_scratch = (float*)take(persistent_scratch_bytes(T));
   int maxN = m->vocab;
   if (2 * m->ffn > maxN) maxN = 2 * m->ffn;
@@ -197,7 +204,7 @@ static int forward_fused_norm(const sb_decoder_t* m, const sb_kvcache_t* kv, con
     SB_TRY(gemm_tc(g, st));
     prof_mark("qkv", st);
     int rc_fa = g_attn_impl == 0 ? launch_attention_tc(w.qkv, kc, vc, w.attn, slot, pos, m->rope_cos, m->rope_sin,
-                                                        n_seq, q_len, nq, nkv, hd, kv->ctx_max, m->max_pos, st)
+                                                        n_seq, q_len, nq, nkv, hd, kv->ctx_max, m->max_pos, st, &w.att_split)
                                   : SB_EUNSUPPORTED;
     if (rc_fa != 0 && rc_fa != SB_EUNSUPPORTED) return rc_fa;
     if (rc_fa == SB_EUNSUPPORTED) {
@@ -296,7 +303,7 @@ static int forward_opt(const sb_decoder_t* m, const sb_kvcache_t* kv, const int3
     int rc_fa = SB_EUNSUPPORTED;
     if (g_attn_impl == 0 && dt == SB_BF16)
       rc_fa = launch_attention_tc(w.qkv, kc, vc, w.attn, slot, pos, m->rope_cos, m->rope_sin, n_seq, q_len, nq, nkv,
-                                  hd, kv->ctx_max, m->max_pos, st);
+                                  hd, kv->ctx_max, m->max_pos, st, &w.att_split);
     if (rc_fa != 0 && rc_fa != SB_EUNSUPPORTED) return rc_fa;
     if (rc_fa == SB_EUNSUPPORTED) {
       SB_TRY(launch_rope_append(dt, w.qkv, w.qr, kc, vc, slot, pos, m->rope_cos, m->rope_sin, T, q_len, nq, nkv, hd,
@@ -370,7 +377,7 @@ static int forward_impl(const sb_decoder_t* m, const sb_kvcache_t* kv, const int
     int rc_fa = SB_EUNSUPPORTED;
     if (g_attn_impl == 0 && dt == SB_BF16)
       rc_fa = launch_attention_tc(w.qkv, kc, vc, w.attn, slot, pos, m->rope_cos, m->rope_sin, n_seq, q_len, nq, nkv,
-                                  hd, kv->ctx_max, m->max_pos, st);
+                                  hd, kv->ctx_max, m->max_pos, st, &w.att_split);
     if (rc_fa != 0 && rc_fa != SB_EUNSUPPORTED) return rc_fa;
     if (rc_fa == SB_EUNSUPPORTED) {  // prefill-sized query blocks / wide GQA: rope+append then attention
       SB_TRY(launch_rope_append(dt, w.qkv, w.qr, kc, vc, slot, pos, m->rope_cos, m->rope_sin, T, q_len, nq, nkv, hd,
@@ -521,6 +528,12 @@ int sb_gemm_autotune(const void* x, const void* w, void* y_f32, int32_t M, int32
 }
 
 int sb_gemm_autotune_clear(void) { return gemm_tc_autotune_clear(); }
+
+int sb_set_attention_splits(int32_t splits) {
+  if (splits < 0 || splits > 8) return SB_EINVAL;
+  g_attn_splits = splits;
+  return 0;
+}
 
 int sb_set_fuse_norm(int32_t enabled) {
   g_fuse_norm = enabled ? 1 : 0;

@@ -73,9 +73,17 @@ int launch_rope_append(int dtype, const void* qkv, void* q_out, void* kc, void* 
 int launch_attention(int dtype, const void* q, const void* kc, const void* vc, void* out, const int32_t* tok_slot,
                      const int32_t* tok_pos, int n_seq, int q_len, int nq, int nkv, int hd, int ctx_max,
                      cudaStream_t st);
+struct AttnScratch {  // flash-decoding key-split partials (forward workspace)
+  float* part;
+  float* ml;
+  int* counter;  // fixed workspace address, zero between launches
+  int max_entries;  // (item, split) partial slots
+  int max_items;    // counters
+};
+extern int g_attn_splits;
 int launch_attention_tc(const void* qkv, void* kc, void* vc, void* out, const int32_t* tok_slot, const int32_t* tok_pos,
                         const float* cosT, const float* sinT, int n_seq, int q_len, int nq, int nkv, int hd,
-                        int ctx_max, int max_pos, cudaStream_t st);
+                        int ctx_max, int max_pos, cudaStream_t st, const AttnScratch* scratch = nullptr);
 int launch_argmax_partials(const float* val, const int* idx, int n_tiles, int rows, int32_t* out_tok, int out_stride,
                            int32_t* next_ids, int32_t* next_pos, const int32_t* base_pos, int pos_offset,
                            cudaStream_t st);

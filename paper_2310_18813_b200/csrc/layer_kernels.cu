@@ -474,6 +474,7 @@ int launch_attention(int dtype, const void* q, const void* kc, const void* vc, v
 // rotated K / V rows to the cache (this CTA is the only reader of its slab).
 constexpr int kTcKT = 64;
 constexpr int kTcStages = 3;
+int g_attn_splits = 1;  // 1 off (default: measured +10% slower at b=1..8), 0 auto, n forced (sb_set_attention_splits)
 
 template <int HD>
 struct TcAttnSmem {
@@ -486,12 +487,24 @@ struct TcAttnSmem {
   static constexpr size_t bytes = q + (ring > comb ? ring : comb);
 };
 
+// Flash-decoding key splits (gridDim.z = n_splits > 1): split z takes an even
+// share of the 64-key tiles, appends only the window rows inside its own key
+// range (no cross-split dependency), and publishes an unnormalised partial
+// (O, running max M, sum L per query row); the last split to finish (per-(seq,
+// kv head) counter) merges the partials in split order -- deterministic -- and
+// resets the counter for the next launch / graph replay.
+struct AttnSplit {
+  float* part;   // [n_seq][nkv][S][16][HD]
+  float* ml;     // [n_seq][nkv][S][16][2]
+  int* counter;  // [n_seq][nkv], zero between launches
+};
+
 template <int HD>
 __global__ void __launch_bounds__(128) attention_tc_kernel(
     const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc,
     __nv_bfloat16* __restrict__ out, const int32_t* __restrict__ tok_slot, const int32_t* __restrict__ tok_pos,
     const float* __restrict__ cosT, const float* __restrict__ sinT, int q_len, int nq, int nkv, int ctx_max,
-    int max_pos, float scale) {
+    int max_pos, float scale, AttnSplit sp) {
   using SM = TcAttnSmem<HD>;
   constexpr int RS = SM::RS, HALF = HD / 2, KSTEP = HD / 16, NT = HD / 8;
   extern __shared__ __align__(128) uint8_t tsm[];
@@ -533,10 +546,18 @@ __global__ void __launch_bounds__(128) attention_tc_kernel(
     Qs[j * RS + i] = a;
     Qs[j * RS + i + HALF] = b;
   }
+  // this split's key range [k_lo, k_hi) (64-key tiles shared evenly)
+  int maxp0 = -1;
+#pragma unroll
+  for (int j = 0; j < 16; ++j) maxp0 = max(maxp0, qpos[j]);
+  const int n_splits = gridDim.z, split = blockIdx.z;
+  const int tiles_all = (maxp0 + 1 + kTcKT - 1) / kTcKT;
+  const int t_lo = (int)((long)split * tiles_all / n_splits), t_hi = (int)((long)(split + 1) * tiles_all / n_splits);
+  const int k_lo = t_lo * kTcKT, k_hi = min(t_hi * kTcKT, maxp0 + 1);
   for (int e = tid; e < q_len * HALF; e += 128) {
     int t = e / HALF, i = e % HALF;
     int p = tok_pos[seq * q_len + t];
-    if (p < 0) continue;
+    if (p < k_lo || p >= k_hi) continue;  // (p < 0: padding, never in range)
     int pc = p >= max_pos ? max_pos - 1 : p;
     const __nv_bfloat16* src = seq_rows + (size_t)t * row_w + (nq + kvh) * HD;
     float x0 = __bfloat162float(src[i]), x1 = __bfloat162float(src[i + HALF]);
@@ -550,15 +571,12 @@ __global__ void __launch_bounds__(128) attention_tc_kernel(
   __threadfence_block();
   __syncthreads();
 
-  int maxp = -1;
-#pragma unroll
-  for (int j = 0; j < 16; ++j) maxp = max(maxp, qpos[j]);
-  const int n_keys = maxp + 1;
-  const int n_tiles = (n_keys + kTcKT - 1) / kTcKT;
+  const int n_keys = k_hi;
+  const int n_tiles = t_hi;  // tiles [t_lo, t_hi) of this split
 
   auto issue = [&](int tile) {
     if (tile < n_tiles) {
-      uint8_t* st = ring + (tile % kTcStages) * SM::stage;
+      uint8_t* st = ring + ((tile - t_lo) % kTcStages) * SM::stage;
       __nv_bfloat16* Kd = reinterpret_cast<__nv_bfloat16*>(st);
       __nv_bfloat16* Vd = reinterpret_cast<__nv_bfloat16*>(st + SM::tile);
       const int k0 = tile * kTcKT;
@@ -578,7 +596,7 @@ __global__ void __launch_bounds__(128) attention_tc_kernel(
     cp_async_commit();  // always commit (possibly empty) to keep group counting uniform
   };
 #pragma unroll
-  for (int i = 0; i < kTcStages - 1; ++i) issue(i);
+  for (int i = 0; i < kTcStages - 1; ++i) issue(t_lo + i);
 
   // Q fragments (A operand), loaded once
   const uint32_t qs_base = (uint32_t)__cvta_generic_to_shared(Qs);
@@ -599,11 +617,11 @@ __global__ void __launch_bounds__(128) attention_tc_kernel(
   for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
   float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;
 
-  for (int tile = 0; tile < n_tiles; ++tile) {
+  for (int tile = t_lo; tile < n_tiles; ++tile) {
     issue(tile + kTcStages - 1);
     cp_async_wait<kTcStages - 1>();
     __syncthreads();
-    const uint8_t* st = ring + (tile % kTcStages) * SM::stage;
+    const uint8_t* st = ring + ((tile - t_lo) % kTcStages) * SM::stage;
     const uint32_t kb = (uint32_t)__cvta_generic_to_shared(st);
     const uint32_t vb = kb + (uint32_t)SM::tile;
     const int kw = warp * 16;  // this warp's 16 keys within the tile
@@ -698,6 +716,28 @@ __global__ void __launch_bounds__(128) attention_tc_kernel(
     cl[warp * 16 + g + 8] = l_hi;
   }
   __syncthreads();
+  if (n_splits == 1) {
+    for (int e = tid; e < nQ * HD; e += 128) {
+      int j = e / HD, d = e % HD;
+      float M = -INFINITY;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) M = fmaxf(M, cm[w * 16 + j]);
+      float L = 0.f, acc = 0.f;
+#pragma unroll
+      for (int w = 0; w < 4; ++w) {
+        float mw = cm[w * 16 + j];
+        float f = (mw == -INFINITY) ? 0.f : __expf(mw - M);
+        L += cl[w * 16 + j] * f;
+        acc += comb[(w * 16 + j) * HD + d] * f;
+      }
+      out[((size_t)(seq * q_len + qtok[j]) * nq + qhead[j]) * HD + d] = __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
+    }
+    return;
+  }
+  // ---- split partial: warps merged in order, unnormalised
+  const size_t item = (size_t)seq * nkv + kvh;
+  float* mypart = sp.part + (item * n_splits + split) * 16 * HD;
+  float* myml = sp.ml + (item * n_splits + split) * 16 * 2;
   for (int e = tid; e < nQ * HD; e += 128) {
     int j = e / HD, d = e % HD;
     float M = -INFINITY;
@@ -711,17 +751,57 @@ __global__ void __launch_bounds__(128) attention_tc_kernel(
       L += cl[w * 16 + j] * f;
       acc += comb[(w * 16 + j) * HD + d] * f;
     }
+    __stcg(mypart + j * HD + d, acc);
+    if (d == 0) {
+      __stcg(myml + j * 2, M);
+      __stcg(myml + j * 2 + 1, L);
+    }
+  }
+  __threadfence();
+  __syncthreads();
+  __shared__ int last;
+  if (tid == 0) last = atomicAdd(sp.counter + item, 1) == n_splits - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  for (int e = tid; e < nQ * HD; e += 128) {
+    int j = e / HD, d = e % HD;
+    float M = -INFINITY;
+    for (int z = 0; z < n_splits; ++z) M = fmaxf(M, __ldcg(sp.ml + ((item * n_splits + z) * 16 + j) * 2));
+    float L = 0.f, acc = 0.f;
+    for (int z = 0; z < n_splits; ++z) {
+      const float mz = __ldcg(sp.ml + ((item * n_splits + z) * 16 + j) * 2);
+      const float f = (mz == -INFINITY) ? 0.f : __expf(mz - M);
+      L += __ldcg(sp.ml + ((item * n_splits + z) * 16 + j) * 2 + 1) * f;
+      acc += __ldcg(sp.part + ((item * n_splits + z) * 16 + j) * HD + d) * f;
+    }
     out[((size_t)(seq * q_len + qtok[j]) * nq + qhead[j]) * HD + d] = __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
   }
+  if (tid == 0) sp.counter[item] = 0;  // ready for the next launch
 }
 
 int launch_attention_tc(const void* qkv, void* kc, void* vc, void* out, const int32_t* tok_slot, const int32_t* tok_pos,
                         const float* cosT, const float* sinT, int n_seq, int q_len, int nq, int nkv, int hd,
-                        int ctx_max, int max_pos, cudaStream_t st) {
+                        int ctx_max, int max_pos, cudaStream_t st, const AttnScratch* scratch) {
   if ((hd != 64 && hd != 128) || nq % nkv != 0 || (nq / nkv) * q_len > 16) return SB_EUNSUPPORTED;
   const float scale = 1.0f / sqrtf((float)hd);
+  // key splits: enough CTAs for ~2 per SM, at most what the scratch holds, and
+  // at least 2 key tiles of the full context per split
+  int splits = 1;
+  if (scratch && scratch->part && g_attn_splits != 1) {
+    const int items = n_seq * nkv;
+    splits = g_attn_splits > 1 ? g_attn_splits : (2 * 148 + items - 1) / items;
+    const int max_tiles = (ctx_max + kTcKT - 1) / kTcKT;
+    if (splits > max_tiles / 2) splits = max_tiles / 2;
+    if (splits > 8) splits = 8;
+    while (splits > 1 && items * splits > scratch->max_entries) --splits;
+    if (items > scratch->max_items) splits = 1;
+    if (splits < 1) splits = 1;
+  }
+  AttnSplit sp{scratch ? scratch->part : nullptr, scratch ? scratch->ml : nullptr,
+               scratch ? scratch->counter : nullptr};
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(nkv, n_seq, 1);
+  cfg.gridDim = dim3(nkv, n_seq, splits);
   cfg.blockDim = dim3(128);
   cfg.stream = st;
   cudaLaunchAttribute at[1];
@@ -740,7 +820,7 @@ int launch_attention_tc(const void* qkv, void* kc, void* vc, void* out, const in
     cfg.dynamicSmemBytes = TcAttnSmem<128>::bytes;
     e = cudaLaunchKernelEx(&cfg, attention_tc_kernel<128>, (const __nv_bfloat16*)qkv, (__nv_bfloat16*)kc,
                            (__nv_bfloat16*)vc, (__nv_bfloat16*)out, tok_slot, tok_pos, cosT, sinT, q_len, nq, nkv,
-                           ctx_max, max_pos, scale);
+                           ctx_max, max_pos, scale, sp);
   } else {
     static bool attr = false;
     if (!attr) {
@@ -751,7 +831,7 @@ int launch_attention_tc(const void* qkv, void* kc, void* vc, void* out, const in
     cfg.dynamicSmemBytes = TcAttnSmem<64>::bytes;
     e = cudaLaunchKernelEx(&cfg, attention_tc_kernel<64>, (const __nv_bfloat16*)qkv, (__nv_bfloat16*)kc,
                            (__nv_bfloat16*)vc, (__nv_bfloat16*)out, tok_slot, tok_pos, cosT, sinT, q_len, nq, nkv,
-                           ctx_max, max_pos, scale);
+                           ctx_max, max_pos, scale, sp);
   }
   if (e != cudaSuccess) return (int)e;
   ++g_kernel_count;

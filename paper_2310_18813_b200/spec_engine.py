@@ -124,6 +124,7 @@ class SpecEngine:
         pf_tok = self.pf_chunk * max(1, prompt_len - 1)
         self.pf_ids = torch.zeros(pf_tok, **i32)
         self.pf_pos = torch.zeros(pf_tok, **i32)
+        self._pf_pos_pattern = torch.arange(max(1, prompt_len - 1), **i32).repeat(self.pf_chunk)
         ws = max(target.workspace_bytes(B * (K + 1)), target.workspace_bytes(pf_tok))
         if draft is not None:
             ws = max(ws, draft.workspace_bytes(2 * B), draft.workspace_bytes(pf_tok))
@@ -231,23 +232,30 @@ class SpecEngine:
 
     # ------------------------------------------------------------- batch lifecycle
     def _load_batch(self, states: list[SequenceState], prompts) -> None:
+        """Stage the formed batch: prompts (a [b, P] int32 tensor -- pinned host
+        memory is copied asynchronously -- or array-likes / the prompt_fn) go to
+        the device token table; lengths and counters reset."""
         b = len(states)
         P = self.prompt_len
-        toks = np.zeros((b, self.cap), dtype=np.int32)
-        for i, st in enumerate(states):
-            pr = prompts[i] if prompts is not None else self.prompt_fn(st.request_id)
-            pr = np.asarray(pr, dtype=np.int32).reshape(-1)
-            if pr.size != P:
-                raise ValueError(f"prompt of request {st.request_id} has {pr.size} tokens, engine expects {P}")
-            toks[i, :P] = pr
-        self.tokens[:b].copy_(torch.from_numpy(toks), non_blocking=False)
+        if torch.is_tensor(prompts):
+            if tuple(prompts.shape) != (b, P):
+                raise ValueError(f"prompts tensor must be [{b}, {P}], got {tuple(prompts.shape)}")
+            self.tokens[:b, :P].copy_(prompts.to(torch.int32), non_blocking=True)
+        else:
+            toks = np.zeros((b, P), dtype=np.int32)
+            for i, st in enumerate(states):
+                pr = prompts[i] if prompts is not None else self.prompt_fn(st.request_id)
+                pr = np.asarray(pr, dtype=np.int32).reshape(-1)
+                if pr.size != P:
+                    raise ValueError(f"prompt of request {st.request_id} has {pr.size} tokens, engine expects {P}")
+                toks[i] = pr
+            self.tokens[:b, :P].copy_(torch.from_numpy(toks))
         self.n_tok[:b].fill_(P)
         self.produced[:b].zero_()
         self.target_len[:b].copy_(torch.tensor([st.target_len for st in states], dtype=torch.int32))
         self.finish_iter.fill_(-1)
         self.iter.zero_()
         self.acc_log.fill_(-1)
-        self._prompts_host = toks
 
     def _prefill(self, b: int) -> None:
         P = self.prompt_len
@@ -256,9 +264,9 @@ class SpecEngine:
         q = P - 1
         for s0 in range(0, b, self.pf_chunk):
             nb = min(self.pf_chunk, b - s0)
-            ids = torch.from_numpy(self._prompts_host[s0:s0 + nb, :q].reshape(-1).copy())
-            self.pf_ids[: nb * q].copy_(ids)
-            self.pf_pos[: nb * q].copy_(torch.arange(q, dtype=torch.int32).repeat(nb))
+            # prompt ids straight from the device token table (no host round trip)
+            self.pf_ids[: nb * q].copy_(self.tokens[s0:s0 + nb, :q].reshape(-1))
+            self.pf_pos[: nb * q].copy_(self._pf_pos_pattern[: nb * q])
             slots = self.slots[s0:]
             self.target.forward(self.kv_t, self.pf_ids, slots, self.pf_pos, nb, q, None, N.LOGITS_NONE,
                                 self.workspace)
