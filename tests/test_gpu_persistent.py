@@ -118,3 +118,25 @@ def test_persistent_workspace_sync_words_reset(cuda_dev):
     for _ in range(5):
         _run(dec, True, ids1, pos1, slots, b, P, N.LOGITS_LAST, ws, kv)
     assert int(ws[: 4 * 200].view(torch.int32).abs().sum().item()) == 0
+
+
+@pytest.mark.parametrize("splits", [2, 4, 8])
+def test_attention_key_splits_match_single_pass(cuda_dev, splits):
+    """Flash-decoding key splits (sb_set_attention_splits) == one pass over the
+    keys: logits within the bf16 tolerance, identical KV appends."""
+    lib = N.load()
+    cfg = replace(CONFIGS["llama-2-7b"], n_layers=2)
+    b, P, k = 2, 150, 3
+    dec, slots, ws, (ids1, pos1), (ids2, pos2) = _case(cfg, cuda_dev, b, P, k, seed=9)
+    outs = []
+    try:
+        for sp in (1, splits):
+            lib.sb_set_attention_splits(sp)
+            kv = dec.new_kv(b, 192)
+            _run(dec, False, ids1, pos1, slots, b, P, N.LOGITS_NONE, ws, kv)
+            lg = _run(dec, False, ids2, pos2, slots, b, k + 1, N.LOGITS_ALL, ws, kv)
+            outs.append((lg, kv.k.clone(), kv.v.clone()))
+    finally:
+        lib.sb_set_attention_splits(1)
+    assert _close(outs[0][0], outs[1][0]) < TOL
+    assert torch.equal(outs[0][1], outs[1][1]) and torch.equal(outs[0][2], outs[1][2])
