@@ -275,6 +275,13 @@ def run_trace(args):
         lat[pol.label] = rep.avg_latency / args.trace_scale  # back to trace seconds
         sizes = [r.served_batch_size for r in rep.records]
         batches[pol.label] = round(float(np.mean(sizes)), 2)
+    # continuous batching: retire / admit every iteration, k from the LUT per iteration
+    from paper_2310_18813_b200.serving import serve_continuous
+    cont = {}
+    for pol in [AdaptivePolicy(lut), FixedPolicy(3)]:
+        rep, extra = serve_continuous(workload, eng, pol, time_scale=args.trace_scale, max_batch=16)
+        cont[pol.label] = {"latency_s": round(rep.avg_latency / args.trace_scale, 4),
+                           "mean_live_batch": round(extra["mean_live_batch"], 2), "mean_k": round(extra["mean_k"], 2)}
     t_run = time.perf_counter() - t_run
     fixed = {k: v for k, v in lat.items() if k.startswith("fixed")}
     best = min(fixed, key=fixed.get)
@@ -288,6 +295,7 @@ def run_trace(args):
             "latency_s_by_policy": {k: round(v, 4) for k, v in lat.items()},
             "mean_batch_by_policy": batches, "best_fixed": best,
             "adaptive_vs_best_fixed_latency": lat[ad] / fixed[best], "wall_s": round(t_run, 1),
+            "continuous_batching": cont,
             "graph_capture_s": round(t_cap, 1)}
     print(json.dumps(line), flush=True)
 

@@ -125,6 +125,7 @@ class SpecEngine:
         self.pf_ids = torch.zeros(pf_tok, **i32)
         self.pf_pos = torch.zeros(pf_tok, **i32)
         self._pf_pos_pattern = torch.arange(max(1, prompt_len - 1), **i32).repeat(self.pf_chunk)
+        self.pf_slots = torch.zeros(max(B, self.pf_chunk), **i32)  # KV slots of rows being prefilled (serving.py)
         ws = max(target.workspace_bytes(B * (K + 1)), target.workspace_bytes(pf_tok))
         if draft is not None:
             ws = max(ws, draft.workspace_bytes(2 * B), draft.workspace_bytes(pf_tok))
