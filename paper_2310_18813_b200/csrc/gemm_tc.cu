@@ -44,6 +44,7 @@ struct TcParams {
   int n_tiles_n;  // ceil(N / 128)
   int kb;         // 64-wide k-blocks of K
   int splits;     // K splits == cluster size (1..8)
+  int wt;         // 128-row weight tiles per CTA sharing each token (X) stage: 1, or 2 (splits == 1, large T)
   int stages;
   int epi;
   void* y;
@@ -102,7 +103,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int tn = p.tn;
-  const uint32_t a_bytes = TC_BM * TC_BK * 2;
+  const int wt = p.wt;
+  const uint32_t a_bytes = wt * TC_BM * TC_BK * 2;
   const uint32_t b_bytes = tn * TC_BK * 2;
   const uint32_t stage_bytes = a_bytes + b_bytes;
   const uint32_t ring_bytes = p.stages * stage_bytes;
@@ -120,14 +122,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int split = p.splits > 1 ? (int)cluster_rank() : 0;
-  const int tile_n = blockIdx.x / p.splits;
-  const int n0 = tile_n * TC_BM;
+  const int tile_n = blockIdx.x / p.splits;  // in units of wt 128-row tiles
+  const int n0 = tile_n * TC_BM * wt;
   const int m0 = blockIdx.y * tn;
   const int kb0 = (int)((long long)split * p.kb / p.splits);
   const int kb1 = (int)((long long)(split + 1) * p.kb / p.splits);
   const int nkb = kb1 - kb0;
   uint32_t tmem_cols = 32;
-  while ((int)tmem_cols < tn) tmem_cols <<= 1;
+  while ((int)tmem_cols < wt * tn) tmem_cols <<= 1;
 
   if (threadIdx.x == 0) {
     for (int s = 0; s < p.stages; ++s) {
@@ -190,10 +192,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         tc_fence_after();
         uint32_t sa = smem_u32(stage_base + stage * stage_bytes);
         uint32_t sb = sa + a_bytes;
+        for (int a = 0; a < wt; ++a) {  // the X stage feeds every weight tile of the CTA
 #pragma unroll
-        for (int kk = 0; kk < TC_BK / TC_UK; ++kk)
-          tc_mma(tmem, sw128_desc(sa + kk * TC_UK * 2), sw128_desc(sb + kk * TC_UK * 2), idesc,
-                 (i > 0 || kk > 0) ? 1u : 0u);
+          for (int kk = 0; kk < TC_BK / TC_UK; ++kk)
+            tc_mma(tmem + (uint32_t)(a * tn), sw128_desc(sa + a * TC_BM * TC_BK * 2 + kk * TC_UK * 2),
+                   sw128_desc(sb + kk * TC_UK * 2), idesc, (i > 0 || kk > 0) ? 1u : 0u);
+        }
         tc_commit(&empty[stage]);
         if (++stage == p.stages) {
           stage = 0;
@@ -226,9 +230,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     mbar_wait(tmem_full, 0);
     tc_fence_after();
     const bool scale = p.ns_part != nullptr;
+    for (int acc = 0; acc < wt; ++acc) {
+    const int n0a = n0 + acc * TC_BM;             // this accumulator's weight rows
+    const int tile_a = tile_n * wt + acc;          // its 128-row tile index
+    if (acc > 0) asm volatile("bar.sync 1, 128;" ::: "memory");  // staging reuse
     for (int j0 = 0; j0 < tn; j0 += 16) {
       float v[16];
-      tmem_ld16(lane_addr + j0, v);
+      tmem_ld16(lane_addr + (uint32_t)(acc * tn) + j0, v);
       if (p.splits > 1) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) red[(j0 + j) * TC_BM + row] = v[j];
@@ -244,7 +252,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         int* qi = reinterpret_cast<int*>(red + 4 * tn);
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          const int m = m0 + j0 + j, n = n0 + row;
+          const int m = m0 + j0 + j, n = n0a + row;
           float val = (n < p.N) ? v[j] : -INFINITY;
           if (p.y && m < p.M && n < p.N) ((float*)p.y)[(size_t)m * p.N + n] = v[j];
           ArgMax a = warp_argmax(ArgMax{val, n < p.N ? n : INT_MAX});
@@ -257,12 +265,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           float other = __shfl_xor_sync(0xffffffffu, v[j], 1);
-          if (!(lane & 1)) epi_pair(p, m0 + j0 + j, n0 + row, v[j], other);
+          if (!(lane & 1)) epi_pair(p, m0 + j0 + j, n0a + row, v[j], other);
         }
       } else {
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          float nv = epi_one(p, m0 + j0 + j, n0 + row, v[j]);
+          float nv = epi_one(p, m0 + j0 + j, n0a + row, v[j]);
           if (p.out_part) {  // per-token sum of squares over the tile's 128 rows (fixed xor tree)
             float s = warp_sum(nv * nv);
             if (lane == 0) sq[quad * tn + j0 + j] = s;
@@ -270,7 +278,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
       }
     }
-    if (p.splits == 1 && (p.epi == EPI_ARGMAX || p.out_part)) {
+    if (p.splits == 1 && (p.epi == EPI_ARGMAX || p.out_part) && tile_a < p.n_tiles_n) {
       asm volatile("bar.sync 1, 128;" ::: "memory");
       for (int j = et; j < tn; j += 128) {
         const int m = m0 + j;
@@ -281,13 +289,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           ArgMax a{qv[j], qi[j]};
 #pragma unroll
           for (int q = 1; q < 4; ++q) a = argmax_merge(a, ArgMax{qv[q * tn + j], qi[q * tn + j]});
-          p.aux_val[(size_t)tile_n * p.M + m] = a.v;
-          p.aux_idx[(size_t)tile_n * p.M + m] = a.i;
+          p.aux_val[(size_t)tile_a * p.M + m] = a.v;
+          p.aux_idx[(size_t)tile_a * p.M + m] = a.i;
         } else {
-          p.out_part[(size_t)tile_n * p.M + m] = ((sq[j] + sq[tn + j]) + sq[2 * tn + j]) + sq[3 * tn + j];
+          p.out_part[(size_t)tile_a * p.M + m] = ((sq[j] + sq[tn + j]) + sq[2 * tn + j]) + sq[3 * tn + j];
         }
       }
     }
+    }  // acc
     tc_fence_before();
   }
   __syncwarp();
@@ -400,15 +409,19 @@ int g_pdl = 1;  // programmatic dependent launch for every forward kernel (sb_se
 static int g_tune_cps = 0, g_tune_stages = 0, g_tune_splits = 0;
 
 struct TcPlan {
-  int tn, n_tiles_n, m_tiles, kb, splits, stages, ctas_per_sm;
+  int tn, n_tiles_n, m_tiles, kb, splits, stages, ctas_per_sm, wt;
   size_t smem;
+};
+struct TcTuned {
+  int cps, splits, wt;
 };
 
 // Measured (CTAs per SM, K splits) per GEMM shape (sb_gemm_autotune, run by the
 // host outside graph capture for the token counts an engine will use); the
 // heuristic below is the fallback.
 static std::mutex g_tuned_mu;
-static std::map<unsigned long long, std::pair<int, int>> g_tuned;
+static std::map<unsigned long long, TcTuned> g_tuned;
+static int g_tune_wt = 0;  // autotune candidate override (0 = plan's choice)
 static unsigned long long tune_key(int tn, int m_tiles, int N, int K) {
   return ((unsigned long long)tn << 48) | ((unsigned long long)m_tiles << 40) | ((unsigned long long)N << 20) |
          (unsigned long long)K;
@@ -424,13 +437,14 @@ static TcPlan plan(int M, int N, int K, int epi) {
   q.m_tiles = (M + q.tn - 1) / q.tn;
   q.kb = (K + TC_BK - 1) / TC_BK;
   q.ctas_per_sm = g_tune_cps ? g_tune_cps : (q.tn >= 128 ? 1 : 2);
-  int tuned_splits = 0;
+  int tuned_splits = 0, tuned_wt = 0;
   if (!g_tune_cps && !g_tune_splits) {
     std::lock_guard<std::mutex> lk(g_tuned_mu);
     auto it = g_tuned.find(tune_key(q.tn, q.m_tiles, N, K));
     if (it != g_tuned.end()) {
-      q.ctas_per_sm = it->second.first;
-      tuned_splits = it->second.second;
+      q.ctas_per_sm = it->second.cps;
+      tuned_splits = it->second.splits;
+      tuned_wt = it->second.wt;
     }
   }
   const int sms = num_sms();
@@ -445,8 +459,15 @@ static TcPlan plan(int M, int N, int K, int epi) {
   if (tuned_splits) q.splits = tuned_splits;
   if (g_tune_splits) q.splits = g_tune_splits;
   if (epi == EPI_ARGMAX) q.splits = 1;  // the fused argmax reads whole tiles straight from TMEM
+  // large token tiles: two 128-row weight tiles per CTA share every X stage
+  // (halves the L2->smem token traffic per FLOP; compute-bound regime)
+  q.wt = 1;
+  if (q.splits == 1 && q.ctas_per_sm == 1 && q.n_tiles_n >= 2 &&
+      (tuned_wt ? tuned_wt == 2 : (q.tn >= 128 && (q.n_tiles_n + 1) / 2 * q.m_tiles >= sms)))
+    q.wt = 2;  // (heuristic: only when the halved grid still covers every SM)
+  if (g_tune_wt) q.wt = (q.splits == 1 && q.ctas_per_sm == 1 && q.n_tiles_n >= 2) ? g_tune_wt : 1;
   size_t budget = q.ctas_per_sm == 2 ? 108 * 1024 : 200 * 1024;
-  size_t stage = (size_t)(TC_BM + q.tn) * TC_BK * 2;
+  size_t stage = (size_t)(TC_BM * q.wt + q.tn) * TC_BK * 2;
   q.stages = (int)((budget - 1024 - 256) / stage);
   if (q.stages > (g_tune_stages ? g_tune_stages : 12)) q.stages = g_tune_stages ? g_tune_stages : 12;
   if (q.stages < 2) q.stages = 2;
@@ -479,13 +500,25 @@ int gemm_tc_autotune(const void* x, const void* w, float* y, int M, int N, int K
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   float best = 1e30f;
-  int best_cps = 0, best_sp = 0, rc = 0;
-  for (int cps = 1; cps <= 2 && !rc; ++cps) {
-    for (int sp = 1; sp <= 8 && !rc; sp *= 2) {
+  int best_cps = 0, best_sp = 0, best_wt = 1, rc = 0;
+  struct Cand {
+    int cps, sp, wt;
+  };
+  Cand cands[16];
+  int nc = 0;
+  for (int cps = 1; cps <= 2; ++cps)
+    for (int sp = 1; sp <= 8; sp *= 2) {
       if (sp > 1 && kb / sp < 2) break;
       if (tiles * sp > 2 * num_sms() * cps) break;  // more than two waves: never the winner
+      cands[nc++] = {cps, sp, 1};
+    }
+  if (tn >= 64 && (N + TC_BM - 1) / TC_BM >= 2) cands[nc++] = {1, 1, 2};
+  for (int ci = 0; ci < nc && !rc; ++ci) {
+    {
+      const int cps = cands[ci].cps, sp = cands[ci].sp;
       g_tune_cps = cps;
       g_tune_splits = sp;
+      g_tune_wt = cands[ci].wt;
       g_tune_stages = 0;
       rc = gemm_tc(a, st);  // warm
       if (rc) break;
@@ -501,9 +534,11 @@ int gemm_tc_autotune(const void* x, const void* w, float* y, int M, int N, int K
         best = us;
         best_cps = cps;
         best_sp = sp;
+        best_wt = cands[ci].wt;
       }
     }
   }
+  g_tune_wt = 0;
   g_tune_cps = save_cps;
   g_tune_stages = save_st;
   g_tune_splits = save_sp;
@@ -512,7 +547,7 @@ int gemm_tc_autotune(const void* x, const void* w, float* y, int M, int N, int K
   if (rc) return rc;
   {
     std::lock_guard<std::mutex> lk(g_tuned_mu);
-    g_tuned[tune_key(tn, m_tiles, N, K)] = {best_cps, best_sp};
+    g_tuned[tune_key(tn, m_tiles, N, K)] = {best_cps, best_sp, best_wt};
   }
   if (cps_out) *cps_out = best_cps;
   if (splits_out) *splits_out = best_sp;
@@ -558,7 +593,7 @@ int gemm_tc(const GemmArgs& a, cudaStream_t st) {
   SB_TRY(gemm_tc_init());
   TcPlan q = plan(a.M, a.N, a.K, a.epi);
   CUtensorMap mw, mx;
-  SB_TRY(make_map(&mw, a.w, a.N, a.K, a.K, TC_BM));
+  SB_TRY(make_map(&mw, a.w, a.N, a.K, a.K, TC_BM * q.wt));
   SB_TRY(make_map(&mx, a.x, a.M, a.K, a.ldx, q.tn));
   TcParams p;
   p.M = a.M;
@@ -568,6 +603,7 @@ int gemm_tc(const GemmArgs& a, cudaStream_t st) {
   p.n_tiles_n = q.n_tiles_n;
   p.kb = q.kb;
   p.splits = q.splits;
+  p.wt = q.wt;
   p.stages = q.stages;
   p.epi = a.epi;
   p.y = a.y;
@@ -588,7 +624,7 @@ int gemm_tc(const GemmArgs& a, cudaStream_t st) {
   if (a.out_part && a.epi != EPI_RESID_ADD) return SB_EINVAL;
   if (a.epi == EPI_ARGMAX && (!a.aux_val || !a.aux_idx)) return SB_EINVAL;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(q.n_tiles_n * q.splits, q.m_tiles, 1);
+  cfg.gridDim = dim3((q.n_tiles_n + q.wt - 1) / q.wt * q.splits, q.m_tiles, 1);
   cfg.blockDim = dim3(TC_THREADS, 1, 1);
   cfg.dynamicSmemBytes = q.smem;
   cfg.stream = st;

@@ -34,11 +34,16 @@ __all__ = ["serve_continuous"]
 
 
 def serve_continuous(workload: list[Request], engine, policy, time_scale: float = 1.0, max_batch: int | None = None,
-                     group_size: int = 40, clock=None, collect: bool = False) -> tuple[SimulationReport, dict]:
+                     group_size: int = 40, clock=None, collect: bool = False, min_admit: int = 1,
+                     max_wait: float = 0.0) -> tuple[SimulationReport, dict]:
     """Serve `workload` with continuous batching on `engine` (a SpecEngine).
 
     `policy.decide(b)` picks k at every iteration for the live batch size b
     (AdaptivePolicy(lut) / FixedPolicy(k)).  Requests need gen_len <= engine.max_new.
+    Admission batching: a prefill streams the whole target once, so admitting
+    one request at a time is expensive; new requests join only when at least
+    `min_admit` can (or the engine is idle, or the oldest has waited
+    `max_wait` wall seconds).
     Returns (report, {"mean_live_batch", "mean_k", "iterations"[, "outputs": {id: tokens}]}).
     """
     if any(nxt.arrival < cur.arrival for cur, nxt in zip(workload, workload[1:])):
@@ -79,7 +84,11 @@ def serve_continuous(workload: list[Request], engine, policy, time_scale: float 
                 continue
             # ---- admission into free rows / KV slots
             new_rows = []
-            while waiting and len(row_req) < B:
+            room = B - len(row_req)
+            admit = bool(waiting) and room > 0 and (
+                not row_req or min(room, len(waiting)) >= min_admit
+                or (max_wait > 0 and now - waiting[0].arrival * time_scale >= max_wait))
+            while admit and waiting and len(row_req) < B:
                 r = waiting.popleft()
                 row = len(row_req)
                 row_req.append(r)
