@@ -68,6 +68,7 @@ def serve_continuous(workload: list[Request], engine, policy, time_scale: float 
     k_hist: list[int] = []
     b_hist: list[int] = []
     outputs: dict[int, list[int]] = {}
+    prof = {"prefills": 0, "prefill_rows": 0, "prefill_s": 0.0, "iter_s": 0.0, "host_s": 0.0, "idle_s": 0.0}
     with torch.cuda.stream(eng.stream):
         eng.iter.zero_()
         eng.finish_iter.fill_(-1)
@@ -81,6 +82,7 @@ def serve_continuous(workload: list[Request], engine, policy, time_scale: float 
                 wait = workload[nxt].arrival * time_scale - now
                 if wait > 0:
                     time.sleep(min(wait, 0.005))
+                    prof["idle_s"] += min(wait, 0.005)
                 continue
             # ---- admission into free rows / KV slots
             new_rows = []
@@ -105,11 +107,16 @@ def serve_continuous(workload: list[Request], engine, policy, time_scale: float 
                 eng.finish_iter[r0:r0 + n].fill_(-1)
                 eng.target_len[r0:r0 + n].copy_(torch.tensor([row_req[i].gen_len for i in new_rows], dtype=torch.int32))
                 eng.slots[:b].copy_(torch.tensor(slot_of_row, dtype=torch.int32))
+                tp = clock()
                 _prefill_rows(eng, new_rows)
                 eng.stream.synchronize()  # pinned staging rows are reused next admission
+                prof["prefill_s"] += clock() - tp
+                prof["prefills"] += 1
+                prof["prefill_rows"] += len(new_rows)
             # ---- one speculative iteration at the LUT's k for the live batch size
             k = policy.decide(b).chosen_s
             k = min(k, eng.max_k)
+            ti = clock()
             eng._graph(b, k).replay() if eng.use_graphs else eng._iteration(b, k)
             k_hist.append(k)
             b_hist.append(b)
@@ -117,6 +124,7 @@ def serve_continuous(workload: list[Request], engine, policy, time_scale: float 
             done = (eng.produced[:b] >= eng.target_len[:b]).to(torch.int32)
             done_host[:b].copy_(done, non_blocking=True)
             eng.stream.synchronize()
+            prof["iter_s"] += clock() - ti
             fin = done_host[:b].numpy().astype(bool)
             if fin.any():
                 t_done = clock() - t0
@@ -144,7 +152,8 @@ def serve_continuous(workload: list[Request], engine, policy, time_scale: float 
         eng.slots.copy_(torch.arange(eng.max_batch, **i32))  # generate() assumes row == slot
     rep = summarize(records, group_size=group_size, policy=f"continuous/{getattr(policy, 'label', 'policy')}")
     extra = {"mean_live_batch": float(np.mean(b_hist)) if b_hist else 0.0,
-             "mean_k": float(np.mean(k_hist)) if k_hist else 0.0, "iterations": len(k_hist)}
+             "mean_k": float(np.mean(k_hist)) if k_hist else 0.0, "iterations": len(k_hist),
+             "wall_s": clock() - t0, **{k_: round(v_, 3) if isinstance(v_, float) else v_ for k_, v_ in prof.items()}}
     if collect:
         extra["outputs"] = outputs
     return rep, extra
