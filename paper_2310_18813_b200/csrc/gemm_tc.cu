@@ -85,6 +85,21 @@ __device__ __forceinline__ float epi_one(const TcParams& p, int m, int n, float 
   }
   return v;
 }
+// EPI_RESID_ADD with the old residual already loaded (`prev`): lets callers
+// issue all residual loads of a chunk before any store (one L2 round trip per
+// chunk instead of one per element).
+__device__ __forceinline__ float epi_resid_pre(const TcParams& p, int m, int n, float v, float prev) {
+  if (m >= p.M || n >= p.N) return 0.f;
+  const size_t o = (size_t)m * p.N + n;
+  if (p.bias) v += __bfloat162float(p.bias[n]);
+  const float nv = prev + v;
+  ((float*)p.y)[o] = nv;
+  if (p.out_xb) p.out_xb[o] = __float2bfloat16_rn(nv);
+  return nv;
+}
+__device__ __forceinline__ float resid_load(const TcParams& p, int m, int n) {
+  return (m < p.M && n < p.N) ? __ldcg((const float*)p.y + (size_t)m * p.N + n) : 0.f;
+}
 // SILU pairs rows (n, n+1) = (gate, up)
 __device__ __forceinline__ void epi_pair(const TcParams& p, int m, int n, float g, float u) {
   if (m >= p.M || n >= p.N) return;
@@ -268,9 +283,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           if (!(lane & 1)) epi_pair(p, m0 + j0 + j, n0a + row, v[j], other);
         }
       } else {
+        float rv[16];
+        if (p.epi == EPI_RESID_ADD) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) rv[j] = resid_load(p, m0 + j0 + j, n0a + row);  // all in flight
+        }
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          float nv = epi_one(p, m0 + j0 + j, n0a + row, v[j]);
+          float nv = p.epi == EPI_RESID_ADD ? epi_resid_pre(p, m0 + j0 + j, n0a + row, v[j], rv[j])
+                                            : epi_one(p, m0 + j0 + j, n0a + row, v[j]);
           if (p.out_part) {  // per-token sum of squares over the tile's 128 rows (fixed xor tree)
             float s = warp_sum(nv * nv);
             if (lane == 0) sq[quad * tn + j0 + j] = s;
@@ -311,29 +332,81 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int et = threadIdx.x - 64;
       const uint32_t red_addr = smem_u32(red);
       const bool scale = p.ns_part != nullptr;
+      // Batches of 4 elements per thread: all DSMEM partial loads of the batch
+      // (4 x splits) and its residual loads are in flight together; the sums
+      // still run in rank order 0..splits-1 (bit-identical to one at a time).
+      constexpr int EB = 4;
       if (p.epi == EPI_SILU_MUL) {
         const int pairs = R / 2;
-        for (int it = et; it < pairs * tn; it += 128) {
-          int r = r_base + 2 * (it % pairs), j = it / pairs;
-          float g = 0.f, u = 0.f;
-          for (int q = 0; q < p.splits; ++q) {
-            g += ld_dsmem_f32(red_addr + (uint32_t)((j * TC_BM + r) * 4), q);
-            u += ld_dsmem_f32(red_addr + (uint32_t)((j * TC_BM + r + 1) * 4), q);
+        for (int it0 = et; it0 < pairs * tn; it0 += 128 * EB) {
+          float t[8][EB][2];
+          int rr[EB], jj[EB];
+#pragma unroll
+          for (int e = 0; e < EB; ++e) {
+            const int it = it0 + e * 128;
+            rr[e] = it < pairs * tn ? r_base + 2 * (it % pairs) : -1;
+            jj[e] = it / pairs;
           }
-          if (scale) {
-            g *= inv_s[j];
-            u *= inv_s[j];
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+#pragma unroll
+            for (int e = 0; e < EB; ++e) {
+              const bool ok = q < p.splits && rr[e] >= 0;
+              const uint32_t ad = red_addr + (uint32_t)((jj[e] * TC_BM + (ok ? rr[e] : 0)) * 4);
+              t[q][e][0] = ok ? ld_dsmem_f32_nc(ad, q) : 0.f;
+              t[q][e][1] = ok ? ld_dsmem_f32_nc(ad + 4, q) : 0.f;
+            }
+#pragma unroll
+          for (int e = 0; e < EB; ++e) {
+            if (rr[e] < 0) continue;
+            float g = 0.f, u = 0.f;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (q < p.splits) {
+                g += t[q][e][0];
+                u += t[q][e][1];
+              }
+            if (scale) {
+              g *= inv_s[jj[e]];
+              u *= inv_s[jj[e]];
+            }
+            epi_pair(p, m0 + jj[e], n0 + rr[e], g, u);
           }
-          epi_pair(p, m0 + j, n0 + r, g, u);
         }
       } else {
-        for (int it = et; it < R * tn; it += 128) {
-          int rl = it % R, j = it / R, r = r_base + rl;
-          float a = 0.f;
-          for (int q = 0; q < p.splits; ++q) a += ld_dsmem_f32(red_addr + (uint32_t)((j * TC_BM + r) * 4), q);
-          if (scale) a *= inv_s[j];
-          float nv = epi_one(p, m0 + j, n0 + r, a);
-          if (p.out_part) sq[j * R + rl] = nv * nv;
+        for (int it0 = et; it0 < R * tn; it0 += 128 * EB) {
+          float t[8][EB], rv[EB];
+          int rl_[EB], jj[EB];
+#pragma unroll
+          for (int e = 0; e < EB; ++e) {
+            const int it = it0 + e * 128;
+            rl_[e] = it < R * tn ? it % R : -1;
+            jj[e] = it / R;
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+#pragma unroll
+            for (int e = 0; e < EB; ++e) {
+              const bool ok = q < p.splits && rl_[e] >= 0;
+              t[q][e] = ok ? ld_dsmem_f32_nc(red_addr + (uint32_t)((jj[e] * TC_BM + r_base + rl_[e]) * 4), q) : 0.f;
+            }
+          if (p.epi == EPI_RESID_ADD) {
+#pragma unroll
+            for (int e = 0; e < EB; ++e) rv[e] = rl_[e] >= 0 ? resid_load(p, m0 + jj[e], n0 + r_base + rl_[e]) : 0.f;
+          }
+#pragma unroll
+          for (int e = 0; e < EB; ++e) {
+            if (rl_[e] < 0) continue;
+            float a = 0.f;
+#pragma unroll
+            for (int q = 0; q < 8; ++q)
+              if (q < p.splits) a += t[q][e];
+            if (scale) a *= inv_s[jj[e]];
+            const int r = r_base + rl_[e];
+            const float nv = p.epi == EPI_RESID_ADD ? epi_resid_pre(p, m0 + jj[e], n0 + r, a, rv[e])
+                                                    : epi_one(p, m0 + jj[e], n0 + r, a);
+            if (p.out_part) sq[jj[e] * R + rl_[e]] = nv * nv;
+          }
         }
         if (p.out_part) {
           asm volatile("bar.sync 1, 128;" ::: "memory");

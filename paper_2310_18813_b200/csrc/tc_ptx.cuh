@@ -106,4 +106,14 @@ __device__ __forceinline__ float ld_dsmem_f32(uint32_t local_addr, uint32_t peer
   return v;
 }
 
+// DSMEM load without a compiler memory barrier: a batch of these can be in
+// flight together (callers order them against the cluster barrier themselves).
+__device__ __forceinline__ float ld_dsmem_f32_nc(uint32_t local_addr, uint32_t peer) {
+  uint32_t remote;
+  asm("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_addr), "r"(peer));
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(remote));
+  return v;
+}
+
 }  // namespace sb
