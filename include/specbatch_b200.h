@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define SB_ABI_VERSION 4
+#define SB_ABI_VERSION 5
 
 /* status codes beyond cudaError_t (which are < 1000) */
 #define SB_OK 0
@@ -268,6 +268,25 @@ int sb_prepare_iteration(int32_t b, int32_t k, const int32_t* tokens, int32_t to
                          int32_t* d_last_pos, uint64_t seed, const int32_t* iter, float* uniforms,
                          int32_t n_u, const int32_t* inj_samples, int32_t inj_count, int32_t* l_inj,
                          void* stream);
+
+/*
+ * The whole greedy draft loop of one iteration in ONE persistent launch (K1):
+ * steps j = 1..k of the draft decoder for b sequences, staged exactly like k
+ * calls of sb_decoder_forward_ex with a token sink -- step 1 feeds d1_ids /
+ * d1_pos (the last two committed tokens per sequence, [b, 2]), step j >= 2
+ * feeds ds_ids / ds_pos -- and writing v_ids[s*(k+1) + j] = d_j,
+ * ds_ids[s] = d_j, ds_pos[s] = d_base[s] + j.  Row-parallel mma.sync GEMMs,
+ * grid barriers between phases.  SB_EUNSUPPORTED outside its envelope (bf16
+ * Llama-arch, 2b <= 16, <= 16 layers, ctx_max <= 288, dims multiple of 64):
+ * the caller then issues the per-step forwards.
+ */
+int sb_draft_loop(const sb_decoder_t* m, const sb_kvcache_t* kv, int32_t b, int32_t k, const int32_t* d1_ids,
+                  const int32_t* d1_pos, const int32_t* slots, const int32_t* d_base, int32_t* v_ids,
+                  int32_t* ds_ids, int32_t* ds_pos, void* workspace, size_t ws_bytes, void* stream);
+/* Enable sb_draft_loop (default 0: measured 2x slower than the per-step forwards); 1 = use it. */
+/* Diagnostics: globaltimer stamps of every draft-loop grid barrier (CTA 0) into device_buf; NULL = off. */
+int sb_debug_draft_loop_trace(void* device_buf);
+int sb_set_draft_loop(int32_t enabled);
 
 /* Compaction (K5): copy KV slabs src_slot[i] -> dst_slot[i] for positions [0, len[i]). */
 int sb_kv_compact(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* src_slot,

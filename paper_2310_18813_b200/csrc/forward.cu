@@ -542,6 +542,34 @@ int sb_set_fuse_norm(int32_t enabled) {
 
 int sb_set_persistent(int32_t enabled) { return set_persistent(enabled); }
 
+static int g_draft_loop = 0;  // sb_set_draft_loop (off by default: measured slower)
+
+int sb_debug_draft_loop_trace(void* device_buf) { return set_draft_loop_trace(device_buf); }
+
+int sb_set_draft_loop(int32_t enabled) {
+  g_draft_loop = enabled ? 1 : 0;
+  return 0;
+}
+
+int sb_draft_loop(const sb_decoder_t* m, const sb_kvcache_t* kv, int32_t b, int32_t k, const int32_t* d1_ids,
+                  const int32_t* d1_pos, const int32_t* slots, const int32_t* d_base, int32_t* v_ids, int32_t* ds_ids,
+                  int32_t* ds_pos, void* workspace, size_t ws_bytes, void* stream) {
+  if (!m || !kv || b < 1 || k < 0) return SB_EINVAL;
+  if (!g_draft_loop || !draft_loop_eligible(m, b)) return SB_EUNSUPPORTED;
+  if (k == 0) return 0;
+  FwdWorkspace w;
+  const size_t need = carve(m, 2 * b, (char*)workspace, &w);
+  if (need > ws_bytes) return SB_EWORKSPACE;
+  g_kernel_count = 0;
+  const int gw = num_sms() * 8;
+  if ((size_t)gw * b * 8 > persistent_scratch_bytes(2 * b)) return SB_EUNSUPPORTED;
+  DlBuffers buf{w.resid, w.qr, w.attn, w.act, w.pk_scratch, (int*)(w.pk_scratch + (size_t)gw * b), w.pk_sync};
+  int rc = launch_draft_loop(m, kv, b, k, d1_ids, d1_pos, slots, d_base, v_ids, ds_ids, ds_pos, buf,
+                             (cudaStream_t)stream);
+  g_last_count = g_kernel_count;
+  return rc;
+}
+
 int sb_debug_persistent_trace(void* device_buf) { return set_persistent_trace(device_buf); }
 
 size_t sb_decoder_tmaps_bytes(const sb_decoder_t* m) { return m ? decoder_tmaps_bytes(m) : 0; }

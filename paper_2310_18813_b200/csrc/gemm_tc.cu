@@ -132,6 +132,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* tmem_full = empty + p.stages;
   uint32_t* tmem_slot = (uint32_t*)(tmem_full + 1);
   float* inv_s = (float*)(tmem_slot + 4);  // [tn] per-token 1/rms (fused RMSNorm)
+  float* nsum = inv_s + tn;                 // [4][tn] per-token partial sums of squares (fused RMSNorm)
   float* red = (float*)smem;               // split-K partial tile [tn][128] (reuses the drained ring)
   float* sq = p.splits > 1 ? red + tn * TC_BM : red + 8 * tn;  // norm squares staging
 
@@ -231,14 +232,34 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // fused RMSNorm (consumer): per-token 1/rms from the producer's partials,
     // computed while the weights stream (these warps are otherwise idle)
     if (p.ns_part) {
-      for (int j = et; j < tn; j += 128) {
+      // the producer GEMM left ns_P partial sums of squares per token (one per
+      // 128-row tile and split): 4 fixed sub-ranges per token, each summed 8
+      // loads at a time by one thread, combined in order -- deterministic and
+      // independent of the token count (batch invariance); the loads overlap
+      // the weight stream of this GEMM
+      constexpr int tpj = 4;
+      for (int jj = et; jj < tn * tpj; jj += 128) {
+        const int j = jj % tn, part = jj / tn;
         const int m = m0 + j;
-        float s = 0.f;
+        const int q0 = part * p.ns_P / tpj, q1 = (part + 1) * p.ns_P / tpj;
+        float acc = 0.f;
         if (m < p.M) {
           const float* src = p.ns_part + (size_t)m * p.ns_row_step + p.ns_row_off;
-          for (int q = 0; q < p.ns_P; ++q) s += src[(size_t)q * p.ns_stride];
+          for (int q = q0; q < q1; q += 8) {
+            float t8[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) t8[i] = q + i < q1 ? __ldcg(src + (size_t)(q + i) * p.ns_stride) : 0.f;
+#pragma unroll
+            for (int i = 0; i < 8; ++i) acc += t8[i];
+          }
         }
-        inv_s[j] = rsqrtf(s * p.ns_inv_h + p.ns_eps);
+        nsum[part * tn + j] = acc;
+      }
+      asm volatile("bar.sync 2, 128;" ::: "memory");
+      for (int j = et; j < tn; j += 128) {
+        float tot = nsum[j];
+        for (int part = 1; part < tpj; ++part) tot += nsum[part * tn + j];
+        inv_s[j] = rsqrtf(tot * p.ns_inv_h + p.ns_eps);
       }
       asm volatile("bar.sync 2, 128;" ::: "memory");
     }
@@ -546,7 +567,7 @@ static TcPlan plan(int M, int N, int K, int epi) {
   if (q.stages < 2) q.stages = 2;
   size_t ring = (size_t)q.stages * stage;
   size_t scratch = q.splits > 1 ? (size_t)q.tn * (TC_BM + split_rows_max(q.splits)) * 4 : (size_t)q.tn * 12 * 4;
-  q.smem = 1024 + (ring > scratch ? ring : scratch) + 256 + 16 + (size_t)q.tn * 4;
+  q.smem = 1024 + (ring > scratch ? ring : scratch) + 256 + 16 + (size_t)q.tn * 4 * 5;
   return q;
 }
 

@@ -96,6 +96,22 @@ int launch_kv_compact(int dtype, void* k, void* v, const int32_t* src, const int
 int launch_tp_resid_add(float* resid, const float* part, void* xb, float* npart, int T, int H, cudaStream_t st);
 int launch_unshard_logits(const float* gathered, float* logits, int world, int rows, int vl, cudaStream_t st);
 
+// ---- draft loop megakernel (draft_loop.cu)
+struct DlBuffers {
+  float* resid;
+  void* qr;
+  void* att;
+  void* act;
+  float* am_val;
+  int* am_idx;
+  unsigned* sync;
+};
+int draft_loop_eligible(const sb_decoder_t* m, int b);
+int set_draft_loop_trace(void* buf);
+int launch_draft_loop(const sb_decoder_t* m, const sb_kvcache_t* kv, int b, int k, const int32_t* d1_ids,
+                      const int32_t* d1_pos, const int32_t* slot, const int32_t* d_base, int32_t* v_ids,
+                      int32_t* ds_ids, int32_t* ds_pos, const DlBuffers& buf, cudaStream_t st);
+
 // ---- persistent forward (persistent.cu)
 struct PkBuffers {
   float* resid;

@@ -24,6 +24,7 @@ Acceptance modes:
 
 from __future__ import annotations
 
+import ctypes as C
 import math
 import time
 from dataclasses import dataclass, field
@@ -166,7 +167,19 @@ class SpecEngine:
         greedy_draft = not sample
         # the fp32 path and a tensor-parallel target select from materialised (full-width) logits
         need_logits = self.target.sb_dtype != N.SB_BF16 or self.target.is_tp
-        if use_draft:
+        draft_done = False
+        if use_draft and greedy_draft:
+            # the whole greedy draft loop in one persistent launch (csrc/draft_loop.cu)
+            rc = lib.sb_draft_loop(C.byref(self.draft.struct), C.byref(self.kv_d.struct), b, k, N.ptr(self.d1_ids),
+                                   N.ptr(self.d1_pos), N.ptr(self.slots), N.ptr(self.d_base), N.ptr(self.v_ids),
+                                   N.ptr(self.ds_ids), N.ptr(self.ds_pos), N.ptr(self.workspace),
+                                   self.workspace.numel(), st)
+            if rc == 0:
+                draft_done = True
+                launches += lib.sb_last_kernel_count()
+            elif rc != N.SB_EUNSUPPORTED:
+                N.check("sb_draft_loop", rc)
+        if use_draft and not draft_done:
             sel = N.SELECT_SAMPLE if sample else N.SELECT_ARGMAX
             u_base = self.uniforms.data_ptr()
             for j in range(1, k + 1):
@@ -377,6 +390,8 @@ def _timed_graph(fn, reps: int, stream) -> float:
 def _stage_context(eng: "SpecEngine", b: int, k: int, ctx: int) -> None:
     """Put b slots at context length ctx with random committed tokens (the KV
     rows are whatever the cache holds: timing only)."""
+    if not 2 <= ctx <= eng.cap - k - 1:
+        raise ValueError(f"context {ctx} outside the engine's token capacity {eng.cap} (k={k})")
     rng = np.random.default_rng(ctx)
     eng.tokens[:b].copy_(torch.from_numpy(rng.integers(0, eng.V, size=(b, eng.cap)).astype(np.int32)))
     eng.n_tok[:b].fill_(ctx)
