@@ -317,6 +317,9 @@ int sb_set_persistent(int32_t enabled);
 int sb_debug_persistent_trace(void* device_buf);
 /* Programmatic dependent launch for every kernel (default on); 0 disables (ablation). */
 int sb_set_pdl(int32_t enabled);
+/* Diagnostics: skip kernel classes of the bf16 forward (bit 0 attention, 1 qkv, 2 o, 3 gate/up, 4 down) to
+   measure their marginal in-graph cost; outputs are meaningless while set.  0 = off. */
+int sb_debug_skip(int32_t mask);
 /* RMSNorm fused into the GEMM epilogues on the bf16 path (default on); 0 = separate norm kernels. */
 int sb_set_fuse_norm(int32_t enabled);
 /* Diagnostics: eager forward with an event after every kernel; per-stage summed ms as "tag=ms;..." in buf. */

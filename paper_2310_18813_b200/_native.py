@@ -76,6 +76,7 @@ _SIGS = {
     "sb_set_gemm_backend": (C.c_int, [_I]),
     "sb_set_pdl": (C.c_int, [_I]),
     "sb_set_fuse_norm": (C.c_int, [_I]),
+    "sb_debug_skip": (C.c_int, [_I]),
     "sb_set_attention_impl": (C.c_int, [_I]),
     "sb_set_attention_splits": (C.c_int, [_I]),
     "sb_set_persistent": (C.c_int, [_I]),

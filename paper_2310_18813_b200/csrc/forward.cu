@@ -112,6 +112,10 @@ static void prof_mark(const char* tag, cudaStream_t st) {
 static int g_attn_impl = 0;
 
 static int g_fuse_norm = 1;  // RMSNorm fused into the GEMMs (bf16 / tcgen05 path), sb_set_fuse_norm
+// diagnostics (sb_debug_skip): skip kernel classes of the fused bf16 forward to
+// measure each one's marginal in-graph cost (outputs are garbage): bit 0
+// attention, 1 qkv, 2 o, 3 gate/up, 4 down
+static int g_skip = 0;
 
 // TP exchange after a row-parallel projection whose partial went to w.tp_part:
 // all-reduce (sum over ranks), then resid += sum (+ bf16 copy / norm partials)
@@ -201,9 +205,9 @@ static int forward_fused_norm(const sb_decoder_t* m, const sb_kvcache_t* kv, con
     g.ns_stride = T;
     g.ns_eps = m->rms_eps;
     g.ns_inv_h = inv_h;
-    SB_TRY(gemm_tc(g, st));
+    if (!(g_skip & 2)) SB_TRY(gemm_tc(g, st));
     prof_mark("qkv", st);
-    int rc_fa = g_attn_impl == 0 ? launch_attention_tc(w.qkv, kc, vc, w.attn, slot, pos, m->rope_cos, m->rope_sin,
+    int rc_fa = (g_skip & 1) ? 0 : g_attn_impl == 0 ? launch_attention_tc(w.qkv, kc, vc, w.attn, slot, pos, m->rope_cos, m->rope_sin,
                                                         n_seq, q_len, nq, nkv, hd, kv->ctx_max, m->max_pos, st, &w.att_split)
                                   : SB_EUNSUPPORTED;
     if (rc_fa != 0 && rc_fa != SB_EUNSUPPORTED) return rc_fa;
@@ -225,7 +229,7 @@ static int forward_fused_norm(const sb_decoder_t* m, const sb_kvcache_t* kv, con
                  w.gemm_ws_bytes};
       o.out_part = w.npart;
       o.out_xb = w.xb;
-      SB_TRY(gemm_tc(o, st));
+      if (!(g_skip & 4)) SB_TRY(gemm_tc(o, st));
       P = gemm_tc_norm_partials(o);
       prof_mark("o", st);
     }
@@ -235,7 +239,7 @@ static int forward_fused_norm(const sb_decoder_t* m, const sb_kvcache_t* kv, con
     gu.ns_stride = T;
     gu.ns_eps = m->rms_eps;
     gu.ns_inv_h = inv_h;
-    SB_TRY(gemm_tc(gu, st));
+    if (!(g_skip & 8)) SB_TRY(gemm_tc(gu, st));
     prof_mark("gu", st);
     if (m->tp) {  // row-parallel down_proj
       GemmArgs dn{SB_BF16, w.act, m->w_down[l], w.tp_part, T, H, m->ffn, m->ffn, EPI_STORE_F32, w.gemm_ws,
@@ -249,7 +253,7 @@ static int forward_fused_norm(const sb_decoder_t* m, const sb_kvcache_t* kv, con
                   w.gemm_ws_bytes};
       dn.out_part = w.npart;
       dn.out_xb = w.xb;
-      SB_TRY(gemm_tc(dn, st));
+      if (!(g_skip & 16)) SB_TRY(gemm_tc(dn, st));
       P = gemm_tc_norm_partials(dn);
       prof_mark("down", st);
     }
@@ -532,6 +536,11 @@ int sb_gemm_autotune_clear(void) { return gemm_tc_autotune_clear(); }
 int sb_set_attention_splits(int32_t splits) {
   if (splits < 0 || splits > 8) return SB_EINVAL;
   g_attn_splits = splits;
+  return 0;
+}
+
+int sb_debug_skip(int32_t mask) {
+  g_skip = mask;
   return 0;
 }
 

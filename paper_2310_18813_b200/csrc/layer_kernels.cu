@@ -511,13 +511,15 @@ __global__ void __launch_bounds__(128) attention_tc_kernel(
   __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(tsm);
   uint8_t* ring = tsm + SM::q;
   __shared__ int qpos[16], qtok[16], qhead[16];
-  griddep_wait();
-  griddep_launch();
 
   const int kvh = blockIdx.x, seq = blockIdx.y;
   const int group = nq / nkv;
   const int nQ = group * q_len;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  // Before the programmatic-dependency wait only data written >= 2 kernels
+  // back is touched (positions, slots, KV history): every kernel of the
+  // engine triggers its dependents after its own wait, so the kernel two
+  // launches back has completed.
   const int slot = tok_slot[seq];
   const int row_w = (nq + 2 * nkv) * HD;
   const __nv_bfloat16* seq_rows = qkv + (size_t)seq * q_len * row_w;
@@ -531,46 +533,17 @@ __global__ void __launch_bounds__(128) attention_tc_kernel(
     qpos[tid] = tid < nQ ? tok_pos[seq * q_len + t] : -1;
   }
   __syncthreads();
-  for (int e = tid; e < 16 * HALF; e += 128) {
-    int j = e / HALF, i = e % HALF;
-    __nv_bfloat16 a = __float2bfloat16_rn(0.f), b = a;
-    if (j < nQ) {
-      int p = qpos[j];
-      int pc = p < 0 ? 0 : (p >= max_pos ? max_pos - 1 : p);
-      const __nv_bfloat16* src = seq_rows + (size_t)qtok[j] * row_w + qhead[j] * HD;
-      float x0 = __bfloat162float(src[i]), x1 = __bfloat162float(src[i + HALF]);
-      float c = cosT[(size_t)pc * HALF + i], sn = sinT[(size_t)pc * HALF + i];
-      a = __float2bfloat16_rn(x0 * c - x1 * sn);
-      b = __float2bfloat16_rn(x1 * c + x0 * sn);
-    }
-    Qs[j * RS + i] = a;
-    Qs[j * RS + i + HALF] = b;
-  }
   // this split's key range [k_lo, k_hi) (64-key tiles shared evenly)
-  int maxp0 = -1;
+  int maxp0 = -1, wmin = INT_MAX;
 #pragma unroll
-  for (int j = 0; j < 16; ++j) maxp0 = max(maxp0, qpos[j]);
+  for (int j = 0; j < 16; ++j) {
+    maxp0 = max(maxp0, qpos[j]);
+    if (qpos[j] >= 0) wmin = min(wmin, qpos[j]);
+  }
   const int n_splits = gridDim.z, split = blockIdx.z;
   const int tiles_all = (maxp0 + 1 + kTcKT - 1) / kTcKT;
   const int t_lo = (int)((long)split * tiles_all / n_splits), t_hi = (int)((long)(split + 1) * tiles_all / n_splits);
   const int k_lo = t_lo * kTcKT, k_hi = min(t_hi * kTcKT, maxp0 + 1);
-  for (int e = tid; e < q_len * HALF; e += 128) {
-    int t = e / HALF, i = e % HALF;
-    int p = tok_pos[seq * q_len + t];
-    if (p < k_lo || p >= k_hi) continue;  // (p < 0: padding, never in range)
-    int pc = p >= max_pos ? max_pos - 1 : p;
-    const __nv_bfloat16* src = seq_rows + (size_t)t * row_w + (nq + kvh) * HD;
-    float x0 = __bfloat162float(src[i]), x1 = __bfloat162float(src[i + HALF]);
-    float c = cosT[(size_t)pc * HALF + i], sn = sinT[(size_t)pc * HALF + i];
-    kslab[(size_t)p * HD + i] = __float2bfloat16_rn(x0 * c - x1 * sn);
-    kslab[(size_t)p * HD + i + HALF] = __float2bfloat16_rn(x1 * c + x0 * sn);
-    const __nv_bfloat16* vsrc = seq_rows + (size_t)t * row_w + (nq + nkv + kvh) * HD;
-    vslab[(size_t)p * HD + i] = vsrc[i];
-    vslab[(size_t)p * HD + i + HALF] = vsrc[i + HALF];
-  }
-  __threadfence_block();
-  __syncthreads();
-
   const int n_keys = k_hi;
   const int n_tiles = t_hi;  // tiles [t_lo, t_hi) of this split
 
@@ -595,8 +568,45 @@ __global__ void __launch_bounds__(128) attention_tc_kernel(
     }
     cp_async_commit();  // always commit (possibly empty) to keep group counting uniform
   };
-#pragma unroll
-  for (int i = 0; i < kTcStages - 1; ++i) issue(t_lo + i);
+  // KV-history tiles (entirely below this forward's window) start loading now,
+  // overlapping the tail of the qkv GEMM; window tiles wait for the append
+  int pre = 0;
+  while (pre < kTcStages - 1 && t_lo + pre < n_tiles && (t_lo + pre + 1) * kTcKT <= wmin) issue(t_lo + pre++);
+
+  griddep_wait();
+  griddep_launch();
+  for (int e = tid; e < 16 * HALF; e += 128) {
+    int j = e / HALF, i = e % HALF;
+    __nv_bfloat16 a = __float2bfloat16_rn(0.f), b = a;
+    if (j < nQ) {
+      int p = qpos[j];
+      int pc = p < 0 ? 0 : (p >= max_pos ? max_pos - 1 : p);
+      const __nv_bfloat16* src = seq_rows + (size_t)qtok[j] * row_w + qhead[j] * HD;
+      float x0 = __bfloat162float(src[i]), x1 = __bfloat162float(src[i + HALF]);
+      float c = cosT[(size_t)pc * HALF + i], sn = sinT[(size_t)pc * HALF + i];
+      a = __float2bfloat16_rn(x0 * c - x1 * sn);
+      b = __float2bfloat16_rn(x1 * c + x0 * sn);
+    }
+    Qs[j * RS + i] = a;
+    Qs[j * RS + i + HALF] = b;
+  }
+  for (int e = tid; e < q_len * HALF; e += 128) {
+    int t = e / HALF, i = e % HALF;
+    int p = tok_pos[seq * q_len + t];
+    if (p < k_lo || p >= k_hi) continue;  // (p < 0: padding, never in range)
+    int pc = p >= max_pos ? max_pos - 1 : p;
+    const __nv_bfloat16* src = seq_rows + (size_t)t * row_w + (nq + kvh) * HD;
+    float x0 = __bfloat162float(src[i]), x1 = __bfloat162float(src[i + HALF]);
+    float c = cosT[(size_t)pc * HALF + i], sn = sinT[(size_t)pc * HALF + i];
+    kslab[(size_t)p * HD + i] = __float2bfloat16_rn(x0 * c - x1 * sn);
+    kslab[(size_t)p * HD + i + HALF] = __float2bfloat16_rn(x1 * c + x0 * sn);
+    const __nv_bfloat16* vsrc = seq_rows + (size_t)t * row_w + (nq + nkv + kvh) * HD;
+    vslab[(size_t)p * HD + i] = vsrc[i];
+    vslab[(size_t)p * HD + i + HALF] = vsrc[i + HALF];
+  }
+  __threadfence_block();
+  __syncthreads();
+  for (int i = pre; i < kTcStages - 1; ++i) issue(t_lo + i);
 
   // Q fragments (A operand), loaded once
   const uint32_t qs_base = (uint32_t)__cvta_generic_to_shared(Qs);
