@@ -519,7 +519,7 @@ int sb_set_attention_impl(int32_t impl) {
 }
 
 int sb_gemm_tune(int32_t ctas_per_sm, int32_t max_stages, int32_t splits) {
-  if (ctas_per_sm < 0 || ctas_per_sm > 2 || max_stages < 0 || max_stages > 16 || splits < 0 || splits > 8)
+  if (ctas_per_sm < 0 || ctas_per_sm > 3 || max_stages < 0 || max_stages > 16 || splits < 0 || splits > 8)
     return SB_EINVAL;
   return gemm_tc_tune(ctas_per_sm, max_stages, splits);
 }

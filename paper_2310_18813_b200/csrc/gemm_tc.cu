@@ -531,6 +531,13 @@ static TcPlan plan(int M, int N, int K, int epi) {
   q.m_tiles = (M + q.tn - 1) / q.tn;
   q.kb = (K + TC_BK - 1) / TC_BK;
   q.ctas_per_sm = g_tune_cps ? g_tune_cps : (q.tn >= 128 ? 1 : 2);
+  // cps 3 (tuning only): size the grid for ONE CTA per SM but keep the smem of
+  // two, leaving each SM a free slot for the next kernel's early weight prefetch (PDL)
+  bool half_smem = false;
+  if (q.ctas_per_sm == 3) {
+    q.ctas_per_sm = 1;
+    half_smem = true;
+  }
   int tuned_splits = 0, tuned_wt = 0;
   if (!g_tune_cps && !g_tune_splits) {
     std::lock_guard<std::mutex> lk(g_tuned_mu);
@@ -560,7 +567,7 @@ static TcPlan plan(int M, int N, int K, int epi) {
       (tuned_wt ? tuned_wt == 2 : (q.tn >= 128 && (q.n_tiles_n + 1) / 2 * q.m_tiles >= sms)))
     q.wt = 2;  // (heuristic: only when the halved grid still covers every SM)
   if (g_tune_wt) q.wt = (q.splits == 1 && q.ctas_per_sm == 1 && q.n_tiles_n >= 2) ? g_tune_wt : 1;
-  size_t budget = q.ctas_per_sm == 2 ? 108 * 1024 : 200 * 1024;
+  size_t budget = (q.ctas_per_sm == 2 || half_smem) ? 108 * 1024 : 200 * 1024;
   size_t stage = (size_t)(TC_BM * q.wt + q.tn) * TC_BK * 2;
   q.stages = (int)((budget - 1024 - 256) / stage);
   if (q.stages > (g_tune_stages ? g_tune_stages : 12)) q.stages = g_tune_stages ? g_tune_stages : 12;
