@@ -351,6 +351,15 @@ def run_ours(args):
     k = args.k if args.k >= 0 else lookup(lut, b).chosen_s
     cells = lut.provenance.get("ms_per_token", {})
     sweep = {int(key.split(",")[1]): 1e3 / v for key, v in cells.items() if int(key.split(",")[0]) == b}
+    # the metric is "tokens/s vs batch size (adaptive k vs best fixed k)": every profiled b
+    by_batch = {}
+    for bb in sorted({int(key.split(",")[0]) for key in cells}):
+        row = {int(key.split(",")[1]): 1e3 / v for key, v in cells.items() if int(key.split(",")[0]) == bb}
+        kb_ = lookup(lut, bb).chosen_s
+        bf = max(row, key=row.get)
+        by_batch[str(bb)] = {"adaptive_k": kb_, "adaptive_tokens_per_s": round(row[kb_], 1), "best_fixed_k": bf,
+                             "best_fixed_tokens_per_s": round(row[bf], 1),
+                             "k_sweep": {str(kk): round(v, 1) for kk, v in sorted(row.items())}}
 
     def batch(step):
         return [SequenceState(request_id=step * 1000 + i, target_len=NEW) for i in range(b)]
@@ -423,6 +432,14 @@ def run_ours(args):
     vb = verify_bytes(tgt.cfg, b, k, ctx_avg)
     v_ms = eng.time_verify(b, k, ctx=ctx_avg, reps=20)
     achieved = vb / (v_ms / 1e3) / 1e9
+    verify_by_batch = {}  # north_star: >= 60% of the HBM roofline for verification at b <= 8
+    for bb in (1, 2, 4, 8):
+        if bb > eng.max_batch:
+            continue
+        kb_ = lookup(lut, bb).chosen_s if str(bb) in by_batch else k
+        ms_ = eng.time_verify(bb, kb_, ctx=ctx_avg, reps=10)
+        verify_by_batch[str(bb)] = {"k": kb_, "verify_ms": round(ms_, 4),
+                                    "frac_hbm": round(verify_bytes(tgt.cfg, bb, kb_, ctx_avg) / (ms_ / 1e3) / 1e9 / hbm, 4)}
     traffic = None
     tf_path = ROOT / "profiles" / "verify_traffic.json"
     if tf_path.exists():
@@ -457,6 +474,8 @@ def run_ours(args):
                        "l2": "inputs (weights >= 13.5 GB) > L2; no flush"},
             "decode_tokens_per_s": jobs * args.steps * b * NEW / (sum(decode_ms) / 1e3) if world == 1 else None,
             "k_sweep_decode_tokens_per_s": {str(kk): round(v, 1) for kk, v in sorted(sweep.items())},
+            "tokens_per_s_by_batch": by_batch,
+            "verify_roofline_by_batch": verify_by_batch,
             "best_fixed_k": best_fixed,
             "adaptive_vs_best_fixed": (sweep[k] / sweep[best_fixed]) if (sweep and k in sweep) else None,
             "iterations_per_step": iters / args.steps,
