@@ -14,6 +14,7 @@
 #include "common.cuh"
 #include "kernels.cuh"
 #include "mma_ptx.cuh"
+#include "attn_tc.cuh"
 
 namespace sb {
 
@@ -472,322 +473,14 @@ int launch_attention(int dtype, const void* q, const void* kc, const void* vc, v
 // cp.async ring; padded 272-byte rows make every ldmatrix conflict-free.  The
 // prologue rotates Q (RoPE, rounded to bf16) and appends this forward's
 // rotated K / V rows to the cache (this CTA is the only reader of its slab).
-constexpr int kTcKT = 64;
 constexpr int kTcStages = 3;
 int g_attn_splits = 1;  // 1 off (default: measured +10% slower at b=1..8), 0 auto, n forced (sb_set_attention_splits)
 
 template <int HD>
-struct TcAttnSmem {
-  static constexpr int RS = HD + 8;                             // padded row (elements)
-  static constexpr size_t tile = (size_t)kTcKT * RS * 2;        // one K or V tile
-  static constexpr size_t stage = 2 * tile;
-  static constexpr size_t q = (size_t)16 * RS * 2;
-  static constexpr size_t comb = (size_t)4 * 16 * HD * 4 + 4 * 16 * 2 * 4;  // warp partials (aliases the ring)
-  static constexpr size_t ring = kTcStages * stage;
-  static constexpr size_t bytes = q + (ring > comb ? ring : comb);
-};
-
-// Flash-decoding key splits (gridDim.z = n_splits > 1): split z takes an even
-// share of the 64-key tiles, appends only the window rows inside its own key
-// range (no cross-split dependency), and publishes an unnormalised partial
-// (O, running max M, sum L per query row); the last split to finish (per-(seq,
-// kv head) counter) merges the partials in split order -- deterministic -- and
-// resets the counter for the next launch / graph replay.
-struct AttnSplit {
-  float* part;   // [n_seq][nkv][S][16][HD]
-  float* ml;     // [n_seq][nkv][S][16][2]
-  int* counter;  // [n_seq][nkv], zero between launches
-};
-
-template <int HD>
-__global__ void __launch_bounds__(128) attention_tc_kernel(
-    const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ kc, __nv_bfloat16* __restrict__ vc,
-    __nv_bfloat16* __restrict__ out, const int32_t* __restrict__ tok_slot, const int32_t* __restrict__ tok_pos,
-    const float* __restrict__ cosT, const float* __restrict__ sinT, int q_len, int nq, int nkv, int ctx_max,
-    int max_pos, float scale, AttnSplit sp) {
-  using SM = TcAttnSmem<HD>;
-  constexpr int RS = SM::RS, HALF = HD / 2, KSTEP = HD / 16, NT = HD / 8;
+__global__ void __launch_bounds__(128) attention_tc_kernel(AttnArgs A) {
   extern __shared__ __align__(128) uint8_t tsm[];
-  __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(tsm);
-  uint8_t* ring = tsm + SM::q;
-  __shared__ int qpos[16], qtok[16], qhead[16];
-
-  const int kvh = blockIdx.x, seq = blockIdx.y;
-  const int group = nq / nkv;
-  const int nQ = group * q_len;
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  // Before the programmatic-dependency wait only data written >= 2 kernels
-  // back is touched (positions, slots, KV history): every kernel of the
-  // engine triggers its dependents after its own wait, so the kernel two
-  // launches back has completed.
-  const int slot = tok_slot[seq];
-  const int row_w = (nq + 2 * nkv) * HD;
-  const __nv_bfloat16* seq_rows = qkv + (size_t)seq * q_len * row_w;
-  __nv_bfloat16* kslab = kc + ((size_t)slot * nkv + kvh) * ctx_max * HD;
-  __nv_bfloat16* vslab = vc + ((size_t)slot * nkv + kvh) * ctx_max * HD;
-
-  if (tid < 16) {
-    int t = tid / group;
-    qtok[tid] = tid < nQ ? t : 0;
-    qhead[tid] = kvh * group + tid % group;
-    qpos[tid] = tid < nQ ? tok_pos[seq * q_len + t] : -1;
-  }
-  __syncthreads();
-  // this split's key range [k_lo, k_hi) (64-key tiles shared evenly)
-  int maxp0 = -1, wmin = INT_MAX;
-#pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    maxp0 = max(maxp0, qpos[j]);
-    if (qpos[j] >= 0) wmin = min(wmin, qpos[j]);
-  }
-  const int n_splits = gridDim.z, split = blockIdx.z;
-  const int tiles_all = (maxp0 + 1 + kTcKT - 1) / kTcKT;
-  const int t_lo = (int)((long)split * tiles_all / n_splits), t_hi = (int)((long)(split + 1) * tiles_all / n_splits);
-  const int k_lo = t_lo * kTcKT, k_hi = min(t_hi * kTcKT, maxp0 + 1);
-  const int n_keys = k_hi;
-  const int n_tiles = t_hi;  // tiles [t_lo, t_hi) of this split
-
-  auto issue = [&](int tile) {
-    if (tile < n_tiles) {
-      uint8_t* st = ring + ((tile - t_lo) % kTcStages) * SM::stage;
-      __nv_bfloat16* Kd = reinterpret_cast<__nv_bfloat16*>(st);
-      __nv_bfloat16* Vd = reinterpret_cast<__nv_bfloat16*>(st + SM::tile);
-      const int k0 = tile * kTcKT;
-      constexpr int CPR = HD / 8;  // 16-byte chunks per row
-      for (int e = tid; e < kTcKT * CPR; e += 128) {
-        int r = e / CPR, c = (e % CPR) * 8;
-        int key = k0 + r;
-        if (key < n_keys) {
-          cp_async16(Kd + r * RS + c, kslab + (size_t)key * HD + c);
-          cp_async16(Vd + r * RS + c, vslab + (size_t)key * HD + c);
-        } else {  // rows past the context: zeros (P is 0 there, and 0 * stale NaN would poison P.V)
-          *reinterpret_cast<uint4*>(Kd + r * RS + c) = make_uint4(0, 0, 0, 0);
-          *reinterpret_cast<uint4*>(Vd + r * RS + c) = make_uint4(0, 0, 0, 0);
-        }
-      }
-    }
-    cp_async_commit();  // always commit (possibly empty) to keep group counting uniform
-  };
-  // KV-history tiles (entirely below this forward's window) start loading now,
-  // overlapping the tail of the qkv GEMM; window tiles wait for the append
-  int pre = 0;
-  while (pre < kTcStages - 1 && t_lo + pre < n_tiles && (t_lo + pre + 1) * kTcKT <= wmin) issue(t_lo + pre++);
-
-  griddep_wait();
-  griddep_launch();
-  for (int e = tid; e < 16 * HALF; e += 128) {
-    int j = e / HALF, i = e % HALF;
-    __nv_bfloat16 a = __float2bfloat16_rn(0.f), b = a;
-    if (j < nQ) {
-      int p = qpos[j];
-      int pc = p < 0 ? 0 : (p >= max_pos ? max_pos - 1 : p);
-      const __nv_bfloat16* src = seq_rows + (size_t)qtok[j] * row_w + qhead[j] * HD;
-      float x0 = __bfloat162float(src[i]), x1 = __bfloat162float(src[i + HALF]);
-      float c = cosT[(size_t)pc * HALF + i], sn = sinT[(size_t)pc * HALF + i];
-      a = __float2bfloat16_rn(x0 * c - x1 * sn);
-      b = __float2bfloat16_rn(x1 * c + x0 * sn);
-    }
-    Qs[j * RS + i] = a;
-    Qs[j * RS + i + HALF] = b;
-  }
-  for (int e = tid; e < q_len * HALF; e += 128) {
-    int t = e / HALF, i = e % HALF;
-    int p = tok_pos[seq * q_len + t];
-    if (p < k_lo || p >= k_hi) continue;  // (p < 0: padding, never in range)
-    int pc = p >= max_pos ? max_pos - 1 : p;
-    const __nv_bfloat16* src = seq_rows + (size_t)t * row_w + (nq + kvh) * HD;
-    float x0 = __bfloat162float(src[i]), x1 = __bfloat162float(src[i + HALF]);
-    float c = cosT[(size_t)pc * HALF + i], sn = sinT[(size_t)pc * HALF + i];
-    kslab[(size_t)p * HD + i] = __float2bfloat16_rn(x0 * c - x1 * sn);
-    kslab[(size_t)p * HD + i + HALF] = __float2bfloat16_rn(x1 * c + x0 * sn);
-    const __nv_bfloat16* vsrc = seq_rows + (size_t)t * row_w + (nq + nkv + kvh) * HD;
-    vslab[(size_t)p * HD + i] = vsrc[i];
-    vslab[(size_t)p * HD + i + HALF] = vsrc[i + HALF];
-  }
-  __threadfence_block();
-  __syncthreads();
-  for (int i = pre; i < kTcStages - 1; ++i) issue(t_lo + i);
-
-  // Q fragments (A operand), loaded once
-  const uint32_t qs_base = (uint32_t)__cvta_generic_to_shared(Qs);
-  uint32_t qa[KSTEP][4];
-  {
-    const int mi = lane >> 3, ri = lane & 7;
-    const int row = ri + (mi & 1) * 8;
-#pragma unroll
-    for (int ks = 0; ks < KSTEP; ++ks) {
-      int col = ks * 16 + (mi >> 1) * 8;
-      ldsm_x4(qs_base + (uint32_t)(row * RS + col) * 2, qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3]);
-    }
-  }
-  const int g = lane >> 2, t4 = lane & 3;
-  const int pos_lo = qpos[g], pos_hi = qpos[g + 8];
-  float o[NT][4];
-#pragma unroll
-  for (int n = 0; n < NT; ++n) o[n][0] = o[n][1] = o[n][2] = o[n][3] = 0.f;
-  float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;
-
-  for (int tile = t_lo; tile < n_tiles; ++tile) {
-    issue(tile + kTcStages - 1);
-    cp_async_wait<kTcStages - 1>();
-    __syncthreads();
-    const uint8_t* st = ring + ((tile - t_lo) % kTcStages) * SM::stage;
-    const uint32_t kb = (uint32_t)__cvta_generic_to_shared(st);
-    const uint32_t vb = kb + (uint32_t)SM::tile;
-    const int kw = warp * 16;  // this warp's 16 keys within the tile
-    // S = Q K^T for keys kw..kw+15 (two n8 tiles)
-    float s0[4] = {0.f, 0.f, 0.f, 0.f}, s1[4] = {0.f, 0.f, 0.f, 0.f};
-    {
-      const int mi = lane >> 3, ri = lane & 7;
-      const int key = kw + ri + (mi >> 1) * 8;
-#pragma unroll
-      for (int ks = 0; ks < KSTEP; ++ks) {
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4(kb + (uint32_t)(key * RS + ks * 16 + (mi & 1) * 8) * 2, b0, b1, b2, b3);
-        mma_bf16(s0, qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b0, b1);
-        mma_bf16(s1, qa[ks][0], qa[ks][1], qa[ks][2], qa[ks][3], b2, b3);
-      }
-    }
-    // mask + scale, online softmax (rows g and g+8)
-    const int kbase = tile * kTcKT + kw + 2 * t4;
-    float v[8] = {s0[0], s0[1], s1[0], s1[1], s0[2], s0[3], s1[2], s1[3]};
-    const int kidx[4] = {kbase, kbase + 1, kbase + 8, kbase + 9};
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      v[i] = (kidx[i] <= pos_lo) ? v[i] * scale : -INFINITY;
-      v[4 + i] = (kidx[i] <= pos_hi) ? v[4 + i] * scale : -INFINITY;
-    }
-    float mx_lo = fmaxf(fmaxf(v[0], v[1]), fmaxf(v[2], v[3]));
-    float mx_hi = fmaxf(fmaxf(v[4], v[5]), fmaxf(v[6], v[7]));
-    mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 1));
-    mx_lo = fmaxf(mx_lo, __shfl_xor_sync(0xffffffffu, mx_lo, 2));
-    mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 1));
-    mx_hi = fmaxf(mx_hi, __shfl_xor_sync(0xffffffffu, mx_hi, 2));
-    const float mn_lo = fmaxf(m_lo, mx_lo), mn_hi = fmaxf(m_hi, mx_hi);
-    const float c_lo = (m_lo == -INFINITY) ? 0.f : __expf(m_lo - mn_lo);
-    const float c_hi = (m_hi == -INFINITY) ? 0.f : __expf(m_hi - mn_hi);
-    float p[8], sum_lo = 0.f, sum_hi = 0.f;
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      p[i] = (mn_lo == -INFINITY) ? 0.f : __expf(v[i] - mn_lo);
-      p[4 + i] = (mn_hi == -INFINITY) ? 0.f : __expf(v[4 + i] - mn_hi);
-      sum_lo += p[i];
-      sum_hi += p[4 + i];
-    }
-    sum_lo += __shfl_xor_sync(0xffffffffu, sum_lo, 1);
-    sum_lo += __shfl_xor_sync(0xffffffffu, sum_lo, 2);
-    sum_hi += __shfl_xor_sync(0xffffffffu, sum_hi, 1);
-    sum_hi += __shfl_xor_sync(0xffffffffu, sum_hi, 2);
-    l_lo = l_lo * c_lo + sum_lo;
-    l_hi = l_hi * c_hi + sum_hi;
-    m_lo = mn_lo;
-    m_hi = mn_hi;
-#pragma unroll
-    for (int n = 0; n < NT; ++n) {
-      o[n][0] *= c_lo;
-      o[n][1] *= c_lo;
-      o[n][2] *= c_hi;
-      o[n][3] *= c_hi;
-    }
-    // P (A operand, k = the warp's 16 keys) straight from the S accumulators
-    const uint32_t pa0 = pack_bf16(p[0], p[1]), pa1 = pack_bf16(p[4], p[5]);
-    const uint32_t pa2 = pack_bf16(p[2], p[3]), pa3 = pack_bf16(p[6], p[7]);
-    {
-      const int mi = lane >> 3, ri = lane & 7;
-      const int key = kw + ri + (mi & 1) * 8;
-#pragma unroll
-      for (int n = 0; n < NT; n += 2) {
-        uint32_t b0, b1, b2, b3;
-        ldsm_x4_t(vb + (uint32_t)(key * RS + n * 8 + (mi >> 1) * 8) * 2, b0, b1, b2, b3);
-        mma_bf16(o[n], pa0, pa1, pa2, pa3, b0, b1);
-        mma_bf16(o[n + 1], pa0, pa1, pa2, pa3, b2, b3);
-      }
-    }
-    __syncthreads();  // this stage may be overwritten by the next issue
-  }
-  cp_async_wait<0>();
-  __syncthreads();
-  // combine the 4 warps in order (smem partials alias the drained ring)
-  float* comb = reinterpret_cast<float*>(ring);
-  float* cm = comb + 4 * 16 * HD;
-  float* cl = cm + 4 * 16;
-#pragma unroll
-  for (int n = 0; n < NT; ++n) {
-    int d = n * 8 + 2 * t4;
-    comb[(warp * 16 + g) * HD + d] = o[n][0];
-    comb[(warp * 16 + g) * HD + d + 1] = o[n][1];
-    comb[(warp * 16 + g + 8) * HD + d] = o[n][2];
-    comb[(warp * 16 + g + 8) * HD + d + 1] = o[n][3];
-  }
-  if (t4 == 0) {
-    cm[warp * 16 + g] = m_lo;
-    cm[warp * 16 + g + 8] = m_hi;
-    cl[warp * 16 + g] = l_lo;
-    cl[warp * 16 + g + 8] = l_hi;
-  }
-  __syncthreads();
-  if (n_splits == 1) {
-    for (int e = tid; e < nQ * HD; e += 128) {
-      int j = e / HD, d = e % HD;
-      float M = -INFINITY;
-#pragma unroll
-      for (int w = 0; w < 4; ++w) M = fmaxf(M, cm[w * 16 + j]);
-      float L = 0.f, acc = 0.f;
-#pragma unroll
-      for (int w = 0; w < 4; ++w) {
-        float mw = cm[w * 16 + j];
-        float f = (mw == -INFINITY) ? 0.f : __expf(mw - M);
-        L += cl[w * 16 + j] * f;
-        acc += comb[(w * 16 + j) * HD + d] * f;
-      }
-      out[((size_t)(seq * q_len + qtok[j]) * nq + qhead[j]) * HD + d] = __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
-    }
-    return;
-  }
-  // ---- split partial: warps merged in order, unnormalised
-  const size_t item = (size_t)seq * nkv + kvh;
-  float* mypart = sp.part + (item * n_splits + split) * 16 * HD;
-  float* myml = sp.ml + (item * n_splits + split) * 16 * 2;
-  for (int e = tid; e < nQ * HD; e += 128) {
-    int j = e / HD, d = e % HD;
-    float M = -INFINITY;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) M = fmaxf(M, cm[w * 16 + j]);
-    float L = 0.f, acc = 0.f;
-#pragma unroll
-    for (int w = 0; w < 4; ++w) {
-      float mw = cm[w * 16 + j];
-      float f = (mw == -INFINITY) ? 0.f : __expf(mw - M);
-      L += cl[w * 16 + j] * f;
-      acc += comb[(w * 16 + j) * HD + d] * f;
-    }
-    __stcg(mypart + j * HD + d, acc);
-    if (d == 0) {
-      __stcg(myml + j * 2, M);
-      __stcg(myml + j * 2 + 1, L);
-    }
-  }
-  __threadfence();
-  __syncthreads();
-  __shared__ int last;
-  if (tid == 0) last = atomicAdd(sp.counter + item, 1) == n_splits - 1;
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  for (int e = tid; e < nQ * HD; e += 128) {
-    int j = e / HD, d = e % HD;
-    float M = -INFINITY;
-    for (int z = 0; z < n_splits; ++z) M = fmaxf(M, __ldcg(sp.ml + ((item * n_splits + z) * 16 + j) * 2));
-    float L = 0.f, acc = 0.f;
-    for (int z = 0; z < n_splits; ++z) {
-      const float mz = __ldcg(sp.ml + ((item * n_splits + z) * 16 + j) * 2);
-      const float f = (mz == -INFINITY) ? 0.f : __expf(mz - M);
-      L += __ldcg(sp.ml + ((item * n_splits + z) * 16 + j) * 2 + 1) * f;
-      acc += __ldcg(sp.part + ((item * n_splits + z) * 16 + j) * HD + d) * f;
-    }
-    out[((size_t)(seq * q_len + qtok[j]) * nq + qhead[j]) * HD + d] = __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
-  }
-  if (tid == 0) sp.counter[item] = 0;  // ready for the next launch
+  __shared__ AttnShared sh;
+  attn_tc_item<HD, 3>(A, blockIdx.x, blockIdx.y, blockIdx.z, gridDim.z, tsm, sh, threadIdx.x, true);
 }
 
 int launch_attention_tc(const void* qkv, void* kc, void* vc, void* out, const int32_t* tok_slot, const int32_t* tok_pos,
@@ -810,6 +503,8 @@ int launch_attention_tc(const void* qkv, void* kc, void* vc, void* out, const in
   }
   AttnSplit sp{scratch ? scratch->part : nullptr, scratch ? scratch->ml : nullptr,
                scratch ? scratch->counter : nullptr};
+  AttnArgs A{(const __nv_bfloat16*)qkv, (__nv_bfloat16*)kc, (__nv_bfloat16*)vc, (__nv_bfloat16*)out, tok_slot, tok_pos,
+             cosT, sinT, q_len, nq, nkv, ctx_max, max_pos, scale, sp};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nkv, n_seq, splits);
   cfg.blockDim = dim3(128);
@@ -828,9 +523,7 @@ int launch_attention_tc(const void* qkv, void* kc, void* vc, void* out, const in
       attr = true;
     }
     cfg.dynamicSmemBytes = TcAttnSmem<128>::bytes;
-    e = cudaLaunchKernelEx(&cfg, attention_tc_kernel<128>, (const __nv_bfloat16*)qkv, (__nv_bfloat16*)kc,
-                           (__nv_bfloat16*)vc, (__nv_bfloat16*)out, tok_slot, tok_pos, cosT, sinT, q_len, nq, nkv,
-                           ctx_max, max_pos, scale, sp);
+    e = cudaLaunchKernelEx(&cfg, attention_tc_kernel<128>, A);
   } else {
     static bool attr = false;
     if (!attr) {
@@ -839,9 +532,7 @@ int launch_attention_tc(const void* qkv, void* kc, void* vc, void* out, const in
       attr = true;
     }
     cfg.dynamicSmemBytes = TcAttnSmem<64>::bytes;
-    e = cudaLaunchKernelEx(&cfg, attention_tc_kernel<64>, (const __nv_bfloat16*)qkv, (__nv_bfloat16*)kc,
-                           (__nv_bfloat16*)vc, (__nv_bfloat16*)out, tok_slot, tok_pos, cosT, sinT, q_len, nq, nkv,
-                           ctx_max, max_pos, scale, sp);
+    e = cudaLaunchKernelEx(&cfg, attention_tc_kernel<64>, A);
   }
   if (e != cudaSuccess) return (int)e;
   ++g_kernel_count;
