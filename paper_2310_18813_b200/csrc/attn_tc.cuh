@@ -13,16 +13,15 @@ constexpr int kTcKT = 64;
 
 __device__ __forceinline__ void attn_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
-template <int HD>
+template <int HD, int STAGES = 3>
 struct TcAttnSmem {
   static constexpr int RS = HD + 8;                             // padded row (elements)
   static constexpr size_t tile = (size_t)kTcKT * RS * 2;        // one K or V tile
   static constexpr size_t stage = 2 * tile;
   static constexpr size_t q = (size_t)16 * RS * 2;
   static constexpr size_t comb = (size_t)4 * 16 * HD * 4 + 4 * 16 * 2 * 4;  // warp partials (aliases the ring)
-  static constexpr size_t ring = 3 * stage;  // the standalone kernel's 3-stage ring
+  static constexpr size_t ring = STAGES * stage;
   static constexpr size_t bytes = q + (ring > comb ? ring : comb);
-  static constexpr size_t bytes2 = q + (2 * stage > comb ? 2 * stage : comb);  // 2-stage (fused into the qkv GEMM)
 };
 
 // Flash-decoding key splits (gridDim.z = n_splits > 1): split z takes an even
@@ -49,9 +48,12 @@ struct AttnArgs {
   int q_len, nq, nkv, ctx_max, max_pos;
   float scale;
   AttnSplit sp;
+  const char* l2_next;  // next GEMM's weights: prefetched into L2 while this latency-bound kernel runs
+  unsigned long long l2_next_bytes;
 };
 struct AttnShared {
   int qpos[16], qtok[16], qhead[16];
+  int wpos[16];  // this forward's positions for the sequence (the window keys)
   int last;
 };
 
@@ -73,7 +75,7 @@ __device__ __forceinline__ void attn_tc_item(const AttnArgs& A, int kvh, int seq
   const int q_len = A.q_len, nq = A.nq, nkv = A.nkv, ctx_max = A.ctx_max, max_pos = A.max_pos;
   const float scale = A.scale;
   const AttnSplit& sp = A.sp;
-  using SM = TcAttnSmem<HD>;
+  using SM = TcAttnSmem<HD, STAGES>;
   constexpr int RS = SM::RS, HALF = HD / 2, KSTEP = HD / 16, NT = HD / 8;
   constexpr int kTcStages = STAGES;
   __nv_bfloat16* Qs = reinterpret_cast<__nv_bfloat16*>(tsm);
@@ -100,6 +102,7 @@ __device__ __forceinline__ void attn_tc_item(const AttnArgs& A, int kvh, int seq
     qtok[tid] = tid < nQ ? t : 0;
     qhead[tid] = kvh * group + tid % group;
     qpos[tid] = tid < nQ ? tok_pos[seq * q_len + t] : -1;
+    sh.wpos[tid] = tid < q_len ? tok_pos[seq * q_len + tid] : -1;
   }
   attn_sync();
   // this split's key range [k_lo, k_hi) (64-key tiles shared evenly)
@@ -109,13 +112,18 @@ __device__ __forceinline__ void attn_tc_item(const AttnArgs& A, int kvh, int seq
     maxp0 = max(maxp0, qpos[j]);
     if (qpos[j] >= 0) wmin = min(wmin, qpos[j]);
   }
+  const int* wpos = sh.wpos;
   const int tiles_all = (maxp0 + 1 + kTcKT - 1) / kTcKT;
   const int t_lo = (int)((long)split * tiles_all / n_splits), t_hi = (int)((long)(split + 1) * tiles_all / n_splits);
   const int k_lo = t_lo * kTcKT, k_hi = min(t_hi * kTcKT, maxp0 + 1);
   const int n_keys = k_hi;
   const int n_tiles = t_hi;  // tiles [t_lo, t_hi) of this split
 
-  auto issue = [&](int tile) {
+  // Tile `tile` -> ring stage (tile - t_lo) % STAGES.  `hist`: skip this
+  // forward's window rows (the append below writes them straight into the
+  // stage), so every resident tile -- window tile included -- can be requested
+  // before the programmatic-dependency wait.
+  auto issue = [&](int tile, bool hist) {
     if (tile < n_tiles) {
       uint8_t* st = ring + ((tile - t_lo) % kTcStages) * (uint32_t)SM::stage;
       __nv_bfloat16* Kd = reinterpret_cast<__nv_bfloat16*>(st);
@@ -126,6 +134,11 @@ __device__ __forceinline__ void attn_tc_item(const AttnArgs& A, int kvh, int seq
         int r = e / CPR, c = (e % CPR) * 8;
         int key = k0 + r;
         if (key < n_keys) {
+          if (hist && key >= wmin) {
+            bool win = false;
+            for (int j = 0; j < q_len; ++j) win |= wpos[j] == key;
+            if (win) continue;
+          }
           cp_async16(Kd + r * RS + c, kslab + (size_t)key * HD + c);
           cp_async16(Vd + r * RS + c, vslab + (size_t)key * HD + c);
         } else {  // rows past the context: zeros (P is 0 there, and 0 * stale NaN would poison P.V)
@@ -136,10 +149,10 @@ __device__ __forceinline__ void attn_tc_item(const AttnArgs& A, int kvh, int seq
     }
     cp_async_commit();  // always commit (possibly empty) to keep group counting uniform
   };
-  // KV-history tiles (entirely below this forward's window) start loading now,
-  // overlapping the tail of the qkv GEMM; window tiles wait for the append
-  int pre = 0;
-  while (pre < kTcStages - 1 && t_lo + pre < n_tiles && (t_lo + pre + 1) * kTcKT <= wmin) issue(t_lo + pre++);
+  // The first STAGES tiles (KV history; the cache rows of this layer were last
+  // written >= 2 launches back) start loading now, overlapping the tail of the
+  // qkv GEMM.
+  for (int i = 0; i < kTcStages; ++i) issue(t_lo + i, true);
 
   if (pdl) {
     griddep_wait();
@@ -160,23 +173,36 @@ __device__ __forceinline__ void attn_tc_item(const AttnArgs& A, int kvh, int seq
     Qs[j * RS + i] = a;
     Qs[j * RS + i + HALF] = b;
   }
+  // append the window's rotated K / V rows to the cache and, for resident
+  // tiles, into their ring stage
   for (int e = tid; e < q_len * HALF; e += 128) {
     int t = e / HALF, i = e % HALF;
-    int p = tok_pos[seq * q_len + t];
+    int p = wpos[t];
     if (p < k_lo || p >= k_hi) continue;  // (p < 0: padding, never in range)
     int pc = p >= max_pos ? max_pos - 1 : p;
     const __nv_bfloat16* src = seq_rows + (size_t)t * row_w + (nq + kvh) * HD;
     float x0 = __bfloat162float(src[i]), x1 = __bfloat162float(src[i + HALF]);
     float c = cosT[(size_t)pc * HALF + i], sn = sinT[(size_t)pc * HALF + i];
-    kslab[(size_t)p * HD + i] = __float2bfloat16_rn(x0 * c - x1 * sn);
-    kslab[(size_t)p * HD + i + HALF] = __float2bfloat16_rn(x1 * c + x0 * sn);
+    const __nv_bfloat16 k_a = __float2bfloat16_rn(x0 * c - x1 * sn), k_b = __float2bfloat16_rn(x1 * c + x0 * sn);
     const __nv_bfloat16* vsrc = seq_rows + (size_t)t * row_w + (nq + nkv + kvh) * HD;
-    vslab[(size_t)p * HD + i] = vsrc[i];
-    vslab[(size_t)p * HD + i + HALF] = vsrc[i + HALF];
+    const __nv_bfloat16 v_a = vsrc[i], v_b = vsrc[i + HALF];
+    kslab[(size_t)p * HD + i] = k_a;
+    kslab[(size_t)p * HD + i + HALF] = k_b;
+    vslab[(size_t)p * HD + i] = v_a;
+    vslab[(size_t)p * HD + i + HALF] = v_b;
+    const int ti = p / kTcKT - t_lo;
+    if (ti < kTcStages) {
+      __nv_bfloat16* Kd = reinterpret_cast<__nv_bfloat16*>(ring + ti * (uint32_t)SM::stage);
+      __nv_bfloat16* Vd = reinterpret_cast<__nv_bfloat16*>(ring + ti * (uint32_t)SM::stage + SM::tile);
+      const int r = p - (p / kTcKT) * kTcKT;
+      Kd[r * RS + i] = k_a;
+      Kd[r * RS + i + HALF] = k_b;
+      Vd[r * RS + i] = v_a;
+      Vd[r * RS + i + HALF] = v_b;
+    }
   }
   __threadfence_block();
   attn_sync();
-  for (int i = pre; i < kTcStages - 1; ++i) issue(t_lo + i);
 
   // Q fragments (A operand), loaded once
   const uint32_t qs_base = (uint32_t)__cvta_generic_to_shared(Qs);
@@ -198,7 +224,6 @@ __device__ __forceinline__ void attn_tc_item(const AttnArgs& A, int kvh, int seq
   float m_lo = -INFINITY, m_hi = -INFINITY, l_lo = 0.f, l_hi = 0.f;
 
   for (int tile = t_lo; tile < n_tiles; ++tile) {
-    issue(tile + kTcStages - 1);
     cp_async_wait<kTcStages - 1>();
     attn_sync();
     const uint8_t* st = ring + ((tile - t_lo) % kTcStages) * (uint32_t)SM::stage;
@@ -273,7 +298,8 @@ __device__ __forceinline__ void attn_tc_item(const AttnArgs& A, int kvh, int seq
         mma_bf16(o[n + 1], pa0, pa1, pa2, pa3, b2, b3);
       }
     }
-    attn_sync();  // this stage may be overwritten by the next issue
+    attn_sync();  // this stage is free: refill it (tiles past the resident ones read the appended cache)
+    issue(tile + kTcStages, false);
   }
   cp_async_wait<0>();
   attn_sync();

@@ -208,7 +208,8 @@ static int forward_fused_norm(const sb_decoder_t* m, const sb_kvcache_t* kv, con
     if (!(g_skip & 2)) SB_TRY(gemm_tc(g, st));
     prof_mark("qkv", st);
     int rc_fa = (g_skip & 1) ? 0 : g_attn_impl == 0 ? launch_attention_tc(w.qkv, kc, vc, w.attn, slot, pos, m->rope_cos, m->rope_sin,
-                                                        n_seq, q_len, nq, nkv, hd, kv->ctx_max, m->max_pos, st, &w.att_split)
+                                                        n_seq, q_len, nq, nkv, hd, kv->ctx_max, m->max_pos, st, &w.att_split,
+                                  m->w_o[l], (size_t)H * nq * hd * 2)
                                   : SB_EUNSUPPORTED;
     if (rc_fa != 0 && rc_fa != SB_EUNSUPPORTED) return rc_fa;
     if (rc_fa == SB_EUNSUPPORTED) {
@@ -307,7 +308,8 @@ static int forward_opt(const sb_decoder_t* m, const sb_kvcache_t* kv, const int3
     int rc_fa = SB_EUNSUPPORTED;
     if (g_attn_impl == 0 && dt == SB_BF16)
       rc_fa = launch_attention_tc(w.qkv, kc, vc, w.attn, slot, pos, m->rope_cos, m->rope_sin, n_seq, q_len, nq, nkv,
-                                  hd, kv->ctx_max, m->max_pos, st, &w.att_split);
+                                  hd, kv->ctx_max, m->max_pos, st, &w.att_split,
+                                  m->w_o[l], (size_t)H * nq * hd * 2);
     if (rc_fa != 0 && rc_fa != SB_EUNSUPPORTED) return rc_fa;
     if (rc_fa == SB_EUNSUPPORTED) {
       SB_TRY(launch_rope_append(dt, w.qkv, w.qr, kc, vc, slot, pos, m->rope_cos, m->rope_sin, T, q_len, nq, nkv, hd,
@@ -381,7 +383,8 @@ static int forward_impl(const sb_decoder_t* m, const sb_kvcache_t* kv, const int
     int rc_fa = SB_EUNSUPPORTED;
     if (g_attn_impl == 0 && dt == SB_BF16)
       rc_fa = launch_attention_tc(w.qkv, kc, vc, w.attn, slot, pos, m->rope_cos, m->rope_sin, n_seq, q_len, nq, nkv,
-                                  hd, kv->ctx_max, m->max_pos, st, &w.att_split);
+                                  hd, kv->ctx_max, m->max_pos, st, &w.att_split,
+                                  m->w_o[l], (size_t)H * nq * hd * 2);
     if (rc_fa != 0 && rc_fa != SB_EUNSUPPORTED) return rc_fa;
     if (rc_fa == SB_EUNSUPPORTED) {  // prefill-sized query blocks / wide GQA: rope+append then attention
       SB_TRY(launch_rope_append(dt, w.qkv, w.qr, kc, vc, slot, pos, m->rope_cos, m->rope_sin, T, q_len, nq, nkv, hd,

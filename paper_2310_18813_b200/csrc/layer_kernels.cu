@@ -475,17 +475,40 @@ int launch_attention(int dtype, const void* q, const void* kc, const void* vc, v
 // rotated K / V rows to the cache (this CTA is the only reader of its slab).
 constexpr int kTcStages = 3;
 int g_attn_splits = 1;  // 1 off (default: measured +10% slower at b=1..8), 0 auto, n forced (sb_set_attention_splits)
+int g_attn_l2pf = -1;   // -1: from env SB_ATTN_L2PF (default off)
 
-template <int HD>
+int g_attn_stages = -1;  // ring stages (3, 4 or 6) when the grid fits one CTA per SM: -1 env SB_ATTN_STAGES
+
+template <int HD, int STAGES>
 __global__ void __launch_bounds__(128) attention_tc_kernel(AttnArgs A) {
   extern __shared__ __align__(128) uint8_t tsm[];
   __shared__ AttnShared sh;
-  attn_tc_item<HD, 3>(A, blockIdx.x, blockIdx.y, blockIdx.z, gridDim.z, tsm, sh, threadIdx.x, true);
+  if (A.l2_next && threadIdx.x < 32) {
+    // The attention reads little (KV history) and waits a lot: keep HBM busy by
+    // pulling this CTA's share of the next GEMM's weights into L2 (bulk prefetch,
+    // no smem, no completion to wait for).  Weights are constant: legal before
+    // the PDL wait.
+    const unsigned long long nblk = (unsigned long long)gridDim.x * gridDim.y * gridDim.z;
+    const unsigned long long b = blockIdx.x + gridDim.x * (blockIdx.y + (unsigned long long)gridDim.y * blockIdx.z);
+    const unsigned long long per = ((A.l2_next_bytes + nblk - 1) / nblk + 4095) & ~4095ull;
+    const unsigned long long lo = b * per, hi = min(lo + per, A.l2_next_bytes);
+    for (unsigned long long o = lo + threadIdx.x * 16384ull; o < hi; o += 32 * 16384ull) {
+      const unsigned n = (unsigned)min(16384ull, hi - o);
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.l2_next + o), "r"(n) : "memory");
+    }
+  }
+  attn_tc_item<HD, STAGES>(A, blockIdx.x, blockIdx.y, blockIdx.z, gridDim.z, tsm, sh, threadIdx.x, true);
 }
 
 int launch_attention_tc(const void* qkv, void* kc, void* vc, void* out, const int32_t* tok_slot, const int32_t* tok_pos,
                         const float* cosT, const float* sinT, int n_seq, int q_len, int nq, int nkv, int hd,
-                        int ctx_max, int max_pos, cudaStream_t st, const AttnScratch* scratch) {
+                        int ctx_max, int max_pos, cudaStream_t st, const AttnScratch* scratch,
+                        const void* l2_next, size_t l2_next_bytes) {
+  if (g_attn_l2pf < 0) {
+    const char* e = getenv("SB_ATTN_L2PF");
+    g_attn_l2pf = e ? atoi(e) : 0;  // measured: no gain at b=8, -5% at b=1 (opt-in)
+  }
+  if (!g_attn_l2pf || (l2_next_bytes & 15)) l2_next = nullptr;
   if ((hd != 64 && hd != 128) || nq % nkv != 0 || (nq / nkv) * q_len > 16) return SB_EUNSUPPORTED;
   const float scale = 1.0f / sqrtf((float)hd);
   // key splits: enough CTAs for ~2 per SM, at most what the scratch holds, and
@@ -504,7 +527,8 @@ int launch_attention_tc(const void* qkv, void* kc, void* vc, void* out, const in
   AttnSplit sp{scratch ? scratch->part : nullptr, scratch ? scratch->ml : nullptr,
                scratch ? scratch->counter : nullptr};
   AttnArgs A{(const __nv_bfloat16*)qkv, (__nv_bfloat16*)kc, (__nv_bfloat16*)vc, (__nv_bfloat16*)out, tok_slot, tok_pos,
-             cosT, sinT, q_len, nq, nkv, ctx_max, max_pos, scale, sp};
+             cosT, sinT, q_len, nq, nkv, ctx_max, max_pos, scale, sp, (const char*)l2_next,
+             l2_next ? (unsigned long long)l2_next_bytes : 0ull};
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(nkv, n_seq, splits);
   cfg.blockDim = dim3(128);
@@ -514,25 +538,39 @@ int launch_attention_tc(const void* qkv, void* kc, void* vc, void* out, const in
   at[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
   cfg.numAttrs = g_pdl ? 1 : 0;
+  if (g_attn_stages < 0) {
+    const char* e = getenv("SB_ATTN_STAGES");
+    g_attn_stages = e ? atoi(e) : 4;  // measured: 4 and 6 tie, 3-5% over 3 at b = 2..4
+  }
+  const int ctas = nkv * n_seq * splits;
+  const int stages = ctas <= num_sms() ? g_attn_stages : 3;
   cudaError_t e;
+  static bool attr = false;
+  if (!attr) {
+#define SB_ATTN_ATTR(H, S) \
+  cudaFuncSetAttribute(attention_tc_kernel<H, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                       (int)TcAttnSmem<H, S>::bytes)
+    SB_ATTN_ATTR(128, 3);
+    SB_ATTN_ATTR(128, 4);
+    SB_ATTN_ATTR(128, 6);
+    SB_ATTN_ATTR(64, 3);
+    SB_ATTN_ATTR(64, 4);
+    SB_ATTN_ATTR(64, 6);
+#undef SB_ATTN_ATTR
+    attr = true;
+  }
+  auto go = [&](void (*kern)(AttnArgs), size_t bytes) {
+    cfg.dynamicSmemBytes = bytes;
+    return cudaLaunchKernelEx(&cfg, kern, A);
+  };
   if (hd == 128) {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(attention_tc_kernel<128>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)TcAttnSmem<128>::bytes);
-      attr = true;
-    }
-    cfg.dynamicSmemBytes = TcAttnSmem<128>::bytes;
-    e = cudaLaunchKernelEx(&cfg, attention_tc_kernel<128>, A);
+    e = stages >= 6   ? go(attention_tc_kernel<128, 6>, TcAttnSmem<128, 6>::bytes)
+        : stages == 4 ? go(attention_tc_kernel<128, 4>, TcAttnSmem<128, 4>::bytes)
+                      : go(attention_tc_kernel<128, 3>, TcAttnSmem<128, 3>::bytes);
   } else {
-    static bool attr = false;
-    if (!attr) {
-      cudaFuncSetAttribute(attention_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)TcAttnSmem<64>::bytes);
-      attr = true;
-    }
-    cfg.dynamicSmemBytes = TcAttnSmem<64>::bytes;
-    e = cudaLaunchKernelEx(&cfg, attention_tc_kernel<64>, A);
+    e = stages >= 6   ? go(attention_tc_kernel<64, 6>, TcAttnSmem<64, 6>::bytes)
+        : stages == 4 ? go(attention_tc_kernel<64, 4>, TcAttnSmem<64, 4>::bytes)
+                      : go(attention_tc_kernel<64, 3>, TcAttnSmem<64, 3>::bytes);
   }
   if (e != cudaSuccess) return (int)e;
   ++g_kernel_count;
