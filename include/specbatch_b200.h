@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define SB_ABI_VERSION 5
+#define SB_ABI_VERSION 6
 
 /* status codes beyond cudaError_t (which are < 1000) */
 #define SB_OK 0
@@ -342,6 +342,13 @@ int sb_gemm_tune(int32_t ctas_per_sm, int32_t max_stages, int32_t splits);
 int sb_gemm_autotune(const void* x, const void* w, void* y_f32, int32_t M, int32_t N, int32_t K, void* stream,
                      int32_t* cps_out, int32_t* splits_out, float* us_out);
 int sb_gemm_autotune_clear(void);
+/*
+ * Read / write one entry of the measured table (key: the token tile of M, N, K)
+ * so a tuned table can be saved and replayed -- e.g. into a profiler run,
+ * whose serialised timings would tune differently.  get: SB_EINVAL if absent.
+ */
+int sb_gemm_tune_get(int32_t M, int32_t N, int32_t K, int32_t* cps, int32_t* splits, int32_t* weight_tiles);
+int sb_gemm_tune_set(int32_t M, int32_t N, int32_t K, int32_t cps, int32_t splits, int32_t weight_tiles);
 int sb_version(void);
 const char* sb_build_info(void);
 int sb_last_kernel_count(void); /* kernels launched by the last sb_decoder_forward */

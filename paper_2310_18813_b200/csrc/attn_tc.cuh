@@ -126,24 +126,29 @@ __device__ __forceinline__ void attn_tc_item(const AttnArgs& A, int kvh, int seq
   auto issue = [&](int tile, bool hist) {
     if (tile < n_tiles) {
       uint8_t* st = ring + ((tile - t_lo) % kTcStages) * (uint32_t)SM::stage;
-      __nv_bfloat16* Kd = reinterpret_cast<__nv_bfloat16*>(st);
-      __nv_bfloat16* Vd = reinterpret_cast<__nv_bfloat16*>(st + SM::tile);
-      const int k0 = tile * kTcKT;
-      constexpr int CPR = HD / 8;  // 16-byte chunks per row
-      for (int e = tid; e < kTcKT * CPR; e += 128) {
-        int r = e / CPR, c = (e % CPR) * 8;
-        int key = k0 + r;
+      constexpr int CPR = HD / 8;         // 16-byte chunks per row
+      constexpr int RPP = 128 / CPR;      // rows per pass
+      const int c = (tid % CPR) * 8, r0 = tid / CPR;
+      __nv_bfloat16* Kd = reinterpret_cast<__nv_bfloat16*>(st) + r0 * RS + c;
+      __nv_bfloat16* Vd = reinterpret_cast<__nv_bfloat16*>(st + SM::tile) + r0 * RS + c;
+      const int k0 = tile * kTcKT + r0;
+      const __nv_bfloat16* ks = kslab + (size_t)k0 * HD + c;
+      const __nv_bfloat16* vs = vslab + (size_t)k0 * HD + c;
+      const bool check = hist && tile * kTcKT + kTcKT > wmin;  // tile holds window rows
+#pragma unroll
+      for (int j = 0; j < kTcKT / RPP; ++j) {
+        const int key = k0 + j * RPP;
         if (key < n_keys) {
-          if (hist && key >= wmin) {
-            bool win = false;
-            for (int j = 0; j < q_len; ++j) win |= wpos[j] == key;
-            if (win) continue;
+          bool win = false;
+          if (check && key >= wmin)
+            for (int q = 0; q < q_len; ++q) win |= wpos[q] == key;
+          if (!win) {
+            cp_async16(Kd + j * RPP * RS, ks + (size_t)j * RPP * HD);
+            cp_async16(Vd + j * RPP * RS, vs + (size_t)j * RPP * HD);
           }
-          cp_async16(Kd + r * RS + c, kslab + (size_t)key * HD + c);
-          cp_async16(Vd + r * RS + c, vslab + (size_t)key * HD + c);
         } else {  // rows past the context: zeros (P is 0 there, and 0 * stale NaN would poison P.V)
-          *reinterpret_cast<uint4*>(Kd + r * RS + c) = make_uint4(0, 0, 0, 0);
-          *reinterpret_cast<uint4*>(Vd + r * RS + c) = make_uint4(0, 0, 0, 0);
+          *reinterpret_cast<uint4*>(Kd + j * RPP * RS) = make_uint4(0, 0, 0, 0);
+          *reinterpret_cast<uint4*>(Vd + j * RPP * RS) = make_uint4(0, 0, 0, 0);
         }
       }
     }
@@ -158,47 +163,78 @@ __device__ __forceinline__ void attn_tc_item(const AttnArgs& A, int kvh, int seq
     griddep_wait();
     griddep_launch();
   }
-  for (int e = tid; e < 16 * HALF; e += 128) {
-    int j = e / HALF, i = e % HALF;
-    __nv_bfloat16 a = __float2bfloat16_rn(0.f), b = a;
-    if (j < nQ) {
-      int p = qpos[j];
-      int pc = p < 0 ? 0 : (p >= max_pos ? max_pos - 1 : p);
-      const __nv_bfloat16* src = seq_rows + (size_t)qtok[j] * row_w + qhead[j] * HD;
-      float x0 = __bfloat162float(src[i]), x1 = __bfloat162float(src[i + HALF]);
-      float c = cosT[(size_t)pc * HALF + i], sn = sinT[(size_t)pc * HALF + i];
-      a = __float2bfloat16_rn(x0 * c - x1 * sn);
-      b = __float2bfloat16_rn(x1 * c + x0 * sn);
+  {
+    // One pass, one round trip: thread -> (row j, 8 rotary pairs from c8).  Q
+    // rows j < 16 are rotated into Qs (zero past nQ); window tokens j < q_len
+    // have K rotated and K / V appended to the cache and, for resident tiles,
+    // to their ring stage.  All global loads are issued before any use.
+    constexpr int CPW = HALF / 8;
+    const int j = tid / CPW, c8 = (tid % CPW) * 8;
+    uint4 qx0 = make_uint4(0, 0, 0, 0), qx1 = qx0, kx0 = qx0, kx1 = qx0, vx0 = qx0, vx1 = qx0;
+    float4 qc0{}, qc1{}, qs0{}, qs1{}, kc0{}, kc1{}, ks0{}, ks1{};
+    const bool qv = j < 16 && j < nQ;
+    if (qv) {
+      const int p = qpos[j];
+      const int pc = p < 0 ? 0 : (p >= max_pos ? max_pos - 1 : p);
+      const __nv_bfloat16* src = seq_rows + (size_t)qtok[j] * row_w + qhead[j] * HD + c8;
+      qx0 = *reinterpret_cast<const uint4*>(src);
+      qx1 = *reinterpret_cast<const uint4*>(src + HALF);
+      const float4* cp = reinterpret_cast<const float4*>(cosT + (size_t)pc * HALF + c8);
+      const float4* sp4 = reinterpret_cast<const float4*>(sinT + (size_t)pc * HALF + c8);
+      qc0 = cp[0], qc1 = cp[1], qs0 = sp4[0], qs1 = sp4[1];
     }
-    Qs[j * RS + i] = a;
-    Qs[j * RS + i + HALF] = b;
-  }
-  // append the window's rotated K / V rows to the cache and, for resident
-  // tiles, into their ring stage
-  for (int e = tid; e < q_len * HALF; e += 128) {
-    int t = e / HALF, i = e % HALF;
-    int p = wpos[t];
-    if (p < k_lo || p >= k_hi) continue;  // (p < 0: padding, never in range)
-    int pc = p >= max_pos ? max_pos - 1 : p;
-    const __nv_bfloat16* src = seq_rows + (size_t)t * row_w + (nq + kvh) * HD;
-    float x0 = __bfloat162float(src[i]), x1 = __bfloat162float(src[i + HALF]);
-    float c = cosT[(size_t)pc * HALF + i], sn = sinT[(size_t)pc * HALF + i];
-    const __nv_bfloat16 k_a = __float2bfloat16_rn(x0 * c - x1 * sn), k_b = __float2bfloat16_rn(x1 * c + x0 * sn);
-    const __nv_bfloat16* vsrc = seq_rows + (size_t)t * row_w + (nq + nkv + kvh) * HD;
-    const __nv_bfloat16 v_a = vsrc[i], v_b = vsrc[i + HALF];
-    kslab[(size_t)p * HD + i] = k_a;
-    kslab[(size_t)p * HD + i + HALF] = k_b;
-    vslab[(size_t)p * HD + i] = v_a;
-    vslab[(size_t)p * HD + i + HALF] = v_b;
-    const int ti = p / kTcKT - t_lo;
-    if (ti < kTcStages) {
-      __nv_bfloat16* Kd = reinterpret_cast<__nv_bfloat16*>(ring + ti * (uint32_t)SM::stage);
-      __nv_bfloat16* Vd = reinterpret_cast<__nv_bfloat16*>(ring + ti * (uint32_t)SM::stage + SM::tile);
-      const int r = p - (p / kTcKT) * kTcKT;
-      Kd[r * RS + i] = k_a;
-      Kd[r * RS + i + HALF] = k_b;
-      Vd[r * RS + i] = v_a;
-      Vd[r * RS + i + HALF] = v_b;
+    const int pk = j < q_len ? wpos[j] : -1;
+    const bool kv = pk >= k_lo && pk < k_hi;  // (pk < 0: padding, never in range)
+    if (kv) {
+      const int pc = pk >= max_pos ? max_pos - 1 : pk;
+      const __nv_bfloat16* src = seq_rows + (size_t)j * row_w + (nq + kvh) * HD + c8;
+      kx0 = *reinterpret_cast<const uint4*>(src);
+      kx1 = *reinterpret_cast<const uint4*>(src + HALF);
+      const __nv_bfloat16* vsrc = seq_rows + (size_t)j * row_w + (nq + nkv + kvh) * HD + c8;
+      vx0 = *reinterpret_cast<const uint4*>(vsrc);
+      vx1 = *reinterpret_cast<const uint4*>(vsrc + HALF);
+      const float4* cp = reinterpret_cast<const float4*>(cosT + (size_t)pc * HALF + c8);
+      const float4* sp4 = reinterpret_cast<const float4*>(sinT + (size_t)pc * HALF + c8);
+      kc0 = cp[0], kc1 = cp[1], ks0 = sp4[0], ks1 = sp4[1];
+    }
+    // (x0, x1) pairs -> (x0 c - x1 s, x1 c + x0 s), bf16
+    auto rot = [](uint4 x0, uint4 x1, float4 c0, float4 c1, float4 s0, float4 s1, uint4& a, uint4& b) {
+      const __nv_bfloat16* u = reinterpret_cast<const __nv_bfloat16*>(&x0);
+      const __nv_bfloat16* w = reinterpret_cast<const __nv_bfloat16*>(&x1);
+      const float cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+      const float ss[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+      __nv_bfloat16* pa = reinterpret_cast<__nv_bfloat16*>(&a);
+      __nv_bfloat16* pb = reinterpret_cast<__nv_bfloat16*>(&b);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const float f0 = __bfloat162float(u[i]), f1 = __bfloat162float(w[i]);
+        pa[i] = __float2bfloat16_rn(f0 * cc[i] - f1 * ss[i]);
+        pb[i] = __float2bfloat16_rn(f1 * cc[i] + f0 * ss[i]);
+      }
+    };
+    if (j < 16) {
+      uint4 a = make_uint4(0, 0, 0, 0), b2 = a;
+      if (qv) rot(qx0, qx1, qc0, qc1, qs0, qs1, a, b2);
+      *reinterpret_cast<uint4*>(Qs + j * RS + c8) = a;
+      *reinterpret_cast<uint4*>(Qs + j * RS + HALF + c8) = b2;
+    }
+    if (kv) {
+      uint4 a, b2;
+      rot(kx0, kx1, kc0, kc1, ks0, ks1, a, b2);
+      *reinterpret_cast<uint4*>(kslab + (size_t)pk * HD + c8) = a;
+      *reinterpret_cast<uint4*>(kslab + (size_t)pk * HD + HALF + c8) = b2;
+      *reinterpret_cast<uint4*>(vslab + (size_t)pk * HD + c8) = vx0;
+      *reinterpret_cast<uint4*>(vslab + (size_t)pk * HD + HALF + c8) = vx1;
+      const int ti = pk / kTcKT - t_lo;
+      if (ti < kTcStages) {
+        const int r = pk - (pk / kTcKT) * kTcKT;
+        __nv_bfloat16* Kd = reinterpret_cast<__nv_bfloat16*>(ring + ti * (uint32_t)SM::stage) + r * RS;
+        __nv_bfloat16* Vd = reinterpret_cast<__nv_bfloat16*>(ring + ti * (uint32_t)SM::stage + SM::tile) + r * RS;
+        *reinterpret_cast<uint4*>(Kd + c8) = a;
+        *reinterpret_cast<uint4*>(Kd + HALF + c8) = b2;
+        *reinterpret_cast<uint4*>(Vd + c8) = vx0;
+        *reinterpret_cast<uint4*>(Vd + HALF + c8) = vx1;
+      }
     }
   }
   __threadfence_block();

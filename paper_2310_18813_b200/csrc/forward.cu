@@ -536,6 +536,14 @@ int sb_gemm_autotune(const void* x, const void* w, void* y_f32, int32_t M, int32
 
 int sb_gemm_autotune_clear(void) { return gemm_tc_autotune_clear(); }
 
+int sb_gemm_tune_get(int32_t M, int32_t N, int32_t K, int32_t* cps, int32_t* splits, int32_t* weight_tiles) {
+  return gemm_tc_tune_get(M, N, K, cps, splits, weight_tiles);
+}
+
+int sb_gemm_tune_set(int32_t M, int32_t N, int32_t K, int32_t cps, int32_t splits, int32_t weight_tiles) {
+  return gemm_tc_tune_set(M, N, K, cps, splits, weight_tiles);
+}
+
 int sb_set_attention_splits(int32_t splits) {
   if (splits < 0 || splits > 8) return SB_EINVAL;
   g_attn_splits = splits;
@@ -600,7 +608,7 @@ int sb_set_pdl(int32_t enabled) {
 int sb_version(void) { return SB_ABI_VERSION; }
 
 const char* sb_build_info(void) {
-  return "specbatch_b200 abi=" "4" " arch=sm_100a tp=nccl models=llama,opt kernels=persistent_forward,layernorm,tp_resid_add,unshard_logits,embed,rmsnorm,rope_append,attention,gemm_simt,gemm_tcgen05,"
+  return "specbatch_b200 abi=" "6" " arch=sm_100a tp=nccl models=llama,opt kernels=persistent_forward,layernorm,tp_resid_add,unshard_logits,embed,rmsnorm,rope_append,attention,gemm_simt,gemm_tcgen05,"
          "argmax,softmax,select,accept,commit,prepare,kv_compact";
 }
 

@@ -656,6 +656,27 @@ int gemm_tc_autotune(const void* x, const void* w, float* y, int M, int N, int K
   return 0;
 }
 
+int gemm_tc_tune_get(int M, int N, int K, int* cps, int* splits, int* wt) {
+  if (M <= 0 || N <= 0 || K <= 0) return SB_EINVAL;
+  const int tn = tn_for(M), m_tiles = (M + tn - 1) / tn;
+  std::lock_guard<std::mutex> lk(g_tuned_mu);
+  auto it = g_tuned.find(tune_key(tn, m_tiles, N, K));
+  if (it == g_tuned.end()) return SB_EINVAL;
+  if (cps) *cps = it->second.cps;
+  if (splits) *splits = it->second.splits;
+  if (wt) *wt = it->second.wt;
+  return 0;
+}
+
+int gemm_tc_tune_set(int M, int N, int K, int cps, int splits, int wt) {
+  if (M <= 0 || N <= 0 || K <= 0 || cps < 1 || cps > 3 || splits < 1 || splits > 8 || wt < 1 || wt > 2)
+    return SB_EINVAL;
+  const int tn = tn_for(M), m_tiles = (M + tn - 1) / tn;
+  std::lock_guard<std::mutex> lk(g_tuned_mu);
+  g_tuned[tune_key(tn, m_tiles, N, K)] = {cps, splits, wt};
+  return 0;
+}
+
 int gemm_tc_autotune_clear() {
   std::lock_guard<std::mutex> lk(g_tuned_mu);
   g_tuned.clear();
@@ -667,6 +688,7 @@ int gemm_tc_init() {
   if (rc < 0) {
     cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     rc = (e == cudaSuccess) ? 0 : (int)e;
+    if (!rc) rc = attention_tc_init();
     num_sms();
     get_encode();
   }

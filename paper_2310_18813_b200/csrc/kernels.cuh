@@ -55,6 +55,8 @@ int gemm_tc_tune(int cps, int stages, int splits);
 int gemm_tc_autotune(const void* x, const void* w, float* y, int M, int N, int K, cudaStream_t st, int* cps_out,
                      int* splits_out, float* us_out);
 int gemm_tc_autotune_clear();
+int gemm_tc_tune_get(int M, int N, int K, int* cps, int* splits, int* wt);
+int gemm_tc_tune_set(int M, int N, int K, int cps, int splits, int wt);
 int num_sms();
 // 2-D bf16 tensor map [rows, cols] (row stride ld elements), box TC_BK x box_rows, 128B swizzle.
 int make_map(CUtensorMap* map, const void* base, int rows, int cols, int ld, int box_rows);
@@ -86,6 +88,7 @@ int launch_attention_tc(const void* qkv, void* kc, void* vc, void* out, const in
                         int ctx_max, int max_pos, cudaStream_t st, const AttnScratch* scratch = nullptr,
                         const void* l2_next = nullptr, size_t l2_next_bytes = 0);
 extern int g_attn_l2pf;
+int attention_tc_init();
 int launch_argmax_partials(const float* val, const int* idx, int n_tiles, int rows, int32_t* out_tok, int out_stride,
                            int32_t* next_ids, int32_t* next_pos, const int32_t* base_pos, int pos_offset,
                            cudaStream_t st);

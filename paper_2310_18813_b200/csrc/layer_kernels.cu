@@ -500,6 +500,27 @@ __global__ void __launch_bounds__(128) attention_tc_kernel(AttnArgs A) {
   attn_tc_item<HD, STAGES>(A, blockIdx.x, blockIdx.y, blockIdx.z, gridDim.z, tsm, sh, threadIdx.x, true);
 }
 
+// Opt every ring variant in to its dynamic shared memory once (outside graph capture).
+int attention_tc_init() {
+  static int rc = -1;
+  if (rc < 0) {
+    cudaError_t e = cudaSuccess;
+#define SB_ATTN_ATTR(H, S)                                                                                        \
+  if (e == cudaSuccess)                                                                                           \
+  e = cudaFuncSetAttribute(attention_tc_kernel<H, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,                \
+                           (int)TcAttnSmem<H, S>::bytes)
+    SB_ATTN_ATTR(128, 3);
+    SB_ATTN_ATTR(128, 4);
+    SB_ATTN_ATTR(128, 6);
+    SB_ATTN_ATTR(64, 3);
+    SB_ATTN_ATTR(64, 4);
+    SB_ATTN_ATTR(64, 6);
+#undef SB_ATTN_ATTR
+    rc = e == cudaSuccess ? 0 : (int)e;
+  }
+  return rc;
+}
+
 int launch_attention_tc(const void* qkv, void* kc, void* vc, void* out, const int32_t* tok_slot, const int32_t* tok_pos,
                         const float* cosT, const float* sinT, int n_seq, int q_len, int nq, int nkv, int hd,
                         int ctx_max, int max_pos, cudaStream_t st, const AttnScratch* scratch,
@@ -545,19 +566,12 @@ int launch_attention_tc(const void* qkv, void* kc, void* vc, void* out, const in
   const int ctas = nkv * n_seq * splits;
   const int stages = ctas <= num_sms() ? g_attn_stages : 3;
   cudaError_t e;
-  static bool attr = false;
-  if (!attr) {
-#define SB_ATTN_ATTR(H, S) \
-  cudaFuncSetAttribute(attention_tc_kernel<H, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                       (int)TcAttnSmem<H, S>::bytes)
-    SB_ATTN_ATTR(128, 3);
-    SB_ATTN_ATTR(128, 4);
-    SB_ATTN_ATTR(128, 6);
-    SB_ATTN_ATTR(64, 3);
-    SB_ATTN_ATTR(64, 4);
-    SB_ATTN_ATTR(64, 6);
-#undef SB_ATTN_ATTR
-    attr = true;
+  {  // normally done by gemm_tc_init outside capture; relaxed so a first call inside a capture is legal
+    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+    cudaThreadExchangeStreamCaptureMode(&mode);
+    const int rc = attention_tc_init();
+    cudaThreadExchangeStreamCaptureMode(&mode);
+    if (rc) return rc;
   }
   auto go = [&](void (*kern)(AttnArgs), size_t bytes) {
     cfg.dynamicSmemBytes = bytes;

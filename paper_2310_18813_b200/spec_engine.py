@@ -25,6 +25,7 @@ Acceptance modes:
 from __future__ import annotations
 
 import ctypes as C
+import gc
 import math
 import time
 from dataclasses import dataclass, field
@@ -236,11 +237,7 @@ class SpecEngine:
         key = (b, k)
         g = self.graphs.get(key)
         if g is None:
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.stream(self.stream):
-                torch.cuda.synchronize(self.dev)
-                with torch.cuda.graph(g, stream=self.stream):
-                    self._iteration(b, k)
+            g = _capture_graph(lambda: self._iteration(b, k), self.stream)
             self.graphs[key] = g
         return g
 
@@ -369,14 +366,30 @@ class SpecEngine:
 
 
 # ---------------------------------------------------------------- timing hooks
+def _capture_graph(fn, stream) -> "torch.cuda.CUDAGraph":
+    """Capture ``fn`` on ``stream`` with the cyclic GC off: a collection inside
+    the capture can finalise an older engine (pinned buffers, graphs) whose CUDA
+    frees are illegal while a stream captures -- the capture is invalidated."""
+    g = torch.cuda.CUDAGraph()
+    gc.collect()
+    gc_was = gc.isenabled()
+    gc.disable()
+    try:
+        with torch.cuda.stream(stream):
+            torch.cuda.synchronize()
+            with torch.cuda.graph(g, stream=stream):
+                fn()
+    finally:
+        if gc_was:
+            gc.enable()
+    return g
+
+
 def _timed_graph(fn, reps: int, stream) -> float:
     """Capture ``fn`` once into a CUDA graph, replay it ``reps`` times and return
     the mean CUDA-event milliseconds per replay (after one warm replay)."""
-    g = torch.cuda.CUDAGraph()
+    g = _capture_graph(fn, stream)
     with torch.cuda.stream(stream):
-        torch.cuda.synchronize()
-        with torch.cuda.graph(g, stream=stream):
-            fn()
         g.replay()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
