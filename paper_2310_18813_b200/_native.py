@@ -9,6 +9,7 @@ computing on the CPU.
 from __future__ import annotations
 
 import ctypes as C
+import os
 from pathlib import Path
 
 from .errors import NativeError
@@ -129,7 +130,8 @@ def load(path: Path | None = None):
     global _lib, _load_error
     if _lib is not None:
         return _lib
-    p = Path(path) if path else LIB_PATH
+    # SB_LIB: an alternative build of the same ABI (A/B timing of kernel variants)
+    p = Path(path) if path else Path(os.environ["SB_LIB"]) if os.environ.get("SB_LIB") else LIB_PATH
     if not p.exists():
         raise NativeError("load", -1, f"{p} not built; run `python -m paper_2310_18813_b200.build` "
                                       "(or __graft_entry__.build())")
