@@ -50,6 +50,10 @@ struct AttnArgs {
   AttnSplit sp;
   const char* l2_next;  // next GEMM's weights: prefetched into L2 while this latency-bound kernel runs
   unsigned long long l2_next_bytes;
+  // prefill blocks: Q already rotated by rope_append (qr [T][nq][HD]) and the
+  // window already in the cache; CTA z takes tokens [z*q_blk, (z+1)*q_blk)
+  const __nv_bfloat16* qr;
+  int q_blk;
 };
 struct AttnShared {
   int qpos[16], qtok[16], qhead[16];
@@ -63,7 +67,7 @@ struct AttnShared {
 // KV-history tiles, then griddepcontrol.wait / launch_dependents.
 template <int HD, int STAGES>
 __device__ __forceinline__ void attn_tc_item(const AttnArgs& A, int kvh, int seq, int split, int n_splits,
-                                             uint8_t* tsm, AttnShared& sh, int tid, bool pdl) {
+                                             uint8_t* tsm, AttnShared& sh, int tid, bool pdl, int qb = 0) {
   const __nv_bfloat16* __restrict__ qkv = A.qkv;
   __nv_bfloat16* __restrict__ kc = A.kc;
   __nv_bfloat16* __restrict__ vc = A.vc;
@@ -85,7 +89,9 @@ __device__ __forceinline__ void attn_tc_item(const AttnArgs& A, int kvh, int seq
   int* qhead = sh.qhead;
 
   const int group = nq / nkv;
-  const int nQ = group * q_len;
+  const bool blk = A.qr != nullptr;  // prefill block of an already rotated / appended window
+  const int t0 = blk ? qb * A.q_blk : 0;
+  const int nQ = group * (blk ? min(A.q_blk, q_len - t0) : q_len);
   const int warp = tid >> 5, lane = tid & 31;
   // Before the programmatic-dependency wait only data written >= 2 kernels
   // back is touched (positions, slots, KV history): every kernel of the
@@ -99,10 +105,10 @@ __device__ __forceinline__ void attn_tc_item(const AttnArgs& A, int kvh, int seq
 
   if (tid < 16) {
     int t = tid / group;
-    qtok[tid] = tid < nQ ? t : 0;
+    qtok[tid] = tid < nQ ? t0 + t : 0;
     qhead[tid] = kvh * group + tid % group;
-    qpos[tid] = tid < nQ ? tok_pos[seq * q_len + t] : -1;
-    sh.wpos[tid] = tid < q_len ? tok_pos[seq * q_len + tid] : -1;
+    qpos[tid] = tid < nQ ? tok_pos[seq * q_len + t0 + t] : -1;
+    sh.wpos[tid] = !blk && tid < q_len ? tok_pos[seq * q_len + tid] : -1;
   }
   attn_sync();
   // this split's key range [k_lo, k_hi) (64-key tiles shared evenly)
@@ -157,12 +163,16 @@ __device__ __forceinline__ void attn_tc_item(const AttnArgs& A, int kvh, int seq
   // The first STAGES tiles (KV history; the cache rows of this layer were last
   // written >= 2 launches back) start loading now, overlapping the tail of the
   // qkv GEMM.
-  for (int i = 0; i < kTcStages; ++i) issue(t_lo + i, true);
+  // (prefill blocks: the preceding rope_append wrote these rows -- after the wait)
+  if (!blk)
+    for (int i = 0; i < kTcStages; ++i) issue(t_lo + i, true);
 
   if (pdl) {
     griddep_wait();
     griddep_launch();
   }
+  if (blk)
+    for (int i = 0; i < kTcStages; ++i) issue(t_lo + i, false);
   {
     // One pass, one round trip: thread -> (row j, 8 rotary pairs from c8).  Q
     // rows j < 16 are rotated into Qs (zero past nQ); window tokens j < q_len
@@ -173,7 +183,11 @@ __device__ __forceinline__ void attn_tc_item(const AttnArgs& A, int kvh, int seq
     uint4 qx0 = make_uint4(0, 0, 0, 0), qx1 = qx0, kx0 = qx0, kx1 = qx0, vx0 = qx0, vx1 = qx0;
     float4 qc0{}, qc1{}, qs0{}, qs1{}, kc0{}, kc1{}, ks0{}, ks1{};
     const bool qv = j < 16 && j < nQ;
-    if (qv) {
+    if (qv && blk) {
+      const __nv_bfloat16* src = A.qr + ((size_t)(seq * q_len + qtok[j]) * nq + qhead[j]) * HD + c8;
+      qx0 = *reinterpret_cast<const uint4*>(src);
+      qx1 = *reinterpret_cast<const uint4*>(src + HALF);
+    } else if (qv) {
       const int p = qpos[j];
       const int pc = p < 0 ? 0 : (p >= max_pos ? max_pos - 1 : p);
       const __nv_bfloat16* src = seq_rows + (size_t)qtok[j] * row_w + qhead[j] * HD + c8;
@@ -183,7 +197,7 @@ __device__ __forceinline__ void attn_tc_item(const AttnArgs& A, int kvh, int seq
       const float4* sp4 = reinterpret_cast<const float4*>(sinT + (size_t)pc * HALF + c8);
       qc0 = cp[0], qc1 = cp[1], qs0 = sp4[0], qs1 = sp4[1];
     }
-    const int pk = j < q_len ? wpos[j] : -1;
+    const int pk = !blk && j < q_len ? wpos[j] : -1;
     const bool kv = pk >= k_lo && pk < k_hi;  // (pk < 0: padding, never in range)
     if (kv) {
       const int pc = pk >= max_pos ? max_pos - 1 : pk;
@@ -214,7 +228,8 @@ __device__ __forceinline__ void attn_tc_item(const AttnArgs& A, int kvh, int seq
     };
     if (j < 16) {
       uint4 a = make_uint4(0, 0, 0, 0), b2 = a;
-      if (qv) rot(qx0, qx1, qc0, qc1, qs0, qs1, a, b2);
+      if (qv && blk) a = qx0, b2 = qx1;
+      else if (qv) rot(qx0, qx1, qc0, qc1, qs0, qs1, a, b2);
       *reinterpret_cast<uint4*>(Qs + j * RS + c8) = a;
       *reinterpret_cast<uint4*>(Qs + j * RS + HALF + c8) = b2;
     }

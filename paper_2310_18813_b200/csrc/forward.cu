@@ -185,6 +185,18 @@ static int lm_head(const sb_decoder_t* m, GemmArgs g, float* logits, const sb_to
 // per-tile sum-of-squares partials; the consuming GEMMs (qkv, gate/up,
 // lm_head) read that copy and scale each token by 1/rms in their epilogue.
 // Norm gains are folded into the consumer weights by the host (ones here).
+// Attention over an already rotated / appended window (prefill-sized blocks):
+// tensor-core flash attention for bf16, the batch-invariant SIMT kernel for fp32.
+static int launch_attention_any(int dt, const void* qr, void* kc, void* vc, void* out, const int32_t* slot,
+                                const int32_t* pos, int n_seq, int q_len, int nq, int nkv, int hd, int ctx_max,
+                                cudaStream_t st) {
+  if (dt == SB_BF16 && g_attn_impl == 0) {
+    const int rc = launch_attention_tc_prefill(qr, kc, vc, out, slot, pos, n_seq, q_len, nq, nkv, hd, ctx_max, st);
+    if (rc != SB_EUNSUPPORTED) return rc;
+  }
+  return launch_attention(dt, qr, kc, vc, out, slot, pos, n_seq, q_len, nq, nkv, hd, ctx_max, st);
+}
+
 static int forward_fused_norm(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* ids, const int32_t* slot,
                               const int32_t* pos, int n_seq, int q_len, float* logits, int logits_mode,
                               const sb_token_sink_t* sink, const FwdWorkspace& w, cudaStream_t st) {
@@ -215,7 +227,7 @@ static int forward_fused_norm(const sb_decoder_t* m, const sb_kvcache_t* kv, con
     if (rc_fa == SB_EUNSUPPORTED) {
       SB_TRY(launch_rope_append(SB_BF16, w.qkv, w.qr, kc, vc, slot, pos, m->rope_cos, m->rope_sin, T, q_len, nq, nkv,
                                 hd, kv->ctx_max, m->max_pos, st));
-      SB_TRY(launch_attention(SB_BF16, w.qr, kc, vc, w.attn, slot, pos, n_seq, q_len, nq, nkv, hd, kv->ctx_max, st));
+      SB_TRY(launch_attention_any(SB_BF16, w.qr, kc, vc, w.attn, slot, pos, n_seq, q_len, nq, nkv, hd, kv->ctx_max, st));
     }
     prof_mark("attn", st);
     if (m->tp) {  // row-parallel o_proj: partial -> all-reduce -> residual
@@ -314,7 +326,7 @@ static int forward_opt(const sb_decoder_t* m, const sb_kvcache_t* kv, const int3
     if (rc_fa == SB_EUNSUPPORTED) {
       SB_TRY(launch_rope_append(dt, w.qkv, w.qr, kc, vc, slot, pos, m->rope_cos, m->rope_sin, T, q_len, nq, nkv, hd,
                                 kv->ctx_max, m->max_pos, st));
-      SB_TRY(launch_attention(dt, w.qr, kc, vc, w.attn, slot, pos, n_seq, q_len, nq, nkv, hd, kv->ctx_max, st));
+      SB_TRY(launch_attention_any(dt, w.qr, kc, vc, w.attn, slot, pos, n_seq, q_len, nq, nkv, hd, kv->ctx_max, st));
     }
     prof_mark("attn", st);
     g = GemmArgs{dt, w.attn, m->w_o[l], w.resid, T, H, nq * hd, nq * hd, EPI_RESID_ADD, w.gemm_ws, w.gemm_ws_bytes};
@@ -389,7 +401,7 @@ static int forward_impl(const sb_decoder_t* m, const sb_kvcache_t* kv, const int
     if (rc_fa == SB_EUNSUPPORTED) {  // prefill-sized query blocks / wide GQA: rope+append then attention
       SB_TRY(launch_rope_append(dt, w.qkv, w.qr, kc, vc, slot, pos, m->rope_cos, m->rope_sin, T, q_len, nq, nkv, hd,
                                 kv->ctx_max, m->max_pos, st));
-      SB_TRY(launch_attention(dt, w.qr, kc, vc, w.attn, slot, pos, n_seq, q_len, nq, nkv, hd, kv->ctx_max, st));
+      SB_TRY(launch_attention_any(dt, w.qr, kc, vc, w.attn, slot, pos, n_seq, q_len, nq, nkv, hd, kv->ctx_max, st));
     }
     prof_mark("attn", st);
     g = GemmArgs{dt, w.attn, m->w_o[l], m->tp ? w.tp_part : w.resid, T, H, nq * hd, nq * hd,

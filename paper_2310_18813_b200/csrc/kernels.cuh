@@ -88,6 +88,9 @@ int launch_attention_tc(const void* qkv, void* kc, void* vc, void* out, const in
                         int ctx_max, int max_pos, cudaStream_t st, const AttnScratch* scratch = nullptr,
                         const void* l2_next = nullptr, size_t l2_next_bytes = 0);
 extern int g_attn_l2pf;
+int launch_attention_tc_prefill(const void* qr, void* kc, void* vc, void* out, const int32_t* tok_slot,
+                                const int32_t* tok_pos, int n_seq, int q_len, int nq, int nkv, int hd, int ctx_max,
+                                cudaStream_t st);
 int attention_tc_init();
 int launch_argmax_partials(const float* val, const int* idx, int n_tiles, int rows, int32_t* out_tok, int out_stride,
                            int32_t* next_ids, int32_t* next_pos, const int32_t* base_pos, int pos_offset,

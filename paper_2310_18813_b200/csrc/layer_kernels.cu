@@ -497,7 +497,10 @@ __global__ void __launch_bounds__(128) attention_tc_kernel(AttnArgs A) {
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.l2_next + o), "r"(n) : "memory");
     }
   }
-  attn_tc_item<HD, STAGES>(A, blockIdx.x, blockIdx.y, blockIdx.z, gridDim.z, tsm, sh, threadIdx.x, true);
+  if (A.qr)
+    attn_tc_item<HD, STAGES>(A, blockIdx.x, blockIdx.y, 0, 1, tsm, sh, threadIdx.x, true, blockIdx.z);
+  else
+    attn_tc_item<HD, STAGES>(A, blockIdx.x, blockIdx.y, blockIdx.z, gridDim.z, tsm, sh, threadIdx.x, true);
 }
 
 // Opt every ring variant in to its dynamic shared memory once (outside graph capture).
@@ -519,6 +522,49 @@ int attention_tc_init() {
     rc = e == cudaSuccess ? 0 : (int)e;
   }
   return rc;
+}
+
+// Launch attention_tc_kernel over grid (nkv, n_seq, z) with the ring depth for its residency.
+static int launch_attn_grid(const AttnArgs& A, int hd, int n_seq, int z, cudaStream_t st) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(A.nkv, n_seq, z);
+  cfg.blockDim = dim3(128);
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = g_pdl ? 1 : 0;
+  if (g_attn_stages < 0) {
+    const char* e = getenv("SB_ATTN_STAGES");
+    g_attn_stages = e ? atoi(e) : 4;  // measured: 4 and 6 tie, 3-5% over 3 at b = 2..4
+  }
+  const int ctas = A.nkv * n_seq * z;
+  const int stages = ctas <= num_sms() ? g_attn_stages : 3;
+  {  // normally done by gemm_tc_init outside capture; relaxed so a first call inside a capture is legal
+    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+    cudaThreadExchangeStreamCaptureMode(&mode);
+    const int rc = attention_tc_init();
+    cudaThreadExchangeStreamCaptureMode(&mode);
+    if (rc) return rc;
+  }
+  auto go = [&](void (*kern)(AttnArgs), size_t bytes) {
+    cfg.dynamicSmemBytes = bytes;
+    return cudaLaunchKernelEx(&cfg, kern, A);
+  };
+  cudaError_t e;
+  if (hd == 128) {
+    e = stages >= 6   ? go(attention_tc_kernel<128, 6>, TcAttnSmem<128, 6>::bytes)
+        : stages == 4 ? go(attention_tc_kernel<128, 4>, TcAttnSmem<128, 4>::bytes)
+                      : go(attention_tc_kernel<128, 3>, TcAttnSmem<128, 3>::bytes);
+  } else {
+    e = stages >= 6   ? go(attention_tc_kernel<64, 6>, TcAttnSmem<64, 6>::bytes)
+        : stages == 4 ? go(attention_tc_kernel<64, 4>, TcAttnSmem<64, 4>::bytes)
+                      : go(attention_tc_kernel<64, 3>, TcAttnSmem<64, 3>::bytes);
+  }
+  if (e != cudaSuccess) return (int)e;
+  ++g_kernel_count;
+  return 0;
 }
 
 int launch_attention_tc(const void* qkv, void* kc, void* vc, void* out, const int32_t* tok_slot, const int32_t* tok_pos,
@@ -549,46 +595,23 @@ int launch_attention_tc(const void* qkv, void* kc, void* vc, void* out, const in
                scratch ? scratch->counter : nullptr};
   AttnArgs A{(const __nv_bfloat16*)qkv, (__nv_bfloat16*)kc, (__nv_bfloat16*)vc, (__nv_bfloat16*)out, tok_slot, tok_pos,
              cosT, sinT, q_len, nq, nkv, ctx_max, max_pos, scale, sp, (const char*)l2_next,
-             l2_next ? (unsigned long long)l2_next_bytes : 0ull};
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(nkv, n_seq, splits);
-  cfg.blockDim = dim3(128);
-  cfg.stream = st;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = g_pdl ? 1 : 0;
-  if (g_attn_stages < 0) {
-    const char* e = getenv("SB_ATTN_STAGES");
-    g_attn_stages = e ? atoi(e) : 4;  // measured: 4 and 6 tie, 3-5% over 3 at b = 2..4
-  }
-  const int ctas = nkv * n_seq * splits;
-  const int stages = ctas <= num_sms() ? g_attn_stages : 3;
-  cudaError_t e;
-  {  // normally done by gemm_tc_init outside capture; relaxed so a first call inside a capture is legal
-    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
-    cudaThreadExchangeStreamCaptureMode(&mode);
-    const int rc = attention_tc_init();
-    cudaThreadExchangeStreamCaptureMode(&mode);
-    if (rc) return rc;
-  }
-  auto go = [&](void (*kern)(AttnArgs), size_t bytes) {
-    cfg.dynamicSmemBytes = bytes;
-    return cudaLaunchKernelEx(&cfg, kern, A);
-  };
-  if (hd == 128) {
-    e = stages >= 6   ? go(attention_tc_kernel<128, 6>, TcAttnSmem<128, 6>::bytes)
-        : stages == 4 ? go(attention_tc_kernel<128, 4>, TcAttnSmem<128, 4>::bytes)
-                      : go(attention_tc_kernel<128, 3>, TcAttnSmem<128, 3>::bytes);
-  } else {
-    e = stages >= 6   ? go(attention_tc_kernel<64, 6>, TcAttnSmem<64, 6>::bytes)
-        : stages == 4 ? go(attention_tc_kernel<64, 4>, TcAttnSmem<64, 4>::bytes)
-                      : go(attention_tc_kernel<64, 3>, TcAttnSmem<64, 3>::bytes);
-  }
-  if (e != cudaSuccess) return (int)e;
-  ++g_kernel_count;
-  return 0;
+             l2_next ? (unsigned long long)l2_next_bytes : 0ull, nullptr, 0};
+  return launch_attn_grid(A, hd, n_seq, splits, st);
+}
+
+// Prefill-sized windows (after launch_rope_append): tensor-core flash attention
+// over blocks of 16 / group query tokens per CTA, causal by position.
+int launch_attention_tc_prefill(const void* qr, void* kc, void* vc, void* out, const int32_t* tok_slot,
+                                const int32_t* tok_pos, int n_seq, int q_len, int nq, int nkv, int hd, int ctx_max,
+                                cudaStream_t st) {
+  if ((hd != 64 && hd != 128) || nq % nkv != 0 || nq / nkv > 16 || q_len < 1) return SB_EUNSUPPORTED;
+  const int q_blk = 16 / (nq / nkv);
+  const int nblk = (q_len + q_blk - 1) / q_blk;
+  if (nblk > 65535) return SB_EUNSUPPORTED;
+  AttnArgs A{nullptr, (__nv_bfloat16*)kc, (__nv_bfloat16*)vc, (__nv_bfloat16*)out, tok_slot, tok_pos, nullptr, nullptr,
+             q_len, nq, nkv, ctx_max, 1, 1.0f / sqrtf((float)hd), AttnSplit{nullptr, nullptr, nullptr}, nullptr, 0ull,
+             (const __nv_bfloat16*)qr, q_blk};
+  return launch_attn_grid(A, hd, n_seq, nblk, st);
 }
 
 // ---------------------------------------------------------------- KV compaction (K5)
