@@ -268,10 +268,65 @@ __global__ void rope_append_kernel(const T* __restrict__ qkv, T* __restrict__ q_
   }
 }
 
+// bf16, 16-byte vectors: a thread rotates 8 (x_i, x_{i+hd/2}) pairs of one head
+// (two 16-byte loads + 2 x 2 float4 of cos / sin) -- same arithmetic as above.
+__global__ void __launch_bounds__(256) rope_append_vec_kernel(
+    const __nv_bfloat16* __restrict__ qkv, __nv_bfloat16* __restrict__ q_out, __nv_bfloat16* __restrict__ kc,
+    __nv_bfloat16* __restrict__ vc, const int32_t* __restrict__ tok_slot, const int32_t* __restrict__ tok_pos,
+    const float* __restrict__ cosT, const float* __restrict__ sinT, int q_len, int nq, int nkv, int hd, int ctx_max,
+    int max_pos) {
+  griddep_wait();
+  griddep_launch();
+  const int t = blockIdx.x;
+  const int slot = tok_slot[t / q_len];
+  const int p = tok_pos[t];
+  const int half = hd / 2, cpr = half / 8;
+  const __nv_bfloat16* row = qkv + (size_t)t * (nq + 2 * nkv) * hd;
+  const int pc = p < 0 ? 0 : (p >= max_pos ? max_pos - 1 : p);
+  const float* cr = cosT + (size_t)pc * half;
+  const float* sr = sinT + (size_t)pc * half;
+  const int n_rot = (p < 0 ? nq : nq + nkv) * cpr;  // padding token: nothing enters the cache
+  for (int e = threadIdx.x; e < n_rot; e += blockDim.x) {
+    const int h = e / cpr, c8 = (e % cpr) * 8;
+    const __nv_bfloat16* src = row + h * hd + c8;
+    const uint4 u0 = *reinterpret_cast<const uint4*>(src), u1 = *reinterpret_cast<const uint4*>(src + half);
+    const float4 c0 = *reinterpret_cast<const float4*>(cr + c8), c1 = *reinterpret_cast<const float4*>(cr + c8 + 4);
+    const float4 s0 = *reinterpret_cast<const float4*>(sr + c8), s1 = *reinterpret_cast<const float4*>(sr + c8 + 4);
+    const __nv_bfloat16* x0 = reinterpret_cast<const __nv_bfloat16*>(&u0);
+    const __nv_bfloat16* x1 = reinterpret_cast<const __nv_bfloat16*>(&u1);
+    const float cc[8] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+    const float ss[8] = {s0.x, s0.y, s0.z, s0.w, s1.x, s1.y, s1.z, s1.w};
+    uint4 oa, ob;
+    __nv_bfloat16* pa = reinterpret_cast<__nv_bfloat16*>(&oa);
+    __nv_bfloat16* pb = reinterpret_cast<__nv_bfloat16*>(&ob);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const float a = __bfloat162float(x0[i]), b = __bfloat162float(x1[i]);
+      pa[i] = __float2bfloat16_rn(a * cc[i] - b * ss[i]);
+      pb[i] = __float2bfloat16_rn(b * cc[i] + a * ss[i]);
+    }
+    __nv_bfloat16* dst = h < nq ? q_out + ((size_t)t * nq + h) * hd
+                                : kc + (((size_t)slot * nkv + (h - nq)) * ctx_max + p) * hd;
+    *reinterpret_cast<uint4*>(dst + c8) = oa;
+    *reinterpret_cast<uint4*>(dst + half + c8) = ob;
+  }
+  if (p < 0) return;
+  const int vpr = hd / 8;
+  for (int e = threadIdx.x; e < nkv * vpr; e += blockDim.x) {
+    const int h = e / vpr, c = (e % vpr) * 8;
+    *reinterpret_cast<uint4*>(vc + (((size_t)slot * nkv + h) * ctx_max + p) * hd + c) =
+        *reinterpret_cast<const uint4*>(row + (nq + nkv + h) * hd + c);
+  }
+}
+
 int launch_rope_append(int dtype, const void* qkv, void* q_out, void* kc, void* vc, const int32_t* tok_slot,
                        const int32_t* tok_pos, const float* cosT, const float* sinT, int n_tok, int q_len, int nq,
                        int nkv, int hd, int ctx_max, int max_pos, cudaStream_t st) {
   if (n_tok <= 0) return 0;
+  if (dtype == SB_BF16 && hd % 16 == 0)
+    return launch_k(rope_append_vec_kernel, dim3(n_tok), dim3(128), 0, st, (const __nv_bfloat16*)qkv,
+                    (__nv_bfloat16*)q_out, (__nv_bfloat16*)kc, (__nv_bfloat16*)vc, tok_slot, tok_pos, cosT, sinT,
+                    q_len, nq, nkv, hd, ctx_max, max_pos);
   if (dtype == SB_BF16)
     return launch_k(rope_append_kernel<__nv_bfloat16>, dim3(n_tok), dim3(256), 0, st, (const __nv_bfloat16*)qkv,
                     (__nv_bfloat16*)q_out, (__nv_bfloat16*)kc, (__nv_bfloat16*)vc, tok_slot, tok_pos, cosT, sinT,
