@@ -15,6 +15,8 @@ ws = torch.zeros(tgt.workspace_bytes(T), device=dev, dtype=torch.uint8)
 ids = torch.randint(0, 32000, (T,), dtype=torch.int32, device=dev)
 pos = torch.arange(q, dtype=torch.int32, device=dev).repeat(b)
 slots = torch.arange(b, dtype=torch.int32, device=dev)
+if os.environ.get("TUNE") == "1":
+    print("tuned:", {k: v for k, v in tgt.autotune([T]).items()})
 buf = C.create_string_buffer(8192)
 for rep in range(3):
     rc = lib.sb_profile_forward(C.byref(tgt.struct), C.byref(kv.struct), ids.data_ptr(), slots.data_ptr(), pos.data_ptr(),
