@@ -347,8 +347,10 @@ int sb_gemm_autotune_clear(void);
  * so a tuned table can be saved and replayed -- e.g. into a profiler run,
  * whose serialised timings would tune differently.  get: SB_EINVAL if absent.
  */
-int sb_gemm_tune_get(int32_t M, int32_t N, int32_t K, int32_t* cps, int32_t* splits, int32_t* weight_tiles);
-int sb_gemm_tune_set(int32_t M, int32_t N, int32_t K, int32_t cps, int32_t splits, int32_t weight_tiles);
+int sb_gemm_tune_get(int32_t M, int32_t N, int32_t K, int32_t* cps, int32_t* splits, int32_t* weight_tiles,
+                     int32_t* token_tile);
+int sb_gemm_tune_set(int32_t M, int32_t N, int32_t K, int32_t cps, int32_t splits, int32_t weight_tiles,
+                     int32_t token_tile);
 int sb_version(void);
 const char* sb_build_info(void);
 int sb_last_kernel_count(void); /* kernels launched by the last sb_decoder_forward */

@@ -548,12 +548,14 @@ int sb_gemm_autotune(const void* x, const void* w, void* y_f32, int32_t M, int32
 
 int sb_gemm_autotune_clear(void) { return gemm_tc_autotune_clear(); }
 
-int sb_gemm_tune_get(int32_t M, int32_t N, int32_t K, int32_t* cps, int32_t* splits, int32_t* weight_tiles) {
-  return gemm_tc_tune_get(M, N, K, cps, splits, weight_tiles);
+int sb_gemm_tune_get(int32_t M, int32_t N, int32_t K, int32_t* cps, int32_t* splits, int32_t* weight_tiles,
+                     int32_t* token_tile) {
+  return gemm_tc_tune_get(M, N, K, cps, splits, weight_tiles, token_tile);
 }
 
-int sb_gemm_tune_set(int32_t M, int32_t N, int32_t K, int32_t cps, int32_t splits, int32_t weight_tiles) {
-  return gemm_tc_tune_set(M, N, K, cps, splits, weight_tiles);
+int sb_gemm_tune_set(int32_t M, int32_t N, int32_t K, int32_t cps, int32_t splits, int32_t weight_tiles,
+                     int32_t token_tile) {
+  return gemm_tc_tune_set(M, N, K, cps, splits, weight_tiles, token_tile);
 }
 
 int sb_set_attention_splits(int32_t splits) {

@@ -507,7 +507,7 @@ struct TcPlan {
   size_t smem;
 };
 struct TcTuned {
-  int cps, splits, wt;
+  int cps, splits, wt, tn;  // tn 0: token tile of tn_for(M)
 };
 
 // Measured (CTAs per SM, K splits) per GEMM shape (sb_gemm_autotune, run by the
@@ -516,6 +516,7 @@ struct TcTuned {
 static std::mutex g_tuned_mu;
 static std::map<unsigned long long, TcTuned> g_tuned;
 static int g_tune_wt = 0;  // autotune candidate override (0 = plan's choice)
+static int g_tune_tn = 0;  // autotune candidate token tile (0 = tn_for(M))
 static unsigned long long tune_key(int tn, int m_tiles, int N, int K) {
   return ((unsigned long long)tn << 48) | ((unsigned long long)m_tiles << 40) | ((unsigned long long)N << 20) |
          (unsigned long long)K;
@@ -529,6 +530,7 @@ static TcPlan plan(int M, int N, int K, int epi) {
   q.tn = tn_for(M);
   q.n_tiles_n = (N + TC_BM - 1) / TC_BM;
   q.m_tiles = (M + q.tn - 1) / q.tn;
+  const unsigned long long key = tune_key(q.tn, q.m_tiles, N, K);  // tuned entries are keyed by the default tile
   q.kb = (K + TC_BK - 1) / TC_BK;
   q.ctas_per_sm = g_tune_cps ? g_tune_cps : (q.tn >= 128 ? 1 : 2);
   // cps 3 (tuning only): size the grid for ONE CTA per SM but keep the smem of
@@ -538,15 +540,22 @@ static TcPlan plan(int M, int N, int K, int epi) {
     q.ctas_per_sm = 1;
     half_smem = true;
   }
-  int tuned_splits = 0, tuned_wt = 0;
+  int tuned_splits = 0, tuned_wt = 0, tuned_tn = 0;
   if (!g_tune_cps && !g_tune_splits) {
     std::lock_guard<std::mutex> lk(g_tuned_mu);
-    auto it = g_tuned.find(tune_key(q.tn, q.m_tiles, N, K));
+    auto it = g_tuned.find(key);
     if (it != g_tuned.end()) {
       q.ctas_per_sm = it->second.cps;
       tuned_splits = it->second.splits;
       tuned_wt = it->second.wt;
+      tuned_tn = it->second.tn;
     }
+  }
+  // a narrower token tile (more, smaller CTAs: wave quantisation of the compute-bound regime)
+  const int tn_over = g_tune_tn ? g_tune_tn : tuned_tn;
+  if (tn_over >= 16 && tn_over < q.tn && tn_over % 16 == 0) {
+    q.tn = tn_over;
+    q.m_tiles = (M + q.tn - 1) / q.tn;
   }
   const int sms = num_sms();
   const int slots = sms * q.ctas_per_sm;
@@ -601,25 +610,34 @@ int gemm_tc_autotune(const void* x, const void* w, float* y, int M, int N, int K
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   float best = 1e30f;
-  int best_cps = 0, best_sp = 0, best_wt = 1, rc = 0;
+  int best_cps = 0, best_sp = 0, best_wt = 1, best_tn = 0, rc = 0;
   struct Cand {
-    int cps, sp, wt;
+    int cps, sp, wt, tn;
   };
-  Cand cands[16];
+  Cand cands[40];
   int nc = 0;
-  for (int cps = 1; cps <= 2; ++cps)
-    for (int sp = 1; sp <= 8; sp *= 2) {
-      if (sp > 1 && kb / sp < 2) break;
-      if (tiles * sp > 2 * num_sms() * cps) break;  // more than two waves: never the winner
-      cands[nc++] = {cps, sp, 1};
-    }
-  if (tn >= 64 && (N + TC_BM - 1) / TC_BM >= 2) cands[nc++] = {1, 1, 2};
+  // token tiles: the default, and for wide M the 128 / 192 tiles (more CTAs per wave)
+  int tns[3] = {0, 0, 0}, ntn = 1;
+  if (M > 128 && tn > 128) tns[ntn++] = 128;
+  if (M > 192 && tn > 192) tns[ntn++] = 192;
+  for (int ti = 0; ti < ntn; ++ti) {
+    const int tn_c = tns[ti] ? tns[ti] : tn;
+    const int tiles_c = ((N + TC_BM - 1) / TC_BM) * ((M + tn_c - 1) / tn_c);
+    for (int cps = 1; cps <= 2; ++cps)
+      for (int sp = 1; sp <= 8; sp *= 2) {
+        if (sp > 1 && kb / sp < 2) break;
+        if (tiles_c * sp > 2 * num_sms() * cps) break;  // more than two waves: never the winner
+        cands[nc++] = {cps, sp, 1, tns[ti]};
+      }
+    if (tn_c >= 64 && (N + TC_BM - 1) / TC_BM >= 2) cands[nc++] = {1, 1, 2, tns[ti]};
+  }
   for (int ci = 0; ci < nc && !rc; ++ci) {
     {
       const int cps = cands[ci].cps, sp = cands[ci].sp;
       g_tune_cps = cps;
       g_tune_splits = sp;
       g_tune_wt = cands[ci].wt;
+      g_tune_tn = cands[ci].tn;
       g_tune_stages = 0;
       rc = gemm_tc(a, st);  // warm
       if (rc) break;
@@ -636,10 +654,12 @@ int gemm_tc_autotune(const void* x, const void* w, float* y, int M, int N, int K
         best_cps = cps;
         best_sp = sp;
         best_wt = cands[ci].wt;
+        best_tn = cands[ci].tn;
       }
     }
   }
   g_tune_wt = 0;
+  g_tune_tn = 0;
   g_tune_cps = save_cps;
   g_tune_stages = save_st;
   g_tune_splits = save_sp;
@@ -648,7 +668,7 @@ int gemm_tc_autotune(const void* x, const void* w, float* y, int M, int N, int K
   if (rc) return rc;
   {
     std::lock_guard<std::mutex> lk(g_tuned_mu);
-    g_tuned[tune_key(tn, m_tiles, N, K)] = {best_cps, best_sp, best_wt};
+    g_tuned[tune_key(tn, m_tiles, N, K)] = {best_cps, best_sp, best_wt, best_tn};
   }
   if (cps_out) *cps_out = best_cps;
   if (splits_out) *splits_out = best_sp;
@@ -656,7 +676,7 @@ int gemm_tc_autotune(const void* x, const void* w, float* y, int M, int N, int K
   return 0;
 }
 
-int gemm_tc_tune_get(int M, int N, int K, int* cps, int* splits, int* wt) {
+int gemm_tc_tune_get(int M, int N, int K, int* cps, int* splits, int* wt, int* tn_out) {
   if (M <= 0 || N <= 0 || K <= 0) return SB_EINVAL;
   const int tn = tn_for(M), m_tiles = (M + tn - 1) / tn;
   std::lock_guard<std::mutex> lk(g_tuned_mu);
@@ -665,15 +685,17 @@ int gemm_tc_tune_get(int M, int N, int K, int* cps, int* splits, int* wt) {
   if (cps) *cps = it->second.cps;
   if (splits) *splits = it->second.splits;
   if (wt) *wt = it->second.wt;
+  if (tn_out) *tn_out = it->second.tn;
   return 0;
 }
 
-int gemm_tc_tune_set(int M, int N, int K, int cps, int splits, int wt) {
-  if (M <= 0 || N <= 0 || K <= 0 || cps < 1 || cps > 3 || splits < 1 || splits > 8 || wt < 1 || wt > 2)
+int gemm_tc_tune_set(int M, int N, int K, int cps, int splits, int wt, int tn_set) {
+  if (M <= 0 || N <= 0 || K <= 0 || cps < 1 || cps > 3 || splits < 1 || splits > 8 || wt < 1 || wt > 2 ||
+      tn_set < 0 || tn_set > TC_MAX_TN || tn_set % 16)
     return SB_EINVAL;
   const int tn = tn_for(M), m_tiles = (M + tn - 1) / tn;
   std::lock_guard<std::mutex> lk(g_tuned_mu);
-  g_tuned[tune_key(tn, m_tiles, N, K)] = {cps, splits, wt};
+  g_tuned[tune_key(tn, m_tiles, N, K)] = {cps, splits, wt, tn_set};
   return 0;
 }
 

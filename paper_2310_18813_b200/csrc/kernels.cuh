@@ -55,8 +55,8 @@ int gemm_tc_tune(int cps, int stages, int splits);
 int gemm_tc_autotune(const void* x, const void* w, float* y, int M, int N, int K, cudaStream_t st, int* cps_out,
                      int* splits_out, float* us_out);
 int gemm_tc_autotune_clear();
-int gemm_tc_tune_get(int M, int N, int K, int* cps, int* splits, int* wt);
-int gemm_tc_tune_set(int M, int N, int K, int cps, int splits, int wt);
+int gemm_tc_tune_get(int M, int N, int K, int* cps, int* splits, int* wt, int* tn);
+int gemm_tc_tune_set(int M, int N, int K, int cps, int splits, int wt, int tn);
 int num_sms();
 // 2-D bf16 tensor map [rows, cols] (row stride ld elements), box TC_BK x box_rows, 128B swizzle.
 int make_map(CUtensorMap* map, const void* base, int rows, int cols, int ld, int box_rows);

@@ -311,8 +311,8 @@ class Decoder:
             with open(cache) as f:
                 table = {tuple(e["key"]): e["val"] for e in json.load(f)}
             if all((T, n, k) in table for _, T, n, k, _ in shapes):
-                for (T, n, k), (cps, sp, wt) in table.items():
-                    N.call("sb_gemm_tune_set", T, n, k, cps, sp, wt)
+                for (T, n, k), (cps, sp, wt, tn) in table.items():
+                    N.call("sb_gemm_tune_set", T, n, k, cps, sp, wt, tn)
                 return {(name, T): tuple(table[(T, n, k)][:2]) + (None,) for name, T, n, k, _ in shapes}
         res = {}
         for name, T, n, k, w in shapes:
@@ -323,9 +323,9 @@ class Decoder:
                    C.byref(sp), C.byref(us))
             res[(name, T)] = (cps.value, sp.value, us.value)
             if cache:
-                wt = C.c_int32()
-                N.call("sb_gemm_tune_get", T, n, k, C.byref(cps), C.byref(sp), C.byref(wt))
-                table[(T, n, k)] = [cps.value, sp.value, wt.value]
+                wt, tn_ = C.c_int32(), C.c_int32()
+                N.call("sb_gemm_tune_get", T, n, k, C.byref(cps), C.byref(sp), C.byref(wt), C.byref(tn_))
+                table[(T, n, k)] = [cps.value, sp.value, wt.value, tn_.value]
         torch.cuda.synchronize(self.device)
         if cache:
             with open(cache, "w") as f:

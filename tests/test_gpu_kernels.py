@@ -1,6 +1,7 @@
 """GPU parity of the token-level kernels (K4 accept, K5 commit, staging, sampling)
 and of the GEMMs, through the C-ABI, against the CPU oracle / torch fp32."""
 
+import ctypes
 import numpy as np
 import pytest
 import torch
@@ -349,3 +350,33 @@ def test_gemm_uneven_cluster_splits(cuda_dev, splits):
     assert (y - (base + ref)).abs().max().item() < 1e-3
     want = torch.nn.functional.silu(ref[:, 0::2]) * ref[:, 1::2]
     assert (ya.float() - want).abs().max().item() <= 1e-2 * want.abs().max().item() + 1e-4
+
+
+@pytest.mark.parametrize("M,N_,K,cps,splits,wt,tn", [
+    (1016, 4096, 4096, 2, 1, 1, 192),   # ragged last token tile
+    (1016, 12288, 4096, 1, 1, 2, 128),  # dual weight tiles on a narrow token tile
+    (300, 4096, 11008, 2, 2, 1, 128),   # cluster split-K with a narrow token tile
+    (257, 1536, 512, 1, 1, 1, 192),
+])
+def test_gemm_tuned_token_tile(cuda_dev, M, N_, K, cps, splits, wt, tn):
+    """A tuned entry may narrow the token tile (wave quantisation of the
+    compute-bound regime, sb_gemm_tune_set): results are the same GEMM."""
+    g = torch.Generator(device=cuda_dev).manual_seed(M + N_ + K + tn)
+    x = (torch.randn(M, K, generator=g, device=cuda_dev) * 0.5).to(torch.bfloat16)
+    w = (torch.randn(N_, K, generator=g, device=cuda_dev) * 0.02).to(torch.bfloat16)
+    ref = x.float() @ w.float().T
+    lib = N.load()
+    ws = torch.zeros(int(lib.sb_gemm_workspace_bytes(M, N_, K)), device=cuda_dev, dtype=torch.uint8)
+    N.call("sb_gemm_tune_set", M, N_, K, cps, splits, wt, tn)
+    try:
+        got = [ctypes.c_int32() for _ in range(4)]
+        N.call("sb_gemm_tune_get", M, N_, K, *[ctypes.byref(v) for v in got])
+        assert [v.value for v in got] == [cps, splits, wt, tn]
+        y = torch.zeros(M, N_, device=cuda_dev)
+        N.call("sb_gemm", N.SB_BF16, x.data_ptr(), w.data_ptr(), y.data_ptr(), M, N_, K, N.EPI_STORE_F32, N.GEMM_TC,
+               ws.data_ptr(), ws.numel(), _st())
+        torch.cuda.synchronize()
+    finally:
+        lib.sb_gemm_autotune_clear()
+    err = (y - ref).abs().max().item()
+    assert err <= 1e-4 * ref.abs().max().item() + 1e-5, err
