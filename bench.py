@@ -281,7 +281,8 @@ def run_trace(args):
     for pol in [AdaptivePolicy(lut), FixedPolicy(3)]:
         rep, extra = serve_continuous(workload, eng, pol, time_scale=args.trace_scale, max_batch=16)
         cont[pol.label] = {"latency_s": round(rep.avg_latency / args.trace_scale, 4),
-                           "mean_live_batch": round(extra["mean_live_batch"], 2), "mean_k": round(extra["mean_k"], 2)}
+                           "mean_live_batch": round(extra["mean_live_batch"], 2), "mean_k": round(extra["mean_k"], 2),
+                           "riding_prefill_rows": extra["ridden_rows"], "separate_prefill_rows": extra["prefill_rows"]}
     t_run = time.perf_counter() - t_run
     fixed = {k: v for k, v in lat.items() if k.startswith("fixed")}
     best = min(fixed, key=fixed.get)

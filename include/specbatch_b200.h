@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define SB_ABI_VERSION 6
+#define SB_ABI_VERSION 7
 
 /* status codes beyond cudaError_t (which are < 1000) */
 #define SB_OK 0
@@ -193,6 +193,24 @@ int sb_decoder_forward_ex(const sb_decoder_t* m, const sb_kvcache_t* kv, const i
                           const int32_t* tok_slot, const int32_t* tok_pos, int32_t n_seq, int32_t q_len,
                           float* logits, int32_t logits_mode, const sb_token_sink_t* sink, void* workspace,
                           size_t ws_bytes, void* stream);
+
+/*
+ * Verify windows plus riding prompts in ONE forward (continuous batching:
+ * prompts admitted into freed slots are prefilled inside the next verify
+ * instead of by a separate weight stream).  tok_ids / tok_pos hold the
+ * n_seq x q_len window tokens (KV slots tok_slot[n_seq]) followed by pf_n
+ * prompts of pf_len tokens (KV slots pf_slot[pf_n]); every token shares the
+ * GEMMs, the prompts get their own attention launch and no logits: logits /
+ * sink cover the window rows exactly as sb_decoder_forward_ex.  Workspace:
+ * sb_decoder_workspace_bytes(n_seq*q_len + pf_n*pf_len).  Llama bf16
+ * (unsharded) only, else SB_EUNSUPPORTED.  Reference: the reference has no
+ * prefill; SURVEY 8(f)2 / 8(f)4.
+ */
+int sb_decoder_forward_mixed(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* tok_ids,
+                             const int32_t* tok_slot, const int32_t* tok_pos, int32_t n_seq, int32_t q_len,
+                             int32_t pf_n, int32_t pf_len, const int32_t* pf_slot, float* logits,
+                             int32_t logits_mode, const sb_token_sink_t* sink, void* workspace, size_t ws_bytes,
+                             void* stream);
 
 /*
  * Next-token selection over logits rows [rows, vocab] (fp32).

@@ -106,6 +106,8 @@ _SIGS = {
                                      C.c_size_t, _P]),
     "sb_decoder_forward_ex": (C.c_int, [C.POINTER(SbDecoder), C.POINTER(SbKVCache), _P, _P, _P, _I, _I, _P, _I,
                                         C.POINTER(SbTokenSink), _P, C.c_size_t, _P]),
+    "sb_decoder_forward_mixed": (C.c_int, [C.POINTER(SbDecoder), C.POINTER(SbKVCache), _P, _P, _P, _I, _I, _I, _I,
+                                           _P, _P, _I, C.POINTER(SbTokenSink), _P, C.c_size_t, _P]),
     "sb_select_tokens": (C.c_int, [_P, _I, _I, _I, _P, _I, _P, C.c_int64, _P, _I, _P, _P, _P, _I, _P]),
     "sb_softmax_rows": (C.c_int, [_P, _I, _I, _P, _P]),
     "sb_argmax_rows": (C.c_int, [_P, _I, _I, _P, _P]),

@@ -197,10 +197,20 @@ static int launch_attention_any(int dt, const void* qr, void* kc, void* vc, void
   return launch_attention(dt, qr, kc, vc, out, slot, pos, n_seq, q_len, nq, nkv, hd, ctx_max, st);
 }
 
+// Prompt rows riding along a verify forward (continuous batching): after the
+// n_seq x q_len window tokens, n prompts of len tokens each (their KV slots in
+// `slots`); they share every GEMM, get their own attention launch, and no logits.
+struct MixedPrefill {
+  int n, len;
+  const int32_t* slots;
+};
+
 static int forward_fused_norm(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* ids, const int32_t* slot,
                               const int32_t* pos, int n_seq, int q_len, float* logits, int logits_mode,
-                              const sb_token_sink_t* sink, const FwdWorkspace& w, cudaStream_t st) {
-  const int T = n_seq * q_len;
+                              const sb_token_sink_t* sink, const FwdWorkspace& w, cudaStream_t st,
+                              const MixedPrefill* mx = nullptr) {
+  const int Tv = n_seq * q_len;                     // window tokens (logits / sink rows)
+  const int T = Tv + (mx ? mx->n * mx->len : 0);    // every token through the GEMMs
   const int nq = m->n_heads, nkv = m->n_kv_heads, hd = m->head_dim, H = m->hidden;
   const int qkv_n = (nq + 2 * nkv) * hd;
   const size_t layer_kv = (size_t)kv->slots * nkv * kv->ctx_max * hd * 2;
@@ -225,9 +235,17 @@ static int forward_fused_norm(const sb_decoder_t* m, const sb_kvcache_t* kv, con
                                   : SB_EUNSUPPORTED;
     if (rc_fa != 0 && rc_fa != SB_EUNSUPPORTED) return rc_fa;
     if (rc_fa == SB_EUNSUPPORTED) {
-      SB_TRY(launch_rope_append(SB_BF16, w.qkv, w.qr, kc, vc, slot, pos, m->rope_cos, m->rope_sin, T, q_len, nq, nkv,
-                                hd, kv->ctx_max, m->max_pos, st));
+      SB_TRY(launch_rope_append(SB_BF16, w.qkv, w.qr, kc, vc, slot, pos, m->rope_cos, m->rope_sin, Tv, q_len, nq,
+                                nkv, hd, kv->ctx_max, m->max_pos, st));
       SB_TRY(launch_attention_any(SB_BF16, w.qr, kc, vc, w.attn, slot, pos, n_seq, q_len, nq, nkv, hd, kv->ctx_max, st));
+    }
+    if (mx && mx->n > 0) {  // the riding prompts: rotate + append, then block attention over their own slots
+      const char* qkv_p = (const char*)w.qkv + (size_t)Tv * qkv_n * 2;
+      char* attn_p = (char*)w.attn + (size_t)Tv * nq * hd * 2;
+      SB_TRY(launch_rope_append(SB_BF16, qkv_p, w.qr, kc, vc, mx->slots, pos + Tv, m->rope_cos, m->rope_sin,
+                                mx->n * mx->len, mx->len, nq, nkv, hd, kv->ctx_max, m->max_pos, st));
+      SB_TRY(launch_attention_any(SB_BF16, w.qr, kc, vc, attn_p, mx->slots, pos + Tv, mx->n, mx->len, nq, nkv, hd,
+                                  kv->ctx_max, st));
     }
     prof_mark("attn", st);
     if (m->tp) {  // row-parallel o_proj: partial -> all-reduce -> residual
@@ -273,7 +291,7 @@ static int forward_fused_norm(const sb_decoder_t* m, const sb_kvcache_t* kv, con
   }
   if (logits_mode == SB_LOGITS_NONE) return 0;
   const bool last = logits_mode == SB_LOGITS_LAST;
-  const int rows = last ? n_seq : T;
+  const int rows = last ? n_seq : Tv;
   const int step = last ? q_len : 1, off = last ? q_len - 1 : 0;
   GemmArgs g{SB_BF16, (const char*)w.xb + (size_t)off * H * 2, m->lm_head, logits, rows, m->vocab, H, step * H,
              EPI_STORE_F32, w.gemm_ws, w.gemm_ws_bytes};
@@ -357,8 +375,9 @@ static int forward_opt(const sb_decoder_t* m, const sb_kvcache_t* kv, const int3
 
 static int forward_impl(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* ids, const int32_t* slot,
                         const int32_t* pos, int n_seq, int q_len, float* logits, int logits_mode,
-                        const sb_token_sink_t* sink, void* ws, size_t ws_bytes, cudaStream_t st) {
-  const int T = n_seq * q_len;
+                        const sb_token_sink_t* sink, void* ws, size_t ws_bytes, cudaStream_t st,
+                        const MixedPrefill* mx = nullptr) {
+  const int T = n_seq * q_len + (mx ? mx->n * mx->len : 0);
   if (T <= 0 || !m || !kv) return SB_EINVAL;
   if ((m->head_dim != 128 && m->head_dim != 64) || m->n_heads % m->n_kv_heads) return SB_EUNSUPPORTED;
   FwdWorkspace w;
@@ -371,6 +390,11 @@ static int forward_impl(const sb_decoder_t* m, const sb_kvcache_t* kv, const int
   const size_t layer_kv = (size_t)kv->slots * nkv * kv->ctx_max * hd * es;
 
   prof_mark("start", st);
+  if (mx) {  // riding prompts: the fused-norm llama path only
+    if (m->arch != SB_ARCH_LLAMA || dt != SB_BF16 || m->tp || !g_fuse_norm || g_backend_override == GEMM_SIMT)
+      return SB_EUNSUPPORTED;
+    return forward_fused_norm(m, kv, ids, slot, pos, n_seq, q_len, logits, logits_mode, sink, w, st, mx);
+  }
   if (m->arch == SB_ARCH_OPT) return forward_opt(m, kv, ids, slot, pos, n_seq, q_len, logits, logits_mode, sink, w, st);
   if (m->arch != SB_ARCH_LLAMA) return SB_EINVAL;
   if (m->tp && (m->tp->world < 1 || !m->tp->all_reduce_sum || !m->tp->all_gather)) return SB_EINVAL;
@@ -462,6 +486,21 @@ int sb_decoder_forward_ex(const sb_decoder_t* m, const sb_kvcache_t* kv, const i
   if (sink && logits_mode == SB_LOGITS_NONE) return SB_EINVAL;
   int rc = forward_impl(m, kv, tok_ids, tok_slot, tok_pos, n_seq, q_len, logits, logits_mode, sink, workspace,
                         ws_bytes, (cudaStream_t)stream);
+  g_last_count = g_kernel_count;
+  return rc;
+}
+
+int sb_decoder_forward_mixed(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* tok_ids,
+                             const int32_t* tok_slot, const int32_t* tok_pos, int32_t n_seq, int32_t q_len,
+                             int32_t pf_n, int32_t pf_len, const int32_t* pf_slot, float* logits,
+                             int32_t logits_mode, const sb_token_sink_t* sink, void* workspace, size_t ws_bytes,
+                             void* stream) {
+  g_kernel_count = 0;
+  if (sink && logits_mode == SB_LOGITS_NONE) return SB_EINVAL;
+  if (n_seq < 1 || q_len < 1 || pf_n < 0 || (pf_n > 0 && (pf_len < 1 || !pf_slot))) return SB_EINVAL;
+  MixedPrefill mx{pf_n, pf_len, pf_slot};
+  int rc = forward_impl(m, kv, tok_ids, tok_slot, tok_pos, n_seq, q_len, logits, logits_mode, sink, workspace,
+                        ws_bytes, (cudaStream_t)stream, pf_n > 0 ? &mx : nullptr);
   g_last_count = g_kernel_count;
   return rc;
 }
@@ -622,7 +661,7 @@ int sb_set_pdl(int32_t enabled) {
 int sb_version(void) { return SB_ABI_VERSION; }
 
 const char* sb_build_info(void) {
-  return "specbatch_b200 abi=" "6" " arch=sm_100a tp=nccl models=llama,opt kernels=persistent_forward,layernorm,tp_resid_add,unshard_logits,embed,rmsnorm,rope_append,attention,gemm_simt,gemm_tcgen05,"
+  return "specbatch_b200 abi=" "7" " arch=sm_100a tp=nccl models=llama,opt kernels=persistent_forward,layernorm,tp_resid_add,unshard_logits,embed,rmsnorm,rope_append,attention,gemm_simt,gemm_tcgen05,"
          "argmax,softmax,select,accept,commit,prepare,kv_compact";
 }
 

@@ -364,6 +364,21 @@ class Decoder:
                N.ptr(pos), n_seq, q_len, N.ptr(logits), logits_mode, C.byref(sink), N.ptr(workspace),
                workspace.numel(), st)
 
+    def forward_mixed(self, kv: "KVCache", ids, slots, pos, n_seq: int, q_len: int, pf_n: int, pf_len: int, pf_slots,
+                      logits, logits_mode: int, workspace, sink: "N.SbTokenSink | None" = None, stream=None) -> int:
+        """Verify windows (n_seq x q_len tokens) plus pf_n riding prompts of pf_len
+        tokens in one forward (sb_decoder_forward_mixed): ``ids`` / ``pos`` hold the
+        window tokens followed by the prompt tokens.  Returns 0, or SB_EUNSUPPORTED
+        when this decoder has no mixed path (caller prefills separately)."""
+        st = torch.cuda.current_stream(self.device).cuda_stream if stream is None else stream
+        rc = N.load().sb_decoder_forward_mixed(C.byref(self.struct), C.byref(kv.struct), N.ptr(ids), N.ptr(slots),
+                                               N.ptr(pos), n_seq, q_len, pf_n, pf_len, N.ptr(pf_slots), N.ptr(logits),
+                                               logits_mode, C.byref(sink) if sink is not None else None,
+                                               N.ptr(workspace), workspace.numel(), st)
+        if rc not in (0, N.SB_EUNSUPPORTED):
+            N.check("sb_decoder_forward_mixed", rc)
+        return rc
+
     def weight_bytes(self) -> int:
         return self.cfg.streamed_bytes_per_forward(2 if self.dtype_name == "bf16" else 4)
 

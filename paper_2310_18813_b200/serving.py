@@ -35,7 +35,7 @@ __all__ = ["serve_continuous"]
 
 def serve_continuous(workload: list[Request], engine, policy, time_scale: float = 1.0, max_batch: int | None = None,
                      group_size: int = 40, clock=None, collect: bool = False, min_admit: int = 1,
-                     max_wait: float = 0.0) -> tuple[SimulationReport, dict]:
+                     max_wait: float = 0.0, riding: bool | None = None) -> tuple[SimulationReport, dict]:
     """Serve `workload` with continuous batching on `engine` (a SpecEngine).
 
     `policy.decide(b)` picks k at every iteration for the live batch size b
@@ -44,6 +44,10 @@ def serve_continuous(workload: list[Request], engine, policy, time_scale: float 
     one request at a time is expensive; new requests join only when at least
     `min_admit` can (or the engine is idle, or the oldest has waited
     `max_wait` wall seconds).
+    Prefill: with ``riding`` (default: whenever the engine supports it) prompts
+    admitted while other rows decode are prefilled INSIDE the next iteration's
+    verify forward (sb_decoder_forward_mixed, one weight stream) and decode from
+    the iteration after; otherwise each admission runs its own prefill forward.
     Returns (report, {"mean_live_batch", "mean_k", "iterations"[, "outputs": {id: tokens}]}).
     """
     if any(nxt.arrival < cur.arrival for cur, nxt in zip(workload, workload[1:])):
@@ -68,7 +72,12 @@ def serve_continuous(workload: list[Request], engine, policy, time_scale: float 
     k_hist: list[int] = []
     b_hist: list[int] = []
     outputs: dict[int, list[int]] = {}
-    prof = {"prefills": 0, "prefill_rows": 0, "prefill_s": 0.0, "iter_s": 0.0, "host_s": 0.0, "idle_s": 0.0}
+    prof = {"prefills": 0, "prefill_rows": 0, "ridden_rows": 0, "prefill_s": 0.0, "iter_s": 0.0, "host_s": 0.0,
+            "idle_s": 0.0}
+    if riding is None:
+        riding = getattr(eng, "supports_ride", False)
+    elif riding and not getattr(eng, "supports_ride", False):
+        raise ValueError("this engine's target has no riding-prefill path (llama bf16 unsharded only)")
     with torch.cuda.stream(eng.stream):
         eng.iter.zero_()
         eng.finish_iter.fill_(-1)
@@ -99,6 +108,7 @@ def serve_continuous(workload: list[Request], engine, policy, time_scale: float 
                 pinned_prompts[len(new_rows)].copy_(torch.from_numpy(np.asarray(eng.prompt_fn(r.id), dtype=np.int32)))
                 new_rows.append(row)
             b = len(row_req)
+            b_run, ride = b, 0  # rows this iteration decodes / prompts riding along its verify
             if new_rows:
                 r0, n = new_rows[0], len(new_rows)  # admitted rows are contiguous at the end
                 eng.tokens[r0:r0 + n, :P].copy_(pinned_prompts[:n], non_blocking=True)
@@ -107,19 +117,28 @@ def serve_continuous(workload: list[Request], engine, policy, time_scale: float 
                 eng.finish_iter[r0:r0 + n].fill_(-1)
                 eng.target_len[r0:r0 + n].copy_(torch.tensor([row_req[i].gen_len for i in new_rows], dtype=torch.int32))
                 eng.slots[:b].copy_(torch.tensor(slot_of_row, dtype=torch.int32))
-                tp = clock()
-                _prefill_rows(eng, new_rows)
-                eng.stream.synchronize()  # pinned staging rows are reused next admission
-                prof["prefill_s"] += clock() - tp
-                prof["prefills"] += 1
-                prof["prefill_rows"] += len(new_rows)
+                if riding and r0 > 0 and n <= eng.pf_chunk:
+                    # chunked prefill: the prompts ride inside the next verify forward
+                    # (one weight stream for both) and decode from the iteration after
+                    b_run, ride = r0, n
+                    prof["ridden_rows"] += n
+                else:
+                    tp = clock()
+                    _prefill_rows(eng, new_rows)
+                    eng.stream.synchronize()  # pinned staging rows are reused next admission
+                    prof["prefill_s"] += clock() - tp
+                    prof["prefills"] += 1
+                    prof["prefill_rows"] += len(new_rows)
             # ---- one speculative iteration at the LUT's k for the live batch size
-            k = policy.decide(b).chosen_s
+            k = policy.decide(b_run).chosen_s
             k = min(k, eng.max_k)
             ti = clock()
-            eng._graph(b, k).replay() if eng.use_graphs else eng._iteration(b, k)
+            if ride:
+                eng._iteration(b_run, k, ride=ride)
+            else:
+                eng._graph(b, k).replay() if eng.use_graphs else eng._iteration(b, k)
             k_hist.append(k)
-            b_hist.append(b)
+            b_hist.append(b_run)
             # ---- retirement: rows whose produced reached target_len
             done = (eng.produced[:b] >= eng.target_len[:b]).to(torch.int32)
             done_host[:b].copy_(done, non_blocking=True)

@@ -128,7 +128,13 @@ class SpecEngine:
         self.pf_pos = torch.zeros(pf_tok, **i32)
         self._pf_pos_pattern = torch.arange(max(1, prompt_len - 1), **i32).repeat(self.pf_chunk)
         self.pf_slots = torch.zeros(max(B, self.pf_chunk), **i32)  # KV slots of rows being prefilled (serving.py)
-        ws = max(target.workspace_bytes(B * (K + 1)), target.workspace_bytes(pf_tok))
+        # (B(k+1) window tokens + one prefill chunk riding along: serving.serve_continuous)
+        ws = max(target.workspace_bytes(B * (K + 1) + pf_tok), target.workspace_bytes(pf_tok))
+        # riding prefill (sb_decoder_forward_mixed): the fused-norm llama bf16 path, unsharded
+        self.supports_ride = (target.sb_dtype == N.SB_BF16 and target.cfg.arch == "llama" and not target.is_tp
+                              and prompt_len > 1)
+        self.mix_ids = torch.zeros(B * (K + 1) + pf_tok, **i32)
+        self.mix_pos = torch.zeros(B * (K + 1) + pf_tok, **i32)
         if draft is not None:
             ws = max(ws, draft.workspace_bytes(2 * B), draft.workspace_bytes(pf_tok))
         self.workspace = torch.zeros(ws, device=self.dev, dtype=torch.uint8)
@@ -154,9 +160,22 @@ class SpecEngine:
         return rng.integers(0, self.V, size=self.prompt_len, dtype=np.int64).astype(np.int32)
 
     # ------------------------------------------------------------- one iteration
-    def _iteration(self, b: int, k: int) -> None:
+    def _iteration(self, b: int, k: int, ride: int = 0) -> None:
+        """One speculative iteration over rows [0, b).  ``ride`` > 0 (eager only):
+        rows [b, b + ride) hold freshly admitted prompts whose target prefill rides
+        inside this iteration's verify forward (sb_decoder_forward_mixed) and whose
+        draft prefill runs alongside; they join the next iteration."""
         st = torch.cuda.current_stream(self.dev).cuda_stream
         lib = N.load()
+        q_pf = self.prompt_len - 1
+        if ride:
+            if q_pf < 1 or ride > self.pf_chunk or b + ride > self.max_batch:
+                raise ValueError("riding prompts exceed the prefill chunk / batch capacity")
+            self.pf_ids[: ride * q_pf].copy_(self.tokens[b:b + ride, :q_pf].reshape(-1))
+            self.pf_pos[: ride * q_pf].copy_(self._pf_pos_pattern[: ride * q_pf])
+            if self.draft is not None:
+                self.draft.forward(self.kv_d, self.pf_ids, self.slots[b:], self.pf_pos, ride, q_pf, None,
+                                   N.LOGITS_NONE, self.workspace, st)
         launches = 3  # prepare, accept, commit (+ softmax in stochastic mode)
         V = self.V
         mode = self.mode_id
@@ -207,7 +226,21 @@ class SpecEngine:
                        probs, k * V, self.v_ids.data_ptr() + j * 4, k + 1, N.ptr(self.ds_ids),
                        N.ptr(self.ds_pos), N.ptr(self.d_base), j, st)
         T = b * (k + 1)
-        if sample:
+        if ride:  # window tokens, then the riding prompts, in one token list
+            Tp = ride * q_pf
+            self.mix_ids[:T].copy_(self.v_ids[:T])
+            self.mix_pos[:T].copy_(self.v_pos[:T])
+            self.mix_ids[T:T + Tp].copy_(self.pf_ids[:Tp])
+            self.mix_pos[T:T + Tp].copy_(self.pf_pos[:Tp])
+            sink = None if sample else N.SbTokenSink(self.t_tok.data_ptr(), 1, None, None, None, 0)
+            rc = self.target.forward_mixed(self.kv_t, self.mix_ids, self.slots, self.mix_pos, b, k + 1, ride, q_pf,
+                                           self.slots[b:], self.t_logits if (sample or need_logits) else None,
+                                           N.LOGITS_ALL, self.workspace, sink, st)
+            if rc != 0:
+                raise N.NativeError("sb_decoder_forward_mixed", rc, "unsupported configuration")
+            if sample:
+                N.call("sb_softmax_rows", N.ptr(self.t_logits), T, V, N.ptr(self.t_logits), st)
+        elif sample:
             self.target.forward(self.kv_t, self.v_ids, self.slots, self.v_pos, b, k + 1, self.t_logits,
                                 N.LOGITS_ALL, self.workspace, st)
             launches += lib.sb_last_kernel_count()
@@ -220,7 +253,8 @@ class SpecEngine:
                                        self.t_logits if need_logits else None, N.LOGITS_ALL, self.workspace, sink,
                                        st)
             launches += lib.sb_last_kernel_count()
-        self._iter_kernels[(b, k)] = launches
+        if not ride:
+            self._iter_kernels[(b, k)] = launches
         u_base = self.uniforms.data_ptr()
         N.call("sb_accept", mode, b, k, V, N.ptr(self.t_tok), N.ptr(self.t_logits),
                N.ptr(self.q_probs) if sample and k > 0 else None, self.v_ids.data_ptr() + 4, k + 1,

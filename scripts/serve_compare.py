@@ -29,8 +29,8 @@ out = {}
 rep = serve_wallclock(wl, ServerConfig(policy=pol, max_batch=16), eng, time_scale=scale)
 out["formed"] = rep.avg_latency / scale
 print("formed", out["formed"], flush=True)
-for ma, mw in [(1, 0.0)]:
-    rep, ex = serve_continuous(wl, eng, pol, time_scale=scale, max_batch=16, min_admit=ma, max_wait=mw)
-    out[f"cont_min{ma}_wait{mw}"] = (rep.avg_latency / scale, ex)
-    print(ma, mw, out[f"cont_min{ma}_wait{mw}"], flush=True)
+for riding in (True, False):
+    rep, ex = serve_continuous(wl, eng, pol, time_scale=scale, max_batch=16, riding=riding)
+    out[f"cont_riding{int(riding)}"] = (rep.avg_latency / scale, ex)
+    print("riding", riding, out[f"cont_riding{int(riding)}"], flush=True)
 print("SUMMARY " + json.dumps(out))
