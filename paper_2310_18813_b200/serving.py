@@ -78,6 +78,8 @@ def serve_continuous(workload: list[Request], engine, policy, time_scale: float 
         riding = getattr(eng, "supports_ride", False)
     elif riding and not getattr(eng, "supports_ride", False):
         raise ValueError("this engine's target has no riding-prefill path (llama bf16 unsharded only)")
+    if riding:
+        eng.tune_riding()  # plans for the mixed token counts (outside the timed replay)
     with torch.cuda.stream(eng.stream):
         eng.iter.zero_()
         eng.finish_iter.fill_(-1)

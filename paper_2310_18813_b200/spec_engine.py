@@ -145,6 +145,7 @@ class SpecEngine:
         self._sinks: list = []  # keep ctypes sink structs alive while graphs reference their contents
         self.stats = IterationStats()
         self.tuning = {}
+        self.autotune = autotune
         if autotune:
             # measured GEMM configurations for every token count the target verify
             # can present (b(k+1) rows, b rows for the lm_head); must precede graph capture
@@ -263,6 +264,17 @@ class SpecEngine:
         N.call("sb_kv_commit", b, k, N.ptr(self.advanced), N.ptr(self.accepted), N.ptr(self.out_tok),
                N.ptr(self.tokens), self.cap, N.ptr(self.n_tok), N.ptr(self.produced), N.ptr(self.target_len),
                N.ptr(self.finish_iter), N.ptr(self.iter), N.ptr(self.live), N.ptr(self.acc_log), self.log_cap, st)
+
+    def tune_riding(self) -> None:
+        """Measure GEMM plans for the token counts of riding-prefill iterations
+        (b(k+1) window tokens + n prompts), once; call outside graph capture."""
+        if getattr(self, "_ride_tuned", False) or not self.supports_ride or not self.autotune:
+            return
+        q = self.prompt_len - 1
+        B, K = self.max_batch, self.max_k
+        Ts = {b * (k + 1) + n * q for b in range(1, B) for k in range(K + 1) for n in range(1, min(B - b, self.pf_chunk) + 1)}
+        self.tuning["target_riding"] = self.target.autotune(Ts)
+        self._ride_tuned = True
 
     def kernels_per_iteration(self, b: int, k: int) -> int:
         """Native kernel launches in one (b, k) iteration, as counted while it was
