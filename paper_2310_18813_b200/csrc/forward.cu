@@ -661,8 +661,9 @@ int sb_set_pdl(int32_t enabled) {
 int sb_version(void) { return SB_ABI_VERSION; }
 
 const char* sb_build_info(void) {
-  return "specbatch_b200 abi=" "7" " arch=sm_100a tp=nccl models=llama,opt kernels=persistent_forward,layernorm,tp_resid_add,unshard_logits,embed,rmsnorm,rope_append,attention,gemm_simt,gemm_tcgen05,"
-         "argmax,softmax,select,accept,commit,prepare,kv_compact";
+  return "specbatch_b200 abi=" "7" " arch=sm_100a tp=nccl models=llama,opt kernels=gemm_tcgen05,attention_tc(decode,"
+         "prefill_blocks),rope_append_vec,embed_norm,layernorm,tp_resid_add,unshard_logits,argmax,softmax,select,accept,"
+         "commit,prepare,kv_compact,draft_loop,persistent_forward,gemm_simt,attention_simt,rmsnorm forward=verify,mixed";
 }
 
 int sb_last_kernel_count(void) { return g_last_count; }
