@@ -283,7 +283,7 @@ class Decoder:
                        down=(H, cfg.ffn, lay["w_down"]))
         return out
 
-    def autotune(self, token_counts, stream=None) -> dict:
+    def autotune(self, token_counts, stream=None, skip=()) -> dict:
         """Measure the tcgen05 GEMM configuration of every projection for the
         token tiles `token_counts` will use (sb_gemm_autotune); later forwards --
         and graphs captured after this -- use the fastest.  bf16 only; returns
@@ -304,7 +304,7 @@ class Decoder:
             if bucket in seen:
                 continue
             seen.add(bucket)
-            shapes += [(name, T, n, k, w) for name, (n, k, w) in self.gemm_shapes().items()]
+            shapes += [(name, T, n, k, w) for name, (n, k, w) in self.gemm_shapes().items() if name not in skip]
         cache = os.environ.get("SB_TUNE_CACHE")
         table = {}
         if cache and os.path.exists(cache):
