@@ -39,6 +39,7 @@ constexpr int TC_MAX_TN = 256;
 
 
 struct TcParams {
+  int k_rot;      // rotate each CTA's k-block order by tile (spreads the shared token-tile reads over L2)
   int m_fast;     // raster: 1 = the m-tiles of one weight tile are adjacent CTAs (grid.x), 0 = grid.y
   int m_tiles;
   int M, N, K;
@@ -179,22 +180,27 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       // programmatic-dependency wait: under PDL the weight stream of this GEMM
       // overlaps the tail of the kernel that produces its activations.
       const int pre = nkb < p.stages ? nkb : p.stages;
+      // single token tile (decode): every CTA reads the same X k-block at the same time -> rotate
+      // each weight tile's k order to spread those reads over L2 (several token tiles share the
+      // weight tile instead: keep their k order aligned so the weight stream hits L2)
+      const int rot = (p.k_rot && p.m_tiles == 1) ? (int)((tile_n * 7u) % (unsigned)nkb) : 0;
+      auto kb_of = [&](int i) { const int j = i + rot; return kb0 + (j >= nkb ? j - nkb : j); };
       for (int i = 0; i < pre; ++i) {
         uint8_t* sa = stage_base + i * stage_bytes;
         mbar_expect_tx(&full[i], stage_bytes);
-        tma_load_2d(sa, &map_w, &full[i], (kb0 + i) * TC_BK, n0);
+        tma_load_2d(sa, &map_w, &full[i], kb_of(i) * TC_BK, n0);
       }
       griddep_wait();
       for (int i = 0; i < pre; ++i)
-        tma_load_2d(stage_base + i * stage_bytes + a_bytes, &map_x, &full[i], (kb0 + i) * TC_BK, m0);
+        tma_load_2d(stage_base + i * stage_bytes + a_bytes, &map_x, &full[i], kb_of(i) * TC_BK, m0);
       int stage = pre % p.stages;
       uint32_t phase = (pre == p.stages) ? 1u : 0u;
       for (int i = pre; i < nkb; ++i) {
         mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* sa = stage_base + stage * stage_bytes;
         mbar_expect_tx(&full[stage], stage_bytes);
-        tma_load_2d(sa, &map_w, &full[stage], (kb0 + i) * TC_BK, n0);
-        tma_load_2d(sa + a_bytes, &map_x, &full[stage], (kb0 + i) * TC_BK, m0);
+        tma_load_2d(sa, &map_w, &full[stage], kb_of(i) * TC_BK, n0);
+        tma_load_2d(sa + a_bytes, &map_x, &full[stage], kb_of(i) * TC_BK, m0);
         if (++stage == p.stages) {
           stage = 0;
           phase ^= 1;
@@ -780,6 +786,12 @@ int gemm_tc(const GemmArgs& a, cudaStream_t st) {
     m_fast = e ? atoi(e) : 1;  // measured: prefill 21.9 -> 21.4 ms, T=288 verify 10.7 -> 10.4 ms
   }
   p.m_fast = m_fast && q.m_tiles > 1;
+  static int k_rot = -1;  // env SB_GEMM_KROT
+  if (k_rot < 0) {
+    const char* e = getenv("SB_GEMM_KROT");
+    k_rot = e ? atoi(e) : 1;  // measured: verify b=8,k=3 3.41 -> 3.35 ms, b=16,k=3 4.40 -> 4.30 ms
+  }
+  p.k_rot = k_rot;
   p.m_tiles = q.m_tiles;
   cfg.gridDim = p.m_fast ? dim3((q.n_tiles_n + q.wt - 1) / q.wt * q.splits * q.m_tiles, 1, 1)
                          : dim3((q.n_tiles_n + q.wt - 1) / q.wt * q.splits, q.m_tiles, 1);

@@ -14,7 +14,7 @@ cfg = CONFIGS["llama-2-7b"]
 from dataclasses import replace
 tgt = Decoder(replace(cfg, n_layers=layers), dtype="bf16", device=dev, init="device", max_pos=320)
 drf = Decoder(CONFIGS["llama-68m"], dtype="bf16", device=dev, seed=1, init="device", max_pos=320)
-eng = SpecEngine(tgt, drf, mode="injected", acceptance=example_trace(), max_batch=max(8, b), max_k=8, prompt_len=128, max_new=128)
+eng = SpecEngine(tgt, drf, mode="injected", acceptance=example_trace(), max_batch=max(8, b), max_k=max(8, k), prompt_len=128, max_new=128)
 _stage_context(eng, b, k, 192)
 for i in range(int(os.environ.get("PREPS", "3"))):
     tgt.forward(eng.kv_t, eng.v_ids, eng.slots, eng.v_pos, b, k + 1, eng.t_logits, N.LOGITS_ALL, eng.workspace)

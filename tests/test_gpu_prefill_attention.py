@@ -52,4 +52,7 @@ def test_prefill_tc_attention_matches_simt(cuda_dev, cfg, b, q_len):
     ref, got = outs
     rel = np.abs(got - ref).max() / np.abs(ref).max()
     assert rel < 2e-2, rel
-    assert (got.argmax(-1) == ref.argmax(-1)).mean() > 0.98
+    # argmax agreement except at near-ties (random-init logits: top-2 gaps within bf16 noise)
+    srt = np.sort(ref, axis=-1)
+    clear = (srt[:, -1] - srt[:, -2]) > 2e-2 * np.abs(ref).max()
+    assert (got.argmax(-1) == ref.argmax(-1))[clear].all()
