@@ -390,6 +390,14 @@ static int forward_impl(const sb_decoder_t* m, const sb_kvcache_t* kv, const int
   const size_t layer_kv = (size_t)kv->slots * nkv * kv->ctx_max * hd * es;
 
   prof_mark("start", st);
+  // weights that cannot stay in L2 (the target) stream evict-first, so a model
+  // that can (the draft, re-run every step) keeps its weights resident
+  {
+    const size_t wbytes = (size_t)m->n_layers *
+                              ((size_t)qkv_n * H + (size_t)H * nq * hd + 3ull * m->ffn * H) * es +
+                          (size_t)m->vocab * H * es;
+    g_w_l2_hint = wbytes > (size_t)(256u << 20) ? 1 : 2;
+  }
   if (mx) {  // riding prompts: the fused-norm llama path only
     if (m->arch != SB_ARCH_LLAMA || dt != SB_BF16 || m->tp || !g_fuse_norm || g_backend_override == GEMM_SIMT)
       return SB_EUNSUPPORTED;

@@ -39,6 +39,7 @@ constexpr int TC_MAX_TN = 256;
 
 
 struct TcParams {
+  int w_hint;  // L2 policy of the weight stream: 0 default, 1 evict-first, 2 evict-last
   int k_rot;      // rotate each CTA's k-block order by tile (spreads the shared token-tile reads over L2)
   int m_fast;     // raster: 1 = the m-tiles of one weight tile are adjacent CTAs (grid.x), 0 = grid.y
   int m_tiles;
@@ -184,11 +185,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       // each weight tile's k order to spread those reads over L2 (several token tiles share the
       // weight tile instead: keep their k order aligned so the weight stream hits L2)
       const int rot = (p.k_rot && p.m_tiles == 1) ? (int)((tile_n * 7u) % (unsigned)nkb) : 0;
+      const uint64_t wpol = p.w_hint == 2 ? l2_policy_evict_last() : l2_policy_evict_first();
       auto kb_of = [&](int i) { const int j = i + rot; return kb0 + (j >= nkb ? j - nkb : j); };
       for (int i = 0; i < pre; ++i) {
         uint8_t* sa = stage_base + i * stage_bytes;
         mbar_expect_tx(&full[i], stage_bytes);
-        tma_load_2d(sa, &map_w, &full[i], kb_of(i) * TC_BK, n0);
+        if (p.w_hint) tma_load_2d_hint(sa, &map_w, &full[i], kb_of(i) * TC_BK, n0, wpol);
+        else tma_load_2d(sa, &map_w, &full[i], kb_of(i) * TC_BK, n0);
       }
       griddep_wait();
       for (int i = 0; i < pre; ++i)
@@ -199,7 +202,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         mbar_wait(&empty[stage], phase ^ 1);
         uint8_t* sa = stage_base + stage * stage_bytes;
         mbar_expect_tx(&full[stage], stage_bytes);
-        tma_load_2d(sa, &map_w, &full[stage], kb_of(i) * TC_BK, n0);
+        if (p.w_hint) tma_load_2d_hint(sa, &map_w, &full[stage], kb_of(i) * TC_BK, n0, wpol);
+        else tma_load_2d(sa, &map_w, &full[stage], kb_of(i) * TC_BK, n0);
         tma_load_2d(sa + a_bytes, &map_x, &full[stage], kb_of(i) * TC_BK, m0);
         if (++stage == p.stages) {
           stage = 0;
@@ -528,6 +532,7 @@ static std::mutex g_tuned_mu;
 static std::map<unsigned long long, TcTuned> g_tuned;
 static int g_tune_wt = 0;  // autotune candidate override (0 = plan's choice)
 static int g_tune_tn = 0;  // autotune candidate token tile (0 = tn_for(M))
+int g_w_l2_hint = 0;       // set per forward: large models stream weights evict-first, small ones keep them
 static unsigned long long tune_key(int tn, int m_tiles, int N, int K) {
   return ((unsigned long long)tn << 48) | ((unsigned long long)m_tiles << 40) | ((unsigned long long)N << 20) |
          (unsigned long long)K;
@@ -792,6 +797,12 @@ int gemm_tc(const GemmArgs& a, cudaStream_t st) {
     k_rot = e ? atoi(e) : 1;  // measured: verify b=8,k=3 3.41 -> 3.35 ms, b=16,k=3 4.40 -> 4.30 ms
   }
   p.k_rot = k_rot;
+  static int w_hint_env = -2;  // env SB_GEMM_W_L2HINT overrides the forward's choice (0/1/2)
+  if (w_hint_env == -2) {
+    const char* e = getenv("SB_GEMM_W_L2HINT");
+    w_hint_env = e ? atoi(e) : -1;
+  }
+  p.w_hint = w_hint_env >= 0 ? w_hint_env : g_w_l2_hint;
   p.m_tiles = q.m_tiles;
   cfg.gridDim = p.m_fast ? dim3((q.n_tiles_n + q.wt - 1) / q.wt * q.splits * q.m_tiles, 1, 1)
                          : dim3((q.n_tiles_n + q.wt - 1) / q.wt * q.splits, q.m_tiles, 1);

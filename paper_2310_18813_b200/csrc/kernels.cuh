@@ -58,6 +58,7 @@ int gemm_tc_autotune_clear();
 int gemm_tc_tune_get(int M, int N, int K, int* cps, int* splits, int* wt, int* tn);
 int gemm_tc_tune_set(int M, int N, int K, int cps, int splits, int wt, int tn);
 int num_sms();
+extern int g_w_l2_hint;  // weight-stream L2 policy for the GEMMs of the running forward
 // 2-D bf16 tensor map [rows, cols] (row stride ld elements), box TC_BK x box_rows, 128B swizzle.
 int make_map(CUtensorMap* map, const void* base, int rows, int cols, int ld, int box_rows);
 
