@@ -54,6 +54,7 @@ struct AttnArgs {
   // window already in the cache; CTA z takes tokens [z*q_blk, (z+1)*q_blk)
   const __nv_bfloat16* qr;
   int q_blk;
+  int kv_evict_first;  // KV history streamed with an L2 evict-first policy (the target's cache)
 };
 struct AttnShared {
   int qpos[16], qtok[16], qhead[16];
@@ -129,6 +130,8 @@ __device__ __forceinline__ void attn_tc_item(const AttnArgs& A, int kvh, int seq
   // forward's window rows (the append below writes them straight into the
   // stage), so every resident tile -- window tile included -- can be requested
   // before the programmatic-dependency wait.
+  uint64_t kvpol = 0;
+  if (A.kv_evict_first) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(kvpol));
   auto issue = [&](int tile, bool hist) {
     if (tile < n_tiles) {
       uint8_t* st = ring + ((tile - t_lo) % kTcStages) * (uint32_t)SM::stage;
@@ -149,8 +152,13 @@ __device__ __forceinline__ void attn_tc_item(const AttnArgs& A, int kvh, int seq
           if (check && key >= wmin)
             for (int q = 0; q < q_len; ++q) win |= wpos[q] == key;
           if (!win) {
-            cp_async16(Kd + j * RPP * RS, ks + (size_t)j * RPP * HD);
-            cp_async16(Vd + j * RPP * RS, vs + (size_t)j * RPP * HD);
+            if (A.kv_evict_first) {
+              cp_async16_hint(Kd + j * RPP * RS, ks + (size_t)j * RPP * HD, kvpol);
+              cp_async16_hint(Vd + j * RPP * RS, vs + (size_t)j * RPP * HD, kvpol);
+            } else {
+              cp_async16(Kd + j * RPP * RS, ks + (size_t)j * RPP * HD);
+              cp_async16(Vd + j * RPP * RS, vs + (size_t)j * RPP * HD);
+            }
           }
         } else {  // rows past the context: zeros (P is 0 there, and 0 * stale NaN would poison P.V)
           *reinterpret_cast<uint4*>(Kd + j * RPP * RS) = make_uint4(0, 0, 0, 0);

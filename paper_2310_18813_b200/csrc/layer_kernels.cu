@@ -530,6 +530,16 @@ int launch_attention(int dtype, const void* q, const void* kc, const void* vc, v
 // rotated K / V rows to the cache (this CTA is the only reader of its slab).
 constexpr int kTcStages = 3;
 int g_attn_splits = 1;  // 1 off (default: measured +10% slower at b=1..8), 0 auto, n forced (sb_set_attention_splits)
+// KV loads of a model whose weights stream evict-first (the target) are evict-first too
+// (env SB_ATTN_KV_L2HINT=0/1 overrides)
+static int g_kv_l2_hint() {
+  static int env = -2;
+  if (env == -2) {
+    const char* e = getenv("SB_ATTN_KV_L2HINT");
+    env = e ? atoi(e) : -1;
+  }
+  return env >= 0 ? env : (g_w_l2_hint == 1 ? 1 : 0);
+}
 int g_attn_l2pf = -1;   // -1: from env SB_ATTN_L2PF (default off)
 
 int g_attn_stages = -1;  // ring stages (3, 4 or 6) when the grid fits one CTA per SM: -1 env SB_ATTN_STAGES
@@ -650,7 +660,7 @@ int launch_attention_tc(const void* qkv, void* kc, void* vc, void* out, const in
                scratch ? scratch->counter : nullptr};
   AttnArgs A{(const __nv_bfloat16*)qkv, (__nv_bfloat16*)kc, (__nv_bfloat16*)vc, (__nv_bfloat16*)out, tok_slot, tok_pos,
              cosT, sinT, q_len, nq, nkv, ctx_max, max_pos, scale, sp, (const char*)l2_next,
-             l2_next ? (unsigned long long)l2_next_bytes : 0ull, nullptr, 0};
+             l2_next ? (unsigned long long)l2_next_bytes : 0ull, nullptr, 0, g_kv_l2_hint()};
   return launch_attn_grid(A, hd, n_seq, splits, st);
 }
 
@@ -665,7 +675,7 @@ int launch_attention_tc_prefill(const void* qr, void* kc, void* vc, void* out, c
   if (nblk > 65535) return SB_EUNSUPPORTED;
   AttnArgs A{nullptr, (__nv_bfloat16*)kc, (__nv_bfloat16*)vc, (__nv_bfloat16*)out, tok_slot, tok_pos, nullptr, nullptr,
              q_len, nq, nkv, ctx_max, 1, 1.0f / sqrtf((float)hd), AttnSplit{nullptr, nullptr, nullptr}, nullptr, 0ull,
-             (const __nv_bfloat16*)qr, q_blk};
+             (const __nv_bfloat16*)qr, q_blk, g_kv_l2_hint()};
   return launch_attn_grid(A, hd, n_seq, nblk, st);
 }
 
