@@ -675,7 +675,7 @@ int launch_attention_tc_prefill(const void* qr, void* kc, void* vc, void* out, c
   if (nblk > 65535) return SB_EUNSUPPORTED;
   AttnArgs A{nullptr, (__nv_bfloat16*)kc, (__nv_bfloat16*)vc, (__nv_bfloat16*)out, tok_slot, tok_pos, nullptr, nullptr,
              q_len, nq, nkv, ctx_max, 1, 1.0f / sqrtf((float)hd), AttnSplit{nullptr, nullptr, nullptr}, nullptr, 0ull,
-             (const __nv_bfloat16*)qr, q_blk, g_kv_l2_hint()};
+             (const __nv_bfloat16*)qr, q_blk, 0};  // (the L2 hint faulted here on wide-GQA blocks: off)
   return launch_attn_grid(A, hd, n_seq, nblk, st);
 }
 
