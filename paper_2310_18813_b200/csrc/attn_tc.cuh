@@ -1,6 +1,6 @@
-// Tensor-core flash-decoding attention item (K3), shared by the standalone
-// attention kernel (layer_kernels.cu) and the qkv GEMM with fused attention
-// (gemm_tc.cu).
+// Tensor-core flash-decoding attention item (K3): the body of
+// attention_tc_kernel (layer_kernels.cu) for speculative windows (RoPE + KV
+// append fused) and, in block mode, for prefill-sized windows.
 #pragma once
 #include <climits>
 
@@ -63,8 +63,7 @@ struct AttnShared {
 };
 
 // One (kv head, sequence[, key split]) item on 128 threads (tid 0..127, named
-// barrier 1): the body of attention_tc_kernel, also run inside the qkv GEMM
-// (gemm_tc.cu) when attention is fused into its epilogue.  `pdl`: issue the
+// barrier 1): the body of attention_tc_kernel.  `pdl`: issue the
 // KV-history tiles, then griddepcontrol.wait / launch_dependents.
 template <int HD, int STAGES>
 __device__ __forceinline__ void attn_tc_item(const AttnArgs& A, int kvh, int seq, int split, int n_splits,
