@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define SB_ABI_VERSION 7
+#define SB_ABI_VERSION 8
 
 /* status codes beyond cudaError_t (which are < 1000) */
 #define SB_OK 0
@@ -360,6 +360,9 @@ int sb_gemm_tune(int32_t ctas_per_sm, int32_t max_stages, int32_t splits);
 int sb_gemm_autotune(const void* x, const void* w, void* y_f32, int32_t M, int32_t N, int32_t K, void* stream,
                      int32_t* cps_out, int32_t* splits_out, float* us_out);
 int sb_gemm_autotune_clear(void);
+/* L2 policy of the weight stream for the next sb_gemm / sb_gemm_autotune calls (0 default, 1 evict-first,
+ * 2 evict-last); every decoder forward sets its own (large models evict-first, small ones evict-last). */
+int sb_set_weight_l2_hint(int32_t hint);
 /*
  * Read / write one entry of the measured table (key: the token tile of M, N, K)
  * so a tuned table can be saved and replayed -- e.g. into a profiler run,

@@ -94,6 +94,7 @@ _SIGS = {
     "sb_gemm_tune": (C.c_int, [_I, _I, _I]),
     "sb_gemm_autotune": (C.c_int, [_P, _P, _P, _I, _I, _I, _P, C.POINTER(_I), C.POINTER(_I), C.POINTER(C.c_float)]),
     "sb_gemm_autotune_clear": (C.c_int, []),
+    "sb_set_weight_l2_hint": (C.c_int, [_I]),
     "sb_gemm_tune_get": (C.c_int, [_I, _I, _I, C.POINTER(_I), C.POINTER(_I), C.POINTER(_I), C.POINTER(_I)]),
     "sb_gemm_tune_set": (C.c_int, [_I, _I, _I, _I, _I, _I, _I]),
     "sb_profile_forward": (C.c_int, [C.POINTER(SbDecoder), C.POINTER(SbKVCache), _P, _P, _P, _I, _I, _P, _I, _P,

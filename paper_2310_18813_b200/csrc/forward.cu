@@ -595,6 +595,12 @@ int sb_gemm_autotune(const void* x, const void* w, void* y_f32, int32_t M, int32
 
 int sb_gemm_autotune_clear(void) { return gemm_tc_autotune_clear(); }
 
+int sb_set_weight_l2_hint(int32_t hint) {
+  if (hint < 0 || hint > 2) return SB_EINVAL;
+  g_w_l2_hint = hint;
+  return 0;
+}
+
 int sb_gemm_tune_get(int32_t M, int32_t N, int32_t K, int32_t* cps, int32_t* splits, int32_t* weight_tiles,
                      int32_t* token_tile) {
   return gemm_tc_tune_get(M, N, K, cps, splits, weight_tiles, token_tile);
@@ -669,7 +675,7 @@ int sb_set_pdl(int32_t enabled) {
 int sb_version(void) { return SB_ABI_VERSION; }
 
 const char* sb_build_info(void) {
-  return "specbatch_b200 abi=" "7" " arch=sm_100a tp=nccl models=llama,opt kernels=gemm_tcgen05,attention_tc(decode,"
+  return "specbatch_b200 abi=" "8" " arch=sm_100a tp=nccl models=llama,opt kernels=gemm_tcgen05,attention_tc(decode,"
          "prefill_blocks),rope_append_vec,embed_norm,layernorm,tp_resid_add,unshard_logits,argmax,softmax,select,accept,"
          "commit,prepare,kv_compact,draft_loop,persistent_forward,gemm_simt,attention_simt,rmsnorm forward=verify,mixed";
 }

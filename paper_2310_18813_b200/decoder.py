@@ -315,6 +315,8 @@ class Decoder:
                     N.call("sb_gemm_tune_set", T, n, k, cps, sp, wt, tn)
                 return {(name, T): tuple(table[(T, n, k)][:2]) + (None,) for name, T, n, k, _ in shapes}
         res = {}
+        # time the plans under the weight-stream L2 policy this model's forwards use (csrc/forward.cu)
+        N.call("sb_set_weight_l2_hint", 1 if self.weight_bytes() > (256 << 20) else 2)
         for name, T, n, k, w in shapes:
             x = torch.randn(T, k, device=self.device, dtype=torch.bfloat16)
             y = torch.empty(T, n, device=self.device, dtype=torch.float32)
