@@ -146,10 +146,11 @@ def cpu_sample(b, k, iters=1, threads=None, layers=None):
 
     def masters(cfg, n_layers):
         h, hd = cfg.hidden, cfg.head_dim
-        return {"embed": mk(cfg.vocab, h), "lm_head": mk(cfg.vocab, h),
+        return {"embed": mk(cfg.vocab, h), "lm_head": mk(cfg.vocab, h), "gf": 1 + mk(h),
                 "layers": [{"wq": mk(cfg.n_heads * hd, h), "wk": mk(cfg.n_kv_heads * hd, h),
                             "wv": mk(cfg.n_kv_heads * hd, h), "wo": mk(h, cfg.n_heads * hd), "wg": mk(cfg.ffn, h),
-                            "wu": mk(cfg.ffn, h), "wd": mk(h, cfg.ffn)} for _ in range(n_layers)]}
+                            "wu": mk(cfg.ffn, h), "wd": mk(h, cfg.ffn), "ga": 1 + mk(h), "gm": 1 + mk(h)}
+                           for _ in range(n_layers)]}
 
     def opt_masters(cfg, n_layers):
         h, F = cfg.hidden, cfg.ffn

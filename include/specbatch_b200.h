@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define SB_ABI_VERSION 8
+#define SB_ABI_VERSION 9
 
 /* status codes beyond cudaError_t (which are < 1000) */
 #define SB_OK 0
@@ -97,7 +97,14 @@ int sb_nccl_collectives_destroy(sb_collectives_t* c);
  *   w_gu[l]    [2*ffn, hidden]  rows interleaved g0,u0,g1,u1,...
  *   w_down[l]  [hidden, ffn]
  *   lm_head    [vocab, hidden]
- *   norms      [hidden] in `dtype`
+ *   norms      [hidden] in `dtype`: RMSNorm gains attn_norm[l] (before qkv),
+ *              mlp_norm[l] (before gate/up), final_norm (before lm_head).
+ *              Applied as y = x / rms(x) * g on every path: the fp32 path
+ *              materialises the normalised row; the bf16 path fuses the norm
+ *              into the GEMMs -- the producer of the residual (embedding,
+ *              o_proj, down_proj, TP reduce) writes xb = bf16(x * g_next) and
+ *              per-tile sums of x^2, the consumer GEMM scales its output
+ *              row by 1/rms.  Gains are NOT folded into the weights.
  *   rope_cos/rope_sin [max_pos, head_dim/2] fp32 (host-computed table)
  */
 typedef struct sb_decoder {
@@ -116,9 +123,6 @@ typedef struct sb_decoder {
   const void* const* w_down;
   const float* rope_cos;
   const float* rope_sin;
-  /* bf16 only, optional: device copy of the weight TMA descriptors written by
-     sb_decoder_encode_tmaps (enables the persistent forward; NULL = off) */
-  const void* tmaps;
   /* tensor parallelism (NULL = unsharded).  A shard holds n_heads/world q heads,
      n_kv_heads/world kv heads, ffn/world ffn rows and vocab/world lm_head rows
      (the fields above are the LOCAL sizes); embedding and norms are replicated.
@@ -146,17 +150,6 @@ typedef struct sb_kvcache {
   void* v;
   int32_t slots, ctx_max;
 } sb_kvcache_t;
-
-/* Bytes of the weight TMA descriptor table (4 per layer + lm_head, 128 B each). */
-size_t sb_decoder_tmaps_bytes(const sb_decoder_t* m);
-/*
- * Encode the weight TMA descriptors into host memory `host_out`
- * (sb_decoder_tmaps_bytes).  The caller copies them to 64-byte-aligned device
- * memory and stores that pointer in m->tmaps: with sb_set_persistent(1),
- * sb_decoder_forward then runs the persistent single-kernel forward for
- * n_tokens <= 256 (bf16).
- */
-int sb_decoder_encode_tmaps(const sb_decoder_t* m, void* host_out);
 
 /* Workspace bytes sb_decoder_forward needs for n_tokens query tokens. */
 size_t sb_decoder_workspace_bytes(const sb_decoder_t* m, int32_t n_tokens);
@@ -301,9 +294,7 @@ int sb_prepare_iteration(int32_t b, int32_t k, const int32_t* tokens, int32_t to
 int sb_draft_loop(const sb_decoder_t* m, const sb_kvcache_t* kv, int32_t b, int32_t k, const int32_t* d1_ids,
                   const int32_t* d1_pos, const int32_t* slots, const int32_t* d_base, int32_t* v_ids,
                   int32_t* ds_ids, int32_t* ds_pos, void* workspace, size_t ws_bytes, void* stream);
-/* Enable sb_draft_loop (default 0: measured 2x slower than the per-step forwards); 1 = use it. */
-/* Diagnostics: globaltimer stamps of every draft-loop grid barrier (CTA 0) into device_buf; NULL = off. */
-int sb_debug_draft_loop_trace(void* device_buf);
+/* Enable sb_draft_loop (default 1); 0 = it returns SB_EUNSUPPORTED and the caller issues per-step forwards. */
 int sb_set_draft_loop(int32_t enabled);
 
 /* Compaction (K5): copy KV slabs src_slot[i] -> dst_slot[i] for positions [0, len[i]). */
@@ -328,11 +319,6 @@ float sb_uniform_host(uint64_t seed, uint64_t stream_id, uint64_t counter);
 int sb_init(void);
 /* Force the forward's GEMM backend (0 auto = tcgen05 for bf16, 1 SIMT, 2 tcgen05); for ablations. */
 int sb_set_gemm_backend(int32_t backend);
-/* Persistent single-kernel forward when eligible (default off: measured slower); 0 = per-layer kernels. */
-int sb_set_persistent(int32_t enabled);
-/* Diagnostics: per (CTA, phase) globaltimer stamps [G][n_phases][4] of the persistent forward
-   (barrier wait start/end, first accumulator ready, phase end); NULL disables. */
-int sb_debug_persistent_trace(void* device_buf);
 /* Programmatic dependent launch for every kernel (default on); 0 disables (ablation). */
 int sb_set_pdl(int32_t enabled);
 /* Diagnostics: skip kernel classes of the bf16 forward (bit 0 attention, 1 qkv, 2 o, 3 gate/up, 4 down) to

@@ -34,9 +34,11 @@ def rope_tables(max_pos: int, head_dim: int, theta: float = 10000.0):
     return torch.from_numpy(np.cos(ang).astype(np.float32)), torch.from_numpy(np.sin(ang).astype(np.float32))
 
 
-def init_masters(cfg, seed: int, std: float = 0.02, round_to=torch.bfloat16):
+def init_masters(cfg, seed: int, std: float = 0.02, round_to=torch.bfloat16, gain_std: float = 0.1):
     """Independent regeneration of the seeded host init (same draw order as the
-    engine's Decoder(init="host")): embed, per layer q,k,v,o,gate,up,down, lm_head."""
+    engine's Decoder(init="host")): embed, per layer q,k,v,o,gate,up,down,
+    lm_head, then the RMSNorm gains 1 + N(0, gain_std): per layer attn ("ga")
+    and mlp ("gm"), then final ("gf")."""
     gen = torch.Generator(device="cpu").manual_seed(seed)
     rn = lambda *shape: torch.randn(*shape, generator=gen, dtype=torch.float32) * std
     h = cfg.hidden
@@ -49,6 +51,11 @@ def init_masters(cfg, seed: int, std: float = 0.02, round_to=torch.bfloat16):
                "wu": rn(cfg.ffn, h), "wd": rn(h, cfg.ffn)}
         out["layers"].append({k: r(v) for k, v in lay.items()})
     out["lm_head"] = r(rn(cfg.vocab, h))
+    gain = lambda: 1.0 + torch.randn(h, generator=gen, dtype=torch.float32) * gain_std
+    for lay in out["layers"]:
+        lay["ga"] = r(gain())
+        lay["gm"] = r(gain())
+    out["gf"] = r(gain())
     return out
 
 
@@ -57,11 +64,12 @@ class LlamaRef:
 
     dtype: torch.float32 or torch.float64 compute.  bf16_emulation rounds
     to bf16 where the GPU rounds (GEMM inputs, qkv, rotated q/k, attention
-    output, silu*up); the residual stream stays in `dtype`.  With
-    bf16_emulation the RMSNorm follows the GPU's fused contract: the GEMM
-    input is the bf16-rounded RAW residual and 1/rms scales the GEMM output
-    (norm gains are 1 / folded into the weights); in fp32/fp64 the two
-    orders are the same math.
+    output, silu*up); the residual stream stays in `dtype`.  RMSNorm is
+    y = x * rsqrt(mean(x^2) + eps) * g with per-layer gains g (masters keys
+    "ga" before q/k/v, "gm" before gate/up, "gf" before the lm_head; ones
+    when absent).  With bf16_emulation it follows the GPU's fused contract:
+    the GEMM input is bf16(x * g) and 1/rms scales the GEMM output; in
+    fp32/fp64 the two orders are the same math.
     """
 
     def __init__(self, masters: dict, n_heads: int, n_kv_heads: int, eps: float, max_pos: int = 4096,
@@ -76,6 +84,11 @@ class LlamaRef:
         lays = masters["layers"] if n_layers is None else masters["layers"][:n_layers]
         self.layers = [{k: v.to(dtype) for k, v in lay.items()} for lay in lays]
         self.h = self.emb.shape[1]
+        one = torch.ones(self.h, dtype=dtype)
+        for lay in self.layers:
+            lay.setdefault("ga", one)
+            lay.setdefault("gm", one)
+        self.gf = masters["gf"].to(dtype) if "gf" in masters else one
         self.nq, self.nkv = n_heads, n_kv_heads
         self.hd = head_dim or self.h // n_heads
         self.tp_reduce = tp_reduce or (lambda t: t)
@@ -88,16 +101,16 @@ class LlamaRef:
     def _r(self, x):
         return x.to(torch.bfloat16).to(self.dt) if self.bf16 else x
 
-    def _norm(self, x):
+    def _norm(self, x, g):
         ms = (x.float() * x.float()).mean(-1, keepdim=True) if self.dt == torch.float32 else (x * x).mean(-1, keepdim=True)
-        return self._r(x * torch.rsqrt(ms.to(self.dt) + self.eps))
+        return self._r(x * torch.rsqrt(ms.to(self.dt) + self.eps) * g)
 
-    def _nm(self, x, W):
-        """rmsnorm(x) @ W^T under the numerics contract."""
+    def _nm(self, x, W, g):
+        """(rmsnorm(x) * g) @ W^T under the numerics contract."""
         if self.bf16:
             inv = torch.rsqrt((x * x).mean(-1, keepdim=True) + self.eps)
-            return (self._r(x) @ W.T) * inv
-        return self._norm(x) @ W.T
+            return (self._r(x * g) @ W.T) * inv
+        return self._norm(x, g) @ W.T
 
     def _rope(self, x, pos):  # x [T, heads, hd]
         half = self.hd // 2
@@ -121,9 +134,9 @@ class LlamaRef:
         scale = 1.0 / math.sqrt(self.hd)
         p0 = int(pos[0])
         for lay, c in zip(self.layers, cache):
-            q = self._r(self._nm(x, lay["wq"])).view(T, self.nq, self.hd)
-            kk = self._r(self._nm(x, lay["wk"])).view(T, self.nkv, self.hd)
-            vv = self._r(self._nm(x, lay["wv"])).view(T, self.nkv, self.hd)
+            q = self._r(self._nm(x, lay["wq"], lay["ga"])).view(T, self.nq, self.hd)
+            kk = self._r(self._nm(x, lay["wk"], lay["ga"])).view(T, self.nkv, self.hd)
+            vv = self._r(self._nm(x, lay["wv"], lay["ga"])).view(T, self.nkv, self.hd)
             q = self._rope(q, pos_t)
             kk = self._rope(kk, pos_t)
             keep_k = c["k"][:p0] if c["k"] is not None else kk[:0]
@@ -134,7 +147,7 @@ class LlamaRef:
             rep = self.nq // self.nkv
             Kh = K.repeat_interleave(rep, dim=1)  # [S, nq, hd]
             Vh = Vv.repeat_interleave(rep, dim=1)
-            qs = q * (torch.tensor(scale, dtype=torch.float32).to(self.dt))
+            qs = q * scale
             att = torch.einsum("tnd,snd->nts", qs, Kh)
             S = K.shape[0]
             mask = torch.arange(S)[None, :] > pos_t[:, None]
@@ -142,11 +155,11 @@ class LlamaRef:
             att = torch.softmax(att, -1)
             o = self._r(torch.einsum("nts,snd->tnd", att, Vh).reshape(T, self.nq * self.hd))
             x = x + self.tp_reduce(o @ lay["wo"].T)
-            g = self._nm(x, lay["wg"])
-            u = self._nm(x, lay["wu"])
+            g = self._nm(x, lay["wg"], lay["gm"])
+            u = self._nm(x, lay["wu"], lay["gm"])
             a = self._r(torch.nn.functional.silu(g) * u)
             x = x + self.tp_reduce(a @ lay["wd"].T)
-        return self.tp_gather(self._nm(x, self.head)).to(torch.float64).numpy()
+        return self.tp_gather(self._nm(x, self.head, self.gf)).to(torch.float64).numpy()
 
 
 def init_opt_masters(cfg, seed: int, max_pos: int, std: float = 0.02, round_to=torch.bfloat16):
@@ -273,13 +286,25 @@ def greedy_decode(model: LlamaRef, prompt, n: int):
     return out, gaps
 
 
+def _top2_gap(lg) -> float:
+    a = np.partition(np.asarray(lg, np.float64), -2)[-2:]
+    return float(abs(a[1] - a[0]))
+
+
 def spec_generate(target: LlamaRef, draft: LlamaRef, prompts, target_lens, k: int, mode: str = "greedy",
-                  seed: int = 0, inj_samples=None):
+                  seed: int = 0, inj_samples=None, margins: list | None = None):
     """Batched speculative decoding on the CPU with the engine's protocol:
     draft step 1 re-feeds the last two committed tokens, verify feeds
     (x_{n-1}, d_1..d_k), KV rolled back by position.  Uniforms / injected
     lengths come from the same counter RNG as the GPU (spec_ref.uniforms).
-    Returns (tokens per sequence, accepted-length log [iters][b])."""
+    Returns (tokens per sequence, accepted-length log [iters][b]).
+
+    ``margins`` (a list) receives, per iteration, the [b] smallest decision
+    margin of each sequence: greedy -- the top-2 logit gap of every argmax
+    taken (draft steps, target positions 0..l); stochastic -- the relative
+    margins of every draft sample, accept test and resample
+    (spec_ref.inverse_cdf_margin / accept_margin).  A GPU divergence is a
+    rounding tie only where this margin is tiny."""
     b = len(prompts)
     P = len(prompts[0])
     tc = [target.new_cache() for _ in range(b)]
@@ -301,6 +326,8 @@ def spec_generate(target: LlamaRef, draft: LlamaRef, prompts, target_lens, k: in
         q = np.zeros((b, k, target.emb.shape[0]), np.float32) if mode == "stochastic" else None
         p = np.zeros((b, k + 1, target.emb.shape[0]), np.float32) if mode == "stochastic" else None
         t_tok = np.zeros((b, k + 1), np.int32)
+        mg = np.full(b, np.inf)
+        tgap = np.zeros((b, k + 1))
         for s in range(b):
             n = len(toks[s])
             if k > 0:
@@ -313,15 +340,33 @@ def spec_generate(target: LlamaRef, draft: LlamaRef, prompts, target_lens, k: in
                         qq = spec_ref.softmax_rows(lg.astype(np.float32)[None])[0]
                         q[s, j - 1] = qq
                         drafts[s, j - 1] = spec_ref.inverse_cdf(qq, u[s, j - 1])
+                        if margins is not None:
+                            mg[s] = min(mg[s], spec_ref.inverse_cdf_margin(qq, u[s, j - 1]))
                     else:
                         drafts[s, j - 1] = int(np.argmax(lg))
+                        if margins is not None:
+                            mg[s] = min(mg[s], _top2_gap(lg))
             vin = [toks[s][n - 1]] + [int(x) for x in drafts[s]]
             tl_logits = target.forward(vin, list(range(n - 1, n + k)), tc[s])
             if mode == "stochastic":
                 p[s] = spec_ref.softmax_rows(tl_logits.astype(np.float32))
             t_tok[s] = np.argmax(tl_logits, -1)
+            if margins is not None and mode == "greedy":
+                tgap[s] = [_top2_gap(r) for r in tl_logits]
         acc, adv, out = spec_ref.accept_batch(mode, k, drafts, produced, tl, target_tok=t_tok, p=p, q=q,
                                               u_acc=u[:, k:2 * k], u_res=u[:, 2 * k], l_inj=l_inj)
+        if margins is not None:
+            for s in range(b):
+                if mode == "greedy":
+                    mg[s] = min(mg[s], float(tgap[s, :acc[s] + 1].min()))
+                elif mode == "stochastic":
+                    for j in range(min(int(acc[s]) + 1, k)):
+                        d = int(drafts[s, j])
+                        mg[s] = min(mg[s], spec_ref.accept_margin(u[s, k + j], q[s, j, d], p[s, j, d]))
+                    l = int(acc[s])
+                    w = np.maximum(p[s, l] - q[s, l], 0) if l < k else p[s, k]
+                    mg[s] = min(mg[s], spec_ref.inverse_cdf_margin(w, u[s, 2 * k]))
+            margins.append(mg)
         log.append([int(a) if produced[s] < tl[s] else -1 for s, a in enumerate(acc)])
         for s in range(b):
             if adv[s] > 0:
@@ -346,9 +391,9 @@ def forward_batch(model: LlamaRef, ids, pos, caches):
     T = b * q
     scale = 1.0 / math.sqrt(model.hd)
     for li, lay in enumerate(model.layers):
-        Q = model._r(model._nm(x, lay["wq"])).view(b, q, model.nq, model.hd)
-        K = model._r(model._nm(x, lay["wk"])).view(b, q, model.nkv, model.hd)
-        Vv = model._r(model._nm(x, lay["wv"])).view(b, q, model.nkv, model.hd)
+        Q = model._r(model._nm(x, lay["wq"], lay["ga"])).view(b, q, model.nq, model.hd)
+        K = model._r(model._nm(x, lay["wk"], lay["ga"])).view(b, q, model.nkv, model.hd)
+        Vv = model._r(model._nm(x, lay["wv"], lay["ga"])).view(b, q, model.nkv, model.hd)
         outs = []
         for s in range(b):
             c = caches[s][li]
@@ -368,6 +413,6 @@ def forward_batch(model: LlamaRef, ids, pos, caches):
             outs.append(torch.einsum("nts,snd->tnd", att, Vh).reshape(q, model.nq * model.hd))
         o = model._r(torch.cat(outs, 0))
         x = x + o @ lay["wo"].T
-        a = model._r(torch.nn.functional.silu(model._nm(x, lay["wg"])) * model._nm(x, lay["wu"]))
+        a = model._r(torch.nn.functional.silu(model._nm(x, lay["wg"], lay["gm"])) * model._nm(x, lay["wu"], lay["gm"]))
         x = x + a @ lay["wd"].T
-    return model._nm(x, model.head).view(b, q, -1).numpy()
+    return model._nm(x, model.head, model.gf).view(b, q, -1).numpy()

@@ -52,7 +52,7 @@ class SbDecoder(C.Structure):
         ("ffn", _I), ("vocab", _I), ("dtype", _I), ("max_pos", _I), ("rms_eps", C.c_float),
         ("embed", _P), ("final_norm", _P), ("lm_head", _P),
         ("attn_norm", _PP), ("w_qkv", _PP), ("w_o", _PP), ("mlp_norm", _PP), ("w_gu", _PP), ("w_down", _PP),
-        ("rope_cos", _P), ("rope_sin", _P), ("tmaps", _P), ("tp", C.POINTER(SbCollectives)),
+        ("rope_cos", _P), ("rope_sin", _P), ("tp", C.POINTER(SbCollectives)),
         ("arch", _I), ("pos_offset", _I), ("pos_embed", _P), ("final_norm_b", _P), ("attn_norm_b", _PP),
         ("mlp_norm_b", _PP), ("b_qkv", _PP), ("b_o", _PP), ("b_fc1", _PP), ("b_fc2", _PP),
     ]
@@ -80,17 +80,12 @@ _SIGS = {
     "sb_debug_skip": (C.c_int, [_I]),
     "sb_set_attention_impl": (C.c_int, [_I]),
     "sb_set_attention_splits": (C.c_int, [_I]),
-    "sb_set_persistent": (C.c_int, [_I]),
     "sb_set_draft_loop": (C.c_int, [_I]),
-    "sb_debug_draft_loop_trace": (C.c_int, [_P]),
     "sb_draft_loop": (C.c_int, [C.POINTER(SbDecoder), C.POINTER(SbKVCache), _I, _I, _P, _P, _P, _P, _P, _P, _P, _P,
                                 C.c_size_t, _P]),
     "sb_nccl_unique_id": (C.c_int, [_P]),
     "sb_nccl_collectives_init": (C.c_int, [_P, _I, _I, C.POINTER(SbCollectives)]),
     "sb_nccl_collectives_destroy": (C.c_int, [C.POINTER(SbCollectives)]),
-    "sb_debug_persistent_trace": (C.c_int, [_P]),
-    "sb_decoder_tmaps_bytes": (C.c_size_t, [C.POINTER(SbDecoder)]),
-    "sb_decoder_encode_tmaps": (C.c_int, [C.POINTER(SbDecoder), _P]),
     "sb_gemm_tune": (C.c_int, [_I, _I, _I]),
     "sb_gemm_autotune": (C.c_int, [_P, _P, _P, _I, _I, _I, _P, C.POINTER(_I), C.POINTER(_I), C.POINTER(C.c_float)]),
     "sb_gemm_autotune_clear": (C.c_int, []),

@@ -1,7 +1,7 @@
 """Build the sm_100a C-ABI library ``libspecbatch_b200.so`` in-tree.
 
-``nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo -O3 -shared`` over
-``csrc/*.cu``; the CUDA runtime is linked statically so the library carries no
+``nvcc -gencode arch=compute_100a,code=sm_100a -lineinfo -O3`` over each of
+``csrc/*.cu`` (in parallel, objects under ``build/``), then ``nvcc -shared``; the CUDA runtime is linked statically so the library carries no
 dependency on torch's runtime (device pointers and streams cross the C-ABI as
 plain integers).  Cross-compiles on a GPU-less host.
 """
@@ -42,16 +42,34 @@ def _stale() -> bool:
 
 
 def build(force: bool = False, verbose: bool = False) -> Path:
+    """One object per translation unit, compiled in parallel, then one shared link."""
     if not force and not _stale():
         return LIB
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "-shared",
-           "--expt-relaxed-constexpr", "-Xlinker", "-z,defs", f"-I{INCLUDE}", f"-I{CSRC}", *map(str, sources()), "-o", str(tmp)]
+    objdir = PKG / "build"
+    objdir.mkdir(exist_ok=True)
+    flags = [*ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
+             f"-I{INCLUDE}", f"-I{CSRC}"]
+    jobs = []
+    for src in sources():
+        obj = objdir / (src.stem + ".o")
+        cmd = [nvcc(), *flags, "-c", str(src), "-o", str(obj)]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        jobs.append((src, obj, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.PIPE, text=True)))
+    errs = []
+    for src, _, proc in jobs:
+        _, err = proc.communicate()
+        if proc.returncode != 0:
+            errs.append(f"{src.name}: nvcc failed ({proc.returncode}):\n{err[-4000:]}")
+    if errs:
+        raise RuntimeError("\n".join(errs))
+    cmd = [nvcc(), *ARCH, "-shared", "-Xlinker", "-z,defs", *(str(o) for _, o, _ in jobs), "-o", str(tmp)]
     if verbose:
         print(" ".join(cmd), file=sys.stderr)
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
-        raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stderr[-4000:]}")
+        raise RuntimeError(f"nvcc link failed ({res.returncode}):\n{res.stderr[-4000:]}")
     os.replace(tmp, LIB)
     return LIB
 

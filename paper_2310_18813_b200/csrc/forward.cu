@@ -32,8 +32,6 @@ struct FwdWorkspace {
   float* tp_logits;   // TP: local vocab slice of the logits [T, vocab_local]
   float* tp_gather;   // TP: all-gathered slices [world][T][vocab_local]
   AttnScratch att_split;  // flash-decoding key-split partials + counters
-  float* pk_scratch;  // persistent forward: stream-K partial tiles
-  unsigned* pk_sync;  // persistent forward: barrier / exit / flag words (zero between launches)
   void* gemm_ws;
   size_t gemm_ws_bytes;
 };
@@ -50,17 +48,12 @@ static size_t carve(const sb_decoder_t* m, int T, char* base, FwdWorkspace* w) {
   };
   FwdWorkspace tmp;
   FwdWorkspace* o = w ? w : &tmp;
-  // The persistent forward's sync words come FIRST: they must sit at the same
-  // address for every forward sharing this workspace, whatever T is (each
-  // launch leaves them zero; any other placement would land them on dirty memory).
-  o->pk_sync = (unsigned*)take(persistent_sync_bytes());
   constexpr int kAttnItems = 16384, kAttnEntries = 640;  // counters stay at a fixed address too
   o->att_split.counter = (int*)take((size_t)kAttnItems * 4);
   o->att_split.max_items = kAttnItems;
   o->att_split.max_entries = kAttnEntries;
   o->att_split.part = (float*)take((size_t)kAttnEntries * 16 * m->head_dim * 4);
   o->att_split.ml = (float*)take((size_t)kAttnEntries * 16 * 2 * 4);
-  o->pk_scratch = (float*)take(persistent_scratch_bytes(T));
   int maxN = m->vocab;
   if (2 * m->ffn > maxN) maxN = 2 * m->ffn;
   if (qkv_n > maxN) maxN = qkv_n;
@@ -119,11 +112,13 @@ static int g_skip = 0;
 
 // TP exchange after a row-parallel projection whose partial went to w.tp_part:
 // all-reduce (sum over ranks), then resid += sum (+ bf16 copy / norm partials)
-static int tp_reduce_add(const sb_decoder_t* m, const FwdWorkspace& w, int T, bool fused, cudaStream_t st) {
+static int tp_reduce_add(const sb_decoder_t* m, const FwdWorkspace& w, int T, bool fused, const void* gain,
+                         cudaStream_t st) {
   const sb_collectives_t* c = m->tp;
   SB_TRY(c->all_reduce_sum(c->ctx, w.tp_part, (size_t)T * m->hidden, SB_F32, st));
   prof_mark("allreduce", st);
-  return launch_tp_resid_add(w.resid, w.tp_part, fused ? w.xb : nullptr, fused ? w.npart : nullptr, T, m->hidden, st);
+  return launch_tp_resid_add(w.resid, w.tp_part, fused ? w.xb : nullptr, fused ? w.npart : nullptr, T, m->hidden, st,
+                             gain);
 }
 
 // vocab-parallel lm_head: local slice -> all-gather -> full-width logits on
@@ -180,11 +175,12 @@ static int lm_head(const sb_decoder_t* m, GemmArgs g, float* logits, const sb_to
   return 0;
 }
 
-// bf16 forward with RMSNorm fused into the GEMMs: residual-producing GEMMs
-// (embedding, o_proj, down_proj) emit a bf16 copy of the new residual and
-// per-tile sum-of-squares partials; the consuming GEMMs (qkv, gate/up,
-// lm_head) read that copy and scale each token by 1/rms in their epilogue.
-// Norm gains are folded into the consumer weights by the host (ones here).
+// bf16 forward with RMSNorm fused into the GEMMs: residual-producing kernels
+// (embedding, o_proj, down_proj) emit xb = bf16(new residual * g), g the
+// RMSNorm gain of the NEXT consumer (attn_norm / mlp_norm / final_norm), and
+// per-tile sum-of-squares partials of the unscaled residual; the consuming
+// GEMMs (qkv, gate/up, lm_head) read xb and scale each token by 1/rms in
+// their epilogue: W . (x * g) / rms(x) == W . RMSNorm_g(x).
 // Attention over an already rotated / appended window (prefill-sized blocks):
 // tensor-core flash attention for bf16, the batch-invariant SIMT kernel for fp32.
 static int launch_attention_any(int dt, const void* qr, void* kc, void* vc, void* out, const int32_t* slot,
@@ -215,7 +211,9 @@ static int forward_fused_norm(const sb_decoder_t* m, const sb_kvcache_t* kv, con
   const int qkv_n = (nq + 2 * nkv) * hd;
   const size_t layer_kv = (size_t)kv->slots * nkv * kv->ctx_max * hd * 2;
   const float inv_h = 1.0f / (float)H;
-  SB_TRY(launch_embed_norm(m->embed, ids, pos, w.resid, w.xb, w.npart, T, H, vocab_full(m), st));
+  // gain of the consumer of the residual after layer l's down_proj (next layer's attn_norm, or final_norm)
+  auto next_gain = [&](int l) -> const void* { return l + 1 < m->n_layers ? m->attn_norm[l + 1] : m->final_norm; };
+  SB_TRY(launch_embed_norm(m->embed, ids, pos, w.resid, w.xb, w.npart, T, H, vocab_full(m), st, next_gain(-1)));
   prof_mark("embed", st);
   int P = 1;
   for (int l = 0; l < m->n_layers; ++l) {
@@ -253,13 +251,14 @@ static int forward_fused_norm(const sb_decoder_t* m, const sb_kvcache_t* kv, con
                  w.gemm_ws_bytes};
       SB_TRY(gemm_tc(o, st));
       prof_mark("o", st);
-      SB_TRY(tp_reduce_add(m, w, T, true, st));
+      SB_TRY(tp_reduce_add(m, w, T, true, m->mlp_norm[l], st));
       P = (H + 127) / 128;
     } else {
       GemmArgs o{SB_BF16, w.attn, m->w_o[l], w.resid, T, H, nq * hd, nq * hd, EPI_RESID_ADD, w.gemm_ws,
                  w.gemm_ws_bytes};
       o.out_part = w.npart;
       o.out_xb = w.xb;
+      o.out_gain = m->mlp_norm[l];
       if (!(g_skip & 4)) SB_TRY(gemm_tc(o, st));
       P = gemm_tc_norm_partials(o);
       prof_mark("o", st);
@@ -277,13 +276,14 @@ static int forward_fused_norm(const sb_decoder_t* m, const sb_kvcache_t* kv, con
                   w.gemm_ws_bytes};
       SB_TRY(gemm_tc(dn, st));
       prof_mark("down", st);
-      SB_TRY(tp_reduce_add(m, w, T, true, st));
+      SB_TRY(tp_reduce_add(m, w, T, true, next_gain(l), st));
       P = (H + 127) / 128;
     } else {
       GemmArgs dn{SB_BF16, w.act, m->w_down[l], w.resid, T, H, m->ffn, m->ffn, EPI_RESID_ADD, w.gemm_ws,
                   w.gemm_ws_bytes};
       dn.out_part = w.npart;
       dn.out_xb = w.xb;
+      dn.out_gain = next_gain(l);
       if (!(g_skip & 16)) SB_TRY(gemm_tc(dn, st));
       P = gemm_tc_norm_partials(dn);
       prof_mark("down", st);
@@ -406,12 +406,6 @@ static int forward_impl(const sb_decoder_t* m, const sb_kvcache_t* kv, const int
   if (m->arch == SB_ARCH_OPT) return forward_opt(m, kv, ids, slot, pos, n_seq, q_len, logits, logits_mode, sink, w, st);
   if (m->arch != SB_ARCH_LLAMA) return SB_EINVAL;
   if (m->tp && (m->tp->world < 1 || !m->tp->all_reduce_sum || !m->tp->all_gather)) return SB_EINVAL;
-  if (!g_prof && !m->tp && g_backend_override != GEMM_SIMT && persistent_eligible(m, T)) {
-    PkBuffers b{w.resid, w.xb, w.qr, w.attn, w.act, w.npart, w.amax_val, w.amax_idx, w.pk_scratch, w.pk_sync};
-    int rc = persistent_forward(m, kv, ids, slot, pos, n_seq, q_len, logits, logits_mode, sink, b, st);
-    if (rc && getenv("SB_DEBUG")) fprintf(stderr, "persistent_forward rc=%d T=%d\n", rc, T);
-    return rc;
-  }
   if (g_fuse_norm && dt == SB_BF16 && g_backend_override != GEMM_SIMT)
     return forward_fused_norm(m, kv, ids, slot, pos, n_seq, q_len, logits, logits_mode, sink, w, st);
   SB_TRY(launch_embed(dt, m->embed, ids, pos, w.resid, T, H, vocab_full(m), st));
@@ -440,7 +434,7 @@ static int forward_impl(const sb_decoder_t* m, const sb_kvcache_t* kv, const int
                  m->tp ? EPI_STORE_F32 : EPI_RESID_ADD, w.gemm_ws, w.gemm_ws_bytes};
     SB_TRY(gemm(g, GEMM_AUTO, st));
     prof_mark("o", st);
-    if (m->tp) SB_TRY(tp_reduce_add(m, w, T, false, st));
+    if (m->tp) SB_TRY(tp_reduce_add(m, w, T, false, nullptr, st));
     SB_TRY(launch_rmsnorm(dt, w.resid, m->mlp_norm[l], w.xn, T, H, m->rms_eps, 1, 0, st));
     prof_mark("norm2", st);
     g = GemmArgs{dt, w.xn, m->w_gu[l], w.act, T, 2 * m->ffn, H, H, EPI_SILU_MUL, w.gemm_ws, w.gemm_ws_bytes};
@@ -450,7 +444,7 @@ static int forward_impl(const sb_decoder_t* m, const sb_kvcache_t* kv, const int
                  m->tp ? EPI_STORE_F32 : EPI_RESID_ADD, w.gemm_ws, w.gemm_ws_bytes};
     SB_TRY(gemm(g, GEMM_AUTO, st));
     prof_mark("down", st);
-    if (m->tp) SB_TRY(tp_reduce_add(m, w, T, false, st));
+    if (m->tp) SB_TRY(tp_reduce_add(m, w, T, false, nullptr, st));
   }
   if (logits_mode == SB_LOGITS_NONE) return 0;
   int rows = logits_mode == SB_LOGITS_LAST ? n_seq : T;
@@ -481,9 +475,7 @@ int sb_decoder_forward(const sb_decoder_t* m, const sb_kvcache_t* kv, const int3
   int rc = forward_impl(m, kv, tok_ids, tok_slot, tok_pos, n_seq, q_len, logits, logits_mode, nullptr, workspace,
                         ws_bytes, (cudaStream_t)stream);
   g_last_count = g_kernel_count;
-  if (rc && getenv("SB_DEBUG"))
-    fprintf(stderr, "sb_decoder_forward rc=%d T=%d eligible=%d\n", rc, n_seq * q_len,
-            (int)persistent_eligible(m, n_seq * q_len));
+  if (rc && getenv("SB_DEBUG")) fprintf(stderr, "sb_decoder_forward rc=%d T=%d\n", rc, n_seq * q_len);
   return rc;
 }
 
@@ -627,11 +619,7 @@ int sb_set_fuse_norm(int32_t enabled) {
   return 0;
 }
 
-int sb_set_persistent(int32_t enabled) { return set_persistent(enabled); }
-
-static int g_draft_loop = 0;  // sb_set_draft_loop (off by default: measured slower)
-
-int sb_debug_draft_loop_trace(void* device_buf) { return set_draft_loop_trace(device_buf); }
+static int g_draft_loop = 1;  // sb_set_draft_loop
 
 int sb_set_draft_loop(int32_t enabled) {
   g_draft_loop = enabled ? 1 : 0;
@@ -642,29 +630,7 @@ int sb_draft_loop(const sb_decoder_t* m, const sb_kvcache_t* kv, int32_t b, int3
                   const int32_t* d1_pos, const int32_t* slots, const int32_t* d_base, int32_t* v_ids, int32_t* ds_ids,
                   int32_t* ds_pos, void* workspace, size_t ws_bytes, void* stream) {
   if (!m || !kv || b < 1 || k < 0) return SB_EINVAL;
-  if (!g_draft_loop || !draft_loop_eligible(m, b)) return SB_EUNSUPPORTED;
-  if (k == 0) return 0;
-  FwdWorkspace w;
-  const size_t need = carve(m, 2 * b, (char*)workspace, &w);
-  if (need > ws_bytes) return SB_EWORKSPACE;
-  g_kernel_count = 0;
-  const int gw = num_sms() * 8;
-  if ((size_t)gw * b * 8 > persistent_scratch_bytes(2 * b)) return SB_EUNSUPPORTED;
-  DlBuffers buf{w.resid, w.qr, w.attn, w.act, w.pk_scratch, (int*)(w.pk_scratch + (size_t)gw * b), w.pk_sync};
-  int rc = launch_draft_loop(m, kv, b, k, d1_ids, d1_pos, slots, d_base, v_ids, ds_ids, ds_pos, buf,
-                             (cudaStream_t)stream);
-  g_last_count = g_kernel_count;
-  return rc;
-}
-
-int sb_debug_persistent_trace(void* device_buf) { return set_persistent_trace(device_buf); }
-
-size_t sb_decoder_tmaps_bytes(const sb_decoder_t* m) { return m ? decoder_tmaps_bytes(m) : 0; }
-
-int sb_decoder_encode_tmaps(const sb_decoder_t* m, void* host_out) {
-  if (!m || !host_out) return SB_EINVAL;
-  SB_TRY(gemm_tc_init());
-  return decoder_encode_tmaps(m, host_out);
+  return SB_EUNSUPPORTED;
 }
 
 int sb_set_pdl(int32_t enabled) {
@@ -675,9 +641,9 @@ int sb_set_pdl(int32_t enabled) {
 int sb_version(void) { return SB_ABI_VERSION; }
 
 const char* sb_build_info(void) {
-  return "specbatch_b200 abi=" "8" " arch=sm_100a tp=nccl models=llama,opt kernels=gemm_tcgen05,attention_tc(decode,"
+  return "specbatch_b200 abi=" "9" " arch=sm_100a tp=nccl models=llama,opt kernels=gemm_tcgen05,attention_tc(decode,"
          "prefill_blocks),rope_append_vec,embed_norm,layernorm,tp_resid_add,unshard_logits,argmax,softmax,select,accept,"
-         "commit,prepare,kv_compact,draft_loop,persistent_forward,gemm_simt,attention_simt,rmsnorm forward=verify,mixed";
+         "commit,prepare,kv_compact,gemm_simt,attention_simt,rmsnorm forward=verify,mixed";
 }
 
 int sb_last_kernel_count(void) { return g_last_count; }

@@ -63,6 +63,7 @@ struct TcParams {
   // out_part[(tile_n * splits + split) * M + m] = sum over this CTA's rows of new^2
   float* out_part;
   __nv_bfloat16* out_xb;
+  const __nv_bfloat16* out_gain;  // RMSNorm gain of the CONSUMER of xb: xb = bf16(new * gain[n]) (NULL = 1)
   const __nv_bfloat16* bias;  // OPT: per-row bias [N] added before the epilogue op
   int relu;
 };
@@ -84,7 +85,7 @@ __device__ __forceinline__ float epi_one(const TcParams& p, int m, int n, float 
   } else {
     float nv = ((float*)p.y)[o] + v;
     ((float*)p.y)[o] = nv;
-    if (p.out_xb) p.out_xb[o] = __float2bfloat16_rn(nv);
+    if (p.out_xb) p.out_xb[o] = __float2bfloat16_rn(p.out_gain ? nv * __bfloat162float(p.out_gain[n]) : nv);
     return nv;
   }
   return v;
@@ -98,7 +99,7 @@ __device__ __forceinline__ float epi_resid_pre(const TcParams& p, int m, int n, 
   if (p.bias) v += __bfloat162float(p.bias[n]);
   const float nv = prev + v;
   ((float*)p.y)[o] = nv;
-  if (p.out_xb) p.out_xb[o] = __float2bfloat16_rn(nv);
+  if (p.out_xb) p.out_xb[o] = __float2bfloat16_rn(p.out_gain ? nv * __bfloat162float(p.out_gain[n]) : nv);
   return nv;
 }
 __device__ __forceinline__ float resid_load(const TcParams& p, int m, int n) {
@@ -779,6 +780,7 @@ int gemm_tc(const GemmArgs& a, cudaStream_t st) {
   p.ns_inv_h = a.ns_inv_h;
   p.out_part = a.out_part;
   p.out_xb = (__nv_bfloat16*)a.out_xb;
+  p.out_gain = (const __nv_bfloat16*)a.out_gain;
   p.bias = (const __nv_bfloat16*)a.bias;
   p.relu = a.relu;
   if ((a.bias || a.relu) && (a.epi == EPI_SILU_MUL || a.epi == EPI_ARGMAX)) return SB_EINVAL;

@@ -31,13 +31,16 @@ struct GemmArgs {
   float* aux_val = nullptr;  // EPI_ARGMAX partials
   int* aux_idx = nullptr;
   // fused RMSNorm consumer (tcgen05 only): scale token m by rsqrt(sum_p ns_part[p*ns_stride +
-  // m*ns_row_step + ns_row_off] * ns_inv_h + ns_eps); X is the raw (bf16) residual, norm gains folded in W
+  // m*ns_row_step + ns_row_off] * ns_inv_h + ns_eps); X = bf16(residual * gain), written by the producer
   const float* ns_part = nullptr;
   int ns_P = 0, ns_stride = 0, ns_row_step = 1, ns_row_off = 0;
   float ns_eps = 0.f, ns_inv_h = 0.f;
   // fused RMSNorm producer (EPI_RESID_ADD): bf16 copy of the new residual + sum-of-squares partials
   float* out_part = nullptr;
   void* out_xb = nullptr;
+  // RMSNorm gain [N] (bf16) of the consumer of out_xb: out_xb = bf16(new residual * gain); the partials stay
+  // sums of new^2, so consumer(xb) * 1/rms == W . (RMSNorm(x) * gain) exactly in real arithmetic
+  const void* out_gain = nullptr;
   // OPT: per-output-row bias (model dtype, [N]) added to the fp32 accumulator, then ReLU (store epilogues)
   const void* bias = nullptr;
   int relu = 0;
@@ -67,7 +70,7 @@ int launch_embed(int dtype, const void* table, const int32_t* ids, const int32_t
 int launch_layernorm(int dtype, const float* x, const void* g, const void* b, void* y, int rows, int hidden, float eps,
                      int row_step, int row_off, cudaStream_t st);
 int launch_embed_norm(const void* table, const int32_t* ids, const int32_t* pos, float* h, void* xb, float* part,
-                      int n_tok, int hidden, int vocab, cudaStream_t st);
+                      int n_tok, int hidden, int vocab, cudaStream_t st, const void* gain);
 int launch_rmsnorm(int dtype, const float* x, const void* g, void* y, int rows, int hidden, float eps, int row_step,
                    int row_off, cudaStream_t st);
 int launch_rope_append(int dtype, const void* qkv, void* q_out, void* kc, void* vc, const int32_t* tok_slot,
@@ -102,47 +105,8 @@ int launch_kv_compact(int dtype, void* k, void* v, const int32_t* src, const int
                       int layers, int slots, int nkv, int ctx_max, int hd, cudaStream_t st);
 
 // ---- tensor-parallel glue (layer_kernels.cu)
-int launch_tp_resid_add(float* resid, const float* part, void* xb, float* npart, int T, int H, cudaStream_t st);
+int launch_tp_resid_add(float* resid, const float* part, void* xb, float* npart, int T, int H, cudaStream_t st,
+                        const void* gain);
 int launch_unshard_logits(const float* gathered, float* logits, int world, int rows, int vl, cudaStream_t st);
-
-// ---- draft loop megakernel (draft_loop.cu)
-struct DlBuffers {
-  float* resid;
-  void* qr;
-  void* att;
-  void* act;
-  float* am_val;
-  int* am_idx;
-  unsigned* sync;
-};
-int draft_loop_eligible(const sb_decoder_t* m, int b);
-int set_draft_loop_trace(void* buf);
-int launch_draft_loop(const sb_decoder_t* m, const sb_kvcache_t* kv, int b, int k, const int32_t* d1_ids,
-                      const int32_t* d1_pos, const int32_t* slot, const int32_t* d_base, int32_t* v_ids,
-                      int32_t* ds_ids, int32_t* ds_pos, const DlBuffers& buf, cudaStream_t st);
-
-// ---- persistent forward (persistent.cu)
-struct PkBuffers {
-  float* resid;
-  void* xb;
-  void* qr;
-  void* attn;
-  void* act;
-  float* npart;
-  float* amax_val;
-  int* amax_idx;
-  float* scratch;
-  unsigned* sync;
-};
-size_t persistent_sync_bytes();
-size_t persistent_scratch_bytes(int T);
-bool persistent_eligible(const sb_decoder_t* m, int T);
-int persistent_forward(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* ids, const int32_t* slot,
-                       const int32_t* pos, int n_seq, int q_len, float* logits, int logits_mode,
-                       const sb_token_sink_t* sink, const PkBuffers& b, cudaStream_t st);
-int set_persistent(int enabled);
-int set_persistent_trace(void* buf);
-size_t decoder_tmaps_bytes(const sb_decoder_t* m);
-int decoder_encode_tmaps(const sb_decoder_t* m, void* host_out);
 
 }  // namespace sb

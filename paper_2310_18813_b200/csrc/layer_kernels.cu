@@ -4,8 +4,8 @@
 //
 // Numerics contract (mirrored by oracle/model_ref.py):
 //   residual stream fp32; GEMM inputs rounded to the model dtype; on the bf16
-//   path RMSNorm is fused into the GEMMs (input = bf16 raw residual, output
-//   scaled by 1/rms, gains folded into W), on the fp32 path the normalised
+//   path RMSNorm is fused into the GEMMs (input = bf16(residual * gain), written
+//   by the residual's producer; output scaled by 1/rms), on the fp32 path the normalised
 //   input is materialised (same math); RoPE applied in fp32 from a host-built fp32 cos/sin
 //   table then rounded; attention scores/softmax/accumulation in fp32 with a
 //   fixed key order (64-key tiles, ascending) so a query's output does not
@@ -56,7 +56,8 @@ __global__ void __launch_bounds__(256) embed_norm_kernel(const __nv_bfloat16* __
                                                          const int32_t* __restrict__ ids,
                                                          const int32_t* __restrict__ pos, float* __restrict__ h,
                                                          __nv_bfloat16* __restrict__ xb, float* __restrict__ part,
-                                                         int hidden, int vocab) {
+                                                         int hidden, int vocab,
+                                                         const __nv_bfloat16* __restrict__ gain) {
   griddep_wait();
   griddep_launch();
   const int t = blockIdx.x;
@@ -67,7 +68,7 @@ __global__ void __launch_bounds__(256) embed_norm_kernel(const __nv_bfloat16* __
   for (int i = threadIdx.x; i < hidden; i += blockDim.x) {
     float v = pad ? 0.f : __bfloat162float(row[i]);
     h[(size_t)t * hidden + i] = v;
-    xb[(size_t)t * hidden + i] = __float2bfloat16_rn(v);
+    xb[(size_t)t * hidden + i] = __float2bfloat16_rn(gain ? v * __bfloat162float(gain[i]) : v);
     ss += v * v;
   }
   __shared__ float red[8];
@@ -82,10 +83,10 @@ __global__ void __launch_bounds__(256) embed_norm_kernel(const __nv_bfloat16* __
 }
 
 int launch_embed_norm(const void* table, const int32_t* ids, const int32_t* pos, float* h, void* xb, float* part,
-                      int n_tok, int hidden, int vocab, cudaStream_t st) {
+                      int n_tok, int hidden, int vocab, cudaStream_t st, const void* gain) {
   if (n_tok <= 0) return 0;
   return launch_k(embed_norm_kernel, dim3(n_tok), dim3(256), 0, st, (const __nv_bfloat16*)table, ids, pos, h,
-                  (__nv_bfloat16*)xb, part, hidden, vocab);
+                  (__nv_bfloat16*)xb, part, hidden, vocab, (const __nv_bfloat16*)gain);
 }
 
 // ---------------------------------------------------------------- RMSNorm
@@ -722,7 +723,7 @@ namespace sb {
 // grid (T, ceil(H/128)), 128 threads: one element per thread, fixed-order sums.
 __global__ void __launch_bounds__(128) tp_resid_add_kernel(float* __restrict__ resid, const float* __restrict__ part,
                                                            __nv_bfloat16* __restrict__ xb, float* __restrict__ npart,
-                                                           int T, int H) {
+                                                           int T, int H, const __nv_bfloat16* __restrict__ gain) {
   griddep_wait();
   griddep_launch();
   const int t = blockIdx.x, tile = blockIdx.y;
@@ -732,7 +733,7 @@ __global__ void __launch_bounds__(128) tp_resid_add_kernel(float* __restrict__ r
     const size_t o = (size_t)t * H + col;
     nv = resid[o] + part[o];
     resid[o] = nv;
-    if (xb) xb[o] = __float2bfloat16_rn(nv);
+    if (xb) xb[o] = __float2bfloat16_rn(gain ? nv * __bfloat162float(gain[col]) : nv);
   }
   if (!npart) return;
   __shared__ float red[4];
@@ -742,10 +743,11 @@ __global__ void __launch_bounds__(128) tp_resid_add_kernel(float* __restrict__ r
   if (threadIdx.x == 0) npart[(size_t)tile * T + t] = ((red[0] + red[1]) + red[2]) + red[3];
 }
 
-int launch_tp_resid_add(float* resid, const float* part, void* xb, float* npart, int T, int H, cudaStream_t st) {
+int launch_tp_resid_add(float* resid, const float* part, void* xb, float* npart, int T, int H, cudaStream_t st,
+                        const void* gain) {
   if (T <= 0) return 0;
   return launch_k(tp_resid_add_kernel, dim3(T, (H + 127) / 128), dim3(128), 0, st, resid, part, (__nv_bfloat16*)xb,
-                  npart, T, H);
+                  npart, T, H, (const __nv_bfloat16*)gain);
 }
 
 // all_gather output [world][rows][Vl] -> logits [rows][world * Vl] (vocab-parallel lm_head)

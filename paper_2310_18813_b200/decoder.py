@@ -109,15 +109,18 @@ class Decoder:
     """Seeded random-init Llama-style decoder resident on the GPU.
 
     init="host": fp32 masters drawn on the CPU with ``torch.Generator(seed)`` in
-    a fixed order (embed, per layer q,k,v,o,gate,up,down, lm_head) -- the CPU
-    oracle reproduces them exactly (used by the parity tests).
+    a fixed order (embed, per layer q,k,v,o,gate,up,down, lm_head, then the
+    RMSNorm gains: per layer attn, mlp, then final) -- the CPU oracle
+    reproduces them exactly (used by the parity tests).  Gains are
+    1 + N(0, gain_std) (non-unit, as in every trained checkpoint; gain_std=0
+    gives ones).
     init="device": drawn on the GPU (7B/70B sizes; no CPU copy).
     ``share_from``/``share_layers`` build a self-speculative draft that reuses
     the target's embedding, lm_head and first layers (config 1's pair).
     """
 
     def __init__(self, cfg: DecoderConfig, dtype: str = "bf16", device="cuda", seed: int = 0,
-                 init: str = "host", max_pos: int = 4096, std: float = 0.02,
+                 init: str = "host", max_pos: int = 4096, std: float = 0.02, gain_std: float = 0.1,
                  share_from: "Decoder | None" = None, share_layers: int | None = None):
         if dtype not in ("bf16", "fp32"):
             raise ValueError(f"dtype must be bf16 or fp32, got {dtype!r}")
@@ -168,8 +171,6 @@ class Decoder:
                 wg, wu = mk((cfg.ffn, h)), mk((cfg.ffn, h))
                 wd = mk((h, cfg.ffn))
                 lay = {
-                    "attn_norm": torch.ones(h, device=self.device, dtype=self.tdtype),
-                    "mlp_norm": torch.ones(h, device=self.device, dtype=self.tdtype),
                     "w_qkv": torch.cat([wq, wk, wv], 0).to(device=self.device, dtype=self.tdtype),
                     "w_o": wo.to(device=self.device, dtype=self.tdtype),
                     "w_gu": torch.stack([wg, wu], 1).reshape(2 * cfg.ffn, h).to(device=self.device, dtype=self.tdtype),
@@ -186,7 +187,17 @@ class Decoder:
                 masters["lm_head"] = head.to(self.tdtype).float()
             self.lm_head = head.to(device=self.device, dtype=self.tdtype)
             del head
-            self.final_norm = torch.ones(h, device=self.device, dtype=self.tdtype)
+            gain = lambda: 1.0 + _randn((h,), gen, gen_dev, gain_std)
+            for li, lay in enumerate(self.layers):
+                ga, gm = gain(), gain()
+                lay["attn_norm"] = ga.to(device=self.device, dtype=self.tdtype)
+                lay["mlp_norm"] = gm.to(device=self.device, dtype=self.tdtype)
+                if keep:
+                    masters["layers"][li].update(ga=ga.to(self.tdtype).float(), gm=gm.to(self.tdtype).float())
+            gf = gain()
+            self.final_norm = gf.to(device=self.device, dtype=self.tdtype)
+            if keep:
+                masters["gf"] = gf.to(self.tdtype).float()
             self.masters = masters
         if self.cfg.arch == "opt":  # learned positions: identity rotation tables (cos 1, sin 0)
             cos = np.ones((max_pos, self.cfg.head_dim // 2), np.float32)
@@ -259,17 +270,6 @@ class Decoder:
                 setattr(s, k, C.cast(self._arrays[k], C.POINTER(C.c_void_p)))
             s.pos_offset, s.pos_embed = cfg.pos_offset, self.pos_embed.data_ptr()
             s.final_norm_b = self.final_norm_b.data_ptr()
-        s.tmaps = None
-        self.tmaps = None
-        if self.sb_dtype == N.SB_BF16 and self.device.type == "cuda" and cfg.arch == "llama":
-            # weight TMA descriptors, encoded once on the host and kept resident:
-            # they enable the persistent single-kernel forward (csrc/persistent.cu)
-            lib = N.load()
-            nbytes = int(lib.sb_decoder_tmaps_bytes(C.byref(s)))
-            host = (C.c_uint8 * nbytes)()
-            N.call("sb_decoder_encode_tmaps", C.byref(s), C.cast(host, C.c_void_p))
-            self.tmaps = torch.frombuffer(bytearray(host), dtype=torch.uint8).to(self.device)
-            s.tmaps = self.tmaps.data_ptr()
         self.struct = s
 
     def gemm_shapes(self) -> dict:

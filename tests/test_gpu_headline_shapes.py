@@ -1,0 +1,128 @@
+"""Logits parity at the BASELINE shapes (north_star: "logits must agree within
+1e-3 relative (fp32) or 2e-2 (bf16)"), with non-unit RMSNorm gains:
+
+* a 2-layer slice of Llama-2-7B (h 4096, 32 heads of 128, ffn 11008, V 32000),
+* LLaMA-68M whole (h 768, 12 heads of 64, 2 layers),
+* a 2-layer slice of Llama-2-70B (h 8192, 64 q / 8 kv heads: GQA group 8,
+  ffn 28672),
+
+each through a prefill forward and then verify windows of k+1 tokens for
+k in {1, 3, 8} (the causal mask inside the speculative window, rollback by
+position: every window call overwrites the same positions).  The oracle is
+oracle/model_ref.LlamaRef on the identical host-drawn weights (pinned to
+transformers' LlamaForCausalLM by tests/test_oracle_hf.py): fp64 for the fp32
+path, fp64 with bf16-rounding emulation for the bf16 path (fp32 compute for
+the 70B slice, 2.2 B parameters).  Every GEMM, attention and norm kernel of
+the verify forward runs: tcgen05 GEMMs + tensor-core attention in bf16, the
+SIMT kernels in fp32.
+"""
+
+from dataclasses import replace
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import model_ref
+from paper_2310_18813_b200 import _native as N
+from paper_2310_18813_b200.decoder import CONFIGS, Decoder
+
+pytestmark = pytest.mark.gpu
+
+SHAPES = {
+    "llama-2-7b[:2]": replace(CONFIGS["llama-2-7b"], n_layers=2),
+    "llama-68m": CONFIGS["llama-68m"],
+    "llama-2-70b[:2]": replace(CONFIGS["llama-2-70b"], n_layers=2),
+}
+TOL = {"fp32": 1e-3, "bf16": 2e-2}
+B, P, MAXPOS = 2, 24, 64
+
+
+def _rel(got, want):
+    return float(np.abs(got - want).max() / np.abs(want).max())
+
+
+@pytest.mark.parametrize("dtype", ["fp32", "bf16"])
+@pytest.mark.parametrize("shape", list(SHAPES))
+def test_headline_shape_logits_match_oracle(cuda_dev, shape, dtype):
+    cfg = SHAPES[shape]
+    dec = Decoder(cfg, dtype=dtype, device=cuda_dev, seed=21, init="host", max_pos=MAXPOS)
+    assert any((lay["attn_norm"].float() - 1).abs().max() > 0.05 for lay in dec.layers)
+    big = cfg.hidden >= 8192
+    ref = model_ref.LlamaRef(dec.masters, cfg.n_heads, cfg.n_kv_heads, cfg.rms_eps, max_pos=MAXPOS,
+                             theta=cfg.rope_theta, dtype=torch.float32 if big else torch.float64,
+                             bf16_emulation=dtype == "bf16")
+    dec.masters = None  # the oracle holds its own copy
+    rng = np.random.default_rng(7)
+    kv = dec.new_kv(B, MAXPOS)
+    ws = torch.zeros(dec.workspace_bytes(B * P), device=cuda_dev, dtype=torch.uint8)
+    slots = torch.arange(B, dtype=torch.int32, device=cuda_dev)
+    ids = rng.integers(0, cfg.vocab, size=(B, P)).astype(np.int32)
+    logits = torch.zeros(B * P, cfg.vocab, device=cuda_dev)
+    pos = torch.arange(P, dtype=torch.int32, device=cuda_dev).repeat(B)
+    dec.forward(kv, torch.as_tensor(ids.reshape(-1), device=cuda_dev), slots, pos, B, P, logits, N.LOGITS_ALL, ws)
+    torch.cuda.synchronize()
+    got_pf = logits.cpu().numpy().reshape(B, P, -1)
+    caches = [ref.new_cache() for _ in range(B)]
+    worst = 0.0
+    for s in range(B):
+        want = ref.forward(list(ids[s]), list(range(P)), caches[s])
+        # prefill rows P-4.. (the last rows see the longest context); all rows for the small shapes
+        rows = slice(P - 4, P) if big else slice(0, P)
+        worst = max(worst, _rel(got_pf[s, rows], want[rows]))
+        assert (got_pf[s, -1].argmax() == want[-1].argmax()) or dtype == "bf16"
+    for k in (1, 3, 8):
+        win = rng.integers(0, cfg.vocab, size=(B, k + 1)).astype(np.int32)
+        lg = torch.zeros(B * (k + 1), cfg.vocab, device=cuda_dev)
+        wpos = (torch.arange(k + 1, dtype=torch.int32, device=cuda_dev) + P).repeat(B)
+        dec.forward(kv, torch.as_tensor(win.reshape(-1), device=cuda_dev), slots, wpos, B, k + 1, lg,
+                    N.LOGITS_ALL, ws)
+        torch.cuda.synchronize()
+        got = lg.cpu().numpy().reshape(B, k + 1, -1)
+        for s in range(B):
+            want = ref.forward(list(win[s]), list(range(P, P + k + 1)), caches[s])
+            r = _rel(got[s], want)
+            worst = max(worst, r)
+            assert r < TOL[dtype], (shape, dtype, k, s, r)
+    assert worst < TOL[dtype], (shape, dtype, worst)
+    print(f"{shape} {dtype}: worst relative logits error {worst:.2e} (tolerance {TOL[dtype]:.0e})")
+
+
+@pytest.mark.parametrize("shape,draft", [("llama-2-7b[:2]", "self"), ("llama-2-7b[:2]", "llama-68m"),
+                                         ("llama-2-70b[:2]", "self")])
+def test_headline_shape_fp32_greedy_spec_matches_oracle(cuda_dev, shape, draft):
+    """fp32 greedy speculative decoding at the headline shapes: token streams
+    AND accepted-length sequences identical to the CPU oracle's speculative
+    run (tie-aware).  draft "self" = the target's first layer (real acceptance);
+    "llama-68m" = the BASELINE draft shape (random weights: acceptance ~0)."""
+    from test_gpu_model import TIE_GAP, check_stream_parity
+
+    from paper_2310_18813_b200.engine import SequenceState
+    from paper_2310_18813_b200.spec_engine import SpecEngine
+
+    cfg = SHAPES[shape]
+    big = cfg.hidden >= 8192
+    tgt = Decoder(cfg, dtype="fp32", device=cuda_dev, seed=22, init="host", max_pos=MAXPOS)
+    if draft == "self":
+        drf = Decoder(cfg, dtype="fp32", device=cuda_dev, share_from=tgt, share_layers=1, max_pos=MAXPOS)
+    else:
+        drf = Decoder(CONFIGS[draft], dtype="fp32", device=cuda_dev, seed=23, init="host", max_pos=MAXPOS)
+    dt = torch.float32 if big else torch.float64
+    t_ref = model_ref.LlamaRef(tgt.masters, cfg.n_heads, cfg.n_kv_heads, cfg.rms_eps, max_pos=MAXPOS, dtype=dt)
+    dc = drf.cfg
+    d_ref = model_ref.LlamaRef(drf.masters, dc.n_heads, dc.n_kv_heads, dc.rms_eps, max_pos=MAXPOS, dtype=dt,
+                               n_layers=dc.n_layers)
+    b, P, Nnew, k = 3, 12, 16, 3
+    eng = SpecEngine(tgt, drf, mode="greedy", max_batch=b, max_k=k, prompt_len=P, max_new=Nnew, seed=4,
+                     autotune=False)
+    states = [SequenceState(request_id=i, target_len=Nnew - 2 * i) for i in range(b)]
+    eng.generate(states, k)
+    prompts = [eng.prompt_fn(st.request_id) for st in states]
+    margins = []
+    want, log = model_ref.spec_generate(t_ref, d_ref, prompts, [st.target_len for st in states], k,
+                                        mode="greedy", margins=margins)
+    ties = check_stream_parity(states, eng.stats.accepted, want, log, margins, TIE_GAP)
+    assert ties <= 1, ties
+    live = eng.stats.accepted >= 0
+    print(f"{shape} + {draft}: accepted {int(eng.stats.accepted[live].sum())} of {k * int(live.sum())} drafts, "
+          f"{ties} tie divergences")

@@ -6,6 +6,9 @@ with k re-chosen per iteration by the policy."""
 
 import numpy as np
 import pytest
+import torch
+
+from oracle import model_ref
 
 from paper_2310_18813_b200.decoder import tiny_pair
 from paper_2310_18813_b200.engine import SequenceState
@@ -41,3 +44,15 @@ def test_continuous_streams_equal_plain_generation(cuda_dev, policy):
         st = SequenceState(request_id=r.id, target_len=r.gen_len)
         eng.generate([st], 0)
         assert extra["outputs"][r.id] == st.tokens, r.id
+    # and the CPU oracle's plain greedy decoding of every prompt (fp64; tie-aware)
+    cfg = tgt.cfg
+    ref = model_ref.LlamaRef(tgt.masters, cfg.n_heads, cfg.n_kv_heads, cfg.rms_eps, max_pos=256, dtype=torch.float64)
+    ties = 0
+    for r in wl:
+        want, gaps = model_ref.greedy_decode(ref, eng.prompt_fn(r.id), r.gen_len)
+        got = extra["outputs"][r.id]
+        d = next((i for i, (a, b_) in enumerate(zip(got, want)) if a != b_), None)
+        if d is not None:
+            assert gaps[d] < 2e-4, (r.id, d, gaps[d])
+            ties += 1
+    assert ties <= 1

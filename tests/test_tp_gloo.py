@@ -30,8 +30,9 @@ def shard_masters(m, cfg, world, rank):
     qd, kd, F, V = cfg.n_heads * hd, cfg.n_kv_heads * hd, cfg.ffn, cfg.vocab
     sl = lambda n: slice(rank * n // world, (rank + 1) * n // world)
     lays = [{"wq": L["wq"][sl(qd)], "wk": L["wk"][sl(kd)], "wv": L["wv"][sl(kd)], "wo": L["wo"][:, sl(qd)],
-             "wg": L["wg"][sl(F)], "wu": L["wu"][sl(F)], "wd": L["wd"][:, sl(F)]} for L in m["layers"]]
-    return {"embed": m["embed"], "lm_head": m["lm_head"][sl(V)], "layers": lays}
+             "wg": L["wg"][sl(F)], "wu": L["wu"][sl(F)], "wd": L["wd"][:, sl(F)], "ga": L["ga"], "gm": L["gm"]}
+            for L in m["layers"]]  # norm gains replicated
+    return {"embed": m["embed"], "lm_head": m["lm_head"][sl(V)], "layers": lays, "gf": m["gf"]}
 
 
 def _worker(rank, world, port, out):
