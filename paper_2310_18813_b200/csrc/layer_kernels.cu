@@ -358,10 +358,13 @@ __global__ void __launch_bounds__(128) attention_kernel(const T* __restrict__ q,
                                                         int nkv, int ctx_max, float scale) {
   constexpr int VE = AttnVec<T>::n;           // elements per 16B
   constexpr int KS = HD + 16 / (int)sizeof(T) * 1;  // padded row stride (elements): +16 bytes
-  __shared__ __align__(16) T Ks[kAttnKT][KS];
-  __shared__ __align__(16) T Vs[kAttnKT][HD];
-  __shared__ float Qs[QG][HD];
-  __shared__ float S[QG][kAttnKT];
+  // dynamic shared memory (fp32 at head_dim 128 needs ~78 KB): K tile | V tile | Q | S
+  extern __shared__ __align__(16) unsigned char attn_smem[];
+  T(*Ks)[KS] = reinterpret_cast<T(*)[KS]>(attn_smem);
+  T(*Vs)[HD] = reinterpret_cast<T(*)[HD]>(attn_smem + sizeof(T) * kAttnKT * KS);
+  float(*Qs)[HD] = reinterpret_cast<float(*)[HD]>(attn_smem + sizeof(T) * kAttnKT * (KS + HD));
+  float(*S)[kAttnKT] = reinterpret_cast<float(*)[kAttnKT]>(attn_smem + sizeof(T) * kAttnKT * (KS + HD) +
+                                                           sizeof(float) * QG * HD);
   __shared__ float m_run[QG], l_run[QG], corr[QG];
   __shared__ int qpos[QG];
   griddep_wait();
@@ -489,13 +492,36 @@ __global__ void __launch_bounds__(128) attention_kernel(const T* __restrict__ q,
   }
 }
 
+// dynamic shared memory of attention_kernel<T, HD, QG> (opted in by attention_tc_init)
+template <typename T, int HD, int QG>
+constexpr size_t attn_simt_smem() {
+  return sizeof(T) * kAttnKT * (2 * HD + 16 / sizeof(T)) + sizeof(float) * QG * (HD + kAttnKT);
+}
+
+template <typename T, int HD>
+static cudaError_t attn_simt_attr() {
+  cudaError_t e = cudaSuccess;
+#define SB_ATTN_SIMT_ATTR(QG)                                                                                   \
+  if (e == cudaSuccess)                                                                                         \
+  e = cudaFuncSetAttribute(attention_kernel<T, HD, QG>, cudaFuncAttributeMaxDynamicSharedMemorySize,            \
+                           (int)attn_simt_smem<T, HD, QG>())
+  SB_ATTN_SIMT_ATTR(1);
+  SB_ATTN_SIMT_ATTR(2);
+  SB_ATTN_SIMT_ATTR(4);
+  SB_ATTN_SIMT_ATTR(8);
+  SB_ATTN_SIMT_ATTR(16);
+#undef SB_ATTN_SIMT_ATTR
+  return e;
+}
+
 template <typename T, int HD>
 static int attn_dispatch(int q_len, dim3 grid_xy, const void* q, const void* kc, const void* vc, void* out,
                          const int32_t* slot, const int32_t* pos, int nq, int nkv, int ctx, float scale,
                          cudaStream_t st) {
 #define SB_ATTN(QG)                                                                                          \
-  return launch_k(attention_kernel<T, HD, QG>, dim3(grid_xy.x, grid_xy.y, (q_len + QG - 1) / QG), dim3(128), 0, st, \
-                  (const T*)q, (const T*)kc, (const T*)vc, (T*)out, slot, pos, q_len, nq, nkv, ctx, scale)
+  return launch_k(attention_kernel<T, HD, QG>, dim3(grid_xy.x, grid_xy.y, (q_len + QG - 1) / QG), dim3(128),   \
+                  attn_simt_smem<T, HD, QG>(), st, (const T*)q, (const T*)kc, (const T*)vc, (T*)out, slot, pos,   \
+                  q_len, nq, nkv, ctx, scale)
   if (q_len <= 1) SB_ATTN(1);
   if (q_len <= 2) SB_ATTN(2);
   if (q_len <= 4) SB_ATTN(4);
@@ -510,13 +536,13 @@ int launch_attention(int dtype, const void* q, const void* kc, const void* vc, v
   if ((hd != 64 && hd != 128) || nq % nkv != 0) return SB_EUNSUPPORTED;
   dim3 g(nq, n_seq, 1);
   float scale = 1.0f / sqrtf((float)hd);
-  if (dtype != SB_BF16 && hd == 128) return SB_EUNSUPPORTED;  // fp32 path: head_dim 64 (config-1 pair)
   if (dtype == SB_BF16)
     return hd == 128 ? attn_dispatch<__nv_bfloat16, 128>(q_len, g, q, kc, vc, out, tok_slot, tok_pos, nq, nkv, ctx_max,
                                                          scale, st)
                      : attn_dispatch<__nv_bfloat16, 64>(q_len, g, q, kc, vc, out, tok_slot, tok_pos, nq, nkv, ctx_max,
                                                         scale, st);
-  return attn_dispatch<float, 64>(q_len, g, q, kc, vc, out, tok_slot, tok_pos, nq, nkv, ctx_max, scale, st);
+  return hd == 128 ? attn_dispatch<float, 128>(q_len, g, q, kc, vc, out, tok_slot, tok_pos, nq, nkv, ctx_max, scale, st)
+                   : attn_dispatch<float, 64>(q_len, g, q, kc, vc, out, tok_slot, tok_pos, nq, nkv, ctx_max, scale, st);
 }
 
 // ---------------------------------------------------------------- tensor-core flash decoding (bf16)
@@ -584,6 +610,10 @@ int attention_tc_init() {
     SB_ATTN_ATTR(64, 3);
     SB_ATTN_ATTR(64, 4);
     SB_ATTN_ATTR(64, 6);
+    if (e == cudaSuccess) e = attn_simt_attr<__nv_bfloat16, 64>();
+    if (e == cudaSuccess) e = attn_simt_attr<__nv_bfloat16, 128>();
+    if (e == cudaSuccess) e = attn_simt_attr<float, 64>();
+    if (e == cudaSuccess) e = attn_simt_attr<float, 128>();
 #undef SB_ATTN_ATTR
     rc = e == cudaSuccess ? 0 : (int)e;
   }
