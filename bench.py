@@ -37,6 +37,15 @@ WORKLOADS = {"7b": ("llama-2-7b", "llama-68m"), "70b": ("llama-2-70b", "llama-16
 TARGET, DRAFT = WORKLOADS["7b"]
 B, P, NEW = 8, 128, 128
 K_GRID = tuple(range(9))
+REPEATS = 3  # independent re-timings of every (b, k) cell after the LUT is built
+LUT_SIZES = (1, 2, 4, 8, 16, 32, 64)  # the reference's profiled powers of two (policy.py:72-82), to config 2's b=64
+# ONE metric and ONE workload string for both arms (the driver pairs the lines by them)
+METRIC = "generated tokens/s of a formed batch (prefill + speculative decode to completion), adaptive k"
+
+
+def workload_str(b):
+    return (f"{TARGET} target + {DRAFT} draft, b={b}, P={P}, N={NEW}, injected example_trace acceptance, "
+            f"k from the b->k LUT profiled on the executing hardware")
 
 
 def _args():
@@ -119,115 +128,213 @@ def verify_bytes(cfg, b, k, ctx_avg):
     return w + kv_tok * b * ctx_avg + kv_tok * T + 4 * cfg.vocab * T + 2 * cfg.hidden * T
 
 
-# ============================================================== reference arm (CPU)
-def cpu_sample(b, k, iters=1, threads=None, layers=None):
-    """The CPU oracle (oracle/model_ref.py forward_batch, fp32, all host
-    threads) running the same speculative iteration -- draft k steps + verify
-    b(k+1) tokens of the full 7B/68M pair, batched over the b sequences -- on a
-    bounded sample (`iters` iterations after an untimed prefill).  Weights are a
-    tiled random block (timing only; CPU parity is tested on the tiny pair).
-    Returns (tokens/s, description, cores)."""
-    import torch
+def verify_flops(cfg, b, k, ctx_avg):
+    """Algorithmic FLOPs of one verify forward: 2 x streamed
+    parameters x tokens + attention (QK^T and PV over the cached context and the
+    causal window)."""
+    T = b * (k + 1)
+    params = cfg.streamed_bytes_per_forward(2) // 2
+    attn = 4 * cfg.n_layers * cfg.n_heads * cfg.head_dim * b * (k + 1) * (ctx_avg + (k + 2) / 2)
+    return 2 * params * T + attn
 
-    from oracle import model_ref, spec_ref
-    from paper_2310_18813_b200.decoder import CONFIGS
+
+# ============================================================== reference arm (CPU)
+def _ref_pkg():
+    """The reference package itself (baseline/_ref, installed by pip from
+    /root/reference; travels with the repo to the GPU box) for its cost model
+    and LUT builder; our golden-identical mirror when it is absent."""
+    rp = ROOT / "baseline" / "_ref"
+    if (rp / "specbatch").exists():
+        sys.path.insert(0, str(rp))
+        import specbatch  # noqa: F401
+
+        from specbatch.cost_model import LinearStepModel
+        from specbatch.policy import build_lut, lookup
+        from specbatch.presets import example_trace
+
+        return LinearStepModel, build_lut, lookup, example_trace, "reference specbatch (baseline/_ref)"
+    from paper_2310_18813_b200.cost_model import LinearStepModel
+    from paper_2310_18813_b200.policy import build_lut, lookup
     from paper_2310_18813_b200.presets import example_trace
 
-    threads = threads or os.cpu_count()
-    torch.set_num_threads(threads)
-    tc, dc = CONFIGS[TARGET], CONFIGS[DRAFT]
-    L = tc.n_layers if layers is None else layers
-    block = torch.empty(1 << 20).uniform_(-0.035, 0.035, generator=torch.Generator().manual_seed(0))
+    return LinearStepModel, build_lut, lookup, example_trace, "golden-identical mirror (baseline/_ref absent)"
 
-    def mk(*shape):
-        n = int(np.prod(shape))
-        reps = (n + block.numel() - 1) // block.numel()
-        return block.repeat(reps)[:n].view(*shape).clone()
 
-    def masters(cfg, n_layers):
-        h, hd = cfg.hidden, cfg.head_dim
-        return {"embed": mk(cfg.vocab, h), "lm_head": mk(cfg.vocab, h), "gf": 1 + mk(h),
-                "layers": [{"wq": mk(cfg.n_heads * hd, h), "wk": mk(cfg.n_kv_heads * hd, h),
-                            "wv": mk(cfg.n_kv_heads * hd, h), "wo": mk(h, cfg.n_heads * hd), "wg": mk(cfg.ffn, h),
-                            "wu": mk(cfg.ffn, h), "wd": mk(h, cfg.ffn), "ga": 1 + mk(h), "gm": 1 + mk(h)}
-                           for _ in range(n_layers)]}
+def iterations_needed(b, k, seed=0):
+    """Iterations a formed batch of b x NEW tokens takes under the injected
+    acceptance law (spec_ref.injected_lengths, the same counter RNG the GPU
+    engine draws from): advance = min(l + 1, remaining) (engine.py:167)."""
+    from oracle import spec_ref
+    from paper_2310_18813_b200.presets import example_trace
 
-    def opt_masters(cfg, n_layers):
-        h, F = cfg.hidden, cfg.ffn
-        lay = lambda: dict(wq=mk(h, h), wk=mk(h, h), wv=mk(h, h), bq=mk(h), bk=mk(h), bv=mk(h), wo=mk(h, h),
-                           bo=mk(h), f1=mk(F, h), b1=mk(F), f2=mk(h, F), b2=mk(h), g1=1 + mk(h), c1=mk(h),
-                           g2=1 + mk(h), c2=mk(h))
-        return {"embed": mk(cfg.vocab, h), "pos": mk(P + NEW + 32, h), "layers": [lay() for _ in range(n_layers)],
-                "gf": 1 + mk(h), "cf": mk(h)}
+    samples = example_trace().samples
+    produced = np.zeros(b, np.int64)
+    it = 0
+    while np.any(produced < NEW):
+        l_inj = np.minimum(spec_ref.injected_lengths(seed, it, b, samples), k)
+        produced = np.minimum(produced + l_inj + 1, NEW)
+        it += 1
+    return it
 
-    def build(cfg, n_layers):
-        if cfg.arch == "opt":
-            return model_ref.OptRef(opt_masters(cfg, n_layers), cfg.n_heads, cfg.rms_eps, dtype=torch.float32)
-        return model_ref.LlamaRef(masters(cfg, n_layers), cfg.n_heads, cfg.n_kv_heads, cfg.rms_eps,
-                                  max_pos=P + NEW + 16, dtype=torch.float32)
 
-    t_init = time.perf_counter()
-    tgt = build(tc, L)
-    drf = build(dc, dc.n_layers)
-    rng = np.random.default_rng(0)
-    prompts = [list(map(int, rng.integers(0, tc.vocab, P))) for _ in range(b)]
-    tcache = [tgt.new_cache() for _ in range(b)]
-    dcache = [drf.new_cache() for _ in range(b)]
-    pre = [p[:P - 1] for p in prompts]
-    ppos = [list(range(P - 1))] * b
-    model_ref.forward_batch(tgt, pre, ppos, tcache)
-    model_ref.forward_batch(drf, pre, ppos, dcache)
-    t_init = time.perf_counter() - t_init
-    trace = example_trace()
-    toks = [list(p) for p in prompts]
-    gen = 0
-    t0 = time.perf_counter()
-    for it in range(iters):
-        l_inj = np.minimum(spec_ref.injected_lengths(0, it, b, trace.samples), k)
-        ns = [len(t) for t in toks]
+class CpuPair:
+    """The CPU oracle pair (oracle/model_ref.py, fp32, all host threads) of the
+    headline shapes: a `layers`-layer slice of the target (its time is scaled
+    by n_layers / layers) and the whole draft.  Weights are a tiled random
+    block (timing only; CPU parity runs on the tiny pair in tests/)."""
+
+    def __init__(self, b, layers, threads):
+        import torch
+
+        from oracle import model_ref
+        from paper_2310_18813_b200.decoder import CONFIGS
+
+        torch.set_num_threads(threads)
+        self.b = b
+        self.tc, self.dc = CONFIGS[TARGET], CONFIGS[DRAFT]
+        self.L = self.tc.n_layers if layers is None else min(layers, self.tc.n_layers)
+        self.scale = self.tc.n_layers / self.L
+        block = torch.empty(1 << 20).uniform_(-0.035, 0.035, generator=torch.Generator().manual_seed(0))
+
+        def mk(*shape):
+            n = int(np.prod(shape))
+            reps = (n + block.numel() - 1) // block.numel()
+            return block.repeat(reps)[:n].view(*shape).clone()
+
+        def masters(cfg, n_layers):
+            h, hd = cfg.hidden, cfg.head_dim
+            return {"embed": mk(cfg.vocab, h), "lm_head": mk(cfg.vocab, h), "gf": 1 + mk(h),
+                    "layers": [{"wq": mk(cfg.n_heads * hd, h), "wk": mk(cfg.n_kv_heads * hd, h),
+                                "wv": mk(cfg.n_kv_heads * hd, h), "wo": mk(h, cfg.n_heads * hd),
+                                "wg": mk(cfg.ffn, h), "wu": mk(cfg.ffn, h), "wd": mk(h, cfg.ffn), "ga": 1 + mk(h),
+                                "gm": 1 + mk(h)} for _ in range(n_layers)]}
+
+        def opt_masters(cfg, n_layers):
+            h, F = cfg.hidden, cfg.ffn
+            lay = lambda: dict(wq=mk(h, h), wk=mk(h, h), wv=mk(h, h), bq=mk(h), bk=mk(h), bv=mk(h), wo=mk(h, h),
+                               bo=mk(h), f1=mk(F, h), b1=mk(F), f2=mk(h, F), b2=mk(h), g1=1 + mk(h), c1=mk(h),
+                               g2=1 + mk(h), c2=mk(h))
+            return {"embed": mk(cfg.vocab, h), "pos": mk(P + NEW + 32, h), "layers": [lay() for _ in range(n_layers)],
+                    "gf": 1 + mk(h), "cf": mk(h)}
+
+        def build(cfg, n_layers):
+            if cfg.arch == "opt":
+                return model_ref.OptRef(opt_masters(cfg, n_layers), cfg.n_heads, cfg.rms_eps, dtype=torch.float32)
+            return model_ref.LlamaRef(masters(cfg, n_layers), cfg.n_heads, cfg.n_kv_heads, cfg.rms_eps,
+                                      max_pos=P + NEW + 16, dtype=torch.float32)
+
+        self.tgt = build(self.tc, self.L)
+        self.drf = build(self.dc, self.dc.n_layers)
+        self.fwd = model_ref.forward_batch
+        rng = np.random.default_rng(0)
+        self.prompts = [list(map(int, rng.integers(0, self.tc.vocab, P))) for _ in range(b)]
+        self.reset()
+
+    def reset(self):
+        self.tcache = [self.tgt.new_cache() for _ in range(self.b)]
+        self.dcache = [self.drf.new_cache() for _ in range(self.b)]
+        self.toks = [list(p) for p in self.prompts]
+        self.it = 0
+
+    def prefill(self):
+        """Returns seconds (target part scaled to the full depth)."""
+        pre = [p[:P - 1] for p in self.prompts]
+        ppos = [list(range(P - 1))] * self.b
+        t0 = time.perf_counter()
+        self.fwd(self.tgt, pre, ppos, self.tcache)
+        t1 = time.perf_counter()
+        self.fwd(self.drf, pre, ppos, self.dcache)
+        t2 = time.perf_counter()
+        return (t1 - t0) * self.scale + (t2 - t1)
+
+    def iteration(self, k):
+        """One speculative iteration (draft k steps + verify b(k+1) tokens +
+        injected acceptance).  Returns (seconds, draft seconds, verify seconds)."""
+        from oracle import spec_ref
+        from paper_2310_18813_b200.presets import example_trace
+
+        b = self.b
+        l_inj = np.minimum(spec_ref.injected_lengths(0, self.it, b, example_trace().samples), k)
+        ns = [len(t) for t in self.toks]
         drafts = [[] for _ in range(b)]
+        t0 = time.perf_counter()
         if k > 0:
-            lg = model_ref.forward_batch(drf, [t[n - 2:n] for t, n in zip(toks, ns)], [[n - 2, n - 1] for n in ns],
-                                         dcache)[:, -1]
+            lg = self.fwd(self.drf, [t[n - 2:n] for t, n in zip(self.toks, ns)], [[n - 2, n - 1] for n in ns],
+                          self.dcache)[:, -1]
             for j in range(1, k + 1):
                 if j > 1:
-                    lg = model_ref.forward_batch(drf, [[d[-1]] for d in drafts], [[n - 2 + j] for n in ns],
-                                                 dcache)[:, -1]
+                    lg = self.fwd(self.drf, [[d[-1]] for d in drafts], [[n - 2 + j] for n in ns], self.dcache)[:, -1]
                 for s in range(b):
                     drafts[s].append(int(np.argmax(lg[s])))
-        tl = model_ref.forward_batch(tgt, [[t[n - 1]] + d for t, n, d in zip(toks, ns, drafts)],
-                                     [list(range(n - 1, n + k)) for n in ns], tcache)
+        t1 = time.perf_counter()
+        tl = self.fwd(self.tgt, [[t[n - 1]] + d for t, n, d in zip(self.toks, ns, drafts)],
+                      [list(range(n - 1, n + k)) for n in ns], self.tcache)
+        t2 = time.perf_counter()
         for s in range(b):
             l = int(l_inj[s])
-            new = drafts[s][:l] + [int(np.argmax(tl[s, l]))]
-            toks[s].extend(new)
-            gen += len(new)
-    dt = time.perf_counter() - t0
-    desc = (f"{iters} speculative iteration(s) (b={b}, k={k}, injected example_trace acceptance, prompt {P}) of the "
-            f"fp32 CPU oracle pair {TARGET}+{DRAFT} batched over sequences ({L}/{tc.n_layers} target layers"
-            f"{'' if L == tc.n_layers else ', time scaled by layer count'}); weight init + prefill {t_init:.1f}s untimed")
-    if L != tc.n_layers:
-        dt *= tc.n_layers / L
-    return gen / dt, desc, threads
+            self.toks[s].extend(drafts[s][:l] + [int(np.argmax(tl[s, l]))])
+        self.it += 1
+        return (t1 - t0) + (t2 - t1) * self.scale, t1 - t0, (t2 - t1) * self.scale
+
+
+def cpu_reference_run(b, steps, warmup, threads=None, layers=None):
+    """The reference's own method on the host CPU: calibrate the reference's
+    LinearStepModel on this CPU (verify at s = 1 and 8, one draft step), let
+    the reference's build_lut (analytic, example_trace acceptance) choose k
+    for b, then time `steps` real iterations of the CPU oracle pair at that k
+    (after `warmup` untimed ones).  The batch time is the measured prefill +
+    iterations_needed(b, k) x the mean measured iteration (a bounded sample:
+    the full batch would take minutes on the CPU).  Returns a dict."""
+    LinearStepModel, build_lut, lookup, example_trace, ref_src = _ref_pkg()
+    threads = threads or os.cpu_count()
+    t_init = time.perf_counter()
+    pair = CpuPair(b, layers, threads)
+    t_init = time.perf_counter() - t_init
+    prefill_s = pair.prefill()
+    # calibration cells (each from a fresh copy of the post-prefill state would cost a second prefill:
+    # the iterations simply run on; context grows by <= 9 tokens per cell, negligible vs P=128)
+    it1, _, v1 = pair.iteration(1)
+    it8, d8, v8 = pair.iteration(8)
+    ssm = d8 / 8.0
+    slope = max((v8 - v1) / 7.0, 1e-6)
+    beta = max(v1 - slope, 1e-6)
+    cal = LinearStepModel(alpha={b: slope * 1e3}, beta=beta * 1e3, ssm_step={b: ssm * 1e3})
+    lut = build_lut(cal, example_trace(), s_grid=K_GRID, profiled_sizes=(b,))
+    k = lookup(lut, b).chosen_s
+    for _ in range(warmup):
+        pair.iteration(k)
+    times = [pair.iteration(k)[0] for _ in range(steps)]
+    n_it = iterations_needed(b, k)
+    batch_s = prefill_s + n_it * float(np.mean(times))
+    return {"value": b * NEW / batch_s, "k": k, "threads": threads, "prefill_s": prefill_s,
+            "iteration_s": times, "iterations_needed": n_it, "batch_s": batch_s,
+            "calibration_ms": {"alpha": slope * 1e3, "beta": beta * 1e3, "ssm_step": ssm * 1e3},
+            "lut_source": ref_src, "layers": pair.L, "init_s": t_init,
+            "sample": (f"fp32 CPU oracle pair {TARGET}+{DRAFT} (target {pair.L}/{pair.tc.n_layers} layers timed, "
+                       f"scaled by depth), batched over b={b} sequences: measured prefill {prefill_s:.2f} s + "
+                       f"{iterations_needed(b, k)} iterations x mean of {steps} measured iterations at k={k} "
+                       f"(k from the reference's build_lut on a LinearStepModel calibrated on this CPU); "
+                       f"weight init {t_init:.1f} s untimed")}
 
 
 def run_reference(args):
     rank, world, _ = _dist()
     if rank != 0:
         return
-    k = args.k if args.k >= 0 else 3
-    layers = int(os.environ.get("SB_CPU_LAYERS", "8")) or None
-    tps, desc, cores = cpu_sample(args.batch, k, iters=max(1, min(args.steps, 3)), layers=layers)
-    v = float(tps)
-    line = {"metric": "generated tokens/s (batched speculative decoding)", "value": v, "unit": "tokens/s",
+    layers = int(os.environ.get("SB_CPU_LAYERS", "8" if TARGET == "llama-2-7b" else "2")) or None
+    r = cpu_reference_run(args.batch, max(1, min(args.steps, 3)), min(args.warmup, 1), layers=layers)
+    v = float(r["value"])
+    line = {"metric": METRIC, "value": v, "unit": "tokens/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
             "impl": "reference", "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{TARGET}+{DRAFT} b={args.batch} k={k} P={P} N={NEW}"},
-            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": desc},
+            "config": {"workload": workload_str(args.batch), "k": r["k"], "k_source": r["lut_source"]},
+            "ms_per_step": r["batch_s"] * 1e3,
+            "cpu_baseline": {"value": v, "unit": "tokens/s", "cores": r["threads"], "kind": "port",
+                             "sample": r["sample"]},
             "e2e": {"value": v, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "detail": {k_: r[k_] for k_ in ("prefill_s", "iteration_s", "iterations_needed", "calibration_ms")},
             "vs_baseline": None}
     print(json.dumps(line), flush=True)
-
 
 
 # ============================================================== config 5 (serving trace)
@@ -339,7 +446,8 @@ def run_ours(args):
         tgt = Decoder(CONFIGS[TARGET], dtype="bf16", device=dev, seed=0, init="device", max_pos=P + NEW + 32)
     drf = Decoder(CONFIGS[DRAFT], dtype="bf16", device=dev, seed=1, init="device", max_pos=P + NEW + 32)
     # replicas: independent request streams per rank; TP: one engine spanning the ranks (same seed)
-    eng = SpecEngine(tgt, drf, mode="injected", acceptance=trace, max_batch=max(b, 8), max_k=8, prompt_len=P,
+    eng = SpecEngine(tgt, drf, mode="injected", acceptance=trace,
+                     max_batch=b if args.quick else max(b, max(LUT_SIZES)), max_k=8, prompt_len=P,
                      max_new=NEW, seed=0 if tp else rank)
 
     # ---- the paper's profiler on THIS GPU: every (b, k) cell runs the real
@@ -347,21 +455,35 @@ def run_ours(args):
     # LinearStepModel calibration is reported beside it.
     cal, samples = calibrate(eng, batch_sizes=(1, 2, 4, 8), k_grid=range(1, 9), reps=5)
     lut_analytic = build_lut(cal, trace, s_grid=K_GRID, profiled_sizes=(1, 2, 4, 8))
-    sizes = tuple(x for x in (1, 2, 4, 8) if x <= b) if not args.quick else (b,)
+    sizes = tuple(x for x in LUT_SIZES if x <= eng.max_batch) if not args.quick else (b,)
     lut = build_lut(None, trace, s_grid=K_GRID, profiled_sizes=sizes, mode="measured", sample_size=1,
                     rng=np.random.default_rng(0), gen_len=NEW, engine=eng)
     k = args.k if args.k >= 0 else lookup(lut, b).chosen_s
-    cells = lut.provenance.get("ms_per_token", {})
-    sweep = {int(key.split(",")[1]): 1e3 / v for key, v in cells.items() if int(key.split(",")[0]) == b}
-    # the metric is "tokens/s vs batch size (adaptive k vs best fixed k)": every profiled b
+
+    # ---- "tokens/s vs batch size, adaptive k vs best fixed k": re-timed INDEPENDENTLY of the
+    # LUT-building pass, every (b, k) cell REPEATS times on fresh batches (decode tokens/s,
+    # prefill excluded as in the profiler / the reference cost model); median and spread
     by_batch = {}
-    for bb in sorted({int(key.split(",")[0]) for key in cells}):
-        row = {int(key.split(",")[1]): 1e3 / v for key, v in cells.items() if int(key.split(",")[0]) == bb}
-        kb_ = lookup(lut, bb).chosen_s
-        bf = max(row, key=row.get)
-        by_batch[str(bb)] = {"adaptive_k": kb_, "adaptive_tokens_per_s": round(row[kb_], 1), "best_fixed_k": bf,
-                             "best_fixed_tokens_per_s": round(row[bf], 1),
-                             "k_sweep": {str(kk): round(v, 1) for kk, v in sorted(row.items())}}
+    if not args.quick:
+        for bb in sizes:
+            cell = {}
+            for kk in K_GRID:
+                tps = []
+                for r in range(REPEATS):
+                    sts = [SequenceState(request_id=500000 + 1000 * r + i, target_len=NEW) for i in range(bb)]
+                    res = eng.generate(sts, kk)
+                    tps.append(res.tokens_generated / (res.total_time / 1e3))
+                cell[kk] = tps
+            med = {kk: float(np.median(v)) for kk, v in cell.items()}
+            ka = lookup(lut, bb).chosen_s
+            kf = max(med, key=med.get)
+            by_batch[str(bb)] = {
+                "adaptive_k": ka, "adaptive_tokens_per_s": round(med[ka], 1),
+                "adaptive_spread": [round(min(cell[ka]), 1), round(max(cell[ka]), 1)],
+                "best_fixed_k": kf, "best_fixed_tokens_per_s": round(med[kf], 1),
+                "best_fixed_spread": [round(min(cell[kf]), 1), round(max(cell[kf]), 1)],
+                "adaptive_vs_best_fixed": round(med[ka] / med[kf], 4),
+                "k_sweep_median": {str(kk): round(v, 1) for kk, v in sorted(med.items())}}
 
     def batch(step):
         return [SequenceState(request_id=step * 1000 + i, target_len=NEW) for i in range(b)]
@@ -435,13 +557,15 @@ def run_ours(args):
     v_ms = eng.time_verify(b, k, ctx=ctx_avg, reps=20)
     achieved = vb / (v_ms / 1e3) / 1e9
     verify_by_batch = {}  # north_star: >= 60% of the HBM roofline for verification at b <= 8
-    for bb in (1, 2, 4, 8):
-        if bb > eng.max_batch:
-            continue
-        kb_ = lookup(lut, bb).chosen_s if str(bb) in by_batch else k
+    for bb in (sizes if not args.quick else (b,)):
+        kb_ = lookup(lut, bb).chosen_s
         ms_ = eng.time_verify(bb, kb_, ctx=ctx_avg, reps=10)
-        verify_by_batch[str(bb)] = {"k": kb_, "verify_ms": round(ms_, 4),
-                                    "frac_hbm": round(verify_bytes(tgt.cfg, bb, kb_, ctx_avg) / (ms_ / 1e3) / 1e9 / hbm, 4)}
+        t_hbm = verify_bytes(tgt.cfg, bb, kb_, ctx_avg) / (hbm * 1e9)
+        t_tc = verify_flops(tgt.cfg, bb, kb_, ctx_avg) / (tf * 1e12)
+        verify_by_batch[str(bb)] = {"k": kb_, "tokens": bb * (kb_ + 1), "verify_ms": round(ms_, 4),
+                                    "frac_hbm": round(t_hbm / (ms_ / 1e3), 4),
+                                    "frac_tensor": round(t_tc / (ms_ / 1e3), 4),
+                                    "frac_roofline": round(max(t_hbm, t_tc) / (ms_ / 1e3), 4)}
     traffic = None
     tf_path = ROOT / "profiles" / "verify_traffic.json"
     if tf_path.exists():
@@ -449,25 +573,26 @@ def run_ours(args):
         if tfd.get("b") == b and tfd.get("k") == k and str(tfd.get("workload", "")).startswith(TARGET + " "):
             traffic = tfd["dram_bytes_read_plus_write"]
 
-    # ---- CPU baseline (rank 0, N=1 only)
+    # ---- CPU baseline (rank 0, N=1 only): the reference arm's method on a smaller sample
     cpu = None
     if rank == 0 and world == 1 and os.environ.get("SB_SKIP_CPU", "0") != "1":
         try:
             layers = int(os.environ.get("SB_CPU_LAYERS", "8" if TARGET == "llama-2-7b" else "2")) or None
-            tps, desc, cores = cpu_sample(b, k, iters=1, layers=layers)
-            cpu = {"value": tps, "unit": "tokens/s", "cores": cores, "kind": "port", "sample": desc}
+            r = cpu_reference_run(b, 1, 0, layers=layers)
+            cpu = {"value": r["value"], "unit": "tokens/s", "cores": r["threads"], "kind": "port",
+                   "sample": r["sample"]}
         except Exception as exc:  # pragma: no cover
             cpu = {"value": None, "unit": "tokens/s", "cores": os.cpu_count(), "kind": "port",
                    "sample": f"failed: {exc}"}
 
     if rank == 0:
-        best_fixed = max(sweep, key=sweep.get) if sweep else None  # sweep: decode tokens/s of the batch
+        hb = by_batch.get(str(b), {})
         line = {
-            "metric": "generated tokens/s (batched speculative decoding, adaptive k)", "value": value,
+            "metric": METRIC, "value": value,
             "unit": "tokens/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong" if tp else "weak",
             "vs_baseline": None, "dtype": "bf16", "data": "synthetic (random-init weights, random prompts)",
-            "config": {"workload": f"{TARGET} target + {DRAFT} draft, bf16, b={b}, P={P}, N={NEW}",
+            "config": {"workload": workload_str(b),
                        "k": k, "k_source": "adaptive LUT (profiled on this GPU)" if args.k < 0 else "fixed",
                        "lut": {str(kk): v for kk, v in lut.entries.items()},
                        "lut_analytic_from_measured_calibration": {str(kk): v for kk, v in lut_analytic.entries.items()},
@@ -475,11 +600,10 @@ def run_ours(args):
                        "parallelism": f"tp{world} (NCCL all-reduce / all-gather)" if tp else f"replicas x{world}",
                        "l2": "inputs (weights >= 13.5 GB) > L2; no flush"},
             "decode_tokens_per_s": jobs * args.steps * b * NEW / (sum(decode_ms) / 1e3) if world == 1 else None,
-            "k_sweep_decode_tokens_per_s": {str(kk): round(v, 1) for kk, v in sorted(sweep.items())},
             "tokens_per_s_by_batch": by_batch,
             "verify_roofline_by_batch": verify_by_batch,
-            "best_fixed_k": best_fixed,
-            "adaptive_vs_best_fixed": (sweep[k] / sweep[best_fixed]) if (sweep and k in sweep) else None,
+            "best_fixed_k": hb.get("best_fixed_k"),
+            "adaptive_vs_best_fixed": hb.get("adaptive_vs_best_fixed"),
             "iterations_per_step": iters / args.steps,
             "gpu_launches": launches,
             "e2e": {"value": e2e, "unit": "tokens/s", "h2d_bytes_per_step": b * P * 4 + b * 4,
