@@ -48,7 +48,7 @@ def serve_continuous(workload: list[Request], engine, policy, time_scale: float 
     admitted while other rows decode are prefilled INSIDE the next iteration's
     verify forward (sb_decoder_forward_mixed, one weight stream) and decode from
     the iteration after; otherwise each admission runs its own prefill forward.
-    Returns (report, {"mean_live_batch", "mean_k", "iterations"[, "outputs": {id: tokens}]}).
+    Returns (report, {"mean_live_batch", "mean_k", "iterations", "acceptance_rate"[, "outputs": {id: tokens}]}).
     """
     if any(nxt.arrival < cur.arrival for cur, nxt in zip(workload, workload[1:])):
         raise ValueError("workload must be sorted by arrival time")
@@ -69,6 +69,8 @@ def serve_continuous(workload: list[Request], engine, policy, time_scale: float 
     nxt, total = 0, len(workload)
     pinned_prompts = torch.zeros(B, P, dtype=torch.int32, pin_memory=True)
     done_host = torch.zeros(eng.max_batch, dtype=torch.int32, pin_memory=True)
+    acc_sum = torch.zeros(1, dtype=torch.int64, device=dev)  # accepted drafts over live rows (k > 0 iterations)
+    proposed = 0
     k_hist: list[int] = []
     b_hist: list[int] = []
     outputs: dict[int, list[int]] = {}
@@ -135,10 +137,17 @@ def serve_continuous(workload: list[Request], engine, policy, time_scale: float 
             k = policy.decide(b_run).chosen_s
             k = min(k, eng.max_k)
             ti = clock()
+            # k = 0 iterations keep the draft KV current: the policy may pick k > 0 next
+            sync = k == 0 and eng.max_k > 0
             if ride:
-                eng._iteration(b_run, k, ride=ride)
+                eng._iteration(b_run, k, ride=ride, draft_sync=sync)
+            elif eng.use_graphs:
+                eng._graph(b, k, draft_sync=sync).replay()
             else:
-                eng._graph(b, k).replay() if eng.use_graphs else eng._iteration(b, k)
+                eng._iteration(b, k, draft_sync=sync)
+            if k > 0:
+                acc_sum += eng.accepted[:b_run].sum()
+                proposed += k * b_run
             k_hist.append(k)
             b_hist.append(b_run)
             # ---- retirement: rows whose produced reached target_len
@@ -174,6 +183,7 @@ def serve_continuous(workload: list[Request], engine, policy, time_scale: float 
     rep = summarize(records, group_size=group_size, policy=f"continuous/{getattr(policy, 'label', 'policy')}")
     extra = {"mean_live_batch": float(np.mean(b_hist)) if b_hist else 0.0,
              "mean_k": float(np.mean(k_hist)) if k_hist else 0.0, "iterations": len(k_hist),
+             "acceptance_rate": float(acc_sum.item()) / proposed if proposed else 0.0,
              "wall_s": clock() - t0, **{k_: round(v_, 3) if isinstance(v_, float) else v_ for k_, v_ in prof.items()}}
     if collect:
         extra["outputs"] = outputs

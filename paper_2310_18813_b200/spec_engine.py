@@ -142,7 +142,6 @@ class SpecEngine:
         self.stream = torch.cuda.Stream(device=self.dev)
         self.graphs: dict[tuple[int, int], torch.cuda.CUDAGraph] = {}
         self._iter_kernels: dict[tuple[int, int], int] = {}
-        self._sinks: list = []  # keep ctypes sink structs alive while graphs reference their contents
         self.stats = IterationStats()
         self.tuning = {}
         self.autotune = autotune
@@ -161,11 +160,17 @@ class SpecEngine:
         return rng.integers(0, self.V, size=self.prompt_len, dtype=np.int64).astype(np.int32)
 
     # ------------------------------------------------------------- one iteration
-    def _iteration(self, b: int, k: int, ride: int = 0) -> None:
+    def _iteration(self, b: int, k: int, ride: int = 0, draft_sync: bool = False) -> None:
         """One speculative iteration over rows [0, b).  ``ride`` > 0 (eager only):
         rows [b, b + ride) hold freshly admitted prompts whose target prefill rides
         inside this iteration's verify forward (sb_decoder_forward_mixed) and whose
-        draft prefill runs alongside; they join the next iteration."""
+        draft prefill runs alongside; they join the next iteration.
+
+        ``draft_sync`` (k = 0 only): also run the draft over the last two committed
+        tokens (KV only).  Draft step 1 of a k > 0 iteration re-feeds just those
+        two, so the draft KV must be valid up to n_tok - 3; a k = 0 iteration
+        advances every row by one token without the draft, which would leave a
+        hole once a caller switches k per iteration (serving.serve_continuous)."""
         st = torch.cuda.current_stream(self.dev).cuda_stream
         lib = N.load()
         q_pf = self.prompt_len - 1
@@ -182,11 +187,17 @@ class SpecEngine:
         mode = self.mode_id
         sample = mode == N.ACCEPT_STOCHASTIC
         use_draft = k > 0 and self.draft is not None
+        sync_draft = draft_sync and k == 0 and self.draft is not None
         N.call("sb_prepare_iteration", b, k, N.ptr(self.tokens), self.cap, N.ptr(self.n_tok),
-               N.ptr(self.d1_ids) if use_draft else None, N.ptr(self.d1_pos) if use_draft else None,
+               N.ptr(self.d1_ids) if use_draft or sync_draft else None,
+               N.ptr(self.d1_pos) if use_draft or sync_draft else None,
                N.ptr(self.v_ids), N.ptr(self.v_pos), N.ptr(self.d_base), self.seed, N.ptr(self.iter),
                N.ptr(self.uniforms), _NU, N.ptr(self.inj_samples), self.inj_samples.numel(),
                N.ptr(self.l_inj), st)
+        if sync_draft:
+            self.draft.forward(self.kv_d, self.d1_ids, self.slots, self.d1_pos, b, 2, None, N.LOGITS_NONE,
+                               self.workspace, st)
+            launches += lib.sb_last_kernel_count()
         greedy_draft = not sample
         # the fp32 path and a tensor-parallel target select from materialised (full-width) logits
         need_logits = self.target.sb_dtype != N.SB_BF16 or self.target.is_tp
@@ -213,7 +224,6 @@ class SpecEngine:
                 if greedy_draft:
                     sink = N.SbTokenSink(self.v_ids.data_ptr() + j * 4, k + 1, self.ds_ids.data_ptr(),
                                          self.ds_pos.data_ptr(), self.d_base.data_ptr(), j)
-                    self._sinks.append(sink)
                     self.draft.forward_greedy(self.kv_d, ids, self.slots, pos, b, q,
                                               self.d_logits if need_logits else None, N.LOGITS_LAST,
                                               self.workspace, sink, st)
@@ -249,12 +259,11 @@ class SpecEngine:
             launches += 1
         else:
             sink = N.SbTokenSink(self.t_tok.data_ptr(), 1, None, None, None, 0)
-            self._sinks.append(sink)
             self.target.forward_greedy(self.kv_t, self.v_ids, self.slots, self.v_pos, b, k + 1,
                                        self.t_logits if need_logits else None, N.LOGITS_ALL, self.workspace, sink,
                                        st)
             launches += lib.sb_last_kernel_count()
-        if not ride:
+        if not ride and not sync_draft:
             self._iter_kernels[(b, k)] = launches
         u_base = self.uniforms.data_ptr()
         N.call("sb_accept", mode, b, k, V, N.ptr(self.t_tok), N.ptr(self.t_logits),
@@ -281,11 +290,12 @@ class SpecEngine:
         last issued (forward driver count + one per token-level kernel)."""
         return self._iter_kernels.get((b, k), 0)
 
-    def _graph(self, b: int, k: int):
-        key = (b, k)
+    def _graph(self, b: int, k: int, draft_sync: bool = False):
+        draft_sync = draft_sync and k == 0 and self.draft is not None
+        key = (b, k, "sync") if draft_sync else (b, k)
         g = self.graphs.get(key)
         if g is None:
-            g = _capture_graph(lambda: self._iteration(b, k), self.stream)
+            g = _capture_graph(lambda: self._iteration(b, k, draft_sync=draft_sync), self.stream)
             self.graphs[key] = g
         return g
 

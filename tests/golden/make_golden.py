@@ -12,6 +12,11 @@ Outputs (committed, small):
   policy.json      -- analytic + simulated LUTs, lookup table, fixed policies
   serving.json     -- traffic generation + run_simulation reports
   cost_model.json  -- predict_runtime / delta / optimum values
+  files/           -- the six file formats written by the reference's own
+                      writers (trace CSV, LUT CSV, calibration JSON, workload
+                      CSV, simulation records CSV, report JSON) plus a
+                      step-sample CSV in the layout of its reader; pins the
+                      byte format of our writers and our readers
 """
 
 from __future__ import annotations
@@ -188,10 +193,57 @@ def cost_cases():
     out["delta"] = [[s, rcm.eval_delta(prm, s)] for s in (0.5, 1, 2, 3, 4.5, 8)]
     out["root"] = rcm.optimal_speculation_continuous(prm, 1, 8, tol=1e-7)
     out["discrete"] = [[b, rcm.optimal_speculation_discrete(cal, fit, 128, b, range(9))] for b in (1, 2, 4, 8, 16, 32)]
+    # OLS fits of step samples (cost_model.py:145-170) and the acceptance power law (acceptance.py:85-106)
+    rng = np.random.default_rng(11)
+    fits = []
+    for b in (1, 4, 16):
+        ys = [float(2.5 + 0.03 * b * s + rng.normal(0, 0.01)) for s in range(1, 9)]
+        smp = [rcm.StepTimeSample(batch_size=b, query_len=s, measured_time=y) for s, y in zip(range(1, 9), ys)]
+        fits.append([b, ys, list(rcm.fit_linear_step_time(smp))])
+    out["fit_linear"] = fits
+    from specbatch import acceptance as racc
+    trace = sbr.example_trace()
+    pts = [(s, racc.estimate_expected_correct(trace, s)) for s in range(1, 9)]
+    pl = racc.fit_power_law(pts)
+    out["power_law"] = {"points": [list(p) for p in pts], "c": pl.c, "gamma": pl.gamma}
     return out
 
 
+def file_cases():
+    from specbatch import acceptance as racc, traffic as rtr
+
+    d = OUT / "files"
+    d.mkdir(exist_ok=True)
+    cal, fit, trace = sbr.example_calibration(), sbr.example_fit(), sbr.example_trace()
+    racc.save_trace(trace, d / "trace.csv")
+    lut = rpol.build_lut(cal, trace)
+    rpol.save_lut(lut, d / "lut.csv", seed=7, calibration="example")
+    rcm.save_calibration(cal, d / "calibration.json", fit=fit)
+    rcm.save_calibration(cal, d / "calibration_nofit.json")
+    wl = sbr.gen_arrivals(sbr.TrafficConfig(0.05, 1.0, 30), np.random.default_rng(42))
+    rtr.save_workload(wl, d / "workload.csv")
+    rep = rsim.run_simulation(wl, rsim.ServerConfig(policy=sbr.AdaptivePolicy(lut), max_batch=16, seed=3), cal,
+                              trace, np.random.default_rng(3))
+    rsim.save_records(rep, d / "records.csv")
+    rsim.save_report(rep, d / "report.json")
+    # the reference reads step samples (cost_model.py:302-314) but has no writer: csv.writer layout
+    import csv
+    with open(d / "step_samples.csv", "w", newline="") as f:
+        w = csv.writer(f)
+        w.writerow(["batch_size", "query_len", "time_ms"])
+        for b, sl, ms in [(1, 1, 3.25), (1, 8, 3.875), (8, 3, 3.5), (64, 1, 7.015625)]:
+            w.writerow([b, sl, repr(ms)])
+    samples = rcm.load_step_samples(d / "step_samples.csv")
+    (d / "expected.json").write_text(json.dumps({
+        "lut_entries": {str(b): v for b, v in lut.entries.items()},
+        "samples": [[x.batch_size, x.query_len, x.measured_time] for x in samples],
+        "workload": [[r.id, r.arrival, r.gen_len] for r in rtr.load_workload(d / "workload.csv")],
+        "avg_latency": rep.avg_latency, "policy": rep.policy,
+    }, indent=1, sort_keys=True) + "\n")
+
+
 if __name__ == "__main__":
+    file_cases()
     dump("tokenlevel.json", tokenlevel_cases())
     dump("engine.json", engine_cases())
     dump("policy.json", policy_cases())

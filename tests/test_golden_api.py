@@ -115,3 +115,19 @@ def test_cost_model_matches_reference():
     assert cm.optimal_speculation_continuous(prm, 1, 8, tol=1e-7) == g["root"]
     for b, s in g["discrete"]:
         assert cm.optimal_speculation_discrete(cal, fit, 128, b, range(9)) == s
+
+
+def test_fits_match_reference():
+    """fit_linear_step_time (cost_model.py:145-170) and fit_power_law over the
+    Eq.4 censored means (acceptance.py:72-106) reproduce the reference's values."""
+    from paper_2310_18813_b200 import acceptance as acc
+
+    g = load_golden("cost_model.json")
+    for b, ys, want in g["fit_linear"]:
+        smp = [cm.StepTimeSample(batch_size=b, query_len=s, measured_time=y) for s, y in zip(range(1, 9), ys)]
+        assert list(cm.fit_linear_step_time(smp)) == want
+    trace = sb.example_trace()
+    pts = [(s, acc.estimate_expected_correct(trace, s)) for s in range(1, 9)]
+    assert [list(p) for p in pts] == g["power_law"]["points"]
+    pl = acc.fit_power_law(pts)
+    assert (pl.c, pl.gamma) == (g["power_law"]["c"], g["power_law"]["gamma"])

@@ -56,3 +56,34 @@ def test_continuous_streams_equal_plain_generation(cuda_dev, policy):
             assert gaps[d] < 2e-4, (r.id, d, gaps[d])
             ties += 1
     assert ties <= 1
+
+
+class _Alternate:
+    """k alternates 0, 0, 3 per call: two consecutive k = 0 iterations, then speculation."""
+
+    label = "alternate"
+
+    def __init__(self):
+        self.n = 0
+
+    def decide(self, b):
+        self.n += 1
+        return PolicyDecision(b, 3 if self.n % 3 == 0 else 0, "test")
+
+
+def test_k0_iterations_keep_draft_kv_current(cuda_dev):
+    """a k = 0 iteration advances every row without the draft; draft
+    step 1 of the next k > 0 iteration re-feeds only the last two committed
+    tokens, so the engine runs the draft over them (KV only) in k = 0
+    iterations of serve_continuous.  Draft == target (all 4 layers shared, fp32,
+    batch-invariant kernels) must then accept EVERY draft; a stale draft KV
+    slot would make the draft's attention read garbage and drop acceptance."""
+    tgt, drf = tiny_pair("fp32", device=cuda_dev, seed=23, max_pos=256, draft_layers=4)
+    eng = SpecEngine(tgt, drf, mode="greedy", max_batch=4, max_k=4, prompt_len=10, max_new=40, seed=7)
+    wl = [Request(id=i, arrival=0.0, gen_len=40) for i in range(3)]
+    rep, extra = serve_continuous(wl, eng, _Alternate(), collect=True, riding=False)
+    assert extra["acceptance_rate"] == 1.0, extra
+    for r in wl:
+        st = SequenceState(request_id=r.id, target_len=r.gen_len)
+        eng.generate([st], 0)
+        assert extra["outputs"][r.id] == st.tokens
