@@ -60,6 +60,7 @@ def _args():
     ap.add_argument("--workload", default="7b", choices=sorted(WORKLOADS))
     ap.add_argument("--trace-scale", type=float, default=0.1,
                     help="config 5: wall seconds per trace second (0.1 = the 6 x 50 s schedule in 30 s)")
+    ap.add_argument("--trace-seeds", type=int, default=3, help="config 5: arrival seeds (rng [seed, 6])")
     return ap.parse_args()
 
 
@@ -338,19 +339,48 @@ def run_reference(args):
 
 
 # ============================================================== config 5 (serving trace)
+def _ref_harness():
+    """The reference's experiment harness + simulator from baseline/_ref (None if absent)."""
+    rp = ROOT / "baseline" / "_ref"
+    if not (rp / "specbatch").exists():
+        return None
+    if str(rp) not in sys.path:
+        sys.path.insert(0, str(rp))
+    import specbatch.cost_model as rcm
+    import specbatch.harness as rh
+    import specbatch.policy as rpol
+    import specbatch.simulator as rsim
+
+    return rh, rsim, rpol, rcm
+
+
 def run_trace(args):
     """BASELINE configs[4]: a time-varying Poisson trace (the reference's
     timeline schedule, harness.py:257-265: alternating intense 0.2 s / sparse
     1.0 s mean gaps, CV 1, 6 x 50 s phases, max_batch 16) replayed in WALL
-    time on the GPU engine (simulator.serve_wallclock), once with the adaptive
-    LUT policy and once per fixed k = 1..8.  Metric: mean request latency
-    (queueing + prefill + decode), lower is better.  The schedule is time
-    compressed by --trace-scale so one policy takes ~30 s."""
+    time on the GPU engine (simulator.serve_wallclock), with the adaptive LUT
+    policy and every fixed k = 1..8, over --trace-seeds arrival seeds (seed 0 =
+    the reference's own timeline workload, rng [0, 6]).  Metric: mean request
+    latency (queueing + prefill + decode), lower is better.  The schedule is
+    time compressed by --trace-scale so one policy takes ~30 s.
+
+    SURVEY §8(f)1 closure: profiler.calibrate's measured B200 costs are written
+    in the reference's formats (calibration JSON, step-sample CSV, trace CSV)
+    and fed to the reference's UNCHANGED harness.cmd_timeline / run_simulation /
+    build_lut (baseline/_ref): their virtual-time predictions are reported
+    beside the wall-clock replay, with the analytic delta-root and the LUTs of
+    every construction (analytic linear, simulated linear, simulated on the
+    measured cost table, measured)."""
     import torch
 
+    from paper_2310_18813_b200.acceptance import estimate_expected_correct, fit_power_law, save_trace
+    from paper_2310_18813_b200.cost_model import OptimalityParams, optimal_speculation_continuous, \
+        save_calibration, save_step_samples
     from paper_2310_18813_b200.decoder import CONFIGS, Decoder
-    from paper_2310_18813_b200.policy import AdaptivePolicy, FixedPolicy, build_lut
+    from paper_2310_18813_b200.policy import AdaptivePolicy, FixedPolicy, build_lut, save_lut
     from paper_2310_18813_b200.presets import example_trace
+    from paper_2310_18813_b200.profiler import calibrate, table_lut
+    from paper_2310_18813_b200.serving import serve_continuous
     from paper_2310_18813_b200.simulator import ServerConfig, serve_wallclock
     from paper_2310_18813_b200.spec_engine import SpecEngine
     from paper_2310_18813_b200.traffic import PhaseSchedule, TrafficConfig, gen_phased
@@ -361,30 +391,93 @@ def run_trace(args):
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
     trace = example_trace()
+    sizes = (1, 2, 4, 8, 16)
     tgt = Decoder(CONFIGS[TARGET], dtype="bf16", device=dev, seed=0, init="device", max_pos=P + NEW + 32)
     drf = Decoder(CONFIGS[DRAFT], dtype="bf16", device=dev, seed=1, init="device", max_pos=P + NEW + 32)
     eng = SpecEngine(tgt, drf, mode="injected", acceptance=trace, max_batch=16, max_k=8, prompt_len=P,
                      max_new=NEW, seed=0)
-    lut = build_lut(None, trace, s_grid=K_GRID, profiled_sizes=(1, 2, 4, 8, 16), mode="measured",
+    lut = build_lut(None, trace, s_grid=K_GRID, profiled_sizes=sizes, mode="measured",
                     sample_size=1, rng=np.random.default_rng(0), gen_len=NEW, engine=eng)
+
+    # ---- (f)1: measured calibration -> reference formats -> the reference's own code
+    out = ROOT / "gpurun_out" / "config5"
+    out.mkdir(parents=True, exist_ok=True)
+    model, samples = calibrate(eng, batch_sizes=sizes, k_grid=range(1, 9), reps=10)
+    ctx = P + NEW // 2
+    verify_ms = {(smp.batch_size, smp.query_len): smp.measured_time for smp in samples}
+    for b in sizes:
+        verify_ms[(b, 0)] = eng.time_verify(b, 0, ctx=ctx, reps=10)
+    draft_ms = {b: eng.time_draft_step(b, ctx=ctx, reps=10) for b in sizes}
+    pts = [(s, estimate_expected_correct(trace, s)) for s in range(1, 9)]
+    fit = fit_power_law(pts)
+    save_calibration(model, out / "calibration.json", fit=fit)
+    save_step_samples(samples, out / "step_samples.csv")
+    save_trace(trace, out / "trace.csv")
+    save_lut(lut, out / "lut_measured.csv", seed=0, calibration="measured on this B200 (build_lut mode=measured)")
+    lut_table, _cells = table_lut(verify_ms, draft_ms, trace, s_grid=K_GRID, profiled_sizes=sizes,
+                                  sample_size=200, rng=np.random.default_rng([0, 2]), gen_len=NEW)
+    delta_root = {str(b): round(optimal_speculation_continuous(OptimalityParams.from_model(model, fit, b), 1, 8,
+                                                               tol=1e-6), 3) for b in sizes}
+    ref = _ref_harness()
+    closure = {"calibration": {"alpha": {str(b): round(v, 5) for b, v in model.alpha.items()},
+                               "beta": round(model.beta, 5),
+                               "ssm_step": {str(b): round(v, 5) for b, v in model.ssm_step.items()}},
+               "verify_ms": {f"{b},{s}": round(v, 4) for (b, s), v in sorted(verify_ms.items())},
+               "draft_step_ms": {str(b): round(v, 4) for b, v in draft_ms.items()},
+               "delta_root_s": delta_root,
+               "lut_measured": {str(b): v for b, v in lut.entries.items()},
+               "lut_table_simulated": {str(b): v for b, v in lut_table.entries.items()}}
+    if ref is not None:
+        rh, rsim, rpol, rcm = ref
+        rmodel, rfit = rcm.load_calibration(out / "calibration.json")
+        import specbatch.acceptance as racc
+        trace_r = racc.load_trace(out / "trace.csv")  # the reference's own AcceptanceTrace type
+        closure["source"] = "reference specbatch (baseline/_ref), unchanged"
+        closure["lut_analytic_linear"] = {str(b): v for b, v in
+                                          rpol.build_lut(rmodel, trace_r, s_grid=K_GRID, profiled_sizes=sizes).entries.items()}
+        closure["lut_simulated_linear"] = {str(b): v for b, v in rpol.build_lut(
+            rmodel, trace_r, s_grid=K_GRID, profiled_sizes=sizes, mode="simulated", sample_size=200,
+            rng=np.random.default_rng([0, 2]), gen_len=NEW).entries.items()}
+        cfg = rh.ExperimentConfig(calibration=str(out / "calibration.json"), trace=str(out / "trace.csv"),
+                                  sizes=sizes, out_dir=str(out / "ref_timeline"))
+        summ = rh.cmd_timeline(cfg)
+        rows = [ln.split(",") for ln in Path(summ).read_text().splitlines() if ln and not ln.startswith("#")]
+        closure["ref_cmd_timeline_latency_s"] = {r[0]: round(float(r[1]), 4) for r in rows[1:]}
+        # the same simulator on every policy of the wall replay (virtual time, trace seconds)
+        import specbatch.traffic as rtr
+        wl0 = rtr.gen_phased(rh.timeline_schedule(cfg), np.random.default_rng([0, 6]), gen_len=NEW)
+        rlut = rpol.build_lut(rmodel, trace_r, s_grid=K_GRID, profiled_sizes=sizes)
+        pred = {}
+        for pol in [rpol.AdaptivePolicy(rlut)] + [rpol.fixed_policy(k) for k in range(1, 9)]:
+            rep = rsim.run_simulation(wl0, rsim.ServerConfig(policy=pol, max_batch=16), rmodel, trace_r,
+                                      np.random.default_rng([0, 7]))
+            pred[pol.label] = round(rep.avg_latency, 4)
+        closure["ref_run_simulation_latency_s"] = pred
+    else:
+        closure["source"] = "baseline/_ref absent: reference harness not run"
+
+    # ---- wall-clock replay on the GPU engine, every policy, several arrival seeds
     phases = tuple((50.0, TrafficConfig(mean_interval=0.2 if i % 2 == 0 else 1.0, cv=1.0, count=1000))
                    for i in range(6))
-    workload = gen_phased(PhaseSchedule(phases=phases), np.random.default_rng([0, 6]), gen_len=NEW)
     policies = [AdaptivePolicy(lut)] + [FixedPolicy(k) for k in range(1, 9)]
-    lat, batches = {}, {}
     t_cap = time.perf_counter()
     for bb in range(1, 17):  # capture every (b, k) iteration graph up front: no capture inside a replay
-        for kk in range(1, 9):
+        for kk in range(0, 9):
             eng._graph(bb, kk)
     t_cap = time.perf_counter() - t_cap
     t_run = time.perf_counter()
-    for pol in policies:
-        rep = serve_wallclock(workload, ServerConfig(policy=pol, max_batch=16), eng, time_scale=args.trace_scale)
-        lat[pol.label] = rep.avg_latency / args.trace_scale  # back to trace seconds
-        sizes = [r.served_batch_size for r in rep.records]
-        batches[pol.label] = round(float(np.mean(sizes)), 2)
+    lat = {pol.label: [] for pol in policies}
+    batches = {pol.label: [] for pol in policies}
+    n_req = []
+    for seed in range(args.trace_seeds):
+        workload = gen_phased(PhaseSchedule(phases=phases), np.random.default_rng([seed, 6]), gen_len=NEW)
+        n_req.append(len(workload))
+        for pol in policies:
+            rep = serve_wallclock(workload, ServerConfig(policy=pol, max_batch=16), eng, time_scale=args.trace_scale)
+            lat[pol.label].append(rep.avg_latency / args.trace_scale)  # back to trace seconds
+            batches[pol.label].append(float(np.mean([r.served_batch_size for r in rep.records])))
     # continuous batching: retire / admit every iteration, k from the LUT per iteration
-    from paper_2310_18813_b200.serving import serve_continuous
+    workload = gen_phased(PhaseSchedule(phases=phases), np.random.default_rng([0, 6]), gen_len=NEW)
     cont = {}
     for pol in [AdaptivePolicy(lut), FixedPolicy(3)]:
         rep, extra = serve_continuous(workload, eng, pol, time_scale=args.trace_scale, max_batch=16)
@@ -392,21 +485,33 @@ def run_trace(args):
                            "mean_live_batch": round(extra["mean_live_batch"], 2), "mean_k": round(extra["mean_k"], 2),
                            "riding_prefill_rows": extra["ridden_rows"], "separate_prefill_rows": extra["prefill_rows"]}
     t_run = time.perf_counter() - t_run
-    fixed = {k: v for k, v in lat.items() if k.startswith("fixed")}
+    mean = {k: float(np.mean(v)) for k, v in lat.items()}
+    fixed = {k: v for k, v in mean.items() if k.startswith("fixed")}
     best = min(fixed, key=fixed.get)
-    ad = [k for k in lat if k not in fixed][0]
-    line = {"metric": "mean request latency, phased Poisson trace (adaptive k)", "value": lat[ad], "unit": "s",
+    ad = "adaptive"
+    per_seed_ratio = [a / f for a, f in zip(lat[ad], lat[best])]
+    per_seed_best = [min(fixed, key=lambda k: lat[k][i]) for i in range(args.trace_seeds)]
+    per_seed_ratio_own_best = [lat[ad][i] / lat[per_seed_best[i]][i] for i in range(args.trace_seeds)]
+    line = {"metric": "mean request latency, phased Poisson trace (adaptive k)", "value": mean[ad], "unit": "s",
             "n_gpus": 1, "higher_is_better": False, "impl": "ours", "dtype": "bf16",
             "data": "synthetic (random-init weights, injected example_trace acceptance)",
             "config": {"workload": f"{TARGET} target + {DRAFT} draft, timeline trace 6x50s (0.2/1.0 s gaps, CV 1), "
                                    f"max_batch 16, N={NEW}, P={P}", "time_scale": args.trace_scale,
-                       "requests": len(workload), "lut": {str(k): v for k, v in lut.entries.items()}},
-            "latency_s_by_policy": {k: round(v, 4) for k, v in lat.items()},
-            "mean_batch_by_policy": batches, "best_fixed": best,
-            "adaptive_vs_best_fixed_latency": lat[ad] / fixed[best], "wall_s": round(t_run, 1),
-            "continuous_batching": cont,
-            "graph_capture_s": round(t_cap, 1)}
+                       "seeds": args.trace_seeds, "requests_per_seed": n_req,
+                       "lut": {str(k): v for k, v in lut.entries.items()}},
+            "latency_s_by_policy": {k: round(v, 4) for k, v in mean.items()},
+            "latency_s_by_policy_per_seed": {k: [round(x, 4) for x in v] for k, v in lat.items()},
+            "mean_batch_by_policy": {k: round(float(np.mean(v)), 2) for k, v in batches.items()},
+            "best_fixed": best,
+            "adaptive_vs_best_fixed_latency": mean[ad] / fixed[best],
+            "adaptive_vs_best_fixed_per_seed": [round(x, 4) for x in per_seed_ratio],
+            "adaptive_vs_per_seed_best_fixed": [round(x, 4) for x in per_seed_ratio_own_best],
+            "per_seed_best_fixed": per_seed_best,
+            "wall_s": round(t_run, 1), "continuous_batching": cont, "graph_capture_s": round(t_cap, 1),
+            "f1_closure": closure}
+    (out / "result.json").write_text(json.dumps(line, indent=1) + "\n")
     print(json.dumps(line), flush=True)
+
 
 # ============================================================== our arm (GPU)
 def run_ours(args):

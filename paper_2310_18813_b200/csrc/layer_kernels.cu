@@ -711,19 +711,22 @@ int launch_attention_tc_prefill(const void* qr, void* kc, void* vc, void* out, c
 }
 
 // ---------------------------------------------------------------- KV compaction (K5)
-template <typename T>
-__global__ void kv_compact_kernel(T* __restrict__ k, T* __restrict__ v, const int32_t* __restrict__ src,
+// One (slab pair, layer) per blockIdx (y, z): copy positions [0, len) of every
+// kv head of slot src -> slot dst, K and V, in 16-byte vectors (a position row
+// is hd * elem_size = 128 / 256 / 512 bytes).  dst slots must not be sources of
+// the same call (compaction moves live rows into freed slots).
+__global__ void kv_compact_kernel(uint4* __restrict__ k, uint4* __restrict__ v, const int32_t* __restrict__ src,
                                   const int32_t* __restrict__ dst, const int32_t* __restrict__ len, int slots,
-                                  int nkv, int ctx_max, int hd) {
+                                  int nkv, size_t slab_vec, size_t row_vec) {
   griddep_wait();
   griddep_launch();
-  int i = blockIdx.y, layer = blockIdx.z;
-  int s = src[i], d = dst[i];
+  const int i = blockIdx.y, layer = blockIdx.z;
+  const int s = src[i], d = dst[i];
   if (s == d) return;
-  size_t per = (size_t)len[i] * hd;
+  const size_t per = (size_t)len[i] * row_vec;
   for (int h = 0; h < nkv; ++h) {
-    size_t so = (((size_t)layer * slots + s) * nkv + h) * ctx_max * hd;
-    size_t doff = (((size_t)layer * slots + d) * nkv + h) * ctx_max * hd;
+    const size_t so = (((size_t)layer * slots + s) * nkv + h) * slab_vec;
+    const size_t doff = (((size_t)layer * slots + d) * nkv + h) * slab_vec;
     for (size_t e = blockIdx.x * blockDim.x + threadIdx.x; e < per; e += (size_t)gridDim.x * blockDim.x) {
       k[doff + e] = k[so + e];
       v[doff + e] = v[so + e];
@@ -734,12 +737,12 @@ __global__ void kv_compact_kernel(T* __restrict__ k, T* __restrict__ v, const in
 int launch_kv_compact(int dtype, void* k, void* v, const int32_t* src, const int32_t* dst, const int32_t* len, int n,
                       int layers, int slots, int nkv, int ctx_max, int hd, cudaStream_t st) {
   if (n <= 0) return 0;
+  const size_t es = dtype == SB_BF16 ? 2 : 4;
+  if ((hd * es) % 16) return SB_EUNSUPPORTED;
+  const size_t row_vec = hd * es / 16;
   dim3 grid(8, n, layers);
-  if (dtype == SB_BF16)
-    return launch_k(kv_compact_kernel<__nv_bfloat16>, grid, dim3(256), 0, st, (__nv_bfloat16*)k, (__nv_bfloat16*)v, src,
-                    dst, len, slots, nkv, ctx_max, hd);
-  return launch_k(kv_compact_kernel<float>, grid, dim3(256), 0, st, (float*)k, (float*)v, src, dst, len, slots, nkv,
-                  ctx_max, hd);
+  return launch_k(kv_compact_kernel, grid, dim3(256), 0, st, (uint4*)k, (uint4*)v, src, dst, len, slots, nkv,
+                  (size_t)ctx_max * row_vec, row_vec);
 }
 
 }  // namespace sb

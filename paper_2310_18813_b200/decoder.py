@@ -381,6 +381,16 @@ class Decoder:
             N.check("sb_decoder_forward_mixed", rc)
         return rc
 
+    def kv_compact(self, kv: "KVCache", src_slots, dst_slots, lengths, stream=None) -> None:
+        """K5 compaction (sb_kv_compact): KV positions [0, lengths[i]) of slot
+        src_slots[i] -> dst_slots[i] in every layer (int32 device tensors)."""
+        n = int(src_slots.numel())
+        if n == 0:
+            return
+        st = torch.cuda.current_stream(self.device).cuda_stream if stream is None else stream
+        N.call("sb_kv_compact", C.byref(self.struct), C.byref(kv.struct), N.ptr(src_slots), N.ptr(dst_slots),
+               N.ptr(lengths), n, st)
+
     def weight_bytes(self) -> int:
         return self.cfg.streamed_bytes_per_forward(2 if self.dtype_name == "bf16" else 4)
 

@@ -64,3 +64,41 @@ def model_from_samples(samples, ssm: dict) -> LinearStepModel:
 def calibrate(engine, batch_sizes=(1, 2, 4, 8), k_grid=range(1, 9), ctx: int | None = None, reps: int = 10):
     samples, ssm = measure_step_samples(engine, batch_sizes, k_grid, ctx, reps)
     return model_from_samples(samples, ssm), samples
+
+
+def table_lut(verify_ms: dict, draft_ms: dict, trace, s_grid=range(9), profiled_sizes=(1, 2, 4, 8, 16),
+              sample_size: int = 200, rng=None, gen_len: int = 128):
+    """b -> k LUT from the MEASURED cost table instead of the linear fit.
+
+    ``verify_ms[(b, s)]`` is the measured verify forward at speculation length s
+    (s + 1 query tokens per sequence, s = 0 included) and ``draft_ms[b]`` one
+    draft step.  Step counts come from the reference's own simulated procedure
+    (run_batch over TraceSampler, policy.py:110-123: a formed batch runs until
+    its LAST sequence finishes); each step is charged verify_ms[(b, s)] +
+    s * draft_ms[b].  This isolates the two things the analytic LUT
+    (policy.py:101-105) does not see on B200: t_L(b, s) is step-shaped in the
+    token count b(s+1) (GEMM token tiles), not linear, and the batch is held
+    for its slowest sequence (max over b of the step counts, not N / (E[l]+1)).
+    Returns (SpeculationLUT, {(b, s): ms per token})."""
+    from .engine import SequenceState, TraceSampler, run_batch
+    from .policy import SpeculationLUT
+
+    rng = rng if rng is not None else np.random.default_rng(0)
+    unit = LinearStepModel(alpha={1: 1e-300}, beta=1.0, ssm_step={1: 1e-300})  # per-step cost ~1: counts steps
+    grid = tuple(sorted(set(s_grid)))
+    entries, cells = {}, {}
+    for b in sorted(profiled_sizes):
+        best, best_t = None, float("inf")
+        for s in grid:
+            steps = toks = 0
+            for j in range(-(-sample_size // b)):
+                states = [SequenceState(request_id=j * b + i, target_len=gen_len) for i in range(b)]
+                res = run_batch(states, s, unit, TraceSampler(trace), rng)
+                steps += res.steps
+                toks += res.tokens_generated
+            t = steps * (verify_ms[(b, s)] + s * draft_ms[b]) / toks
+            cells[(b, s)] = t
+            if t < best_t:
+                best, best_t = s, t
+        entries[b] = best
+    return SpeculationLUT(entries=entries, s_grid=grid, provenance={"mode": "table-simulated"}), cells

@@ -35,7 +35,8 @@ __all__ = ["serve_continuous"]
 
 def serve_continuous(workload: list[Request], engine, policy, time_scale: float = 1.0, max_batch: int | None = None,
                      group_size: int = 40, clock=None, collect: bool = False, min_admit: int = 1,
-                     max_wait: float = 0.0, riding: bool | None = None) -> tuple[SimulationReport, dict]:
+                     max_wait: float = 0.0, riding: bool | None = None,
+                     compact: bool = False) -> tuple[SimulationReport, dict]:
     """Serve `workload` with continuous batching on `engine` (a SpecEngine).
 
     `policy.decide(b)` picks k at every iteration for the live batch size b
@@ -48,7 +49,13 @@ def serve_continuous(workload: list[Request], engine, policy, time_scale: float 
     admitted while other rows decode are prefilled INSIDE the next iteration's
     verify forward (sb_decoder_forward_mixed, one weight stream) and decode from
     the iteration after; otherwise each admission runs its own prefill forward.
-    Returns (report, {"mean_live_batch", "mean_k", "iterations", "acceptance_rate"[, "outputs": {id: tokens}]}).
+    Slots: by default a retired row's KV slot is simply freed and the row->slot
+    map permuted (no KV moves).  ``compact=True`` keeps row == slot instead: the
+    KV slabs of surviving rows in slots >= the new live count are moved into the
+    freed low slots by the K5 compaction kernel (sb_kv_compact, target + draft),
+    so live KV stays dense in slots [0, b).
+    Returns (report, {"mean_live_batch", "mean_k", "iterations", "acceptance_rate",
+    "compacted_rows"[, "outputs": {id: tokens}]}).
     """
     if any(nxt.arrival < cur.arrival for cur, nxt in zip(workload, workload[1:])):
         raise ValueError("workload must be sorted by arrival time")
@@ -75,7 +82,7 @@ def serve_continuous(workload: list[Request], engine, policy, time_scale: float 
     b_hist: list[int] = []
     outputs: dict[int, list[int]] = {}
     prof = {"prefills": 0, "prefill_rows": 0, "ridden_rows": 0, "prefill_s": 0.0, "iter_s": 0.0, "host_s": 0.0,
-            "idle_s": 0.0}
+            "idle_s": 0.0, "compacted_rows": 0}
     if riding is None:
         riding = getattr(eng, "supports_ride", False)
     elif riding and not getattr(eng, "supports_ride", False):
@@ -176,6 +183,9 @@ def serve_continuous(workload: list[Request], engine, policy, time_scale: float 
                 row_req = [row_req[i] for i in keep]
                 row_start = [row_start[i] for i in keep]
                 slot_of_row = [slot_of_row[i] for i in keep]
+                if compact and keep:
+                    n_moved = _compact_slots(eng, slot_of_row, free_slots)
+                    prof["compacted_rows"] += n_moved
                 if keep:  # the compacted rows keep their KV slots
                     eng.slots[: len(keep)].copy_(torch.tensor(slot_of_row, dtype=torch.int32))
         torch.cuda.synchronize(dev)
@@ -188,6 +198,34 @@ def serve_continuous(workload: list[Request], engine, policy, time_scale: float 
     if collect:
         extra["outputs"] = outputs
     return rep, extra
+
+
+def _compact_slots(eng, slot_of_row: list[int], free_slots: list[int]) -> int:
+    """Move the KV of live rows whose slot is >= the live count into free slots
+    below it (sb_kv_compact on target and draft caches), so row r uses slot r.
+    Mutates slot_of_row / free_slots; the row state is already compacted.
+    Returns the number of rows moved."""
+    b = len(slot_of_row)
+    holes = sorted(set(range(b)) - set(slot_of_row))
+    movers = [r for r, s in enumerate(slot_of_row) if s >= b]
+    assert len(holes) == len(movers)
+    if not movers:
+        return 0
+    dev = eng.dev
+    src = torch.tensor([slot_of_row[r] for r in movers], device=dev, dtype=torch.int32)
+    dst = torch.tensor(holes, device=dev, dtype=torch.int32)
+    rows = torch.tensor(movers, device=dev, dtype=torch.long)
+    lens = eng.n_tok[rows].clone()  # every written position (target KV valid to n_tok - 1, draft to n_tok - 3)
+    eng.target.kv_compact(eng.kv_t, src, dst, lens)
+    if eng.draft is not None:
+        eng.draft.kv_compact(eng.kv_d, src, dst, lens)
+    for r, h in zip(movers, holes):
+        free_slots.append(slot_of_row[r])
+        free_slots.remove(h)
+        slot_of_row[r] = h
+    free_slots.sort(reverse=True)  # pop() hands out the lowest free slot next
+    eng.slots[:b].copy_(torch.tensor(slot_of_row, dtype=torch.int32))
+    return len(movers)
 
 
 def _prefill_rows(eng, rows: list[int]) -> None:

@@ -87,3 +87,40 @@ def test_k0_iterations_keep_draft_kv_current(cuda_dev):
         st = SequenceState(request_id=r.id, target_len=r.gen_len)
         eng.generate([st], 0)
         assert extra["outputs"][r.id] == st.tokens
+
+
+@pytest.mark.parametrize("dtype", ["bf16", "fp32"])
+def test_kv_compact_matches_torch_gather(cuda_dev, dtype):
+    """K5 compaction (sb_kv_compact) against a torch copy of the same slab ranges."""
+    tgt, _ = tiny_pair(dtype, device=cuda_dev, seed=3, max_pos=256)
+    kv = tgt.new_kv(6, 96)
+    g = torch.Generator(device=cuda_dev).manual_seed(0)
+    kv.k.copy_(torch.randn(kv.k.shape, generator=g, device=cuda_dev).to(kv.k.dtype))
+    kv.v.copy_(torch.randn(kv.v.shape, generator=g, device=cuda_dev).to(kv.v.dtype))
+    want_k, want_v = kv.k.clone(), kv.v.clone()
+    src, dst, lens = [5, 3, 4], [0, 1, 2], [96, 17, 1]
+    for s_, d_, n_ in zip(src, dst, lens):
+        want_k[:, d_, :, :n_] = want_k[:, s_, :, :n_]
+        want_v[:, d_, :, :n_] = want_v[:, s_, :, :n_]
+    i32 = dict(device=cuda_dev, dtype=torch.int32)
+    tgt.kv_compact(kv, torch.tensor(src, **i32), torch.tensor(dst, **i32), torch.tensor(lens, **i32))
+    torch.cuda.synchronize()
+    assert torch.equal(kv.k, want_k) and torch.equal(kv.v, want_v)
+
+
+def test_continuous_with_slot_compaction_equals_plain_generation(cuda_dev):
+    """serve_continuous(compact=True): retirements move surviving rows' KV into
+    the freed low slots (target and draft caches) so row == slot; the streams
+    must stay exactly those of plain generation."""
+    tgt, drf = tiny_pair("fp32", device=cuda_dev, seed=21, max_pos=256)
+    eng = SpecEngine(tgt, drf, mode="greedy", max_batch=4, max_k=4, prompt_len=10, max_new=24, seed=5)
+    rng = np.random.default_rng(1)
+    gens = rng.integers(4, 24, size=12)
+    arrivals = np.cumsum(rng.exponential(0.002, size=12))
+    wl = [Request(id=i, arrival=float(a), gen_len=int(g)) for i, (a, g) in enumerate(zip(arrivals, gens))]
+    rep, extra = serve_continuous(wl, eng, _ByBatch(), collect=True, compact=True)
+    assert extra["compacted_rows"] > 0, extra
+    for r in wl:
+        st = SequenceState(request_id=r.id, target_len=r.gen_len)
+        eng.generate([st], 0)
+        assert extra["outputs"][r.id] == st.tokens, r.id
