@@ -443,16 +443,19 @@ def run_trace(args):
         summ = rh.cmd_timeline(cfg)
         rows = [ln.split(",") for ln in Path(summ).read_text().splitlines() if ln and not ln.startswith("#")]
         closure["ref_cmd_timeline_latency_s"] = {r[0]: round(float(r[1]), 4) for r in rows[1:]}
-        # the same simulator on every policy of the wall replay (virtual time, trace seconds)
+        # the same simulator on every policy of the wall replay, at the replay's load: arrivals
+        # compressed by time_scale exactly as replayed, latency / time_scale (trace seconds)
         import specbatch.traffic as rtr
-        wl0 = rtr.gen_phased(rh.timeline_schedule(cfg), np.random.default_rng([0, 6]), gen_len=NEW)
         rlut = rpol.build_lut(rmodel, trace_r, s_grid=K_GRID, profiled_sizes=sizes)
         pred = {}
-        for pol in [rpol.AdaptivePolicy(rlut)] + [rpol.fixed_policy(k) for k in range(1, 9)]:
-            rep = rsim.run_simulation(wl0, rsim.ServerConfig(policy=pol, max_batch=16), rmodel, trace_r,
-                                      np.random.default_rng([0, 7]))
-            pred[pol.label] = round(rep.avg_latency, 4)
-        closure["ref_run_simulation_latency_s"] = pred
+        for seed in range(args.trace_seeds):
+            wl0 = rtr.gen_phased(rh.timeline_schedule(cfg), np.random.default_rng([seed, 6]), gen_len=NEW)
+            wls = [rtr.Request(id=r.id, arrival=r.arrival * args.trace_scale, gen_len=r.gen_len) for r in wl0]
+            for pol in [rpol.AdaptivePolicy(rlut)] + [rpol.fixed_policy(k) for k in range(1, 9)]:
+                rep = rsim.run_simulation(wls, rsim.ServerConfig(policy=pol, max_batch=16), rmodel, trace_r,
+                                          np.random.default_rng([0, 7]))
+                pred.setdefault(pol.label, []).append(round(rep.avg_latency / args.trace_scale, 4))
+        closure["ref_run_simulation_latency_s_at_replay_load"] = pred
     else:
         closure["source"] = "baseline/_ref absent: reference harness not run"
 

@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define SB_ABI_VERSION 9
+#define SB_ABI_VERSION 10
 
 /* status codes beyond cudaError_t (which are < 1000) */
 #define SB_OK 0
@@ -281,19 +281,28 @@ int sb_prepare_iteration(int32_t b, int32_t k, const int32_t* tokens, int32_t to
                          void* stream);
 
 /*
- * The whole greedy draft loop of one iteration in ONE persistent launch (K1):
- * steps j = 1..k of the draft decoder for b sequences, staged exactly like k
- * calls of sb_decoder_forward_ex with a token sink -- step 1 feeds d1_ids /
+ * The whole greedy draft loop of one iteration in ONE persistent launch (K1),
+ * replacing k x (draft forward + token sink) -- the draft proposals of
+ * DraftOracle.step / TokenLevel.draft_tokens (engine.py:100-106, 138-145).
+ * Steps j = 1..k of the draft decoder for b sequences, staged exactly like k
+ * calls of sb_decoder_forward_ex with a token sink: step 1 feeds d1_ids /
  * d1_pos (the last two committed tokens per sequence, [b, 2]), step j >= 2
- * feeds ds_ids / ds_pos -- and writing v_ids[s*(k+1) + j] = d_j,
- * ds_ids[s] = d_j, ds_pos[s] = d_base[s] + j.  Row-parallel mma.sync GEMMs,
- * grid barriers between phases.  SB_EUNSUPPORTED outside its envelope (bf16
- * Llama-arch, 2b <= 16, <= 16 layers, ctx_max <= 288, dims multiple of 64):
- * the caller then issues the per-step forwards.
+ * feeds d_{j-1} at position d_base[s] + j - 1; writes v_ids[s*(k+1) + j] = d_j,
+ * ds_ids[s] = d_j, ds_pos[s] = d_base[s] + j.  One CTA per SM (thread-block
+ * clusters of ffn/hidden CTAs), grid barriers between phases, a producer warp
+ * streaming weight tiles ahead of the barriers.  workspace: at least
+ * sb_draft_loop_workspace_bytes(m) bytes (contents scratch); sync_words: 64
+ * zero-initialised bytes owned by this call site (self-resetting barrier words,
+ * never shared with a concurrently running launch).  SB_EUNSUPPORTED outside
+ * its envelope (bf16 Llama-arch, unsharded, head_dim 64, 2b <= 16, ffn/hidden
+ * in {2,4,8}, hidden <= 1024) or when disabled: the caller then issues the
+ * per-step forwards.
  */
 int sb_draft_loop(const sb_decoder_t* m, const sb_kvcache_t* kv, int32_t b, int32_t k, const int32_t* d1_ids,
                   const int32_t* d1_pos, const int32_t* slots, const int32_t* d_base, int32_t* v_ids,
-                  int32_t* ds_ids, int32_t* ds_pos, void* workspace, size_t ws_bytes, void* stream);
+                  int32_t* ds_ids, int32_t* ds_pos, void* workspace, size_t ws_bytes, void* sync_words,
+                  void* stream);
+size_t sb_draft_loop_workspace_bytes(const sb_decoder_t* m);
 /* Enable sb_draft_loop (default 1); 0 = it returns SB_EUNSUPPORTED and the caller issues per-step forwards. */
 int sb_set_draft_loop(int32_t enabled);
 

@@ -83,7 +83,7 @@ static size_t carve(const sb_decoder_t* m, int T, char* base, FwdWorkspace* w) {
 // the embedding is replicated: token ids range over the full vocabulary even on a TP shard
 static inline int vocab_full(const sb_decoder_t* m) { return m->vocab * (m->tp ? m->tp->world : 1); }
 
-static int g_last_count = 0;
+int g_last_count = 0;  // kernels of the last forward / draft loop (sb_last_kernel_count)
 // event profiling (sb_profile_forward): an event after every kernel of the forward
 static bool g_prof = false;
 static std::vector<cudaEvent_t> g_prof_ev;
@@ -525,7 +525,8 @@ int sb_kv_compact(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* 
 int sb_init(void) {
   // one-time host setup outside any stream capture: kernel attributes and the
   // driver's tensor-map encoder (TMA descriptors are built per GEMM call)
-  return gemm_tc_init();
+  SB_TRY(gemm_tc_init());
+  return draft_loop_init();
 }
 
 int sb_set_gemm_backend(int32_t backend) {
@@ -619,20 +620,6 @@ int sb_set_fuse_norm(int32_t enabled) {
   return 0;
 }
 
-static int g_draft_loop = 1;  // sb_set_draft_loop
-
-int sb_set_draft_loop(int32_t enabled) {
-  g_draft_loop = enabled ? 1 : 0;
-  return 0;
-}
-
-int sb_draft_loop(const sb_decoder_t* m, const sb_kvcache_t* kv, int32_t b, int32_t k, const int32_t* d1_ids,
-                  const int32_t* d1_pos, const int32_t* slots, const int32_t* d_base, int32_t* v_ids, int32_t* ds_ids,
-                  int32_t* ds_pos, void* workspace, size_t ws_bytes, void* stream) {
-  if (!m || !kv || b < 1 || k < 0) return SB_EINVAL;
-  return SB_EUNSUPPORTED;
-}
-
 int sb_set_pdl(int32_t enabled) {
   g_pdl = enabled ? 1 : 0;
   return 0;
@@ -641,9 +628,9 @@ int sb_set_pdl(int32_t enabled) {
 int sb_version(void) { return SB_ABI_VERSION; }
 
 const char* sb_build_info(void) {
-  return "specbatch_b200 abi=" "9" " arch=sm_100a tp=nccl models=llama,opt kernels=gemm_tcgen05,attention_tc(decode,"
+  return "specbatch_b200 abi=" "10" " arch=sm_100a tp=nccl models=llama,opt kernels=gemm_tcgen05,attention_tc(decode,"
          "prefill_blocks),rope_append_vec,embed_norm,layernorm,tp_resid_add,unshard_logits,argmax,softmax,select,accept,"
-         "commit,prepare,kv_compact,gemm_simt,attention_simt,rmsnorm forward=verify,mixed";
+         "commit,prepare,kv_compact,gemm_simt,attention_simt,rmsnorm,draft_loop(persistent,cluster) forward=verify,mixed";
 }
 
 int sb_last_kernel_count(void) { return g_last_count; }

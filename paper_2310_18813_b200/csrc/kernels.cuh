@@ -101,6 +101,8 @@ int launch_argmax_partials(const float* val, const int* idx, int n_tiles, int ro
                            cudaStream_t st);
 int launch_select_argmax(const float* logits, int rows, int vocab, int32_t* out_tok, int out_stride, int32_t* next_ids,
                          int32_t* next_pos, const int32_t* base_pos, int pos_offset, cudaStream_t st);
+extern int g_last_count;  // forward.cu: kernels of the last forward / draft loop
+int draft_loop_init();     // draft_loop.cu: kernel attributes + co-resident cluster counts (sb_init)
 int launch_kv_compact(int dtype, void* k, void* v, const int32_t* src, const int32_t* dst, const int32_t* len, int n,
                       int layers, int slots, int nkv, int ctx_max, int hd, cudaStream_t st);
 

@@ -137,7 +137,10 @@ class SpecEngine:
         self.mix_pos = torch.zeros(B * (K + 1) + pf_tok, **i32)
         if draft is not None:
             ws = max(ws, draft.workspace_bytes(2 * B), draft.workspace_bytes(pf_tok))
+        if draft is not None:
+            ws = max(ws, int(N.load().sb_draft_loop_workspace_bytes(C.byref(draft.struct))))
         self.workspace = torch.zeros(ws, device=self.dev, dtype=torch.uint8)
+        self.dl_sync = torch.zeros(8, device=self.dev, dtype=torch.int64)  # sb_draft_loop barrier words
         self.live_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
         self.stream = torch.cuda.Stream(device=self.dev)
         self.graphs: dict[tuple[int, int], torch.cuda.CUDAGraph] = {}
@@ -207,7 +210,7 @@ class SpecEngine:
             rc = lib.sb_draft_loop(C.byref(self.draft.struct), C.byref(self.kv_d.struct), b, k, N.ptr(self.d1_ids),
                                    N.ptr(self.d1_pos), N.ptr(self.slots), N.ptr(self.d_base), N.ptr(self.v_ids),
                                    N.ptr(self.ds_ids), N.ptr(self.ds_pos), N.ptr(self.workspace),
-                                   self.workspace.numel(), st)
+                                   self.workspace.numel(), N.ptr(self.dl_sync), st)
             if rc == 0:
                 draft_done = True
                 launches += lib.sb_last_kernel_count()
