@@ -298,11 +298,20 @@ int sb_prepare_iteration(int32_t b, int32_t k, const int32_t* tokens, int32_t to
  * in {2,4,8}, hidden <= 1024) or when disabled: the caller then issues the
  * per-step forwards.
  */
-int sb_draft_loop(const sb_decoder_t* m, const sb_kvcache_t* kv, int32_t b, int32_t k, const int32_t* d1_ids,
-                  const int32_t* d1_pos, const int32_t* slots, const int32_t* d_base, int32_t* v_ids,
-                  int32_t* ds_ids, int32_t* ds_pos, void* workspace, size_t ws_bytes, void* sync_words,
-                  void* stream);
+int sb_draft_loop(const sb_decoder_t* m, const sb_kvcache_t* kv, const void* packed, int32_t b, int32_t k,
+                  const int32_t* d1_ids, const int32_t* d1_pos, const int32_t* slots, const int32_t* d_base,
+                  int32_t* v_ids, int32_t* ds_ids, int32_t* ds_pos, void* workspace, size_t ws_bytes,
+                  void* sync_words, void* stream);
+/* The draft's weights re-laid for sb_draft_loop ("packed"): every 16-row x hidden tile contiguous and
+   128B-swizzled so one bulk copy feeds a conflict-free ldmatrix; written by sb_draft_loop_pack (once,
+   and again whenever the weights change) into a caller buffer of sb_draft_loop_packed_bytes(m)
+   bytes (0 = outside the envelope). */
+size_t sb_draft_loop_packed_bytes(const sb_decoder_t* m);
+int sb_draft_loop_pack(const sb_decoder_t* m, void* dst, size_t bytes, void* stream);
 size_t sb_draft_loop_workspace_bytes(const sb_decoder_t* m);
+/* Diagnostics: device buffer (>= 4096 + 512*160 u64, zeroed) receiving globaltimer stamps of every grid
+   barrier of the next sb_draft_loop launches (NULL = off). */
+int sb_debug_draft_trace(void* buf);
 /* Enable sb_draft_loop (default 1); 0 = it returns SB_EUNSUPPORTED and the caller issues per-step forwards. */
 int sb_set_draft_loop(int32_t enabled);
 

@@ -81,9 +81,12 @@ _SIGS = {
     "sb_set_attention_impl": (C.c_int, [_I]),
     "sb_set_attention_splits": (C.c_int, [_I]),
     "sb_set_draft_loop": (C.c_int, [_I]),
-    "sb_draft_loop": (C.c_int, [C.POINTER(SbDecoder), C.POINTER(SbKVCache), _I, _I, _P, _P, _P, _P, _P, _P, _P, _P,
-                                C.c_size_t, _P, _P]),
+    "sb_draft_loop": (C.c_int, [C.POINTER(SbDecoder), C.POINTER(SbKVCache), _P, _I, _I, _P, _P, _P, _P, _P, _P, _P,
+                                _P, C.c_size_t, _P, _P]),
+    "sb_draft_loop_packed_bytes": (C.c_size_t, [C.POINTER(SbDecoder)]),
+    "sb_draft_loop_pack": (C.c_int, [C.POINTER(SbDecoder), _P, C.c_size_t, _P]),
     "sb_draft_loop_workspace_bytes": (C.c_size_t, [C.POINTER(SbDecoder)]),
+    "sb_debug_draft_trace": (C.c_int, [_P]),
     "sb_nccl_unique_id": (C.c_int, [_P]),
     "sb_nccl_collectives_init": (C.c_int, [_P, _I, _I, C.POINTER(SbCollectives)]),
     "sb_nccl_collectives_destroy": (C.c_int, [C.POINTER(SbCollectives)]),

@@ -141,6 +141,14 @@ class SpecEngine:
             ws = max(ws, int(N.load().sb_draft_loop_workspace_bytes(C.byref(draft.struct))))
         self.workspace = torch.zeros(ws, device=self.dev, dtype=torch.uint8)
         self.dl_sync = torch.zeros(8, device=self.dev, dtype=torch.int64)  # sb_draft_loop barrier words
+        # the draft's weights re-laid as swizzled 16-row tiles for the one-launch draft loop (K1)
+        self.dl_packed = None
+        if draft is not None and mode != "stochastic":
+            nb = int(N.load().sb_draft_loop_packed_bytes(C.byref(draft.struct)))
+            if nb:
+                self.dl_packed = torch.empty(nb, device=self.dev, dtype=torch.uint8)
+                N.call("sb_draft_loop_pack", C.byref(draft.struct), N.ptr(self.dl_packed), nb,
+                       torch.cuda.current_stream(self.dev).cuda_stream)
         self.live_host = torch.zeros(1, dtype=torch.int32, pin_memory=True)
         self.stream = torch.cuda.Stream(device=self.dev)
         self.graphs: dict[tuple[int, int], torch.cuda.CUDAGraph] = {}
@@ -205,9 +213,10 @@ class SpecEngine:
         # the fp32 path and a tensor-parallel target select from materialised (full-width) logits
         need_logits = self.target.sb_dtype != N.SB_BF16 or self.target.is_tp
         draft_done = False
-        if use_draft and greedy_draft:
+        if use_draft and greedy_draft and self.dl_packed is not None:
             # the whole greedy draft loop in one persistent launch (csrc/draft_loop.cu)
-            rc = lib.sb_draft_loop(C.byref(self.draft.struct), C.byref(self.kv_d.struct), b, k, N.ptr(self.d1_ids),
+            rc = lib.sb_draft_loop(C.byref(self.draft.struct), C.byref(self.kv_d.struct), N.ptr(self.dl_packed), b, k,
+                                   N.ptr(self.d1_ids),
                                    N.ptr(self.d1_pos), N.ptr(self.slots), N.ptr(self.d_base), N.ptr(self.v_ids),
                                    N.ptr(self.ds_ids), N.ptr(self.ds_pos), N.ptr(self.workspace),
                                    self.workspace.numel(), N.ptr(self.dl_sync), st)

@@ -20,12 +20,15 @@ cfg = CONFIGS["llama-68m"]
 drf = Decoder(cfg, dtype="bf16", device=dev, seed=1, init="device", max_pos=512)
 lib = N.load()
 i32 = dict(device=dev, dtype=torch.int32)
-P = 192
+import os
+P = int(os.environ.get('DL_P', '192'))
 kv = drf.new_kv(8, 320)
 ws = torch.zeros(max(drf.workspace_bytes(8 * P), int(lib.sb_draft_loop_workspace_bytes(C.byref(drf.struct)))),
                  device=dev, dtype=torch.uint8)
 slots = torch.arange(8, **i32)
 sync = torch.zeros(8, device=dev, dtype=torch.int64)
+packed = torch.empty(int(lib.sb_draft_loop_packed_bytes(C.byref(drf.struct))), device=dev, dtype=torch.uint8)
+N.call("sb_draft_loop_pack", C.byref(drf.struct), N.ptr(packed), packed.numel(), torch.cuda.current_stream().cuda_stream)
 junk = torch.empty(256 << 20, device=dev, dtype=torch.uint8)
 st = torch.cuda.Stream()
 
@@ -61,7 +64,8 @@ def timed(fn, reps=50):
     return float(np.median(ts))
 
 
-for b in (1, 2, 4, 8):
+RUN = "--no-run" not in sys.argv
+for b in ((1, 2, 4, 8) if RUN else ()):
     d1_ids, d1_pos, d_base = setup(b)
     for k in (1, 3, 8):
         v_ids = torch.zeros(b * (k + 1), **i32)
@@ -70,7 +74,7 @@ for b in (1, 2, 4, 8):
 
         def loop():
             s = torch.cuda.current_stream().cuda_stream
-            rc = lib.sb_draft_loop(C.byref(drf.struct), C.byref(kv.struct), b, k, N.ptr(d1_ids), N.ptr(d1_pos),
+            rc = lib.sb_draft_loop(C.byref(drf.struct), C.byref(kv.struct), N.ptr(packed), b, k, N.ptr(d1_ids), N.ptr(d1_pos),
                                    N.ptr(slots), N.ptr(d_base), N.ptr(v_ids), N.ptr(ds_ids), N.ptr(ds_pos),
                                    N.ptr(ws), ws.numel(), N.ptr(sync), s)
             assert rc == 0, rc

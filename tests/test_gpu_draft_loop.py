@@ -52,7 +52,11 @@ def _run(drf, prompts, k, mode, dev):
     st = torch.cuda.current_stream().cuda_stream
     if mode == "loop":
         sync = torch.zeros(8, device=dev, dtype=torch.int64)
-        rc = lib.sb_draft_loop(C.byref(drf.struct), C.byref(kv.struct), b, k, N.ptr(d1_ids), N.ptr(d1_pos),
+        nb = int(lib.sb_draft_loop_packed_bytes(C.byref(drf.struct)))
+        assert nb > 0
+        packed = torch.empty(nb, device=dev, dtype=torch.uint8)
+        N.call("sb_draft_loop_pack", C.byref(drf.struct), N.ptr(packed), nb, torch.cuda.current_stream().cuda_stream)
+        rc = lib.sb_draft_loop(C.byref(drf.struct), C.byref(kv.struct), N.ptr(packed), b, k, N.ptr(d1_ids), N.ptr(d1_pos),
                                N.ptr(slots), N.ptr(d_base), N.ptr(v_ids), N.ptr(ds_ids), N.ptr(ds_pos), N.ptr(ws),
                                ws.numel(), N.ptr(sync), st)
         assert rc == 0, rc
