@@ -942,7 +942,7 @@ static size_t g_dl_persist = 0;
 int draft_loop_init() {
   {
     const char* env = getenv("SB_DL_PERSIST_MB");
-    const long want_mb = env ? atol(env) : 96;
+    const long want_mb = env ? atol(env) : 0;  // measured: no gain for the draft, and it shrinks the target's L2
     int dev = 0, max_persist = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
