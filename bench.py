@@ -638,23 +638,50 @@ def run_ours(args):
     run_batch(chk, k, None, eng, np.random.default_rng(0))
     e2e = jobs * args.steps * b * NEW / e2e_s
 
-    # ---- config 3 names stochastic rejection sampling: the same pair in stochastic mode
-    # (REAL acceptance of the random-init weights at temperature 1, canonical inverse-CDF
-    # resampling, materialised fp32 logits/probabilities), device-timed
+    # ---- config 3 (BASELINE configs[2]): stochastic rejection sampling min(1, p/q) with residual
+    # resampling and an ADAPTIVE k TABLE: the same pair in stochastic mode (REAL acceptance of the
+    # random-init weights at temperature 1), its own measured b -> k LUT (build_lut mode="measured"),
+    # then every (b, k) cell re-timed independently: tokens/s by b, adaptive vs best fixed k
     stoch = None
-    if not tp:
-        eng_s = SpecEngine(tgt, drf, mode="stochastic", max_batch=max(b, 8), max_k=8, prompt_len=P, max_new=NEW,
-                           seed=rank, autotune=False)
-        eng_s.generate(batch(90000), k)
-        ms_s, acc_s, prop_s = 0.0, 0, 0
+    if not tp and os.environ.get("SB_SKIP_STOCH", "0") != "1":
+        s_sizes = tuple(x for x in (1, 2, 4, 8, 16) if x <= eng.max_batch) if not args.quick else (b,)
+        eng_s = SpecEngine(tgt, drf, mode="stochastic", max_batch=max(s_sizes), max_k=8, prompt_len=P,
+                           max_new=NEW, seed=rank, autotune=False)
+        # (real acceptance is random per batch: 3 batches per cell for the profile)
+        lut_s = build_lut(None, trace, s_grid=K_GRID, profiled_sizes=s_sizes, mode="measured", sample_size=3 * max(s_sizes),
+                          rng=np.random.default_rng(1), gen_len=NEW, engine=eng_s)
+        s_by_batch = {}
+        acc_s = prop_s = 0
+        for bb in s_sizes:
+            med = {}
+            for kk in K_GRID:
+                tps = []
+                for r in range(3):
+                    sts = [SequenceState(request_id=700000 + 1000 * r + i, target_len=NEW) for i in range(bb)]
+                    res = eng_s.generate(sts, kk)
+                    tps.append(res.tokens_generated / (res.total_time / 1e3))
+                    if kk > 0:
+                        log = eng_s.stats.accepted
+                        acc_s += int(log[log >= 0].sum())
+                        prop_s += int(kk * (log >= 0).sum())
+                med[kk] = float(np.median(tps))
+            ka = lookup(lut_s, bb).chosen_s
+            kf = max(med, key=med.get)
+            s_by_batch[str(bb)] = {"adaptive_k": ka, "adaptive_tokens_per_s": round(med[ka], 1), "best_fixed_k": kf,
+                                   "best_fixed_tokens_per_s": round(med[kf], 1),
+                                   "adaptive_vs_best_fixed": round(med[ka] / med[kf], 4),
+                                   "k_sweep_median": {str(kk): round(v, 1) for kk, v in sorted(med.items())}}
+        ks = lookup(lut_s, b).chosen_s
+        ms_s = 0.0
         for s in range(2):
-            r = eng_s.generate(batch(91000 + s), k)
+            r = eng_s.generate(batch(91000 + s), ks)
             ms_s += r.total_time + eng_s.stats.prefill_ms
-            log = eng_s.stats.accepted
-            acc_s += int(log[log >= 0].sum())
-            prop_s += int(k * (log >= 0).sum())
-        stoch = {"tokens_per_s": 2 * b * NEW / (ms_s / 1e3), "k": k,
-                 "acceptance_rate": acc_s / max(prop_s, 1), "acceptance": "real (random-init pair, T=1)"}
+        stoch = {"tokens_per_s": 2 * b * NEW / (ms_s / 1e3), "k": ks,
+                 "lut": {str(x): v for x, v in lut_s.entries.items()},
+                 "acceptance_rate": round(acc_s / max(prop_s, 1), 4),
+                 "acceptance": "real (random-init pair, temperature 1): min(1, p/q) + residual resampling",
+                 "tokens_per_s_by_batch": s_by_batch,
+                 "timing": "decode tokens/s (prefill excluded), median of 3 fresh batches per (b, k) cell"}
         del eng_s
         torch.cuda.empty_cache()
 

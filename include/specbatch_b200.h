@@ -209,7 +209,7 @@ int sb_decoder_forward_mixed(const sb_decoder_t* m, const sb_kvcache_t* kv, cons
  * Next-token selection over logits rows [rows, vocab] (fp32).
  *   ARGMAX: ties -> lowest index (np.argmax); probs_out optional.
  *   SAMPLE: probs_out[r*probs_stride + v] = softmax(logits[r]) (fp32), token =
- *           canonical inverse CDF at u[r*u_stride] (see sb_accept).
+ *           canonical exact inverse CDF at u[r*u_stride] (see sb_accept).
  * Token r is written to out_tok[r*out_stride] (if non-NULL), next_ids[r], and
  * next_pos[r] = base_pos[r] + pos_offset (staging the next draft step).
  * Reference: TokenLevel.draft_tokens (engine.py:138-145) -- here the draft is
@@ -239,8 +239,11 @@ int sb_argmax_rows(const float* logits, int32_t rows, int32_t vocab, int32_t* ou
  * INJECTED:   l = min(l_inj, k)                        (TraceSampler, engine.py:109-118)
  * STOCHASTIC: accept d_j iff fp32(u_acc_j * q_j(d_j)) < p_j(d_j); on the first
  *             rejection resample from max(0, p_l - q_l), else the bonus from p_k.
- *             Inverse CDF: 256-entry chunks summed sequentially in fp64, chunk
- *             prefix sequential, first index whose running sum exceeds u*total.
+ *             One warp lane per draft position (ballot: the first rejection).
+ *             Inverse CDF over exact fixed point: W_v = floor(w_v * 2^80) (w in
+ *             [0,1] fp32), pick = first v with P_v * 2^32 > floor(u * 2^32) * total
+ *             (P_v inclusive prefix; integer sums, so any parallel order is exact
+ *             and the oracle reproduces every draw bit for bit).  vocab < 65536.
  * Outputs: accepted_len[b]; advanced[b] = min(l+1, remaining) or 0 if finished
  *          (engine.py:167); out_tok[b, k+1] = d_1..d_l, next, then -1 padding.
  */

@@ -98,9 +98,6 @@ __host__ __device__ __forceinline__ float u01(uint64_t seed, uint64_t stream, ui
   return (float)(mix3(seed, stream, ctr) >> 40) * (1.0f / 16777216.0f);
 }
 
-// Canonical inverse-CDF chunking shared with the oracle: chunk sums in fp64,
-// sequential within a chunk, sequential over chunks.
-constexpr int kCdfChunk = 256;
 
 inline int grid_for(long n, int per_block, int cap = 148 * 16) {
   long g = (n + per_block - 1) / per_block;

@@ -31,6 +31,8 @@ struct FwdWorkspace {
   float* tp_part;     // TP: fp32 partial residual update, all-reduced in place [T, H]
   float* tp_logits;   // TP: local vocab slice of the logits [T, vocab_local]
   float* tp_gather;   // TP: all-gathered slices [world][T][vocab_local]
+  float* tp_pair;     // TP greedy: this rank's (max, global argmax) per row [T][2]
+  float* tp_pairs;    // TP greedy: all-gathered pairs [world][T][2]
   AttnScratch att_split;  // flash-decoding key-split partials + counters
   void* gemm_ws;
   size_t gemm_ws_bytes;
@@ -77,6 +79,8 @@ static size_t carve(const sb_decoder_t* m, int T, char* base, FwdWorkspace* w) {
   o->tp_part = tpw ? (float*)take((size_t)T * m->hidden * 4) : nullptr;
   o->tp_logits = tpw ? (float*)take((size_t)T * m->vocab * 4) : nullptr;
   o->tp_gather = tpw ? (float*)take((size_t)tpw * T * m->vocab * 4) : nullptr;
+  o->tp_pair = tpw ? (float*)take((size_t)T * 8) : nullptr;
+  o->tp_pairs = tpw ? (float*)take((size_t)tpw * T * 8) : nullptr;
   return off;
 }
 
@@ -112,21 +116,47 @@ static int g_skip = 0;
 
 // TP exchange after a row-parallel projection whose partial went to w.tp_part:
 // all-reduce (sum over ranks), then resid += sum (+ bf16 copy / norm partials)
+// The exchange runs in the model dtype: a bf16 model's o / down GEMMs store their partial in bf16
+// (half the NVLink bytes of fp32) and the all-reduce sums bf16; the fp32 path keeps fp32.
 static int tp_reduce_add(const sb_decoder_t* m, const FwdWorkspace& w, int T, bool fused, const void* gain,
                          cudaStream_t st) {
   const sb_collectives_t* c = m->tp;
-  SB_TRY(c->all_reduce_sum(c->ctx, w.tp_part, (size_t)T * m->hidden, SB_F32, st));
+  const int dt = m->dtype == SB_BF16 ? SB_BF16 : SB_F32;
+  SB_TRY(c->all_reduce_sum(c->ctx, w.tp_part, (size_t)T * m->hidden, dt, st));
   prof_mark("allreduce", st);
-  return launch_tp_resid_add(w.resid, w.tp_part, fused ? w.xb : nullptr, fused ? w.npart : nullptr, T, m->hidden, st,
-                             gain);
+  return launch_tp_resid_add(w.resid, w.tp_part, dt == SB_BF16, fused ? w.xb : nullptr, fused ? w.npart : nullptr, T,
+                             m->hidden, st, gain);
 }
 
 // vocab-parallel lm_head: local slice -> all-gather -> full-width logits on
 // every rank (+ greedy sink from the full row)
 static int tp_lm_head(const sb_decoder_t* m, GemmArgs g, float* logits, const sb_token_sink_t* sink,
                       const FwdWorkspace& w, int rows, cudaStream_t st) {
-  if (!logits) return SB_EINVAL;
   const sb_collectives_t* c = m->tp;
+  if (sink && m->dtype == SB_BF16 && g_backend_override != GEMM_SIMT) {
+    // greedy: local argmax fused in the lm_head epilogue, then only (max, global index) per row
+    // crosses the ranks (8 bytes instead of vocab_local * 4); logits stay unmaterialised unless asked for
+    g.epi = EPI_ARGMAX;
+    g.y = logits ? w.tp_logits : nullptr;
+    g.aux_val = w.amax_val;
+    g.aux_idx = w.amax_idx;
+    if (gemm_tc_supported(g)) {
+      SB_TRY(gemm_tc(g, st));
+      prof_mark("lm_head", st);
+      SB_TRY(launch_tp_argmax_pack(w.amax_val, w.amax_idx, (m->vocab + 127) / 128, rows, c->rank * m->vocab,
+                                   w.tp_pair, st));
+      SB_TRY(c->all_gather(c->ctx, w.tp_pair, w.tp_pairs, (size_t)rows * 2, SB_F32, st));
+      SB_TRY(launch_tp_argmax_final(w.tp_pairs, c->world, rows, sink->out_tok, sink->out_stride, sink->next_ids,
+                                    sink->next_pos, sink->base_pos, sink->pos_offset, st));
+      prof_mark("argmax", st);
+      if (logits) {  // full-width logits on request (tests / fp32 consumers)
+        SB_TRY(c->all_gather(c->ctx, w.tp_logits, w.tp_gather, (size_t)rows * m->vocab, SB_F32, st));
+        SB_TRY(launch_unshard_logits(w.tp_gather, logits, c->world, rows, m->vocab, st));
+      }
+      return 0;
+    }
+  }
+  if (!logits) return SB_EINVAL;
   g.epi = EPI_STORE_F32;
   g.y = w.tp_logits;
   SB_TRY(gemm(g, GEMM_AUTO, st));
@@ -247,8 +277,8 @@ static int forward_fused_norm(const sb_decoder_t* m, const sb_kvcache_t* kv, con
     }
     prof_mark("attn", st);
     if (m->tp) {  // row-parallel o_proj: partial -> all-reduce -> residual
-      GemmArgs o{SB_BF16, w.attn, m->w_o[l], w.tp_part, T, H, nq * hd, nq * hd, EPI_STORE_F32, w.gemm_ws,
-                 w.gemm_ws_bytes};
+      GemmArgs o{SB_BF16, w.attn, m->w_o[l], w.tp_part, T, H, nq * hd, nq * hd, EPI_STORE, w.gemm_ws,
+                 w.gemm_ws_bytes};  // bf16 partial: the all-reduce moves half the bytes
       SB_TRY(gemm_tc(o, st));
       prof_mark("o", st);
       SB_TRY(tp_reduce_add(m, w, T, true, m->mlp_norm[l], st));
@@ -272,7 +302,7 @@ static int forward_fused_norm(const sb_decoder_t* m, const sb_kvcache_t* kv, con
     if (!(g_skip & 8)) SB_TRY(gemm_tc(gu, st));
     prof_mark("gu", st);
     if (m->tp) {  // row-parallel down_proj
-      GemmArgs dn{SB_BF16, w.act, m->w_down[l], w.tp_part, T, H, m->ffn, m->ffn, EPI_STORE_F32, w.gemm_ws,
+      GemmArgs dn{SB_BF16, w.act, m->w_down[l], w.tp_part, T, H, m->ffn, m->ffn, EPI_STORE, w.gemm_ws,
                   w.gemm_ws_bytes};
       SB_TRY(gemm_tc(dn, st));
       prof_mark("down", st);
@@ -431,7 +461,7 @@ static int forward_impl(const sb_decoder_t* m, const sb_kvcache_t* kv, const int
     }
     prof_mark("attn", st);
     g = GemmArgs{dt, w.attn, m->w_o[l], m->tp ? w.tp_part : w.resid, T, H, nq * hd, nq * hd,
-                 m->tp ? EPI_STORE_F32 : EPI_RESID_ADD, w.gemm_ws, w.gemm_ws_bytes};
+                 m->tp ? EPI_STORE : EPI_RESID_ADD, w.gemm_ws, w.gemm_ws_bytes};
     SB_TRY(gemm(g, GEMM_AUTO, st));
     prof_mark("o", st);
     if (m->tp) SB_TRY(tp_reduce_add(m, w, T, false, nullptr, st));
@@ -441,7 +471,7 @@ static int forward_impl(const sb_decoder_t* m, const sb_kvcache_t* kv, const int
     SB_TRY(gemm(g, GEMM_AUTO, st));
     prof_mark("gu", st);
     g = GemmArgs{dt, w.act, m->w_down[l], m->tp ? w.tp_part : w.resid, T, H, m->ffn, m->ffn,
-                 m->tp ? EPI_STORE_F32 : EPI_RESID_ADD, w.gemm_ws, w.gemm_ws_bytes};
+                 m->tp ? EPI_STORE : EPI_RESID_ADD, w.gemm_ws, w.gemm_ws_bytes};
     SB_TRY(gemm(g, GEMM_AUTO, st));
     prof_mark("down", st);
     if (m->tp) SB_TRY(tp_reduce_add(m, w, T, false, nullptr, st));

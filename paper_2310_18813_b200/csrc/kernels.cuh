@@ -107,8 +107,13 @@ int launch_kv_compact(int dtype, void* k, void* v, const int32_t* src, const int
                       int layers, int slots, int nkv, int ctx_max, int hd, cudaStream_t st);
 
 // ---- tensor-parallel glue (layer_kernels.cu)
-int launch_tp_resid_add(float* resid, const float* part, void* xb, float* npart, int T, int H, cudaStream_t st,
-                        const void* gain);
+int launch_tp_resid_add(float* resid, const void* part, int part_bf16, void* xb, float* npart, int T, int H,
+                        cudaStream_t st, const void* gain);
+int launch_tp_argmax_pack(const float* val, const int* idx, int n_tiles, int rows, int vocab_off, float* pair,
+                          cudaStream_t st);
+int launch_tp_argmax_final(const float* pairs, int world, int rows, int32_t* out_tok, int out_stride,
+                           int32_t* next_ids, int32_t* next_pos, const int32_t* base_pos, int pos_offset,
+                           cudaStream_t st);
 int launch_unshard_logits(const float* gathered, float* logits, int world, int rows, int vl, cudaStream_t st);
 
 }  // namespace sb

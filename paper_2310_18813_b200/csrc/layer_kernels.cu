@@ -754,9 +754,11 @@ namespace sb {
 // fused-norm path also the bf16 residual copy and the per-128-column
 // sum-of-squares partials npart[tile][t] the next GEMM's 1/rms reads.
 // grid (T, ceil(H/128)), 128 threads: one element per thread, fixed-order sums.
-__global__ void __launch_bounds__(128) tp_resid_add_kernel(float* __restrict__ resid, const float* __restrict__ part,
-                                                           __nv_bfloat16* __restrict__ xb, float* __restrict__ npart,
-                                                           int T, int H, const __nv_bfloat16* __restrict__ gain) {
+// part is the all-reduced update: fp32, or bf16 when part_bf16 (the bf16 model's exchange dtype).
+__global__ void __launch_bounds__(128) tp_resid_add_kernel(float* __restrict__ resid, const void* __restrict__ part,
+                                                           int part_bf16, __nv_bfloat16* __restrict__ xb,
+                                                           float* __restrict__ npart, int T, int H,
+                                                           const __nv_bfloat16* __restrict__ gain) {
   griddep_wait();
   griddep_launch();
   const int t = blockIdx.x, tile = blockIdx.y;
@@ -764,7 +766,8 @@ __global__ void __launch_bounds__(128) tp_resid_add_kernel(float* __restrict__ r
   float nv = 0.f;
   if (col < H) {
     const size_t o = (size_t)t * H + col;
-    nv = resid[o] + part[o];
+    const float pv = part_bf16 ? __bfloat162float(((const __nv_bfloat16*)part)[o]) : ((const float*)part)[o];
+    nv = resid[o] + pv;
     resid[o] = nv;
     if (xb) xb[o] = __float2bfloat16_rn(gain ? nv * __bfloat162float(gain[col]) : nv);
   }
@@ -776,11 +779,60 @@ __global__ void __launch_bounds__(128) tp_resid_add_kernel(float* __restrict__ r
   if (threadIdx.x == 0) npart[(size_t)tile * T + t] = ((red[0] + red[1]) + red[2]) + red[3];
 }
 
-int launch_tp_resid_add(float* resid, const float* part, void* xb, float* npart, int T, int H, cudaStream_t st,
-                        const void* gain) {
+int launch_tp_resid_add(float* resid, const void* part, int part_bf16, void* xb, float* npart, int T, int H,
+                        cudaStream_t st, const void* gain) {
   if (T <= 0) return 0;
-  return launch_k(tp_resid_add_kernel, dim3(T, (H + 127) / 128), dim3(128), 0, st, resid, part, (__nv_bfloat16*)xb,
-                  npart, T, H, (const __nv_bfloat16*)gain);
+  return launch_k(tp_resid_add_kernel, dim3(T, (H + 127) / 128), dim3(128), 0, st, resid, part, part_bf16,
+                  (__nv_bfloat16*)xb, npart, T, H, (const __nv_bfloat16*)gain);
+}
+
+// Vocab-parallel greedy lm_head.  pack: this rank's per-128-row argmax partials [n_tiles][rows]
+// -> one (value, global index) pair per row, pair[r] = {v, bits(i + vocab_off)} (the all-gather
+// payload: 8 bytes per row instead of the logits row).  final: merge the world gathered pairs
+// [world][rows][2] (ties -> lowest global index: identical to an argmax of the full row).
+__global__ void tp_argmax_pack_kernel(const float* __restrict__ val, const int* __restrict__ idx, int n_tiles, int rows,
+                                      int vocab_off, float2* __restrict__ pair) {
+  griddep_wait();
+  griddep_launch();
+  const int r = blockIdx.x, lane = threadIdx.x;
+  ArgMax a{-INFINITY, INT_MAX};
+  for (int t = lane; t < n_tiles; t += 32) a = argmax_merge(a, ArgMax{val[(size_t)t * rows + r], idx[(size_t)t * rows + r]});
+  a = warp_argmax(a);
+  if (lane == 0) pair[r] = make_float2(a.v, __int_as_float(a.i == INT_MAX ? INT_MAX : a.i + vocab_off));
+}
+
+__global__ void tp_argmax_final_kernel(const float2* __restrict__ pairs, int world, int rows, int32_t* out_tok,
+                                       int out_stride, int32_t* next_ids, int32_t* next_pos,
+                                       const int32_t* base_pos, int pos_offset) {
+  griddep_wait();
+  griddep_launch();
+  const int r = blockIdx.x, lane = threadIdx.x;
+  ArgMax a{-INFINITY, INT_MAX};
+  for (int w = lane; w < world; w += 32) {
+    const float2 pr = pairs[(size_t)w * rows + r];
+    a = argmax_merge(a, ArgMax{pr.x, __float_as_int(pr.y)});
+  }
+  a = warp_argmax(a);
+  if (lane == 0) {
+    if (out_tok) out_tok[(size_t)r * out_stride] = a.i;
+    if (next_ids) next_ids[r] = a.i;
+    if (next_pos) next_pos[r] = base_pos[r] + pos_offset;
+  }
+}
+
+int launch_tp_argmax_pack(const float* val, const int* idx, int n_tiles, int rows, int vocab_off, float* pair,
+                          cudaStream_t st) {
+  if (rows <= 0) return 0;
+  return launch_k(tp_argmax_pack_kernel, dim3(rows), dim3(32), 0, st, val, idx, n_tiles, rows, vocab_off,
+                  (float2*)pair);
+}
+
+int launch_tp_argmax_final(const float* pairs, int world, int rows, int32_t* out_tok, int out_stride,
+                           int32_t* next_ids, int32_t* next_pos, const int32_t* base_pos, int pos_offset,
+                           cudaStream_t st) {
+  if (rows <= 0) return 0;
+  return launch_k(tp_argmax_final_kernel, dim3(rows), dim3(32), 0, st, (const float2*)pairs, world, rows, out_tok,
+                  out_stride, next_ids, next_pos, base_pos, pos_offset);
 }
 
 // all_gather output [world][rows][Vl] -> logits [rows][world * Vl] (vocab-parallel lm_head)

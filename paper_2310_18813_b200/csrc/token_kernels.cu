@@ -11,9 +11,12 @@
 // The stochastic mode is standard speculative sampling (Leviathan/Chen, cited
 // by PAPER.md:43): accept d_j iff u_j * q_j(d_j) < p_j(d_j) (fp32 product),
 // else resample from max(0, p_j - q_j); if all k accepted, sample the bonus
-// from p_k.  Sampling is a canonical inverse CDF (chunk sums of kCdfChunk
-// entries, each chunk summed sequentially in fp64, chunks prefix-summed
-// sequentially) so oracle/spec_ref.py reproduces every draw bit-for-bit.
+// from p_k.  Sampling is a canonical inverse CDF over EXACT fixed-point sums:
+// every weight w in [0, 1] becomes the integer W = floor(w * 2^80) (exact from
+// the fp32 bits for w >= 2^-57), the pick is the first index v whose inclusive
+// prefix P_v satisfies P_v * 2^32 > floor(u * 2^32) * total.  Integer sums are
+// associative, so the block computes them in any parallel order and still
+// reproduces oracle/spec_ref.py's draw bit for bit.
 #include <climits>
 
 #include "common.cuh"
@@ -82,68 +85,76 @@ __device__ void block_softmax_row(const float* x, float* p, int V) {
   __syncthreads();
 }
 
-// Canonical inverse CDF over weights w[v] = f(v) (non-negative fp32).
-// Mode 0: w = a[v].  Mode 1: w = max(a[v] - b[v], 0).  Returns the index.
+// Canonical inverse CDF over weights w[v] = f(v) in [0, 1] (fp32), exact fixed point.
+// Mode 0: w = a[v].  Mode 1: w = max(a[v] - b[v], 0).  Returns the index, or -1 if
+// every weight is 0.  Thread t owns the contiguous range [t*n, (t+1)*n); range sums
+// are exclusive-scanned across the block (128-bit integers: any order is exact); the
+// one thread whose range holds the crossing walks it (<= n integer adds).
+typedef unsigned __int128 u128;
+
+__device__ __forceinline__ u128 fix80(float w) {
+  const uint32_t bits = __float_as_uint(w);
+  if ((int32_t)bits <= 0) return 0;        // +0, -0 and negatives
+  const uint32_t e = bits >> 23;           // biased exponent (sign bit is 0 here)
+  if (e >= 0xFF) return 0;                 // inf / NaN never count
+  if (e >= 127) return (u128)1 << 80;      // weights are probabilities: clamp at 1
+  if (e == 0) return 0;                    // subnormal (< 2^-126): below the 2^-80 resolution
+  const u128 m = (bits & 0x7FFFFF) | 0x800000;
+  return e >= 70 ? m << (e - 70) : m >> (70 - e);  // floor(m * 2^(e - 150) * 2^80)
+}
+
+__device__ __forceinline__ u128 shfl_up_u128(u128 v, int d) {
+  const uint64_t lo = __shfl_up_sync(0xffffffffu, (unsigned long long)(uint64_t)v, d);
+  const uint64_t hi = __shfl_up_sync(0xffffffffu, (unsigned long long)(uint64_t)(v >> 64), d);
+  return ((u128)hi << 64) | lo;
+}
+
 __device__ int block_inverse_cdf(const float* a, const float* b, int mode, int V, float u) {
-  __shared__ double csum[512];
+  __shared__ u128 wsum[32];
+  __shared__ u128 total_s;
   __shared__ int pick;
-  const int nch = (V + kCdfChunk - 1) / kCdfChunk;
-  for (int c = threadIdx.x; c < nch; c += blockDim.x) {
-    double s = 0.0;
-    int v1 = min(V, (c + 1) * kCdfChunk);
-    for (int v = c * kCdfChunk; v < v1; ++v) {
-      float w = mode ? fmaxf(a[v] - b[v], 0.f) : a[v];
-      s += (double)w;
+  const int nt = blockDim.x, t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int n = (V + nt - 1) / nt;
+  const int v0 = min(V, t * n), v1 = min(V, v0 + n);
+  u128 mine = 0;
+  for (int v = v0; v < v1; ++v) mine += fix80(mode ? fmaxf(a[v] - b[v], 0.f) : a[v]);
+  // inclusive warp scan, then warp totals
+  u128 inc = mine;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const u128 o = shfl_up_u128(inc, d);
+    if (lane >= d) inc += o;
+  }
+  if (t == 0) pick = -1;
+  if (lane == 31) wsum[w] = inc;
+  __syncthreads();
+  if (t == 0) {
+    u128 run = 0;
+    for (int i = 0; i < (nt >> 5); ++i) {
+      const u128 x = wsum[i];
+      wsum[i] = run;
+      run += x;
     }
-    csum[c] = s;
+    total_s = run;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double total = 0.0;
-    for (int c = 0; c < nch; ++c) total += csum[c];
-    int res = -1;
-    if (total > 0.0) {
-      double target = (double)u * total;
-      double cum = 0.0;
-      int chosen = -1;
-      double before = 0.0;
-      for (int c = 0; c < nch; ++c) {
-        double nxt = cum + csum[c];
-        if (nxt > target) {
-          chosen = c;
-          before = cum;
-          break;
-        }
-        cum = nxt;
-      }
-      if (chosen < 0) {  // rounding: take the last chunk with mass
-        for (int c = nch - 1; c >= 0; --c)
-          if (csum[c] > 0.0) {
-            chosen = c;
-            break;
-          }
-        before = 0.0;
-        for (int c = 0; c < chosen; ++c) before += csum[c];
-        target = before + csum[chosen];  // forces the last massive entry
-      }
-      double local = 0.0;
-      int last_pos = -1;
-      int v1 = min(V, (chosen + 1) * kCdfChunk);
-      for (int v = chosen * kCdfChunk; v < v1; ++v) {
-        float w = mode ? fmaxf(a[v] - b[v], 0.f) : a[v];
-        if (w > 0.f) last_pos = v;
-        local += (double)w;
-        if (before + local > target) {
-          res = v;
+  const u128 total = total_s;
+  if (total != 0) {
+    const u128 excl = wsum[w] + inc - mine;
+    const u128 target = (u128)(uint64_t)(u * 4294967296.0f) * total;  // floor(u * 2^32) * total < 2^128
+    if (mine != 0 && (excl << 32) <= target && ((excl + mine) << 32) > target) {
+      u128 run = excl;
+      for (int v = v0; v < v1; ++v) {
+        run += fix80(mode ? fmaxf(a[v] - b[v], 0.f) : a[v]);
+        if ((run << 32) > target) {
+          pick = v;
           break;
         }
       }
-      if (res < 0) res = last_pos;
     }
-    pick = res;
   }
   __syncthreads();
-  int r = pick;
+  const int r = pick;
   __syncthreads();
   return r;
 }
@@ -240,16 +251,18 @@ __global__ void accept_kernel(int mode, int k, int V, const int32_t* __restrict_
     }
     next = t[l];
   } else {
-    if (threadIdx.x == 0) {
-      int j = 0;
-      for (; j < k; ++j) {
-        int tok = d[j];
-        float pj = p_probs[((size_t)s * (k + 1) + j) * V + tok];
-        float qj = q_probs[((size_t)s * k + j) * V + tok];
-        float uq = u_acc[(size_t)s * u_stride + j] * qj;
-        if (!(uq < pj)) break;
+    if (threadIdx.x < 32) {  // lane j tests draft j (k <= 32); the first rejection ends the run
+      const int j = threadIdx.x;
+      bool rej = false;
+      if (j < k) {
+        const int tok = d[j];
+        const float pj = p_probs[((size_t)s * (k + 1) + j) * V + tok];
+        const float qj = q_probs[((size_t)s * k + j) * V + tok];
+        const float uq = u_acc[(size_t)s * u_stride + j] * qj;
+        rej = !(uq < pj);
       }
-      sh_l = j;
+      const unsigned m = __ballot_sync(0xffffffffu, rej);
+      if (j == 0) sh_l = m ? __ffs(m) - 1 : k;
     }
     __syncthreads();
     l = sh_l;
@@ -361,7 +374,7 @@ int sb_select_tokens(const float* logits, int32_t rows, int32_t vocab, int32_t m
   if (rows <= 0) return 0;
   if (mode == SB_SELECT_SAMPLE && (probs_out == nullptr || u == nullptr)) return SB_EINVAL;
   if (next_pos && !base_pos) return SB_EINVAL;
-  if ((vocab + kCdfChunk - 1) / kCdfChunk > 512) return SB_EUNSUPPORTED;
+  if (vocab >= 65536) return SB_EUNSUPPORTED;  // fixed-point totals stay below 2^96
   return launch_k(select_kernel, dim3(rows), dim3(256), 0, (cudaStream_t)stream, logits, vocab, mode, u, u_stride, probs_out, probs_stride,
                                                         out_tok, out_stride, next_ids, next_pos, base_pos, pos_offset);
 }
@@ -370,12 +383,12 @@ int sb_accept(int32_t mode, int32_t b, int32_t k, int32_t vocab, const int32_t* 
               const float* q_probs, const int32_t* draft_tok, int32_t draft_stride, const float* u_acc,
               const float* u_res, int32_t u_stride, const int32_t* l_inj, const int32_t* produced,
               const int32_t* target_len, int32_t* accepted_len, int32_t* advanced, int32_t* out_tok, void* stream) {
-  if (b <= 0 || k < 0) return SB_EINVAL;
+  if (b <= 0 || k < 0 || k > 32) return SB_EINVAL;  // (one warp lane per draft position)
   if (mode == SB_ACCEPT_STOCHASTIC && (!p_probs || (k > 0 && (!q_probs || !u_acc)) || !u_res)) return SB_EINVAL;
   if ((mode == SB_ACCEPT_GREEDY || mode == SB_ACCEPT_INJECTED) && !target_tok) return SB_EINVAL;
   if (mode == SB_ACCEPT_INJECTED && !l_inj) return SB_EINVAL;
   if (mode < 0 || mode > 2) return SB_EINVAL;
-  if ((vocab + kCdfChunk - 1) / kCdfChunk > 512) return SB_EUNSUPPORTED;
+  if (vocab >= 65536) return SB_EUNSUPPORTED;  // fixed-point totals stay below 2^96
   return launch_k(accept_kernel, dim3(b), dim3(256), 0, (cudaStream_t)stream, mode, k, vocab, target_tok, p_probs, q_probs, draft_tok,
                                                      draft_stride, u_acc, u_res, u_stride, l_inj, produced,
                                                      target_len, accepted_len, advanced, out_tok);

@@ -210,8 +210,9 @@ class SpecEngine:
                                self.workspace, st)
             launches += lib.sb_last_kernel_count()
         greedy_draft = not sample
-        # the fp32 path and a tensor-parallel target select from materialised (full-width) logits
-        need_logits = self.target.sb_dtype != N.SB_BF16 or self.target.is_tp
+        # the fp32 path selects from materialised logits; bf16 (a tensor-parallel shard included: local
+        # argmax in the lm_head epilogue, (max, index) pairs across ranks) never materialises them
+        need_logits = self.target.sb_dtype != N.SB_BF16
         draft_done = False
         if use_draft and greedy_draft and self.dl_packed is not None:
             # the whole greedy draft loop in one persistent launch (csrc/draft_loop.cu)

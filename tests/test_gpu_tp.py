@@ -34,9 +34,10 @@ def test_tp2_two_processes_one_gpu(dtype, tol):
     out = mgr.dict()
     mp.spawn(tp_worker.run, args=(2, _free_port(), dtype, out), nprocs=2, join=True)
     for r in (0, 1):
-        err, full_toks, tp_toks, calls = out[r]
+        err, full_toks, tp_toks, calls, sink_match = out[r]
         assert err < tol, (r, err)
         assert calls > 0
+        assert sink_match  # vocab-parallel greedy reduction == argmax of the gathered logits
         if dtype == "fp32":
             assert full_toks == tp_toks
     assert out[0][2] == out[1][2]  # replicated token state on both ranks

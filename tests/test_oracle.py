@@ -82,3 +82,32 @@ def test_uniforms_are_in_unit_interval_and_deterministic():
     assert u.dtype == np.float32 and (u >= 0).all() and (u < 1).all()
     assert np.array_equal(u, spec_ref.uniforms(7, 3, 4))
     assert not np.array_equal(u, spec_ref.uniforms(7, 4, 4))
+
+
+def test_inverse_cdf_fixed_point_protocol():
+    """The exact fixed-point sampler (token_kernels.cu block_inverse_cdf): W = floor(w * 2^80),
+    pick = first v with P_v * 2^32 > floor(u * 2^32) * total -- checked against a direct
+    Python-integer restatement and on the encoding's edge values."""
+    f = spec_ref.fix80
+    assert f(np.array([1.0, 0.5, 2.0 ** -57, 2.0 ** -81, 3.0, -1.0, np.nan, np.inf, 0.0], np.float32)) == \
+        [2 ** 80, 2 ** 79, 2 ** 23, 0, 2 ** 80, 0, 0, 0, 0]
+    rng = np.random.default_rng(3)
+    for trial in range(20):
+        V = int(rng.integers(1, 3000))
+        w = (rng.random(V) ** 8).astype(np.float32)
+        w[rng.random(V) < 0.3] = 0
+        u = np.float32(rng.random())
+        W = [int(float(x) * 2 ** 80) for x in w.astype(np.float64)]
+        tot = sum(W)
+        ut = int(float(u) * 2 ** 32)
+        want = -1
+        run = 0
+        for v, x in enumerate(W):
+            run += x
+            if tot and run * 2 ** 32 > ut * tot:
+                want = v
+                break
+        assert spec_ref.inverse_cdf(w, u) == want
+        # order independence of the exact total (what lets the kernel scan in parallel)
+        perm = rng.permutation(V)
+        assert sum(spec_ref.fix80(w[perm])) == tot

@@ -6,6 +6,7 @@ its shard and must reproduce the unsharded oracle's logits (fp64)."""
 
 import os
 import socket
+from dataclasses import replace
 
 import numpy as np
 import torch
@@ -35,12 +36,14 @@ def shard_masters(m, cfg, world, rank):
     return {"embed": m["embed"], "lm_head": m["lm_head"][sl(V)], "layers": lays, "gf": m["gf"]}
 
 
-def _worker(rank, world, port, out):
+def _worker(rank, world, port, out, kv_heads=None):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         cfg = CONFIGS["tiny-target"]
+        if kv_heads is not None:  # GQA: kv_heads / world kv heads per rank (TP=8 on 70B gives 1)
+            cfg = replace(cfg, n_kv_heads=kv_heads)
         m = model_ref.init_masters(cfg, 7, round_to=None)
         hd = cfg.hidden // cfg.n_heads
 
@@ -65,7 +68,22 @@ def _worker(rank, world, port, out):
         # a speculative-window-shaped second call against the sharded KV cache
         a2 = full.forward(ids[:3], [9, 10, 11], _prefilled(full, ids))
         b2 = shard.forward(ids[:3], [9, 10, 11], cache)
-        out[rank] = (float(np.abs(a - b).max()), float(np.abs(a2 - b2).max()), float(np.abs(a).max()))
+        # the vocab-parallel greedy reduction (forward.cu tp_lm_head): each rank's local argmax over
+        # its vocab slice -> (max, global index) pairs all-gathered -> the max (ties: lowest index)
+        # must equal the argmax of the full row
+        local = model_ref.LlamaRef(shard_masters(m, cfg, world, rank), cfg.n_heads // world,
+                                   cfg.n_kv_heads // world, cfg.rms_eps, max_pos=64, head_dim=hd,
+                                   tp_reduce=reduce)  # no gather: this rank's logits slice
+        lg = local.forward(ids, list(range(9)), local.new_cache())
+        vl = cfg.vocab // world
+        pair = torch.tensor(np.stack([lg.max(-1), lg.argmax(-1) + rank * vl], -1), dtype=torch.float64)
+        parts = [torch.empty_like(pair) for _ in range(world)]
+        dist.all_gather(parts, pair)
+        allp = torch.stack(parts)  # [world][rows][2]
+        best = [min(range(world), key=lambda w_: (-allp[w_, r, 0].item(), allp[w_, r, 1].item())) for r in range(9)]
+        red = [int(allp[best[r], r, 1].item()) for r in range(9)]
+        argmax_ok = red == [int(x) for x in a.argmax(-1)]
+        out[rank] = (float(np.abs(a - b).max()), float(np.abs(a2 - b2).max()), float(np.abs(a).max()), argmax_ok)
     finally:
         dist.destroy_process_group()
 
@@ -76,10 +94,15 @@ def _prefilled(model, ids):
     return c
 
 
-def test_tp_decomposition_two_ranks():
+import pytest  # noqa: E402
+
+
+@pytest.mark.parametrize("kv_heads", [None, 2], ids=["mha", "gqa-1kv-per-rank"])
+def test_tp_decomposition_two_ranks(kv_heads):
     mgr = mp.Manager()
     out = mgr.dict()
-    mp.spawn(_worker, args=(2, _free_port(), out), nprocs=2, join=True)
+    mp.spawn(_worker, args=(2, _free_port(), out, kv_heads), nprocs=2, join=True)
     for r in (0, 1):
-        e1, e2, scale = out[r]
+        e1, e2, scale, argmax_ok = out[r]
         assert e1 < 1e-9 * max(scale, 1.0) and e2 < 1e-9 * max(scale, 1.0), out[r]
+        assert argmax_ok, out[r]

@@ -41,6 +41,16 @@ def run(rank, world, port, dtype, out):
             res[name] = lg.cpu()
         scale = res["full"].abs().max().item()
         logit_err = (res["full"] - res["tp"]).abs().max().item() / scale
+        # greedy sink through the vocab-parallel reduction ((max, global index) pairs across ranks)
+        # == argmax of the same shard's gathered logits, exactly
+        kv = shard.new_kv(b, 64)
+        ws = torch.zeros(shard.workspace_bytes(b * P), device=dev, dtype=torch.uint8)
+        tp.register(ws)
+        sink_tok = torch.full((b * P,), -1, dtype=torch.int32, device=dev)
+        sink = N.SbTokenSink(sink_tok.data_ptr(), 1, None, None, None, 0)
+        shard.forward_greedy(kv, ids, slots, pos, b, P, None, N.LOGITS_ALL, ws, sink)
+        torch.cuda.synchronize()
+        sink_match = bool(torch.equal(sink_tok.cpu().long(), res["tp"].argmax(-1)))
         # speculative greedy decoding with the sharded target (replicated draft = target layer 0)
         toks = {}
         for name, tgt in (("full", full), ("tp", shard)):
@@ -52,6 +62,6 @@ def run(rank, world, port, dtype, out):
             states = [SequenceState(request_id=i, target_len=10) for i in range(2)]
             eng.generate(states, k)
             toks[name] = [list(s.tokens) for s in states]
-        out[rank] = (logit_err, toks["full"], toks["tp"], tp.calls)
+        out[rank] = (logit_err, toks["full"], toks["tp"], tp.calls, sink_match)
     finally:
         dist.destroy_process_group()
