@@ -647,9 +647,12 @@ def run_ours(args):
         s_sizes = tuple(x for x in (1, 2, 4, 8, 16) if x <= eng.max_batch) if not args.quick else (b,)
         eng_s = SpecEngine(tgt, drf, mode="stochastic", max_batch=max(s_sizes), max_k=8, prompt_len=P,
                            max_new=NEW, seed=rank, autotune=False)
-        # (real acceptance is random per batch: 3 batches per cell for the profile)
-        lut_s = build_lut(None, trace, s_grid=K_GRID, profiled_sizes=s_sizes, mode="measured", sample_size=3 * max(s_sizes),
-                          rng=np.random.default_rng(1), gen_len=NEW, engine=eng_s)
+        # (real acceptance is random per batch: 3 batches per (b, k) cell for the profile)
+        from paper_2310_18813_b200.policy import SpeculationLUT
+        cells = {bb: build_lut(None, trace, s_grid=K_GRID, profiled_sizes=(bb,), mode="measured", sample_size=3 * bb,
+                               rng=np.random.default_rng(1), gen_len=NEW, engine=eng_s) for bb in s_sizes}
+        lut_s = SpeculationLUT(entries={bb: c.entries[bb] for bb, c in cells.items()}, s_grid=K_GRID,
+                               provenance={"mode": "measured", "sample_size": "3 batches per cell"})
         s_by_batch = {}
         acc_s = prop_s = 0
         for bb in s_sizes:
