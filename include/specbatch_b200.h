@@ -345,6 +345,15 @@ int sb_set_pdl(int32_t enabled);
 /* Diagnostics: skip kernel classes of the bf16 forward (bit 0 attention, 1 qkv, 2 o, 3 gate/up, 4 down) to
    measure their marginal in-graph cost; outputs are meaningless while set.  0 = off. */
 int sb_debug_skip(int32_t mask);
+/* Diagnostics: per-CTA timeline of the GEMM / attention launches issued after this call (until called
+   with NULL; graphs captured meanwhile keep recording).  buf (zeroed, u64): buf[0] = record count, record r
+   at buf + 8 + 8r = {launch id, block, smid, t_entry, t_dependency_resolved, t_mainloop_done, t_exit,
+   kind (1 gemm, 2 attention)}, globaltimer ns.  The caller sizes buf for the CTAs it launches. */
+int sb_debug_cta_trace(void* buf);
+/* Experiments: GEMM weight stages requested before the PDL wait (0 = the whole ring) and where the GEMM
+   triggers its dependents (0 after its last load, 1 after its epilogue); flags bit 0 skips the epilogue
+   stores (outputs meaningless).  Takes effect for later launches. */
+int sb_debug_gemm_pdl(int32_t pre_max, int32_t launch_late, int32_t flags);
 /* RMSNorm fused into the GEMM epilogues on the bf16 path (default on); 0 = separate norm kernels. */
 int sb_set_fuse_norm(int32_t enabled);
 /* Diagnostics: eager forward with an event after every kernel; per-stage summed ms as "tag=ms;..." in buf. */

@@ -78,6 +78,8 @@ _SIGS = {
     "sb_set_pdl": (C.c_int, [_I]),
     "sb_set_fuse_norm": (C.c_int, [_I]),
     "sb_debug_skip": (C.c_int, [_I]),
+    "sb_debug_cta_trace": (C.c_int, [_P]),
+    "sb_debug_gemm_pdl": (C.c_int, [_I, _I, _I]),
     "sb_set_attention_impl": (C.c_int, [_I]),
     "sb_set_attention_splits": (C.c_int, [_I]),
     "sb_set_draft_loop": (C.c_int, [_I]),

@@ -55,6 +55,9 @@ struct AttnArgs {
   const __nv_bfloat16* qr;
   int q_blk;
   int kv_evict_first;  // KV history streamed with an L2 evict-first policy (the target's cache)
+  unsigned long long* trace;  // sb_debug_cta_trace (NULL = off)
+  int trace_id;
+  unsigned long long* tr_t;   // this CTA's stamps (shared memory)
 };
 struct AttnShared {
   int qpos[16], qtok[16], qhead[16];
@@ -178,6 +181,7 @@ __device__ __forceinline__ void attn_tc_item(const AttnArgs& A, int kvh, int seq
     griddep_wait();
     griddep_launch();
   }
+  if (A.trace && tid == 0) A.tr_t[1] = gtime();
   if (blk)
     for (int i = 0; i < kTcStages; ++i) issue(t_lo + i, false);
   {

@@ -29,6 +29,34 @@ extern int g_pdl;                        // launch with programmatic stream seri
 __device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// Diagnostics (sb_debug_cta_trace): per-CTA timeline records of the traced kernels.
+// buf[0] = record count (atomic); record r at buf + 8 + 8 r:
+//   {launch id | kind << 32 | smid << 40, linear block id, t_entry, t_dependency_resolved,
+//    t_first_stage (first operands on chip), t_mainloop_done, t_exit, 0}   (globaltimer ns)
+extern unsigned long long* g_cta_trace;  // NULL = off
+extern int g_cta_trace_seq;
+extern int g_gemm_pre_max, g_gemm_launch_late, g_gemm_dbg;              // launch ids since the last sb_debug_cta_trace call
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void cta_trace_write(unsigned long long* buf, int id, int kind, const unsigned long long* t) {
+  unsigned smid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  const unsigned long long now = gtime();
+  const unsigned long long r = atomicAdd(buf, 1ull);
+  unsigned long long* o = buf + 8 + 8 * r;
+  o[0] = (unsigned long long)(unsigned)id | ((unsigned long long)kind << 32) | ((unsigned long long)smid << 40);
+  o[1] = blockIdx.x + (unsigned long long)gridDim.x * (blockIdx.y + (unsigned long long)gridDim.y * blockIdx.z);
+  o[2] = t[0];
+  o[3] = t[1];
+  o[4] = t[2];
+  o[5] = t[3];
+  o[6] = now;
+  o[7] = 0;
+}
+
 // Launch helper: cudaLaunchKernelEx with the PDL attribute (and optional cluster).
 template <typename... KArgs, typename... Args>
 inline int launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args... args) {

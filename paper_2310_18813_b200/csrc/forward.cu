@@ -156,11 +156,19 @@ static int tp_lm_head(const sb_decoder_t* m, GemmArgs g, float* logits, const sb
       return 0;
     }
   }
-  if (!logits) return SB_EINVAL;
+  if (!logits && !sink) return SB_EINVAL;
   g.epi = EPI_STORE_F32;
   g.y = w.tp_logits;
   SB_TRY(gemm(g, GEMM_AUTO, st));
   prof_mark("lm_head", st);
+  if (!logits) {  // greedy without logits (fp32): (max, global index) per row of the local slice crosses the ranks
+    SB_TRY(launch_tp_argmax_pack(w.tp_logits, nullptr, m->vocab, rows, c->rank * m->vocab, w.tp_pair, st));
+    SB_TRY(c->all_gather(c->ctx, w.tp_pair, w.tp_pairs, (size_t)rows * 2, SB_F32, st));
+    SB_TRY(launch_tp_argmax_final(w.tp_pairs, c->world, rows, sink->out_tok, sink->out_stride, sink->next_ids,
+                                  sink->next_pos, sink->base_pos, sink->pos_offset, st));
+    prof_mark("argmax", st);
+    return 0;
+  }
   SB_TRY(c->all_gather(c->ctx, w.tp_logits, w.tp_gather, (size_t)rows * m->vocab, SB_F32, st));
   SB_TRY(launch_unshard_logits(w.tp_gather, logits, c->world, rows, m->vocab, st));
   if (sink)
@@ -642,6 +650,19 @@ int sb_set_attention_splits(int32_t splits) {
 
 int sb_debug_skip(int32_t mask) {
   g_skip = mask;
+  return 0;
+}
+
+int sb_debug_gemm_pdl(int32_t pre_max, int32_t launch_late, int32_t flags) {
+  sb::g_gemm_pre_max = pre_max;
+  sb::g_gemm_launch_late = launch_late;
+  sb::g_gemm_dbg = flags;
+  return 0;
+}
+
+int sb_debug_cta_trace(void* buf) {
+  sb::g_cta_trace = (unsigned long long*)buf;
+  sb::g_cta_trace_seq = 0;
   return 0;
 }
 

@@ -66,9 +66,24 @@ struct TcParams {
   const __nv_bfloat16* out_gain;  // RMSNorm gain of the CONSUMER of xb: xb = bf16(new * gain[n]) (NULL = 1)
   const __nv_bfloat16* bias;  // OPT: per-row bias [N] added before the epilogue op
   int relu;
+  unsigned long long* trace;  // sb_debug_cta_trace (NULL = off)
+  int trace_id;
+  int pre_max;      // ring stages of weights requested before the PDL wait (0 = all)
+  int launch_late;  // 1: trigger dependents at the end of the epilogue instead of after the last load
+  int dbg;          // experiments (sb_debug_gemm_pdl): bit 0 skip the epilogue stores, bit 3 plain stores,
+                    // bit 4 scalar (per-element) epilogue
 };
 
 __device__ __forceinline__ float silu_f(float g) { return g / (1.f + __expf(-g)); }
+
+// Epilogue stores are streaming (st.global.cs): with the weight stream saturating HBM, default
+// write-back stores took ~2 us per 16-token chunk (measured: scripts/epi_micro.py, 2.40 -> 0.90 us at
+// 9 tokens, 10.6 -> 3.4 us at 72); dbg bit 3 restores plain stores for A/B.
+template <typename T>
+__device__ __forceinline__ void st_o(const TcParams& p, T* dst, T v) {
+  if (p.dbg & 8) *dst = v;
+  else __stcs(dst, v);
+}
 
 
 // Output of one (token m, weight row n) element.  Returns the value the
@@ -79,13 +94,13 @@ __device__ __forceinline__ float epi_one(const TcParams& p, int m, int n, float 
   if (p.bias) v += __bfloat162float(p.bias[n]);
   if (p.relu && p.epi != EPI_RESID_ADD) v = fmaxf(v, 0.f);
   if (p.epi == EPI_STORE) {
-    ((__nv_bfloat16*)p.y)[o] = __float2bfloat16_rn(v);
+    st_o(p, (__nv_bfloat16*)p.y + o, __float2bfloat16_rn(v));
   } else if (p.epi == EPI_STORE_F32) {
-    ((float*)p.y)[o] = v;
+    st_o(p, (float*)p.y + o, v);
   } else {
     float nv = ((float*)p.y)[o] + v;
-    ((float*)p.y)[o] = nv;
-    if (p.out_xb) p.out_xb[o] = __float2bfloat16_rn(p.out_gain ? nv * __bfloat162float(p.out_gain[n]) : nv);
+    st_o(p, (float*)p.y + o, nv);
+    if (p.out_xb) st_o(p, p.out_xb + o, __float2bfloat16_rn(p.out_gain ? nv * __bfloat162float(p.out_gain[n]) : nv));
     return nv;
   }
   return v;
@@ -98,8 +113,8 @@ __device__ __forceinline__ float epi_resid_pre(const TcParams& p, int m, int n, 
   const size_t o = (size_t)m * p.N + n;
   if (p.bias) v += __bfloat162float(p.bias[n]);
   const float nv = prev + v;
-  ((float*)p.y)[o] = nv;
-  if (p.out_xb) p.out_xb[o] = __float2bfloat16_rn(p.out_gain ? nv * __bfloat162float(p.out_gain[n]) : nv);
+  st_o(p, (float*)p.y + o, nv);
+  if (p.out_xb) st_o(p, p.out_xb + o, __float2bfloat16_rn(p.out_gain ? nv * __bfloat162float(p.out_gain[n]) : nv));
   return nv;
 }
 __device__ __forceinline__ float resid_load(const TcParams& p, int m, int n) {
@@ -108,7 +123,56 @@ __device__ __forceinline__ float resid_load(const TcParams& p, int m, int n) {
 // SILU pairs rows (n, n+1) = (gate, up)
 __device__ __forceinline__ void epi_pair(const TcParams& p, int m, int n, float g, float u) {
   if (m >= p.M || n >= p.N) return;
-  ((__nv_bfloat16*)p.y)[(size_t)m * (p.N / 2) + n / 2] = __float2bfloat16_rn(silu_f(g) * u);
+  st_o(p, (__nv_bfloat16*)p.y + (size_t)m * (p.N / 2) + n / 2, __float2bfloat16_rn(silu_f(g) * u));
+}
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+  return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(a)) |
+         ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(b)) << 16);
+}
+// Vector epilogue: the output op on weight rows n..n+3 (n % 4 == 0, N % 4 == 0) of token m, one 8-16
+// byte streaming store per output tensor.  Returns the sum of squares of the new residual
+// (EPI_RESID_ADD, for the consumer's RMSNorm partials), else 0.
+__device__ __forceinline__ float epi4(const TcParams& p, int m, int n, float (&x)[4]) {
+  if (m >= p.M || n >= p.N) return 0.f;
+  const size_t o = (size_t)m * p.N + n;
+  if (p.bias) {
+    const uint2 bb = *reinterpret_cast<const uint2*>(p.bias + n);
+    x[0] += __bfloat162float(__ushort_as_bfloat16((unsigned short)(bb.x & 0xffff)));
+    x[1] += __bfloat162float(__ushort_as_bfloat16((unsigned short)(bb.x >> 16)));
+    x[2] += __bfloat162float(__ushort_as_bfloat16((unsigned short)(bb.y & 0xffff)));
+    x[3] += __bfloat162float(__ushort_as_bfloat16((unsigned short)(bb.y >> 16)));
+  }
+  if (p.relu && p.epi != EPI_RESID_ADD)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) x[i] = fmaxf(x[i], 0.f);
+  if (p.epi == EPI_STORE) {
+    __stcs(reinterpret_cast<uint2*>((__nv_bfloat16*)p.y + o), make_uint2(pack_bf16x2(x[0], x[1]), pack_bf16x2(x[2], x[3])));
+  } else if (p.epi == EPI_STORE_F32) {
+    __stcs(reinterpret_cast<float4*>((float*)p.y + o), make_float4(x[0], x[1], x[2], x[3]));
+  } else if (p.epi == EPI_SILU_MUL) {
+    __stcs(reinterpret_cast<unsigned int*>((__nv_bfloat16*)p.y + (size_t)m * (p.N / 2) + n / 2),
+           pack_bf16x2(silu_f(x[0]) * x[1], silu_f(x[2]) * x[3]));
+  } else {  // EPI_RESID_ADD
+    float4* rp = reinterpret_cast<float4*>((float*)p.y + o);
+    const float4 pr = __ldcg(rp);
+    const float a0 = pr.x + x[0], a1 = pr.y + x[1], a2 = pr.z + x[2], a3 = pr.w + x[3];
+    __stcs(rp, make_float4(a0, a1, a2, a3));
+    if (p.out_xb) {
+      float g[4] = {1.f, 1.f, 1.f, 1.f};
+      if (p.out_gain) {
+        const uint2 gg = *reinterpret_cast<const uint2*>(p.out_gain + n);
+        g[0] = __bfloat162float(__ushort_as_bfloat16((unsigned short)(gg.x & 0xffff)));
+        g[1] = __bfloat162float(__ushort_as_bfloat16((unsigned short)(gg.x >> 16)));
+        g[2] = __bfloat162float(__ushort_as_bfloat16((unsigned short)(gg.y & 0xffff)));
+        g[3] = __bfloat162float(__ushort_as_bfloat16((unsigned short)(gg.y >> 16)));
+      }
+      __stcs(reinterpret_cast<uint2*>(p.out_xb + o),
+             make_uint2(pack_bf16x2(a0 * g[0], a1 * g[1]), pack_bf16x2(a2 * g[2], a3 * g[3])));
+    }
+    return ((a0 * a0 + a1 * a1) + a2 * a2) + a3 * a3;
+  }
+  return 0.f;
 }
 
 // Rows of the 128-row tile reduced by cluster rank `split` (pairs, so the
@@ -121,6 +185,8 @@ __host__ __device__ __forceinline__ int split_rows_max(int splits) { return 2 * 
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x, TcParams p) {
   extern __shared__ uint8_t smem_raw[];
+  __shared__ unsigned long long tr_t[4];
+  if (p.trace && threadIdx.x == 0) tr_t[0] = gtime();
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const int tn = p.tn;
   const int wt = p.wt;
@@ -181,7 +247,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       // kernel, so the first ring of weight tiles is requested BEFORE the
       // programmatic-dependency wait: under PDL the weight stream of this GEMM
       // overlaps the tail of the kernel that produces its activations.
-      const int pre = nkb < p.stages ? nkb : p.stages;
+      int pre = nkb < p.stages ? nkb : p.stages;
+      if (p.pre_max > 0 && pre > p.pre_max) pre = p.pre_max;
       // single token tile (decode): every CTA reads the same X k-block at the same time -> rotate
       // each weight tile's k order to spread those reads over L2 (several token tiles share the
       // weight tile instead: keep their k order aligned so the weight stream hits L2)
@@ -195,6 +262,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         else tma_load_2d(sa, &map_w, &full[i], kb_of(i) * TC_BK, n0);
       }
       griddep_wait();
+      if (p.trace) tr_t[1] = gtime();
       for (int i = 0; i < pre; ++i)
         tma_load_2d(stage_base + i * stage_bytes + a_bytes, &map_x, &full[i], kb_of(i) * TC_BK, m0);
       int stage = pre % p.stages;
@@ -211,7 +279,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           phase ^= 1;
         }
       }
-      griddep_launch();
+      if (!p.launch_late) griddep_launch();
     }
   } else if (warp == 1) {
     if (lane == 0) {
@@ -222,6 +290,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       for (int i = 0; i < nkb; ++i) {
         mbar_wait(&full[stage], phase);
         tc_fence_after();
+        if (p.trace && i == 0) tr_t[2] = gtime();
         uint32_t sa = smem_u32(stage_base + stage * stage_bytes);
         uint32_t sb = sa + a_bytes;
         for (int a = 0; a < wt; ++a) {  // the X stage feeds every weight tile of the CTA
@@ -281,7 +350,61 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     mbar_wait(tmem_full, 0);
     tc_fence_after();
+    if (p.trace && et == 0) tr_t[3] = gtime();
+    const bool vec = (p.N % 4 == 0) && !(p.dbg & 16);  // dbg bit 4: legacy scalar epilogue (A/B)
     const bool scale = p.ns_part != nullptr;
+    if (vec && p.splits == 1) {
+      // Vector epilogue: each 16-token chunk goes TMEM -> registers -> shared memory ([16][128] fp32,
+      // double-buffered in the drained ring), then warp ew takes tokens ew, ew+4, ...: lane l owns
+      // rows 4l..4l+3, so every warp-wide load / store covers one token's 128 contiguous rows.
+      const int ew = warp - 2;
+      for (int acc = 0; acc < wt; ++acc) {
+        const int n0a = n0 + acc * TC_BM;
+        const int tile_a = tile_n * wt + acc;
+        for (int j0 = 0; j0 < tn; j0 += 16) {
+          float* sb = red + ((j0 >> 4) & 1) * 16 * TC_BM;
+          {
+            float v[16];
+            tmem_ld16(lane_addr + (uint32_t)(acc * tn) + j0, v);
+#pragma unroll
+            for (int j = 0; j < 16; ++j) sb[j * TC_BM + row] = v[j];
+          }
+          asm volatile("bar.sync 1, 128;" ::: "memory");
+#pragma unroll
+          for (int jj = 0; jj < 4; ++jj) {
+            const int j = ew + 4 * jj;
+            const int m = m0 + j0 + j;
+            const int n = n0a + 4 * lane;
+            const float4 a = *reinterpret_cast<const float4*>(sb + j * TC_BM + 4 * lane);
+            float x[4] = {a.x, a.y, a.z, a.w};
+            if (scale) {
+              const float sc = inv_s[j0 + j];
+#pragma unroll
+              for (int i = 0; i < 4; ++i) x[i] *= sc;
+            }
+            if (p.epi == EPI_ARGMAX) {
+              ArgMax b{-INFINITY, INT_MAX};
+#pragma unroll
+              for (int i = 0; i < 4; ++i)
+                if (n + i < p.N && x[i] > b.v) b = ArgMax{x[i], n + i};
+              if (p.y && m < p.M && n < p.N)
+                __stcs(reinterpret_cast<float4*>((float*)p.y + (size_t)m * p.N + n), make_float4(x[0], x[1], x[2], x[3]));
+              b = warp_argmax(b);
+              if (lane == 0 && m < p.M && tile_a < p.n_tiles_n) {
+                st_o(p, p.aux_val + (size_t)tile_a * p.M + m, b.v);
+                st_o(p, p.aux_idx + (size_t)tile_a * p.M + m, b.i);
+              }
+            } else {
+              float sq = epi4(p, m, n, x);
+              if (p.out_part) {
+                sq = warp_sum(sq);
+                if (lane == 0 && m < p.M && tile_a < p.n_tiles_n) st_o(p, p.out_part + (size_t)tile_a * p.M + m, sq);
+              }
+            }
+          }
+        }
+      }
+    } else
     for (int acc = 0; acc < wt; ++acc) {
     const int n0a = n0 + acc * TC_BM;             // this accumulator's weight rows
     const int tile_a = tile_n * wt + acc;          // its 128-row tile index
@@ -289,6 +412,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     for (int j0 = 0; j0 < tn; j0 += 16) {
       float v[16];
       tmem_ld16(lane_addr + (uint32_t)(acc * tn) + j0, v);
+      if (p.dbg & 1) {  // experiment: no epilogue stores
+        if (v[0] == 12345.f) ((float*)p.y)[0] = v[1];
+        continue;
+      }
       if (p.splits > 1) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) red[(j0 + j) * TC_BM + row] = v[j];
@@ -306,7 +433,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int j = 0; j < 16; ++j) {
           const int m = m0 + j0 + j, n = n0a + row;
           float val = (n < p.N) ? v[j] : -INFINITY;
-          if (p.y && m < p.M && n < p.N) ((float*)p.y)[(size_t)m * p.N + n] = v[j];
+          if (p.y && m < p.M && n < p.N) st_o(p, (float*)p.y + (size_t)m * p.N + n, v[j]);
           ArgMax a = warp_argmax(ArgMax{val, n < p.N ? n : INT_MAX});
           if (lane == 0) {
             qv[quad * tn + j0 + j] = a.v;
@@ -318,6 +445,15 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         for (int j = 0; j < 16; ++j) {
           float other = __shfl_xor_sync(0xffffffffu, v[j], 1);
           if (!(lane & 1)) epi_pair(p, m0 + j0 + j, n0a + row, v[j], other);
+        }
+      } else if ((p.dbg & 6) && p.epi == EPI_STORE_F32) {  // experiments: one store per chunk / streaming stores
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const int m = m0 + j0 + j, n = n0a + row;
+          if (m < p.M && n < p.N && (!(p.dbg & 2) || j == 0)) {
+            float* dst = (float*)p.y + (size_t)m * p.N + n;
+            if (p.dbg & 4) __stcs(dst, v[j]); else *dst = v[j];
+          }
         }
       } else {
         float rv[16];
@@ -347,10 +483,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           ArgMax a{qv[j], qi[j]};
 #pragma unroll
           for (int q = 1; q < 4; ++q) a = argmax_merge(a, ArgMax{qv[q * tn + j], qi[q * tn + j]});
-          p.aux_val[(size_t)tile_a * p.M + m] = a.v;
-          p.aux_idx[(size_t)tile_a * p.M + m] = a.i;
+          st_o(p, p.aux_val + (size_t)tile_a * p.M + m, a.v);
+          st_o(p, p.aux_idx + (size_t)tile_a * p.M + m, a.i);
         } else {
-          p.out_part[(size_t)tile_a * p.M + m] = ((sq[j] + sq[tn + j]) + sq[2 * tn + j]) + sq[3 * tn + j];
+          st_o(p, p.out_part + (size_t)tile_a * p.M + m, ((sq[j] + sq[tn + j]) + sq[2 * tn + j]) + sq[3 * tn + j]);
         }
       }
     }
@@ -363,7 +499,49 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // CTA `split` owns rows [split*R, (split+1)*R) of the tile and sums the
     // cluster's partials in rank order 0..splits-1.
     cluster_sync_all();
-    if (warp >= 2) {
+    // (power-of-two splits: every rank's row range is a multiple of 16 rows)
+    const bool vec = (p.N % 4 == 0) && !(p.dbg & 16) && !(p.splits & (p.splits - 1));
+    if (warp >= 2 && vec) {
+      // rank `split` reduces rows [r_base, r_base + R): item = (token j, 4-row group q4); the G = R / 4
+      // lanes of one token are adjacent in a warp (G divides 32), so the norm partial is a fixed xor
+      // tree over them.  One v4 DSMEM load per rank, summed in rank order.
+      const int r_base = split_row_lo(split, p.splits);
+      const int R = split_row_lo(split + 1, p.splits) - r_base;
+      const int G = R / 4;
+      const int et = threadIdx.x - 64;
+      const uint32_t red_addr = smem_u32(red);
+      const bool scale = p.ns_part != nullptr;
+      const int total = tn * G;
+      for (int it0 = 0; it0 < total; it0 += 128) {
+        const int it = it0 + et;
+        const bool ok = it < total;
+        const int j = ok ? it / G : 0, q4 = it % G;
+        const int r = r_base + 4 * q4;
+        float4 t[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q < p.splits && ok) t[q] = ld_dsmem_v4_nc(red_addr + (uint32_t)((j * TC_BM + r) * 4), q);
+        float x[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+          if (q < p.splits && ok) {
+            x[0] += t[q].x;
+            x[1] += t[q].y;
+            x[2] += t[q].z;
+            x[3] += t[q].w;
+          }
+        if (scale && ok) {
+          const float sc = inv_s[j];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) x[i] *= sc;
+        }
+        float sq = ok ? epi4(p, m0 + j, n0 + r, x) : 0.f;
+        if (p.out_part) {
+          for (int o = G >> 1; o >= 1; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+          if (ok && q4 == 0 && m0 + j < p.M) st_o(p, p.out_part + ((size_t)tile_n * p.splits + split) * p.M + m0 + j, sq);
+        }
+      }
+    } else if (warp >= 2) {
       const int r_base = split_row_lo(split, p.splits);
       const int R = split_row_lo(split + 1, p.splits) - r_base;
       const int et = threadIdx.x - 64;
@@ -452,15 +630,17 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             if (m >= p.M) continue;
             float s = 0.f;
             for (int rl = 0; rl < R; ++rl) s += sq[j * R + rl];
-            p.out_part[((size_t)tile_n * p.splits + split) * p.M + m] = s;
+            st_o(p, p.out_part + ((size_t)tile_n * p.splits + split) * p.M + m, s);
           }
         }
       }
     }
-    cluster_sync_all();
+    cluster_sync_relaxed();
   }
   tc_fence_before();
   __syncthreads();
+  if (p.launch_late) griddep_launch();
+  if (p.trace && threadIdx.x == 0) cta_trace_write(p.trace, p.trace_id, 1, tr_t);
   if (warp == 1) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(tmem_cols));
@@ -515,6 +695,7 @@ static int tn_for(int M) {
 }
 
 int g_pdl = 1;  // programmatic dependent launch for every forward kernel (sb_set_pdl)
+int g_gemm_pre_max = 0, g_gemm_launch_late = 0, g_gemm_dbg = 0;  // sb_debug_gemm_pdl experiments
 // tuning overrides (sb_gemm_tune): 0 = automatic
 static int g_tune_cps = 0, g_tune_stages = 0, g_tune_splits = 0;
 
@@ -783,6 +964,11 @@ int gemm_tc(const GemmArgs& a, cudaStream_t st) {
   p.out_gain = (const __nv_bfloat16*)a.out_gain;
   p.bias = (const __nv_bfloat16*)a.bias;
   p.relu = a.relu;
+  p.pre_max = g_gemm_pre_max;
+  p.launch_late = g_gemm_launch_late;
+  p.dbg = g_gemm_dbg;
+  p.trace = g_cta_trace;
+  p.trace_id = g_cta_trace ? g_cta_trace_seq++ : 0;
   if ((a.bias || a.relu) && (a.epi == EPI_SILU_MUL || a.epi == EPI_ARGMAX)) return SB_EINVAL;
   if (a.out_part && a.epi != EPI_RESID_ADD) return SB_EINVAL;
   if (a.epi == EPI_ARGMAX && (!a.aux_val || !a.aux_idx)) return SB_EINVAL;

@@ -19,6 +19,8 @@
 namespace sb {
 
 thread_local int g_kernel_count = 0;
+unsigned long long* g_cta_trace = nullptr;
+int g_cta_trace_seq = 0;
 
 // ---------------------------------------------------------------- embedding
 template <typename T>
@@ -575,6 +577,8 @@ template <int HD, int STAGES>
 __global__ void __launch_bounds__(128) attention_tc_kernel(AttnArgs A) {
   extern __shared__ __align__(128) uint8_t tsm[];
   __shared__ AttnShared sh;
+  __shared__ unsigned long long tr_t[4];
+  if (A.trace && threadIdx.x == 0) tr_t[0] = tr_t[2] = tr_t[3] = gtime();
   if (A.l2_next && threadIdx.x < 32) {
     // The attention reads little (KV history) and waits a lot: keep HBM busy by
     // pulling this CTA's share of the next GEMM's weights into L2 (bulk prefetch,
@@ -588,6 +592,17 @@ __global__ void __launch_bounds__(128) attention_tc_kernel(AttnArgs A) {
       const unsigned n = (unsigned)min(16384ull, hi - o);
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.l2_next + o), "r"(n) : "memory");
     }
+  }
+  if (A.trace) {
+    AttnArgs B = A;
+    B.tr_t = tr_t;
+    if (A.qr)
+      attn_tc_item<HD, STAGES>(B, blockIdx.x, blockIdx.y, 0, 1, tsm, sh, threadIdx.x, true, blockIdx.z);
+    else
+      attn_tc_item<HD, STAGES>(B, blockIdx.x, blockIdx.y, blockIdx.z, gridDim.z, tsm, sh, threadIdx.x, true);
+    __syncthreads();
+    if (threadIdx.x == 0) cta_trace_write(A.trace, A.trace_id, 2, tr_t);
+    return;
   }
   if (A.qr)
     attn_tc_item<HD, STAGES>(A, blockIdx.x, blockIdx.y, 0, 1, tsm, sh, threadIdx.x, true, blockIdx.z);
@@ -621,7 +636,11 @@ int attention_tc_init() {
 }
 
 // Launch attention_tc_kernel over grid (nkv, n_seq, z) with the ring depth for its residency.
-static int launch_attn_grid(const AttnArgs& A, int hd, int n_seq, int z, cudaStream_t st) {
+static int launch_attn_grid(const AttnArgs& A0, int hd, int n_seq, int z, cudaStream_t st) {
+  AttnArgs A = A0;
+  A.trace = g_cta_trace;
+  A.trace_id = g_cta_trace ? g_cta_trace_seq++ : 0;
+  A.tr_t = nullptr;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(A.nkv, n_seq, z);
   cfg.blockDim = dim3(128);
@@ -790,13 +809,18 @@ int launch_tp_resid_add(float* resid, const void* part, int part_bf16, void* xb,
 // -> one (value, global index) pair per row, pair[r] = {v, bits(i + vocab_off)} (the all-gather
 // payload: 8 bytes per row instead of the logits row).  final: merge the world gathered pairs
 // [world][rows][2] (ties -> lowest global index: identical to an argmax of the full row).
+// idx == NULL: val is this rank's raw logits slice [rows][n_tiles] (fp32 path: no fused partials) and
+// the column is the local index.
 __global__ void tp_argmax_pack_kernel(const float* __restrict__ val, const int* __restrict__ idx, int n_tiles, int rows,
                                       int vocab_off, float2* __restrict__ pair) {
   griddep_wait();
   griddep_launch();
   const int r = blockIdx.x, lane = threadIdx.x;
   ArgMax a{-INFINITY, INT_MAX};
-  for (int t = lane; t < n_tiles; t += 32) a = argmax_merge(a, ArgMax{val[(size_t)t * rows + r], idx[(size_t)t * rows + r]});
+  if (idx)
+    for (int t = lane; t < n_tiles; t += 32) a = argmax_merge(a, ArgMax{val[(size_t)t * rows + r], idx[(size_t)t * rows + r]});
+  else
+    for (int t = lane; t < n_tiles; t += 32) a = argmax_merge(a, ArgMax{val[(size_t)r * n_tiles + t], t});
   a = warp_argmax(a);
   if (lane == 0) pair[r] = make_float2(a.v, __int_as_float(a.i == INT_MAX ? INT_MAX : a.i + vocab_off));
 }
