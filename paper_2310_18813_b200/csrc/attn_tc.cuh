@@ -265,6 +265,7 @@ __device__ __forceinline__ void attn_tc_item(const AttnArgs& A, int kvh, int seq
   }
   __threadfence_block();
   attn_sync();
+  if (A.trace && tid == 0) A.tr_t[2] = gtime();
 
   // Q fragments (A operand), loaded once
   const uint32_t qs_base = (uint32_t)__cvta_generic_to_shared(Qs);
@@ -365,6 +366,7 @@ __device__ __forceinline__ void attn_tc_item(const AttnArgs& A, int kvh, int seq
   }
   cp_async_wait<0>();
   attn_sync();
+  if (A.trace && tid == 0) A.tr_t[3] = gtime();
   // combine the 4 warps in order (smem partials alias the drained ring)
   float* comb = reinterpret_cast<float*>(ring);
   float* cm = comb + 4 * 16 * HD;
@@ -385,20 +387,33 @@ __device__ __forceinline__ void attn_tc_item(const AttnArgs& A, int kvh, int seq
   }
   attn_sync();
   if (n_splits == 1) {
-    for (int e = tid; e < nQ * HD; e += 128) {
-      int j = e / HD, d = e % HD;
+    // 8 consecutive dims per thread: one 16-byte streaming store (scalar 2-byte stores of the output
+    // row cost ~2 us under the weight stream, like the GEMM epilogue's)
+    for (int e = tid; e < nQ * (HD / 8); e += 128) {
+      const int j = e / (HD / 8), d0 = (e % (HD / 8)) * 8;
       float M = -INFINITY;
 #pragma unroll
       for (int w = 0; w < 4; ++w) M = fmaxf(M, cm[w * 16 + j]);
-      float L = 0.f, acc = 0.f;
+      float f[4], L = 0.f;
 #pragma unroll
       for (int w = 0; w < 4; ++w) {
-        float mw = cm[w * 16 + j];
-        float f = (mw == -INFINITY) ? 0.f : __expf(mw - M);
-        L += cl[w * 16 + j] * f;
-        acc += comb[(w * 16 + j) * HD + d] * f;
+        const float mw = cm[w * 16 + j];
+        f[w] = (mw == -INFINITY) ? 0.f : __expf(mw - M);
+        L += cl[w * 16 + j] * f[w];
       }
-      out[((size_t)(seq * q_len + qtok[j]) * nq + qhead[j]) * HD + d] = __float2bfloat16_rn(L > 0.f ? acc / L : 0.f);
+      float acc[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        acc[i] = 0.f;
+#pragma unroll
+        for (int w = 0; w < 4; ++w) acc[i] += comb[(w * 16 + j) * HD + d0 + i] * f[w];
+      }
+      uint4 pk;
+      uint32_t* pw = reinterpret_cast<uint32_t*>(&pk);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        pw[i] = pack_bf16(L > 0.f ? acc[2 * i] / L : 0.f, L > 0.f ? acc[2 * i + 1] / L : 0.f);
+      __stcs(reinterpret_cast<uint4*>(out + ((size_t)(seq * q_len + qtok[j]) * nq + qhead[j]) * HD + d0), pk);
     }
     return;
   }

@@ -72,7 +72,25 @@ struct TcParams {
   int launch_late;  // 1: trigger dependents at the end of the epilogue instead of after the last load
   int dbg;          // experiments (sb_debug_gemm_pdl): bit 0 skip the epilogue stores, bit 3 plain stores,
                     // bit 4 scalar (per-element) epilogue
+  int vec;          // bulk-copy epilogue (N % 16 == 0, 16-byte aligned outputs, power-of-two splits)
+  int res_bytes;    // EPI_RESID_ADD: bytes of residual rows prefetched into shared memory (0 = loaded per row)
 };
+
+// Shared-memory scratch of the epilogue (reuses the drained operand ring).  Bulk-copy epilogue:
+// staging (split-K: the partial tile [tn][128] f32 the cluster reads; else [2][16][128] f32), then
+// per epilogue warp two 768-byte output rows (f32 row + bf16 row), then the prefetched residual rows.
+constexpr uint32_t TC_OB_BYTES = 4 * 2 * 768;
+__host__ __device__ inline uint32_t tc_stage_bytes(int tn, int splits) {
+  return splits > 1 ? (uint32_t)tn * TC_BM * 4 : 2u * 16 * TC_BM * 4;
+}
+__host__ __device__ inline uint32_t tc_scratch_bytes(int tn, int splits, int vec, int rows_max) {
+  if (vec) return tc_stage_bytes(tn, splits) + TC_OB_BYTES;
+  return splits > 1 ? (uint32_t)tn * (TC_BM + rows_max) * 4 : (uint32_t)tn * 12 * 4;
+}
+// The prefetched residual rows live AFTER max(ring, scratch): they land while the ring is in use.
+__host__ __device__ inline uint32_t tc_res_offset(uint32_t ring_bytes, uint32_t scratch_bytes) {
+  return ((ring_bytes > scratch_bytes ? ring_bytes : scratch_bytes) + 127) & ~127u;
+}
 
 __device__ __forceinline__ float silu_f(float g) { return g / (1.f + __expf(-g)); }
 
@@ -175,6 +193,124 @@ __device__ __forceinline__ float epi4(const TcParams& p, int m, int n, float (&x
   return 0.f;
 }
 
+// Bulk-copy epilogue: emit token j's row of the 128-row tile at n0a (lane l holds rows 4l..4l+3 in x):
+// the output op writes the row(s) into this warp's shared-memory slot, one thread bulk-copies them
+// to global memory (TMA engine: the SM's store path is off the critical path -- thread stores of
+// the same rows cost ~2 us per 16 tokens while the weight stream saturates HBM), then the norm
+// partial / argmax of the row are reduced over the warp (fixed xor trees).
+__device__ __forceinline__ void tc_emit_row(const TcParams& p, uint8_t* smem, int tn, int ew, int lane, int& slot,
+                                            int j, int jr, int acc, int m0, int n0a, int tile_a, float (&x)[4],
+                                            float sc, uint64_t* res_bar, const float* rb) {
+  const int m = m0 + j;
+  if (m >= p.M) return;  // (warp-uniform) padding token: nothing to write
+  const int n = n0a + 4 * lane;
+  const bool nv = n < p.N;
+  // dbg bit 8: bulk (TMA engine) copies of the formatted rows instead of direct 8-16 byte streaming stores
+  // (measured slower in the forward: 3.15 vs 3.01 ms verify at b=8, k=3 -- each copy waits on its slot)
+  const bool bulk = (p.dbg & 256) != 0 || ((p.dbg & 512) && p.splits == 1);
+  uint8_t* ob = smem + tc_stage_bytes(tn, p.splits) + (uint32_t)(ew * 2 + slot) * 768;
+  float* of = reinterpret_cast<float*>(ob);
+  __nv_bfloat16* oh = reinterpret_cast<__nv_bfloat16*>(ob + 512);
+  if (bulk) {
+    slot ^= 1;
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // this slot's last copy has read it
+    __syncwarp();
+  }
+  const size_t o = (size_t)m * p.N + n;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) x[i] *= sc;
+  if (p.bias && nv) {
+    const uint2 bb = *reinterpret_cast<const uint2*>(p.bias + n);
+    x[0] += __bfloat162float(__ushort_as_bfloat16((unsigned short)(bb.x & 0xffff)));
+    x[1] += __bfloat162float(__ushort_as_bfloat16((unsigned short)(bb.x >> 16)));
+    x[2] += __bfloat162float(__ushort_as_bfloat16((unsigned short)(bb.y & 0xffff)));
+    x[3] += __bfloat162float(__ushort_as_bfloat16((unsigned short)(bb.y >> 16)));
+  }
+  if (p.relu && p.epi != EPI_RESID_ADD)
+#pragma unroll
+    for (int i = 0; i < 4; ++i) x[i] = fmaxf(x[i], 0.f);
+  float sq = 0.f;
+  ArgMax am{-INFINITY, INT_MAX};
+  if (p.epi == EPI_STORE) {
+    const uint2 v = make_uint2(pack_bf16x2(x[0], x[1]), pack_bf16x2(x[2], x[3]));
+    if (bulk) *reinterpret_cast<uint2*>(oh + 4 * lane) = v;
+    else if (nv) __stcs(reinterpret_cast<uint2*>((__nv_bfloat16*)p.y + o), v);
+  } else if (p.epi == EPI_STORE_F32) {
+    const float4 v = make_float4(x[0], x[1], x[2], x[3]);
+    if (bulk) *reinterpret_cast<float4*>(of + 4 * lane) = v;
+    else if (nv) __stcs(reinterpret_cast<float4*>((float*)p.y + o), v);
+  } else if (p.epi == EPI_SILU_MUL) {
+    const uint32_t v = pack_bf16x2(silu_f(x[0]) * x[1], silu_f(x[2]) * x[3]);
+    if (bulk) *reinterpret_cast<uint32_t*>(oh + 2 * lane) = v;
+    else if (nv) __stcs(reinterpret_cast<unsigned int*>((__nv_bfloat16*)p.y + (size_t)m * (p.N / 2) + n / 2), v);
+  } else if (p.epi == EPI_ARGMAX) {
+    if (p.y) {
+      const float4 v = make_float4(x[0], x[1], x[2], x[3]);
+      if (bulk) *reinterpret_cast<float4*>(of + 4 * lane) = v;
+      else if (nv) __stcs(reinterpret_cast<float4*>((float*)p.y + o), v);
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (n + i < p.N && x[i] > am.v) am = ArgMax{x[i], n + i};
+  } else {  // EPI_RESID_ADD
+    float4 pr = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (p.res_bytes) {
+      mbar_wait(res_bar, 0);
+      pr = *reinterpret_cast<const float4*>(rb + ((size_t)acc * tn + jr) * TC_BM + 4 * lane);
+    } else if (nv) {
+      pr = __ldcg(reinterpret_cast<const float4*>((const float*)p.y + o));
+    }
+    const float a0 = pr.x + x[0], a1 = pr.y + x[1], a2 = pr.z + x[2], a3 = pr.w + x[3];
+    const float4 v = make_float4(a0, a1, a2, a3);
+    if (bulk) *reinterpret_cast<float4*>(of + 4 * lane) = v;
+    else if (nv) __stcs(reinterpret_cast<float4*>((float*)p.y + o), v);
+    if (p.out_xb) {
+      float g[4] = {1.f, 1.f, 1.f, 1.f};
+      if (p.out_gain && nv) {
+        const uint2 gg = *reinterpret_cast<const uint2*>(p.out_gain + n);
+        g[0] = __bfloat162float(__ushort_as_bfloat16((unsigned short)(gg.x & 0xffff)));
+        g[1] = __bfloat162float(__ushort_as_bfloat16((unsigned short)(gg.x >> 16)));
+        g[2] = __bfloat162float(__ushort_as_bfloat16((unsigned short)(gg.y & 0xffff)));
+        g[3] = __bfloat162float(__ushort_as_bfloat16((unsigned short)(gg.y >> 16)));
+      }
+      const uint2 hv = make_uint2(pack_bf16x2(a0 * g[0], a1 * g[1]), pack_bf16x2(a2 * g[2], a3 * g[3]));
+      if (bulk) *reinterpret_cast<uint2*>(oh + 4 * lane) = hv;
+      else if (nv) __stcs(reinterpret_cast<uint2*>(p.out_xb + o), hv);
+    }
+    sq = nv ? ((a0 * a0 + a1 * a1) + a2 * a2) + a3 * a3 : 0.f;
+  }
+  if (bulk) {
+    fence_proxy_async_smem();
+    __syncwarp();
+    const int rows = min(TC_BM, p.N - n0a);
+    if (lane == 0) {
+      if (rows > 0) {
+        const size_t o0 = (size_t)m * p.N + n0a;
+        if (p.epi == EPI_STORE) bulk_s2g((__nv_bfloat16*)p.y + o0, smem_u32(oh), rows * 2);
+        else if (p.epi == EPI_STORE_F32) bulk_s2g((float*)p.y + o0, smem_u32(of), rows * 4);
+        else if (p.epi == EPI_SILU_MUL) bulk_s2g((__nv_bfloat16*)p.y + (size_t)m * (p.N / 2) + n0a / 2, smem_u32(oh), rows);
+        else if (p.epi == EPI_ARGMAX) { if (p.y) bulk_s2g((float*)p.y + o0, smem_u32(of), rows * 4); }
+        else {
+          bulk_s2g((float*)p.y + o0, smem_u32(of), rows * 4);
+          if (p.out_xb) bulk_s2g(p.out_xb + o0, smem_u32(oh), rows * 2);
+        }
+      }
+      bulk_commit();
+    }
+  }
+  if (p.out_part) {
+    sq = warp_sum(sq);
+    if (lane == 0 && tile_a < p.n_tiles_n) st_o(p, p.out_part + (size_t)tile_a * p.M + m, sq);
+  }
+  if (p.epi == EPI_ARGMAX) {
+    am = warp_argmax(am);
+    if (lane == 0 && tile_a < p.n_tiles_n) {
+      st_o(p, p.aux_val + (size_t)tile_a * p.M + m, am.v);
+      st_o(p, p.aux_idx + (size_t)tile_a * p.M + m, am.i);
+    }
+  }
+}
+
 // Rows of the 128-row tile reduced by cluster rank `split` (pairs, so the
 // silu(gate)*up epilogue never straddles two ranks): [2*(split*64/s), 2*((split+1)*64/s)).
 __host__ __device__ __forceinline__ int split_row_lo(int split, int splits) { return 2 * (split * (TC_BM / 2) / splits); }
@@ -196,12 +332,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const uint32_t ring_bytes = p.stages * stage_bytes;
   // scratch (reuses the drained ring): split>1: partial tile [tn][128] + squares [tn][rows_max];
   // split==1: argmax staging [2][4][tn] + squares [4][tn]
-  const uint32_t scratch_bytes = p.splits > 1 ? (uint32_t)tn * (TC_BM + split_rows_max(p.splits)) * 4 : (uint32_t)tn * 12 * 4;
+  const uint32_t scratch_bytes = tc_scratch_bytes(tn, p.splits, p.vec, split_rows_max(p.splits));
   uint8_t* stage_base = smem;
-  uint64_t* full = (uint64_t*)(smem + (ring_bytes > scratch_bytes ? ring_bytes : scratch_bytes));
+  float* res_rows = (float*)(smem + tc_res_offset(ring_bytes, scratch_bytes));  // [wt][tn][128] (res_bytes)
+  uint64_t* full = (uint64_t*)(smem + tc_res_offset(ring_bytes, scratch_bytes) + p.res_bytes);
   uint64_t* empty = full + p.stages;
   uint64_t* tmem_full = empty + p.stages;
-  uint32_t* tmem_slot = (uint32_t*)(tmem_full + 1);
+  uint64_t* res_bar = tmem_full + 1;  // residual rows landed (bulk-copy epilogue)
+  uint32_t* tmem_slot = (uint32_t*)(res_bar + 1);
   float* inv_s = (float*)(tmem_slot + 4);  // [tn] per-token 1/rms (fused RMSNorm)
   float* nsum = inv_s + tn;                 // [4][tn] per-token partial sums of squares (fused RMSNorm)
   float* red = (float*)smem;               // split-K partial tile [tn][128] (reuses the drained ring)
@@ -227,6 +365,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       mbar_init(&empty[s], 1);
     }
     mbar_init(tmem_full, 1);
+    mbar_init(res_bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_w) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(&map_x) : "memory");
@@ -255,6 +394,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const int rot = (p.k_rot && p.m_tiles == 1) ? (int)((tile_n * 7u) % (unsigned)nkb) : 0;
       const uint64_t wpol = p.w_hint == 2 ? l2_policy_evict_last() : l2_policy_evict_first();
       auto kb_of = [&](int i) { const int j = i + rot; return kb0 + (j >= nkb ? j - nkb : j); };
+      if (p.dbg & 64) griddep_launch();  // experiment: dependents may launch right away
       for (int i = 0; i < pre; ++i) {
         uint8_t* sa = stage_base + i * stage_bytes;
         mbar_expect_tx(&full[i], stage_bytes);
@@ -311,6 +451,24 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // ---------------- epilogue warps: TMEM -> registers -> (DSMEM reduce) -> global
     griddep_wait();
     const int et = threadIdx.x - 64;
+    if (p.vec && p.res_bytes && et == 0) {
+      // the residual rows this CTA will update (final since the previous kernel completed) head for
+      // shared memory now, under the weight stream: one 512-byte bulk copy per (tile, token)
+      const int jlo = p.splits > 1 ? split * tn / p.splits : 0, jhi = p.splits > 1 ? (split + 1) * tn / p.splits : tn;
+      const int nj = min(jhi, p.M - m0) - jlo;
+      float* rb = res_rows;
+      if (nj > 0) {
+        int nt = 0;
+        for (int a = 0; a < wt; ++a) nt += (n0 + a * TC_BM < p.N) ? 1 : 0;
+        mbar_expect_tx(res_bar, (uint32_t)(nt * nj * TC_BM * 4));
+        for (int a = 0; a < nt; ++a)
+          for (int j = 0; j < nj; ++j)
+            bulk_g2s_bar(rb + ((size_t)a * tn + j) * TC_BM, (const float*)p.y + (size_t)(m0 + jlo + j) * p.N + n0 + a * TC_BM,
+                         TC_BM * 4, res_bar);
+      } else {
+        mbar_arrive(res_bar);
+      }
+    }
     const int quad = warp & 3;
     const int row = quad * 32 + lane;  // weight row within the tile (= TMEM lane)
     const uint32_t lane_addr = tmem + ((uint32_t)(quad * 32) << 16);
@@ -351,58 +509,42 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     mbar_wait(tmem_full, 0);
     tc_fence_after();
     if (p.trace && et == 0) tr_t[3] = gtime();
-    const bool vec = (p.N % 4 == 0) && !(p.dbg & 16);  // dbg bit 4: legacy scalar epilogue (A/B)
     const bool scale = p.ns_part != nullptr;
-    if (vec && p.splits == 1) {
-      // Vector epilogue: each 16-token chunk goes TMEM -> registers -> shared memory ([16][128] fp32,
-      // double-buffered in the drained ring), then warp ew takes tokens ew, ew+4, ...: lane l owns
-      // rows 4l..4l+3, so every warp-wide load / store covers one token's 128 contiguous rows.
-      const int ew = warp - 2;
-      for (int acc = 0; acc < wt; ++acc) {
-        const int n0a = n0 + acc * TC_BM;
-        const int tile_a = tile_n * wt + acc;
+    if (p.vec) {
+      if (p.splits > 1) {
+        // split-K: dump this CTA's partial tile for the cluster (reduced after the cluster barrier)
         for (int j0 = 0; j0 < tn; j0 += 16) {
-          float* sb = red + ((j0 >> 4) & 1) * 16 * TC_BM;
-          {
-            float v[16];
-            tmem_ld16(lane_addr + (uint32_t)(acc * tn) + j0, v);
+          float v[16];
+          tmem_ld16(lane_addr + (uint32_t)j0, v);
 #pragma unroll
-            for (int j = 0; j < 16; ++j) sb[j * TC_BM + row] = v[j];
-          }
-          asm volatile("bar.sync 1, 128;" ::: "memory");
+          for (int j = 0; j < 16; ++j) red[(j0 + j) * TC_BM + row] = v[j];
+        }
+      } else {
+        // Each 16-token chunk goes TMEM -> registers -> shared memory ([16][128] f32, double-buffered),
+        // then warp ew emits tokens ew, ew+4, ...: lane l owns rows 4l..4l+3 of the token's row.
+        const int ew = warp - 2;
+        int slot = 0;
+        for (int acc = 0; acc < wt; ++acc) {
+          for (int j0 = 0; j0 < tn; j0 += 16) {
+            float* sb = red + ((j0 >> 4) & 1) * 16 * TC_BM;
+            {
+              float v[16];
+              tmem_ld16(lane_addr + (uint32_t)(acc * tn) + j0, v);
 #pragma unroll
-          for (int jj = 0; jj < 4; ++jj) {
-            const int j = ew + 4 * jj;
-            const int m = m0 + j0 + j;
-            const int n = n0a + 4 * lane;
-            const float4 a = *reinterpret_cast<const float4*>(sb + j * TC_BM + 4 * lane);
-            float x[4] = {a.x, a.y, a.z, a.w};
-            if (scale) {
-              const float sc = inv_s[j0 + j];
-#pragma unroll
-              for (int i = 0; i < 4; ++i) x[i] *= sc;
+              for (int j = 0; j < 16; ++j) sb[j * TC_BM + row] = v[j];
             }
-            if (p.epi == EPI_ARGMAX) {
-              ArgMax b{-INFINITY, INT_MAX};
+            asm volatile("bar.sync 1, 128;" ::: "memory");
 #pragma unroll
-              for (int i = 0; i < 4; ++i)
-                if (n + i < p.N && x[i] > b.v) b = ArgMax{x[i], n + i};
-              if (p.y && m < p.M && n < p.N)
-                __stcs(reinterpret_cast<float4*>((float*)p.y + (size_t)m * p.N + n), make_float4(x[0], x[1], x[2], x[3]));
-              b = warp_argmax(b);
-              if (lane == 0 && m < p.M && tile_a < p.n_tiles_n) {
-                st_o(p, p.aux_val + (size_t)tile_a * p.M + m, b.v);
-                st_o(p, p.aux_idx + (size_t)tile_a * p.M + m, b.i);
-              }
-            } else {
-              float sq = epi4(p, m, n, x);
-              if (p.out_part) {
-                sq = warp_sum(sq);
-                if (lane == 0 && m < p.M && tile_a < p.n_tiles_n) st_o(p, p.out_part + (size_t)tile_a * p.M + m, sq);
-              }
+            for (int jj = 0; jj < 4; ++jj) {
+              const int j = j0 + ew + 4 * jj;
+              const float4 a = *reinterpret_cast<const float4*>(sb + (ew + 4 * jj) * TC_BM + 4 * lane);
+              float x[4] = {a.x, a.y, a.z, a.w};
+              tc_emit_row(p, smem, tn, ew, lane, slot, j, j, acc, m0, n0 + acc * TC_BM, tile_n * wt + acc, x,
+                          scale ? inv_s[j] : 1.f, res_bar, res_rows);
             }
           }
         }
+        if ((p.dbg & 768) && lane == 0) bulk_wait_read0();  // (global visibility: at grid completion)
       }
     } else
     for (int acc = 0; acc < wt; ++acc) {
@@ -499,48 +641,32 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // CTA `split` owns rows [split*R, (split+1)*R) of the tile and sums the
     // cluster's partials in rank order 0..splits-1.
     cluster_sync_all();
-    // (power-of-two splits: every rank's row range is a multiple of 16 rows)
-    const bool vec = (p.N % 4 == 0) && !(p.dbg & 16) && !(p.splits & (p.splits - 1));
-    if (warp >= 2 && vec) {
-      // rank `split` reduces rows [r_base, r_base + R): item = (token j, 4-row group q4); the G = R / 4
-      // lanes of one token are adjacent in a warp (G divides 32), so the norm partial is a fixed xor
-      // tree over them.  One v4 DSMEM load per rank, summed in rank order.
-      const int r_base = split_row_lo(split, p.splits);
-      const int R = split_row_lo(split + 1, p.splits) - r_base;
-      const int G = R / 4;
-      const int et = threadIdx.x - 64;
+    if (warp >= 2 && p.vec) {
+      // rank `split` owns tokens [jlo, jhi) of the tile, all 128 rows: warp ew reduces token jlo+ew,
+      // +4, ... (lane l: rows 4l..4l+3, one v4 DSMEM load per rank, summed in rank order) and emits it
+      const int ew = warp - 2;
       const uint32_t red_addr = smem_u32(red);
       const bool scale = p.ns_part != nullptr;
-      const int total = tn * G;
-      for (int it0 = 0; it0 < total; it0 += 128) {
-        const int it = it0 + et;
-        const bool ok = it < total;
-        const int j = ok ? it / G : 0, q4 = it % G;
-        const int r = r_base + 4 * q4;
+      const int jlo = split * tn / p.splits, jhi = (split + 1) * tn / p.splits;
+      int slot = 0;
+      for (int j = jlo + ew; j < jhi; j += 4) {
         float4 t[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-          if (q < p.splits && ok) t[q] = ld_dsmem_v4_nc(red_addr + (uint32_t)((j * TC_BM + r) * 4), q);
+          if (q < p.splits) t[q] = ld_dsmem_v4_nc(red_addr + (uint32_t)((j * TC_BM + 4 * lane) * 4), q);
         float x[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int q = 0; q < 8; ++q)
-          if (q < p.splits && ok) {
+          if (q < p.splits) {
             x[0] += t[q].x;
             x[1] += t[q].y;
             x[2] += t[q].z;
             x[3] += t[q].w;
           }
-        if (scale && ok) {
-          const float sc = inv_s[j];
-#pragma unroll
-          for (int i = 0; i < 4; ++i) x[i] *= sc;
-        }
-        float sq = ok ? epi4(p, m0 + j, n0 + r, x) : 0.f;
-        if (p.out_part) {
-          for (int o = G >> 1; o >= 1; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-          if (ok && q4 == 0 && m0 + j < p.M) st_o(p, p.out_part + ((size_t)tile_n * p.splits + split) * p.M + m0 + j, sq);
-        }
+        tc_emit_row(p, smem, tn, ew, lane, slot, j, j - jlo, 0, m0, n0, tile_n, x, scale ? inv_s[j] : 1.f, res_bar,
+                    res_rows);
       }
+      if ((p.dbg & 256) && lane == 0) bulk_wait_read0();  // (global visibility: at grid completion)
     } else if (warp >= 2) {
       const int r_base = split_row_lo(split, p.splits);
       const int R = split_row_lo(split + 1, p.splits) - r_base;
@@ -702,6 +828,7 @@ static int g_tune_cps = 0, g_tune_stages = 0, g_tune_splits = 0;
 struct TcPlan {
   int tn, n_tiles_n, m_tiles, kb, splits, stages, ctas_per_sm, wt;
   size_t smem;
+  int vec, res_bytes;
 };
 struct TcTuned {
   int cps, splits, wt, tn;  // tn 0: token tile of tn_for(M)
@@ -720,6 +847,13 @@ static unsigned long long tune_key(int tn, int m_tiles, int N, int K) {
          (unsigned long long)K;
 }
 
+static void tc_plan_smem(TcPlan& q) {
+  const size_t stage = (size_t)(TC_BM * q.wt + q.tn) * TC_BK * 2;
+  const size_t ring = (size_t)q.stages * stage;
+  const size_t scratch = tc_scratch_bytes(q.tn, q.splits, q.vec, split_rows_max(q.splits));
+  q.smem = 1024 + tc_res_offset((uint32_t)ring, (uint32_t)scratch) + q.res_bytes + 256 + 16 + (size_t)q.tn * 4 * 5;
+}
+
 // Split-K policy for the HBM-bound regime: enough CTAs that every SM streams
 // weights (>= one per SM), at most one resident wave, >= 2 k-blocks per CTA,
 // cluster size <= 8 (portable).
@@ -733,7 +867,7 @@ static TcPlan plan(int M, int N, int K, int epi) {
   q.ctas_per_sm = g_tune_cps ? g_tune_cps : (q.tn >= 128 ? 1 : 2);
   // cps 3 (tuning only): size the grid for ONE CTA per SM but keep the smem of
   // two, leaving each SM a free slot for the next kernel's early weight prefetch (PDL)
-  bool half_smem = false;
+  bool half_smem = (g_gemm_dbg & 32) != 0;  // experiment: every GEMM CTA fits beside another one (PDL prefetch)
   if (q.ctas_per_sm == 3) {
     q.ctas_per_sm = 1;
     half_smem = true;
@@ -779,10 +913,30 @@ static TcPlan plan(int M, int N, int K, int epi) {
   q.stages = (int)((budget - 1024 - 256) / stage);
   if (q.stages > (g_tune_stages ? g_tune_stages : 12)) q.stages = g_tune_stages ? g_tune_stages : 12;
   if (q.stages < 2) q.stages = 2;
-  size_t ring = (size_t)q.stages * stage;
-  size_t scratch = q.splits > 1 ? (size_t)q.tn * (TC_BM + split_rows_max(q.splits)) * 4 : (size_t)q.tn * 12 * 4;
-  q.smem = 1024 + (ring > scratch ? ring : scratch) + 256 + 16 + (size_t)q.tn * 4 * 5;
+  q.vec = 0;
+  q.res_bytes = 0;
+  tc_plan_smem(q);
   return q;
+}
+
+// Bulk-copy epilogue eligibility (16-byte rows, aligned outputs, power-of-two split ranks) and the
+// residual prefetch of EPI_RESID_ADD (when this CTA's rows fit in 32 KB).
+static void tc_plan_vec(TcPlan& q, const GemmArgs& a) {
+  q.vec = !(g_gemm_dbg & 16) && a.N % 16 == 0 && !(q.splits & (q.splits - 1)) && !((uintptr_t)a.y & 15) &&
+          !(a.out_xb && ((uintptr_t)a.out_xb & 15)) && !(a.bias && ((uintptr_t)a.bias & 7)) &&
+          !(a.out_gain && ((uintptr_t)a.out_gain & 7));
+  q.res_bytes = 0;
+  if (q.vec && a.epi == EPI_RESID_ADD) {
+    const int tok = q.splits > 1 ? (q.tn + q.splits - 1) / q.splits : q.tn;
+    const int bytes = q.wt * tok * TC_BM * 4;
+    if (bytes <= 32 * 1024) q.res_bytes = bytes;
+  }
+  tc_plan_smem(q);
+  if (q.res_bytes && (q.smem > 220 * 1024 || (q.ctas_per_sm >= 2 && q.smem > 110 * 1024))) {
+    // (within the kernel's smem limit, and two CTAs per SM stay resident)
+    q.res_bytes = 0;
+    tc_plan_smem(q);
+  }
 }
 
 int gemm_tc_tune(int cps, int stages, int splits) {
@@ -917,7 +1071,8 @@ int gemm_tc_init() {
 
 int gemm_tc_norm_partials(const GemmArgs& a) {
   TcPlan q = plan(a.M, a.N, a.K, a.epi);
-  return q.n_tiles_n * q.splits;
+  tc_plan_vec(q, a);
+  return q.vec ? q.n_tiles_n : q.n_tiles_n * q.splits;  // bulk-copy epilogue: one complete partial per tile
 }
 
 bool gemm_tc_supported(const GemmArgs& a) {
@@ -935,6 +1090,7 @@ int gemm_tc(const GemmArgs& a, cudaStream_t st) {
   if (a.M <= 0 || a.N <= 0 || a.K <= 0) return SB_EINVAL;
   SB_TRY(gemm_tc_init());
   TcPlan q = plan(a.M, a.N, a.K, a.epi);
+  tc_plan_vec(q, a);
   CUtensorMap mw, mx;
   SB_TRY(make_map(&mw, a.w, a.N, a.K, a.K, TC_BM * q.wt));
   SB_TRY(make_map(&mx, a.x, a.M, a.K, a.ldx, q.tn));
@@ -967,6 +1123,8 @@ int gemm_tc(const GemmArgs& a, cudaStream_t st) {
   p.pre_max = g_gemm_pre_max;
   p.launch_late = g_gemm_launch_late;
   p.dbg = g_gemm_dbg;
+  p.vec = q.vec;
+  p.res_bytes = q.res_bytes;
   p.trace = g_cta_trace;
   p.trace_id = g_cta_trace ? g_cta_trace_seq++ : 0;
   if ((a.bias || a.relu) && (a.epi == EPI_SILU_MUL || a.epi == EPI_ARGMAX)) return SB_EINVAL;

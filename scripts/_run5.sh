@@ -1,0 +1,3 @@
+timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_model.py tests/test_gpu_headline_shapes.py tests/test_gpu_opt.py -x -q -p no:cacheprovider > gpurun_out/t5.txt 2>&1
+tail -3 gpurun_out/t5.txt
+timeout 800 python scripts/ab_dbg.py 0 16 > gpurun_out/ab_vec.txt 2>&1; cat gpurun_out/ab_vec.txt

@@ -16,7 +16,7 @@ for (Nw, K) in [(22016, 4096)]:
         for epi, name in [(N.EPI_STORE_F32, "f32")]:
             if epi == 3 and Nw % 2: continue
             y = torch.zeros(M, Nw, device=dev)
-            for dbg in (0, 1, 2, 4):
+            for dbg in (0, 1, 128):
                 lib.sb_debug_gemm_pdl(0, 0, dbg)
                 for _ in range(3):
                     N.call("sb_gemm", N.SB_BF16, x.data_ptr(), w.data_ptr(), y.data_ptr(), M, Nw, K, epi, N.GEMM_TC, None, 0, st)
@@ -25,6 +25,10 @@ for (Nw, K) in [(22016, 4096)]:
                 N.call("sb_gemm", N.SB_BF16, x.data_ptr(), w.data_ptr(), y.data_ptr(), M, Nw, K, epi, N.GEMM_TC, None, 0, st)
                 lib.sb_debug_cta_trace(None)
                 torch.cuda.synchronize()
+                if dbg != 1:
+                    ref = x.float() @ w.float().T
+                    err = (y - ref).abs().max().item()
+                    assert err < 1e-2, (M, dbg, err)
                 n = int(buf[0].item())
                 raw = buf[8:8 + 8 * n].view(n, 8).cpu().numpy().astype(np.int64)
                 t = (raw[:, 2:7] - raw[:, 2].min()) / 1e3
