@@ -323,7 +323,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   extern __shared__ uint8_t smem_raw[];
   __shared__ unsigned long long tr_t[4];
   if (p.trace && threadIdx.x == 0) tr_t[0] = gtime();
-  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // 1024-aligned base by pointer arithmetic on smem_raw (keeps the shared address space visible to the
+  // compiler: STS / LDS instead of generic ST / LD for the epilogue staging)
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   const int tn = p.tn;
   const int wt = p.wt;
   const uint32_t a_bytes = wt * TC_BM * TC_BK * 2;
