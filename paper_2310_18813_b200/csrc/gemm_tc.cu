@@ -80,8 +80,9 @@ struct TcParams {
 // staging (split-K: the partial tile [tn][128] f32 the cluster reads; else [2][16][128] f32), then
 // per epilogue warp two 768-byte output rows (f32 row + bf16 row), then the prefetched residual rows.
 constexpr uint32_t TC_OB_BYTES = 4 * 2 * 768;
+constexpr int TC_EPI_CH = 32;  // tokens per staged epilogue chunk (splits == 1)
 __host__ __device__ inline uint32_t tc_stage_bytes(int tn, int splits) {
-  return splits > 1 ? (uint32_t)tn * TC_BM * 4 : 2u * 16 * TC_BM * 4;
+  return splits > 1 ? (uint32_t)tn * TC_BM * 4 : 2u * TC_EPI_CH * TC_BM * 4;
 }
 __host__ __device__ inline uint32_t tc_scratch_bytes(int tn, int splits, int vec, int rows_max) {
   if (vec) return tc_stage_bytes(tn, splits) + TC_OB_BYTES;
@@ -522,24 +523,30 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           for (int j = 0; j < 16; ++j) red[(j0 + j) * TC_BM + row] = v[j];
         }
       } else {
-        // Each 16-token chunk goes TMEM -> registers -> shared memory ([16][128] f32, double-buffered),
-        // then warp ew emits tokens ew, ew+4, ...: lane l owns rows 4l..4l+3 of the token's row.
+        // Each chunk of up to 32 tokens goes TMEM -> registers -> shared memory ([32][128] f32,
+        // double-buffered; one tcgen05.wait per chunk), then warp ew emits tokens ew, ew+4, ...:
+        // lane l owns rows 4l..4l+3 of the token's row.
         const int ew = warp - 2;
-        int slot = 0;
+        int slot = 0, ci = 0;
         for (int acc = 0; acc < wt; ++acc) {
-          for (int j0 = 0; j0 < tn; j0 += 16) {
-            float* sb = red + ((j0 >> 4) & 1) * 16 * TC_BM;
+          for (int j0 = 0; j0 < tn; j0 += TC_EPI_CH, ++ci) {
+            float* sb = red + (ci & 1) * TC_EPI_CH * TC_BM;
+            const int cn = min(TC_EPI_CH, tn - j0);  // 16 or 32 (tn % 16 == 0)
             {
-              float v[16];
-              tmem_ld16(lane_addr + (uint32_t)(acc * tn) + j0, v);
+              uint32_t r0[16], r1[16];
+              tmem_ld16_nw(lane_addr + (uint32_t)(acc * tn) + j0, r0);
+              if (cn > 16) tmem_ld16_nw(lane_addr + (uint32_t)(acc * tn) + j0 + 16, r1);
+              tmem_ld_wait();
 #pragma unroll
-              for (int j = 0; j < 16; ++j) sb[j * TC_BM + row] = v[j];
+              for (int j = 0; j < 16; ++j) sb[j * TC_BM + row] = __uint_as_float(r0[j]);
+              if (cn > 16)
+#pragma unroll
+                for (int j = 0; j < 16; ++j) sb[(16 + j) * TC_BM + row] = __uint_as_float(r1[j]);
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");
-#pragma unroll
-            for (int jj = 0; jj < 4; ++jj) {
-              const int j = j0 + ew + 4 * jj;
-              const float4 a = *reinterpret_cast<const float4*>(sb + (ew + 4 * jj) * TC_BM + 4 * lane);
+            for (int jl = ew; jl < cn; jl += 4) {
+              const int j = j0 + jl;
+              const float4 a = *reinterpret_cast<const float4*>(sb + jl * TC_BM + 4 * lane);
               float x[4] = {a.x, a.y, a.z, a.w};
               tc_emit_row(p, smem, tn, ew, lane, slot, j, j, acc, m0, n0 + acc * TC_BM, tile_n * wt + acc, x,
                           scale ? inv_s[j] : 1.f, res_bar, res_rows);
