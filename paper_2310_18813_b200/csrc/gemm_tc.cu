@@ -107,14 +107,15 @@ __device__ __forceinline__ void st_o(const TcParams& p, T* dst, T v) {
 
 // Output of one (token m, weight row n) element.  Returns the value the
 // element ends with (the new residual for EPI_RESID_ADD) for norm partials.
+template <int E_>
 __device__ __forceinline__ float epi_one(const TcParams& p, int m, int n, float v) {
   if (m >= p.M || n >= p.N) return 0.f;
   size_t o = (size_t)m * p.N + n;
   if (p.bias) v += __bfloat162float(p.bias[n]);
-  if (p.relu && p.epi != EPI_RESID_ADD) v = fmaxf(v, 0.f);
-  if (p.epi == EPI_STORE) {
+  if (p.relu && E_ != EPI_RESID_ADD) v = fmaxf(v, 0.f);
+  if (E_ == EPI_STORE) {
     st_o(p, (__nv_bfloat16*)p.y + o, __float2bfloat16_rn(v));
-  } else if (p.epi == EPI_STORE_F32) {
+  } else if (E_ == EPI_STORE_F32) {
     st_o(p, (float*)p.y + o, v);
   } else {
     float nv = ((float*)p.y)[o] + v;
@@ -127,6 +128,7 @@ __device__ __forceinline__ float epi_one(const TcParams& p, int m, int n, float 
 // EPI_RESID_ADD with the old residual already loaded (`prev`): lets callers
 // issue all residual loads of a chunk before any store (one L2 round trip per
 // chunk instead of one per element).
+template <int E_>
 __device__ __forceinline__ float epi_resid_pre(const TcParams& p, int m, int n, float v, float prev) {
   if (m >= p.M || n >= p.N) return 0.f;
   const size_t o = (size_t)m * p.N + n;
@@ -149,56 +151,12 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(a)) |
          ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(b)) << 16);
 }
-// Vector epilogue: the output op on weight rows n..n+3 (n % 4 == 0, N % 4 == 0) of token m, one 8-16
-// byte streaming store per output tensor.  Returns the sum of squares of the new residual
-// (EPI_RESID_ADD, for the consumer's RMSNorm partials), else 0.
-__device__ __forceinline__ float epi4(const TcParams& p, int m, int n, float (&x)[4]) {
-  if (m >= p.M || n >= p.N) return 0.f;
-  const size_t o = (size_t)m * p.N + n;
-  if (p.bias) {
-    const uint2 bb = *reinterpret_cast<const uint2*>(p.bias + n);
-    x[0] += __bfloat162float(__ushort_as_bfloat16((unsigned short)(bb.x & 0xffff)));
-    x[1] += __bfloat162float(__ushort_as_bfloat16((unsigned short)(bb.x >> 16)));
-    x[2] += __bfloat162float(__ushort_as_bfloat16((unsigned short)(bb.y & 0xffff)));
-    x[3] += __bfloat162float(__ushort_as_bfloat16((unsigned short)(bb.y >> 16)));
-  }
-  if (p.relu && p.epi != EPI_RESID_ADD)
-#pragma unroll
-    for (int i = 0; i < 4; ++i) x[i] = fmaxf(x[i], 0.f);
-  if (p.epi == EPI_STORE) {
-    __stcs(reinterpret_cast<uint2*>((__nv_bfloat16*)p.y + o), make_uint2(pack_bf16x2(x[0], x[1]), pack_bf16x2(x[2], x[3])));
-  } else if (p.epi == EPI_STORE_F32) {
-    __stcs(reinterpret_cast<float4*>((float*)p.y + o), make_float4(x[0], x[1], x[2], x[3]));
-  } else if (p.epi == EPI_SILU_MUL) {
-    __stcs(reinterpret_cast<unsigned int*>((__nv_bfloat16*)p.y + (size_t)m * (p.N / 2) + n / 2),
-           pack_bf16x2(silu_f(x[0]) * x[1], silu_f(x[2]) * x[3]));
-  } else {  // EPI_RESID_ADD
-    float4* rp = reinterpret_cast<float4*>((float*)p.y + o);
-    const float4 pr = __ldcg(rp);
-    const float a0 = pr.x + x[0], a1 = pr.y + x[1], a2 = pr.z + x[2], a3 = pr.w + x[3];
-    __stcs(rp, make_float4(a0, a1, a2, a3));
-    if (p.out_xb) {
-      float g[4] = {1.f, 1.f, 1.f, 1.f};
-      if (p.out_gain) {
-        const uint2 gg = *reinterpret_cast<const uint2*>(p.out_gain + n);
-        g[0] = __bfloat162float(__ushort_as_bfloat16((unsigned short)(gg.x & 0xffff)));
-        g[1] = __bfloat162float(__ushort_as_bfloat16((unsigned short)(gg.x >> 16)));
-        g[2] = __bfloat162float(__ushort_as_bfloat16((unsigned short)(gg.y & 0xffff)));
-        g[3] = __bfloat162float(__ushort_as_bfloat16((unsigned short)(gg.y >> 16)));
-      }
-      __stcs(reinterpret_cast<uint2*>(p.out_xb + o),
-             make_uint2(pack_bf16x2(a0 * g[0], a1 * g[1]), pack_bf16x2(a2 * g[2], a3 * g[3])));
-    }
-    return ((a0 * a0 + a1 * a1) + a2 * a2) + a3 * a3;
-  }
-  return 0.f;
-}
-
 // Bulk-copy epilogue: emit token j's row of the 128-row tile at n0a (lane l holds rows 4l..4l+3 in x):
 // the output op writes the row(s) into this warp's shared-memory slot, one thread bulk-copies them
 // to global memory (TMA engine: the SM's store path is off the critical path -- thread stores of
 // the same rows cost ~2 us per 16 tokens while the weight stream saturates HBM), then the norm
 // partial / argmax of the row are reduced over the warp (fixed xor trees).
+template <int E_>
 __device__ __forceinline__ void tc_emit_row(const TcParams& p, uint8_t* smem, int tn, int ew, int lane, int& slot,
                                             int j, int jr, int acc, int m0, int n0a, int tile_a, float (&x)[4],
                                             float sc, uint64_t* res_bar, const float* rb) {
@@ -227,24 +185,24 @@ __device__ __forceinline__ void tc_emit_row(const TcParams& p, uint8_t* smem, in
     x[2] += __bfloat162float(__ushort_as_bfloat16((unsigned short)(bb.y & 0xffff)));
     x[3] += __bfloat162float(__ushort_as_bfloat16((unsigned short)(bb.y >> 16)));
   }
-  if (p.relu && p.epi != EPI_RESID_ADD)
+  if (p.relu && E_ != EPI_RESID_ADD)
 #pragma unroll
     for (int i = 0; i < 4; ++i) x[i] = fmaxf(x[i], 0.f);
   float sq = 0.f;
   ArgMax am{-INFINITY, INT_MAX};
-  if (p.epi == EPI_STORE) {
+  if (E_ == EPI_STORE) {
     const uint2 v = make_uint2(pack_bf16x2(x[0], x[1]), pack_bf16x2(x[2], x[3]));
     if (bulk) *reinterpret_cast<uint2*>(oh + 4 * lane) = v;
     else if (nv) __stcs(reinterpret_cast<uint2*>((__nv_bfloat16*)p.y + o), v);
-  } else if (p.epi == EPI_STORE_F32) {
+  } else if (E_ == EPI_STORE_F32) {
     const float4 v = make_float4(x[0], x[1], x[2], x[3]);
     if (bulk) *reinterpret_cast<float4*>(of + 4 * lane) = v;
     else if (nv) __stcs(reinterpret_cast<float4*>((float*)p.y + o), v);
-  } else if (p.epi == EPI_SILU_MUL) {
+  } else if (E_ == EPI_SILU_MUL) {
     const uint32_t v = pack_bf16x2(silu_f(x[0]) * x[1], silu_f(x[2]) * x[3]);
     if (bulk) *reinterpret_cast<uint32_t*>(oh + 2 * lane) = v;
     else if (nv) __stcs(reinterpret_cast<unsigned int*>((__nv_bfloat16*)p.y + (size_t)m * (p.N / 2) + n / 2), v);
-  } else if (p.epi == EPI_ARGMAX) {
+  } else if (E_ == EPI_ARGMAX) {
     if (p.y) {
       const float4 v = make_float4(x[0], x[1], x[2], x[3]);
       if (bulk) *reinterpret_cast<float4*>(of + 4 * lane) = v;
@@ -287,10 +245,10 @@ __device__ __forceinline__ void tc_emit_row(const TcParams& p, uint8_t* smem, in
     if (lane == 0) {
       if (rows > 0) {
         const size_t o0 = (size_t)m * p.N + n0a;
-        if (p.epi == EPI_STORE) bulk_s2g((__nv_bfloat16*)p.y + o0, smem_u32(oh), rows * 2);
-        else if (p.epi == EPI_STORE_F32) bulk_s2g((float*)p.y + o0, smem_u32(of), rows * 4);
-        else if (p.epi == EPI_SILU_MUL) bulk_s2g((__nv_bfloat16*)p.y + (size_t)m * (p.N / 2) + n0a / 2, smem_u32(oh), rows);
-        else if (p.epi == EPI_ARGMAX) { if (p.y) bulk_s2g((float*)p.y + o0, smem_u32(of), rows * 4); }
+        if (E_ == EPI_STORE) bulk_s2g((__nv_bfloat16*)p.y + o0, smem_u32(oh), rows * 2);
+        else if (E_ == EPI_STORE_F32) bulk_s2g((float*)p.y + o0, smem_u32(of), rows * 4);
+        else if (E_ == EPI_SILU_MUL) bulk_s2g((__nv_bfloat16*)p.y + (size_t)m * (p.N / 2) + n0a / 2, smem_u32(oh), rows);
+        else if (E_ == EPI_ARGMAX) { if (p.y) bulk_s2g((float*)p.y + o0, smem_u32(of), rows * 4); }
         else {
           bulk_s2g((float*)p.y + o0, smem_u32(of), rows * 4);
           if (p.out_xb) bulk_s2g(p.out_xb + o0, smem_u32(oh), rows * 2);
@@ -303,7 +261,7 @@ __device__ __forceinline__ void tc_emit_row(const TcParams& p, uint8_t* smem, in
     sq = warp_sum(sq);
     if (lane == 0 && tile_a < p.n_tiles_n) st_o(p, p.out_part + (size_t)tile_a * p.M + m, sq);
   }
-  if (p.epi == EPI_ARGMAX) {
+  if (E_ == EPI_ARGMAX) {
     am = warp_argmax(am);
     if (lane == 0 && tile_a < p.n_tiles_n) {
       st_o(p, p.aux_val + (size_t)tile_a * p.M + m, am.v);
@@ -319,6 +277,7 @@ __host__ __device__ __forceinline__ int split_rows_max(int splits) { return 2 * 
 
 // grid = (n_tiles_n * splits, m_tiles), cluster = (splits, 1, 1): the `splits`
 // CTAs of a cluster share one 128 x tn output tile and split its K range.
+template <int E_, int V_>
 __global__ void __launch_bounds__(TC_THREADS, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x, TcParams p) {
   extern __shared__ uint8_t smem_raw[];
@@ -335,7 +294,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   const uint32_t ring_bytes = p.stages * stage_bytes;
   // scratch (reuses the drained ring): split>1: partial tile [tn][128] + squares [tn][rows_max];
   // split==1: argmax staging [2][4][tn] + squares [4][tn]
-  const uint32_t scratch_bytes = tc_scratch_bytes(tn, p.splits, p.vec, split_rows_max(p.splits));
+  const uint32_t scratch_bytes = tc_scratch_bytes(tn, p.splits, V_, split_rows_max(p.splits));
   uint8_t* stage_base = smem;
   float* res_rows = (float*)(smem + tc_res_offset(ring_bytes, scratch_bytes));  // [wt][tn][128] (res_bytes)
   uint64_t* full = (uint64_t*)(smem + tc_res_offset(ring_bytes, scratch_bytes) + p.res_bytes);
@@ -454,7 +413,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // ---------------- epilogue warps: TMEM -> registers -> (DSMEM reduce) -> global
     griddep_wait();
     const int et = threadIdx.x - 64;
-    if (p.vec && p.res_bytes && et == 0) {
+    if (V_ && p.res_bytes && et == 0) {
       // the residual rows this CTA will update (final since the previous kernel completed) head for
       // shared memory now, under the weight stream: one 512-byte bulk copy per (tile, token)
       const int jlo = p.splits > 1 ? split * tn / p.splits : 0, jhi = p.splits > 1 ? (split + 1) * tn / p.splits : tn;
@@ -513,7 +472,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     tc_fence_after();
     if (p.trace && et == 0) tr_t[3] = gtime();
     const bool scale = p.ns_part != nullptr;
-    if (p.vec) {
+    if (V_) {
       if (p.splits > 1) {
         // split-K: dump this CTA's partial tile for the cluster (reduced after the cluster barrier)
         for (int j0 = 0; j0 < tn; j0 += 16) {
@@ -548,7 +507,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               const int j = j0 + jl;
               const float4 a = *reinterpret_cast<const float4*>(sb + jl * TC_BM + 4 * lane);
               float x[4] = {a.x, a.y, a.z, a.w};
-              tc_emit_row(p, smem, tn, ew, lane, slot, j, j, acc, m0, n0 + acc * TC_BM, tile_n * wt + acc, x,
+              tc_emit_row<E_>(p, smem, tn, ew, lane, slot, j, j, acc, m0, n0 + acc * TC_BM, tile_n * wt + acc, x,
                           scale ? inv_s[j] : 1.f, res_bar, res_rows);
             }
           }
@@ -576,7 +535,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
         for (int j = 0; j < 16; ++j) v[j] *= inv_s[j0 + j];
       }
-      if (p.epi == EPI_ARGMAX) {
+      if (E_ == EPI_ARGMAX) {
         // per token: warp argmax over its 32 rows (ties -> lowest row), staged per quadrant
         float* qv = red;
         int* qi = reinterpret_cast<int*>(red + 4 * tn);
@@ -591,31 +550,22 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             qi[quad * tn + j0 + j] = a.i;
           }
         }
-      } else if (p.epi == EPI_SILU_MUL) {
+      } else if (E_ == EPI_SILU_MUL) {
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           float other = __shfl_xor_sync(0xffffffffu, v[j], 1);
           if (!(lane & 1)) epi_pair(p, m0 + j0 + j, n0a + row, v[j], other);
         }
-      } else if ((p.dbg & 6) && p.epi == EPI_STORE_F32) {  // experiments: one store per chunk / streaming stores
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const int m = m0 + j0 + j, n = n0a + row;
-          if (m < p.M && n < p.N && (!(p.dbg & 2) || j == 0)) {
-            float* dst = (float*)p.y + (size_t)m * p.N + n;
-            if (p.dbg & 4) __stcs(dst, v[j]); else *dst = v[j];
-          }
-        }
       } else {
         float rv[16];
-        if (p.epi == EPI_RESID_ADD) {
+        if (E_ == EPI_RESID_ADD) {
 #pragma unroll
           for (int j = 0; j < 16; ++j) rv[j] = resid_load(p, m0 + j0 + j, n0a + row);  // all in flight
         }
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
-          float nv = p.epi == EPI_RESID_ADD ? epi_resid_pre(p, m0 + j0 + j, n0a + row, v[j], rv[j])
-                                            : epi_one(p, m0 + j0 + j, n0a + row, v[j]);
+          float nv = E_ == EPI_RESID_ADD ? epi_resid_pre<E_>(p, m0 + j0 + j, n0a + row, v[j], rv[j])
+                                            : epi_one<E_>(p, m0 + j0 + j, n0a + row, v[j]);
           if (p.out_part) {  // per-token sum of squares over the tile's 128 rows (fixed xor tree)
             float s = warp_sum(nv * nv);
             if (lane == 0) sq[quad * tn + j0 + j] = s;
@@ -623,12 +573,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         }
       }
     }
-    if (p.splits == 1 && (p.epi == EPI_ARGMAX || p.out_part) && tile_a < p.n_tiles_n) {
+    if (p.splits == 1 && (E_ == EPI_ARGMAX || p.out_part) && tile_a < p.n_tiles_n) {
       asm volatile("bar.sync 1, 128;" ::: "memory");
       for (int j = et; j < tn; j += 128) {
         const int m = m0 + j;
         if (m >= p.M) continue;
-        if (p.epi == EPI_ARGMAX) {
+        if (E_ == EPI_ARGMAX) {
           const float* qv = red;
           const int* qi = reinterpret_cast<const int*>(red + 4 * tn);
           ArgMax a{qv[j], qi[j]};
@@ -650,7 +600,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // CTA `split` owns rows [split*R, (split+1)*R) of the tile and sums the
     // cluster's partials in rank order 0..splits-1.
     cluster_sync_all();
-    if (warp >= 2 && p.vec) {
+    if (warp >= 2 && V_) {
       // rank `split` owns tokens [jlo, jhi) of the tile, all 128 rows: warp ew reduces token jlo+ew,
       // +4, ... (lane l: rows 4l..4l+3, one v4 DSMEM load per rank, summed in rank order) and emits it
       const int ew = warp - 2;
@@ -672,7 +622,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             x[2] += t[q].z;
             x[3] += t[q].w;
           }
-        tc_emit_row(p, smem, tn, ew, lane, slot, j, j - jlo, 0, m0, n0, tile_n, x, scale ? inv_s[j] : 1.f, res_bar,
+        tc_emit_row<E_>(p, smem, tn, ew, lane, slot, j, j - jlo, 0, m0, n0, tile_n, x, scale ? inv_s[j] : 1.f, res_bar,
                     res_rows);
       }
       if ((p.dbg & 256) && lane == 0) bulk_wait_read0();  // (global visibility: at grid completion)
@@ -686,7 +636,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       // (4 x splits) and its residual loads are in flight together; the sums
       // still run in rank order 0..splits-1 (bit-identical to one at a time).
       constexpr int EB = 4;
-      if (p.epi == EPI_SILU_MUL) {
+      if (E_ == EPI_SILU_MUL) {
         const int pairs = R / 2;
         for (int it0 = et; it0 < pairs * tn; it0 += 128 * EB) {
           float t[8][EB][2];
@@ -740,7 +690,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               const bool ok = q < p.splits && rl_[e] >= 0;
               t[q][e] = ok ? ld_dsmem_f32_nc(red_addr + (uint32_t)((jj[e] * TC_BM + r_base + rl_[e]) * 4), q) : 0.f;
             }
-          if (p.epi == EPI_RESID_ADD) {
+          if (E_ == EPI_RESID_ADD) {
 #pragma unroll
             for (int e = 0; e < EB; ++e) rv[e] = rl_[e] >= 0 ? resid_load(p, m0 + jj[e], n0 + r_base + rl_[e]) : 0.f;
           }
@@ -753,8 +703,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               if (q < p.splits) a += t[q][e];
             if (scale) a *= inv_s[jj[e]];
             const int r = r_base + rl_[e];
-            const float nv = p.epi == EPI_RESID_ADD ? epi_resid_pre(p, m0 + jj[e], n0 + r, a, rv[e])
-                                                    : epi_one(p, m0 + jj[e], n0 + r, a);
+            const float nv = E_ == EPI_RESID_ADD ? epi_resid_pre<E_>(p, m0 + jj[e], n0 + r, a, rv[e])
+                                                    : epi_one<E_>(p, m0 + jj[e], n0 + r, a);
             if (p.out_part) sq[jj[e] * R + rl_[e]] = nv * nv;
           }
         }
@@ -1066,10 +1016,28 @@ int gemm_tc_autotune_clear() {
   return 0;
 }
 
+// One instantiation per epilogue kind and style: each carries only its own epilogue code (the
+// all-in-one kernel was 173 KB of SASS; its cold epilogue paths missed in the instruction cache
+// under the saturated weight stream -- ncu: stall_no_inst / branch_resolving in the epilogue).
+typedef void (*TcKernel)(CUtensorMap, CUtensorMap, TcParams);
+static TcKernel tc_kernel_for(int epi, int vec) {
+  static const TcKernel k[5][2] = {
+      {gemm_tc_kernel<EPI_STORE, 0>, gemm_tc_kernel<EPI_STORE, 1>},
+      {gemm_tc_kernel<EPI_STORE_F32, 0>, gemm_tc_kernel<EPI_STORE_F32, 1>},
+      {gemm_tc_kernel<EPI_RESID_ADD, 0>, gemm_tc_kernel<EPI_RESID_ADD, 1>},
+      {gemm_tc_kernel<EPI_SILU_MUL, 0>, gemm_tc_kernel<EPI_SILU_MUL, 1>},
+      {gemm_tc_kernel<EPI_ARGMAX, 0>, gemm_tc_kernel<EPI_ARGMAX, 1>},
+  };
+  return k[epi < 0 || epi > 4 ? 1 : epi][vec ? 1 : 0];
+}
+
 int gemm_tc_init() {
   static int rc = -1;
   if (rc < 0) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaError_t e = cudaSuccess;
+    for (int ep = 0; ep < 5 && e == cudaSuccess; ++ep)
+      for (int v = 0; v < 2 && e == cudaSuccess; ++v)
+        e = cudaFuncSetAttribute(tc_kernel_for(ep, v), cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     rc = (e == cudaSuccess) ? 0 : (int)e;
     if (!rc) rc = attention_tc_init();
     num_sms();
@@ -1178,7 +1146,7 @@ int gemm_tc(const GemmArgs& a, cudaStream_t st) {
   }
   cfg.attrs = at;
   cfg.numAttrs = na;
-  cudaError_t e = cudaLaunchKernelEx(&cfg, gemm_tc_kernel, mw, mx, p);
+  cudaError_t e = cudaLaunchKernelEx(&cfg, tc_kernel_for(a.epi, q.vec), mw, mx, p);
   if (e != cudaSuccess) return (int)e;
   g_kernel_count++;
   return 0;
