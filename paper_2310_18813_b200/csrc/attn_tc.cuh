@@ -68,7 +68,7 @@ struct AttnShared {
 // One (kv head, sequence[, key split]) item on 128 threads (tid 0..127, named
 // barrier 1): the body of attention_tc_kernel.  `pdl`: issue the
 // KV-history tiles, then griddepcontrol.wait / launch_dependents.
-template <int HD, int STAGES>
+template <int HD, int STAGES, bool BLK, bool SPLIT>
 __device__ __forceinline__ void attn_tc_item(const AttnArgs& A, int kvh, int seq, int split, int n_splits,
                                              uint8_t* tsm, AttnShared& sh, int tid, bool pdl, int qb = 0) {
   const __nv_bfloat16* __restrict__ qkv = A.qkv;
@@ -92,7 +92,7 @@ __device__ __forceinline__ void attn_tc_item(const AttnArgs& A, int kvh, int seq
   int* qhead = sh.qhead;
 
   const int group = nq / nkv;
-  const bool blk = A.qr != nullptr;  // prefill block of an already rotated / appended window
+  constexpr bool blk = BLK;  // prefill block of an already rotated / appended window (A.qr)
   const int t0 = blk ? qb * A.q_blk : 0;
   const int nQ = group * (blk ? min(A.q_blk, q_len - t0) : q_len);
   const int warp = tid >> 5, lane = tid & 31;
@@ -132,8 +132,6 @@ __device__ __forceinline__ void attn_tc_item(const AttnArgs& A, int kvh, int seq
   // forward's window rows (the append below writes them straight into the
   // stage), so every resident tile -- window tile included -- can be requested
   // before the programmatic-dependency wait.
-  uint64_t kvpol = 0;
-  if (A.kv_evict_first) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(kvpol));
   auto issue = [&](int tile, bool hist) {
     if (tile < n_tiles) {
       uint8_t* st = ring + ((tile - t_lo) % kTcStages) * (uint32_t)SM::stage;
@@ -154,13 +152,10 @@ __device__ __forceinline__ void attn_tc_item(const AttnArgs& A, int kvh, int seq
           if (check && key >= wmin)
             for (int q = 0; q < q_len; ++q) win |= wpos[q] == key;
           if (!win) {
-            if (A.kv_evict_first) {
-              cp_async16_hint(Kd + j * RPP * RS, ks + (size_t)j * RPP * HD, kvpol);
-              cp_async16_hint(Vd + j * RPP * RS, vs + (size_t)j * RPP * HD, kvpol);
-            } else {
-              cp_async16(Kd + j * RPP * RS, ks + (size_t)j * RPP * HD);
-              cp_async16(Vd + j * RPP * RS, vs + (size_t)j * RPP * HD);
-            }
+            // (plain cp.async: the L2::cache_hint evict-first variant raised illegal-instruction faults
+            // in the templated decode kernel as it did in wide-GQA block mode before)
+            cp_async16(Kd + j * RPP * RS, ks + (size_t)j * RPP * HD);
+            cp_async16(Vd + j * RPP * RS, vs + (size_t)j * RPP * HD);
           }
         } else {  // rows past the context: zeros (P is 0 there, and 0 * stale NaN would poison P.V)
           *reinterpret_cast<uint4*>(Kd + j * RPP * RS) = make_uint4(0, 0, 0, 0);
@@ -386,7 +381,7 @@ __device__ __forceinline__ void attn_tc_item(const AttnArgs& A, int kvh, int seq
     cl[warp * 16 + g + 8] = l_hi;
   }
   attn_sync();
-  if (n_splits == 1) {
+  if (!SPLIT || n_splits == 1) {
     // 8 consecutive dims per thread: one 16-byte streaming store (scalar 2-byte stores of the output
     // row cost ~2 us under the weight stream, like the GEMM epilogue's)
     for (int e = tid; e < nQ * (HD / 8); e += 128) {

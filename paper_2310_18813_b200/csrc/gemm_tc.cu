@@ -72,20 +72,18 @@ struct TcParams {
   int launch_late;  // 1: trigger dependents at the end of the epilogue instead of after the last load
   int dbg;          // experiments (sb_debug_gemm_pdl): bit 0 skip the epilogue stores, bit 3 plain stores,
                     // bit 4 scalar (per-element) epilogue
-  int vec;          // bulk-copy epilogue (N % 16 == 0, 16-byte aligned outputs, power-of-two splits)
+  int vec;          // row epilogue (N % 16 == 0, 16-byte aligned outputs, power-of-two splits)
   int res_bytes;    // EPI_RESID_ADD: bytes of residual rows prefetched into shared memory (0 = loaded per row)
 };
 
-// Shared-memory scratch of the epilogue (reuses the drained operand ring).  Bulk-copy epilogue:
-// staging (split-K: the partial tile [tn][128] f32 the cluster reads; else [2][16][128] f32), then
-// per epilogue warp two 768-byte output rows (f32 row + bf16 row), then the prefetched residual rows.
-constexpr uint32_t TC_OB_BYTES = 4 * 2 * 768;
+// Shared-memory scratch of the epilogue (reuses the drained operand ring).  Row epilogue: staging
+// (split-K: the partial tile [tn][128] f32 the cluster reads; else [2][TC_EPI_CH][128] f32).
 constexpr int TC_EPI_CH = 32;  // tokens per staged epilogue chunk (splits == 1)
 __host__ __device__ inline uint32_t tc_stage_bytes(int tn, int splits) {
   return splits > 1 ? (uint32_t)tn * TC_BM * 4 : 2u * TC_EPI_CH * TC_BM * 4;
 }
 __host__ __device__ inline uint32_t tc_scratch_bytes(int tn, int splits, int vec, int rows_max) {
-  if (vec) return tc_stage_bytes(tn, splits) + TC_OB_BYTES;
+  if (vec) return tc_stage_bytes(tn, splits);
   return splits > 1 ? (uint32_t)tn * (TC_BM + rows_max) * 4 : (uint32_t)tn * 12 * 4;
 }
 // The prefetched residual rows live AFTER max(ring, scratch): they land while the ring is in use.
@@ -151,30 +149,20 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
   return (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(a)) |
          ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(b)) << 16);
 }
-// Bulk-copy epilogue: emit token j's row of the 128-row tile at n0a (lane l holds rows 4l..4l+3 in x):
-// the output op writes the row(s) into this warp's shared-memory slot, one thread bulk-copies them
-// to global memory (TMA engine: the SM's store path is off the critical path -- thread stores of
-// the same rows cost ~2 us per 16 tokens while the weight stream saturates HBM), then the norm
-// partial / argmax of the row are reduced over the warp (fixed xor trees).
+// Row epilogue: emit token j's row of the 128-row tile at n0a (lane l holds rows 4l..4l+3 in x): the
+// output op, one 8-16 byte streaming store per lane and output tensor (a warp covers the token's 128
+// contiguous rows), then the norm partial / argmax of the row reduced over the warp (fixed xor trees).
+// (Measured alternatives, slower in the forward: per-element stores -- one 2-4 byte store per row and
+// token, ~2 us per 16 tokens under the weight stream; bulk (TMA engine) copies of rows formatted in
+// shared memory -- 3.15 vs 3.01 ms verify at b=8, k=3.)
 template <int E_>
-__device__ __forceinline__ void tc_emit_row(const TcParams& p, uint8_t* smem, int tn, int ew, int lane, int& slot,
-                                            int j, int jr, int acc, int m0, int n0a, int tile_a, float (&x)[4],
-                                            float sc, uint64_t* res_bar, const float* rb) {
+__device__ __forceinline__ void tc_emit_row(const TcParams& p, int lane, int j, int jr, int acc, int tn, int m0,
+                                            int n0a, int tile_a, float (&x)[4], float sc, uint64_t* res_bar,
+                                            const float* rb) {
   const int m = m0 + j;
-  if (m >= p.M) return;  // (warp-uniform) padding token: nothing to write
+  if (m >= p.M) return;  // (warp-uniform) padding token
   const int n = n0a + 4 * lane;
   const bool nv = n < p.N;
-  // dbg bit 8: bulk (TMA engine) copies of the formatted rows instead of direct 8-16 byte streaming stores
-  // (measured slower in the forward: 3.15 vs 3.01 ms verify at b=8, k=3 -- each copy waits on its slot)
-  const bool bulk = (p.dbg & 256) != 0 || ((p.dbg & 512) && p.splits == 1);
-  uint8_t* ob = smem + tc_stage_bytes(tn, p.splits) + (uint32_t)(ew * 2 + slot) * 768;
-  float* of = reinterpret_cast<float*>(ob);
-  __nv_bfloat16* oh = reinterpret_cast<__nv_bfloat16*>(ob + 512);
-  if (bulk) {
-    slot ^= 1;
-    if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");  // this slot's last copy has read it
-    __syncwarp();
-  }
   const size_t o = (size_t)m * p.N + n;
 #pragma unroll
   for (int i = 0; i < 4; ++i) x[i] *= sc;
@@ -185,33 +173,29 @@ __device__ __forceinline__ void tc_emit_row(const TcParams& p, uint8_t* smem, in
     x[2] += __bfloat162float(__ushort_as_bfloat16((unsigned short)(bb.y & 0xffff)));
     x[3] += __bfloat162float(__ushort_as_bfloat16((unsigned short)(bb.y >> 16)));
   }
-  if (p.relu && E_ != EPI_RESID_ADD)
+  if (E_ != EPI_RESID_ADD && p.relu)
 #pragma unroll
     for (int i = 0; i < 4; ++i) x[i] = fmaxf(x[i], 0.f);
-  float sq = 0.f;
-  ArgMax am{-INFINITY, INT_MAX};
   if (E_ == EPI_STORE) {
-    const uint2 v = make_uint2(pack_bf16x2(x[0], x[1]), pack_bf16x2(x[2], x[3]));
-    if (bulk) *reinterpret_cast<uint2*>(oh + 4 * lane) = v;
-    else if (nv) __stcs(reinterpret_cast<uint2*>((__nv_bfloat16*)p.y + o), v);
+    if (nv) __stcs(reinterpret_cast<uint2*>((__nv_bfloat16*)p.y + o), make_uint2(pack_bf16x2(x[0], x[1]), pack_bf16x2(x[2], x[3])));
   } else if (E_ == EPI_STORE_F32) {
-    const float4 v = make_float4(x[0], x[1], x[2], x[3]);
-    if (bulk) *reinterpret_cast<float4*>(of + 4 * lane) = v;
-    else if (nv) __stcs(reinterpret_cast<float4*>((float*)p.y + o), v);
+    if (nv) __stcs(reinterpret_cast<float4*>((float*)p.y + o), make_float4(x[0], x[1], x[2], x[3]));
   } else if (E_ == EPI_SILU_MUL) {
-    const uint32_t v = pack_bf16x2(silu_f(x[0]) * x[1], silu_f(x[2]) * x[3]);
-    if (bulk) *reinterpret_cast<uint32_t*>(oh + 2 * lane) = v;
-    else if (nv) __stcs(reinterpret_cast<unsigned int*>((__nv_bfloat16*)p.y + (size_t)m * (p.N / 2) + n / 2), v);
+    if (nv)
+      __stcs(reinterpret_cast<unsigned int*>((__nv_bfloat16*)p.y + (size_t)m * (p.N / 2) + n / 2),
+             pack_bf16x2(silu_f(x[0]) * x[1], silu_f(x[2]) * x[3]));
   } else if (E_ == EPI_ARGMAX) {
-    if (p.y) {
-      const float4 v = make_float4(x[0], x[1], x[2], x[3]);
-      if (bulk) *reinterpret_cast<float4*>(of + 4 * lane) = v;
-      else if (nv) __stcs(reinterpret_cast<float4*>((float*)p.y + o), v);
-    }
+    if (p.y && nv) __stcs(reinterpret_cast<float4*>((float*)p.y + o), make_float4(x[0], x[1], x[2], x[3]));
+    ArgMax am{-INFINITY, INT_MAX};
 #pragma unroll
     for (int i = 0; i < 4; ++i)
       if (n + i < p.N && x[i] > am.v) am = ArgMax{x[i], n + i};
-  } else {  // EPI_RESID_ADD
+    am = warp_argmax(am);
+    if (lane == 0 && tile_a < p.n_tiles_n) {
+      st_o(p, p.aux_val + (size_t)tile_a * p.M + m, am.v);
+      st_o(p, p.aux_idx + (size_t)tile_a * p.M + m, am.i);
+    }
+  } else {  // EPI_RESID_ADD: new residual, its bf16 copy scaled by the consumer's gain, norm partial
     float4 pr = make_float4(0.f, 0.f, 0.f, 0.f);
     if (p.res_bytes) {
       mbar_wait(res_bar, 0);
@@ -220,52 +204,21 @@ __device__ __forceinline__ void tc_emit_row(const TcParams& p, uint8_t* smem, in
       pr = __ldcg(reinterpret_cast<const float4*>((const float*)p.y + o));
     }
     const float a0 = pr.x + x[0], a1 = pr.y + x[1], a2 = pr.z + x[2], a3 = pr.w + x[3];
-    const float4 v = make_float4(a0, a1, a2, a3);
-    if (bulk) *reinterpret_cast<float4*>(of + 4 * lane) = v;
-    else if (nv) __stcs(reinterpret_cast<float4*>((float*)p.y + o), v);
-    if (p.out_xb) {
+    if (nv) __stcs(reinterpret_cast<float4*>((float*)p.y + o), make_float4(a0, a1, a2, a3));
+    if (p.out_xb && nv) {
       float g[4] = {1.f, 1.f, 1.f, 1.f};
-      if (p.out_gain && nv) {
+      if (p.out_gain) {
         const uint2 gg = *reinterpret_cast<const uint2*>(p.out_gain + n);
         g[0] = __bfloat162float(__ushort_as_bfloat16((unsigned short)(gg.x & 0xffff)));
         g[1] = __bfloat162float(__ushort_as_bfloat16((unsigned short)(gg.x >> 16)));
         g[2] = __bfloat162float(__ushort_as_bfloat16((unsigned short)(gg.y & 0xffff)));
         g[3] = __bfloat162float(__ushort_as_bfloat16((unsigned short)(gg.y >> 16)));
       }
-      const uint2 hv = make_uint2(pack_bf16x2(a0 * g[0], a1 * g[1]), pack_bf16x2(a2 * g[2], a3 * g[3]));
-      if (bulk) *reinterpret_cast<uint2*>(oh + 4 * lane) = hv;
-      else if (nv) __stcs(reinterpret_cast<uint2*>(p.out_xb + o), hv);
+      __stcs(reinterpret_cast<uint2*>(p.out_xb + o), make_uint2(pack_bf16x2(a0 * g[0], a1 * g[1]), pack_bf16x2(a2 * g[2], a3 * g[3])));
     }
-    sq = nv ? ((a0 * a0 + a1 * a1) + a2 * a2) + a3 * a3 : 0.f;
-  }
-  if (bulk) {
-    fence_proxy_async_smem();
-    __syncwarp();
-    const int rows = min(TC_BM, p.N - n0a);
-    if (lane == 0) {
-      if (rows > 0) {
-        const size_t o0 = (size_t)m * p.N + n0a;
-        if (E_ == EPI_STORE) bulk_s2g((__nv_bfloat16*)p.y + o0, smem_u32(oh), rows * 2);
-        else if (E_ == EPI_STORE_F32) bulk_s2g((float*)p.y + o0, smem_u32(of), rows * 4);
-        else if (E_ == EPI_SILU_MUL) bulk_s2g((__nv_bfloat16*)p.y + (size_t)m * (p.N / 2) + n0a / 2, smem_u32(oh), rows);
-        else if (E_ == EPI_ARGMAX) { if (p.y) bulk_s2g((float*)p.y + o0, smem_u32(of), rows * 4); }
-        else {
-          bulk_s2g((float*)p.y + o0, smem_u32(of), rows * 4);
-          if (p.out_xb) bulk_s2g(p.out_xb + o0, smem_u32(oh), rows * 2);
-        }
-      }
-      bulk_commit();
-    }
-  }
-  if (p.out_part) {
-    sq = warp_sum(sq);
-    if (lane == 0 && tile_a < p.n_tiles_n) st_o(p, p.out_part + (size_t)tile_a * p.M + m, sq);
-  }
-  if (E_ == EPI_ARGMAX) {
-    am = warp_argmax(am);
-    if (lane == 0 && tile_a < p.n_tiles_n) {
-      st_o(p, p.aux_val + (size_t)tile_a * p.M + m, am.v);
-      st_o(p, p.aux_idx + (size_t)tile_a * p.M + m, am.i);
+    if (p.out_part) {
+      const float sq = warp_sum(nv ? ((a0 * a0 + a1 * a1) + a2 * a2) + a3 * a3 : 0.f);
+      if (lane == 0 && tile_a < p.n_tiles_n) st_o(p, p.out_part + (size_t)tile_a * p.M + m, sq);
     }
   }
 }
@@ -300,7 +253,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* full = (uint64_t*)(smem + tc_res_offset(ring_bytes, scratch_bytes) + p.res_bytes);
   uint64_t* empty = full + p.stages;
   uint64_t* tmem_full = empty + p.stages;
-  uint64_t* res_bar = tmem_full + 1;  // residual rows landed (bulk-copy epilogue)
+  uint64_t* res_bar = tmem_full + 1;  // prefetched residual rows landed (row epilogue)
   uint32_t* tmem_slot = (uint32_t*)(res_bar + 1);
   float* inv_s = (float*)(tmem_slot + 4);  // [tn] per-token 1/rms (fused RMSNorm)
   float* nsum = inv_s + tn;                 // [4][tn] per-token partial sums of squares (fused RMSNorm)
@@ -486,7 +439,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         // double-buffered; one tcgen05.wait per chunk), then warp ew emits tokens ew, ew+4, ...:
         // lane l owns rows 4l..4l+3 of the token's row.
         const int ew = warp - 2;
-        int slot = 0, ci = 0;
+        int ci = 0;
         for (int acc = 0; acc < wt; ++acc) {
           for (int j0 = 0; j0 < tn; j0 += TC_EPI_CH, ++ci) {
             float* sb = red + (ci & 1) * TC_EPI_CH * TC_BM;
@@ -507,12 +460,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               const int j = j0 + jl;
               const float4 a = *reinterpret_cast<const float4*>(sb + jl * TC_BM + 4 * lane);
               float x[4] = {a.x, a.y, a.z, a.w};
-              tc_emit_row<E_>(p, smem, tn, ew, lane, slot, j, j, acc, m0, n0 + acc * TC_BM, tile_n * wt + acc, x,
-                          scale ? inv_s[j] : 1.f, res_bar, res_rows);
+              tc_emit_row<E_>(p, lane, j, j, acc, tn, m0, n0 + acc * TC_BM, tile_n * wt + acc, x,
+                              scale ? inv_s[j] : 1.f, res_bar, res_rows);
             }
           }
         }
-        if ((p.dbg & 768) && lane == 0) bulk_wait_read0();  // (global visibility: at grid completion)
       }
     } else
     for (int acc = 0; acc < wt; ++acc) {
@@ -600,14 +552,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     // CTA `split` owns rows [split*R, (split+1)*R) of the tile and sums the
     // cluster's partials in rank order 0..splits-1.
     cluster_sync_all();
-    if (warp >= 2 && V_) {
+    if (V_) {
+      if (warp >= 2) {
       // rank `split` owns tokens [jlo, jhi) of the tile, all 128 rows: warp ew reduces token jlo+ew,
       // +4, ... (lane l: rows 4l..4l+3, one v4 DSMEM load per rank, summed in rank order) and emits it
       const int ew = warp - 2;
       const uint32_t red_addr = smem_u32(red);
       const bool scale = p.ns_part != nullptr;
       const int jlo = split * tn / p.splits, jhi = (split + 1) * tn / p.splits;
-      int slot = 0;
       for (int j = jlo + ew; j < jhi; j += 4) {
         float4 t[8];
 #pragma unroll
@@ -622,10 +574,9 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             x[2] += t[q].z;
             x[3] += t[q].w;
           }
-        tc_emit_row<E_>(p, smem, tn, ew, lane, slot, j, j - jlo, 0, m0, n0, tile_n, x, scale ? inv_s[j] : 1.f, res_bar,
-                    res_rows);
+        tc_emit_row<E_>(p, lane, j, j - jlo, 0, tn, m0, n0, tile_n, x, scale ? inv_s[j] : 1.f, res_bar, res_rows);
       }
-      if ((p.dbg & 256) && lane == 0) bulk_wait_read0();  // (global visibility: at grid completion)
+      }
     } else if (warp >= 2) {
       const int r_base = split_row_lo(split, p.splits);
       const int R = split_row_lo(split + 1, p.splits) - r_base;
@@ -1049,7 +1000,7 @@ int gemm_tc_init() {
 int gemm_tc_norm_partials(const GemmArgs& a) {
   TcPlan q = plan(a.M, a.N, a.K, a.epi);
   tc_plan_vec(q, a);
-  return q.vec ? q.n_tiles_n : q.n_tiles_n * q.splits;  // bulk-copy epilogue: one complete partial per tile
+  return q.vec ? q.n_tiles_n : q.n_tiles_n * q.splits;  // row epilogue: one complete partial per tile
 }
 
 bool gemm_tc_supported(const GemmArgs& a) {

@@ -573,7 +573,9 @@ int g_attn_l2pf = -1;   // -1: from env SB_ATTN_L2PF (default off)
 
 int g_attn_stages = -1;  // ring stages (3, 4 or 6) when the grid fits one CTA per SM: -1 env SB_ATTN_STAGES
 
-template <int HD, int STAGES>
+// BLK: prefill blocks (A.qr set); SPLIT: flash-decoding key splits (gridDim.z > 1) -- compile-time, so
+// each launch carries only its own paths (one inlined item; the instruction cache holds it).
+template <int HD, int STAGES, bool BLK, bool SPLIT>
 __global__ void __launch_bounds__(128) attention_tc_kernel(AttnArgs A) {
   extern __shared__ __align__(128) uint8_t tsm[];
   __shared__ AttnShared sh;
@@ -593,21 +595,17 @@ __global__ void __launch_bounds__(128) attention_tc_kernel(AttnArgs A) {
       asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(A.l2_next + o), "r"(n) : "memory");
     }
   }
+  AttnArgs B = A;
+  B.tr_t = tr_t;
+  if (BLK)
+    attn_tc_item<HD, STAGES, true, false>(B, blockIdx.x, blockIdx.y, 0, 1, tsm, sh, threadIdx.x, true, blockIdx.z);
+  else
+    attn_tc_item<HD, STAGES, false, SPLIT>(B, blockIdx.x, blockIdx.y, SPLIT ? (int)blockIdx.z : 0,
+                                           SPLIT ? (int)gridDim.z : 1, tsm, sh, threadIdx.x, true);
   if (A.trace) {
-    AttnArgs B = A;
-    B.tr_t = tr_t;
-    if (A.qr)
-      attn_tc_item<HD, STAGES>(B, blockIdx.x, blockIdx.y, 0, 1, tsm, sh, threadIdx.x, true, blockIdx.z);
-    else
-      attn_tc_item<HD, STAGES>(B, blockIdx.x, blockIdx.y, blockIdx.z, gridDim.z, tsm, sh, threadIdx.x, true);
     __syncthreads();
     if (threadIdx.x == 0) cta_trace_write(A.trace, A.trace_id, 2, tr_t);
-    return;
   }
-  if (A.qr)
-    attn_tc_item<HD, STAGES>(A, blockIdx.x, blockIdx.y, 0, 1, tsm, sh, threadIdx.x, true, blockIdx.z);
-  else
-    attn_tc_item<HD, STAGES>(A, blockIdx.x, blockIdx.y, blockIdx.z, gridDim.z, tsm, sh, threadIdx.x, true);
 }
 
 // Opt every ring variant in to its dynamic shared memory once (outside graph capture).
@@ -617,14 +615,18 @@ int attention_tc_init() {
     cudaError_t e = cudaSuccess;
 #define SB_ATTN_ATTR(H, S)                                                                                        \
   if (e == cudaSuccess)                                                                                           \
-  e = cudaFuncSetAttribute(attention_tc_kernel<H, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,                \
-                           (int)TcAttnSmem<H, S>::bytes)
+    e = cudaFuncSetAttribute(attention_tc_kernel<H, S, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
+                             (int)TcAttnSmem<H, S>::bytes);                                                        \
+  if (e == cudaSuccess)                                                                                           \
+    e = cudaFuncSetAttribute(attention_tc_kernel<H, S, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                             (int)TcAttnSmem<H, S>::bytes);                                                        \
+  if (e == cudaSuccess)                                                                                           \
+    e = cudaFuncSetAttribute(attention_tc_kernel<H, S, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
+                             (int)TcAttnSmem<H, S>::bytes)
     SB_ATTN_ATTR(128, 3);
     SB_ATTN_ATTR(128, 4);
-    SB_ATTN_ATTR(128, 6);
     SB_ATTN_ATTR(64, 3);
     SB_ATTN_ATTR(64, 4);
-    SB_ATTN_ATTR(64, 6);
     if (e == cudaSuccess) e = attn_simt_attr<__nv_bfloat16, 64>();
     if (e == cudaSuccess) e = attn_simt_attr<__nv_bfloat16, 128>();
     if (e == cudaSuccess) e = attn_simt_attr<float, 64>();
@@ -667,16 +669,15 @@ static int launch_attn_grid(const AttnArgs& A0, int hd, int n_seq, int z, cudaSt
     cfg.dynamicSmemBytes = bytes;
     return cudaLaunchKernelEx(&cfg, kern, A);
   };
+  const bool blk = A.qr != nullptr, spl = z > 1 && !blk;
+#define SB_ATTN_GO(H, S) \
+  (blk ? go(attention_tc_kernel<H, S, true, false>, TcAttnSmem<H, S>::bytes) \
+       : spl ? go(attention_tc_kernel<H, S, false, true>, TcAttnSmem<H, S>::bytes) \
+             : go(attention_tc_kernel<H, S, false, false>, TcAttnSmem<H, S>::bytes))
   cudaError_t e;
-  if (hd == 128) {
-    e = stages >= 6   ? go(attention_tc_kernel<128, 6>, TcAttnSmem<128, 6>::bytes)
-        : stages == 4 ? go(attention_tc_kernel<128, 4>, TcAttnSmem<128, 4>::bytes)
-                      : go(attention_tc_kernel<128, 3>, TcAttnSmem<128, 3>::bytes);
-  } else {
-    e = stages >= 6   ? go(attention_tc_kernel<64, 6>, TcAttnSmem<64, 6>::bytes)
-        : stages == 4 ? go(attention_tc_kernel<64, 4>, TcAttnSmem<64, 4>::bytes)
-                      : go(attention_tc_kernel<64, 3>, TcAttnSmem<64, 3>::bytes);
-  }
+  if (hd == 128) e = stages >= 4 ? SB_ATTN_GO(128, 4) : SB_ATTN_GO(128, 3);
+  else e = stages >= 4 ? SB_ATTN_GO(64, 4) : SB_ATTN_GO(64, 3);
+#undef SB_ATTN_GO
   if (e != cudaSuccess) return (int)e;
   ++g_kernel_count;
   return 0;

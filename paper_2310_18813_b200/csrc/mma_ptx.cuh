@@ -10,11 +10,17 @@ __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
                : "memory");
 }
 // with an L2 cache policy (createpolicy descriptor)
-__device__ __forceinline__ void cp_async16_hint(void* smem, const void* gmem, uint64_t pol) {
-  asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;" ::"r"(
-                   (uint32_t)__cvta_generic_to_shared(smem)),
-               "l"(gmem), "l"(pol)
-               : "memory");
+// 16-byte cp.async whose line is evict-first in L2.  The policy is created in the same asm block as
+// its use: a policy value carried across code (hoisted / merged by the compiler) faulted with an
+// illegal instruction in some instantiations.
+__device__ __forceinline__ void cp_async16_ef(void* smem, const void* gmem) {
+  asm volatile(
+      "{\n\t.reg .b64 pol;\n\t"
+      "createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n\t"
+      "cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, pol;\n\t}" ::"r"(
+          (uint32_t)__cvta_generic_to_shared(smem)),
+      "l"(gmem)
+      : "memory");
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
