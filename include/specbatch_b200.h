@@ -315,7 +315,8 @@ size_t sb_draft_loop_workspace_bytes(const sb_decoder_t* m);
 /* Diagnostics: device buffer (>= 4096 + 512*160 u64, zeroed) receiving globaltimer stamps of every grid
    barrier of the next sb_draft_loop launches (NULL = off). */
 int sb_debug_draft_trace(void* buf);
-/* Enable sb_draft_loop (default 1); 0 = it returns SB_EUNSUPPORTED and the caller issues per-step forwards. */
+/* Enable sb_draft_loop (default 0: the per-step forwards measured faster); 0 = it returns SB_EUNSUPPORTED and
+   the caller issues per-step forwards. */
 int sb_set_draft_loop(int32_t enabled);
 
 /* Compaction (K5): copy KV slabs src_slot[i] -> dst_slot[i] for positions [0, len[i]). */

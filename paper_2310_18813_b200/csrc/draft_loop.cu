@@ -921,7 +921,10 @@ __global__ void __launch_bounds__(kThreads, 1) draft_loop_kernel(const __grid_co
 
 }  // namespace dl
 
-static int g_dl_enabled = 1;
+// Off by default: with the templated per-step kernels (small, instruction-cache resident) the per-step
+// forwards are faster at every b <= 8, k (profiles/r2/draft_loop_vs_per_step_r2c.txt: b=8,k=3 186 vs
+// 196 us, b=1,k=8 442 vs 446 us); sb_set_draft_loop(1) opts in.
+static int g_dl_enabled = 0;
 static unsigned long long* g_dl_trace = nullptr;
 static int g_dl_clusters[9] = {0};  // max co-resident clusters per cluster size (1 CTA per SM)
 

@@ -9,7 +9,8 @@ draft proposals of DraftOracle.step / TokenLevel.draft_tokens, engine.py:100-106
   k up to 8; the same holds for the per-step forwards it replaces.
 * Its KV appends equal the per-step path's (bf16 tolerance) and the token-sink
   outputs follow the protocol (ds_ids = d_k, ds_pos = d_base + k).
-* Inside SpecEngine (graph-captured, default for greedy bf16 drafts it fits) a
+* Inside SpecEngine (graph-captured; opt-in via sb_set_draft_loop(1) -- the per-step forwards are the
+  default since they measured faster) a
   draft identical to the target accepts essentially every draft, and the
   output equals plain greedy decoding.
 """
@@ -56,9 +57,11 @@ def _run(drf, prompts, k, mode, dev):
         assert nb > 0
         packed = torch.empty(nb, device=dev, dtype=torch.uint8)
         N.call("sb_draft_loop_pack", C.byref(drf.struct), N.ptr(packed), nb, torch.cuda.current_stream().cuda_stream)
+        lib.sb_set_draft_loop(1)  # opt-in (default off: the per-step forwards measured faster)
         rc = lib.sb_draft_loop(C.byref(drf.struct), C.byref(kv.struct), N.ptr(packed), b, k, N.ptr(d1_ids), N.ptr(d1_pos),
                                N.ptr(slots), N.ptr(d_base), N.ptr(v_ids), N.ptr(ds_ids), N.ptr(ds_pos), N.ptr(ws),
                                ws.numel(), N.ptr(sync), st)
+        lib.sb_set_draft_loop(0)
         assert rc == 0, rc
         torch.cuda.synchronize()
         assert int(sync.abs().sum()) == 0  # barrier words reset for the next launch
@@ -124,9 +127,14 @@ def test_engine_uses_draft_loop_and_self_draft_accepts(cuda_dev):
     tgt = Decoder(cfg, dtype="bf16", device=cuda_dev, seed=41, init="host", max_pos=MAXPOS)
     drf = Decoder(cfg, dtype="bf16", device=cuda_dev, share_from=tgt, share_layers=cfg.n_layers, max_pos=MAXPOS)
     b, k, Nnew = 6, 4, 48
-    eng = SpecEngine(tgt, drf, mode="greedy", max_batch=8, max_k=8, prompt_len=24, max_new=Nnew, seed=9)
-    states = [SequenceState(request_id=i, target_len=Nnew) for i in range(b)]
-    eng.generate(states, k)
+    lib = N.load()
+    lib.sb_set_draft_loop(1)
+    try:
+        eng = SpecEngine(tgt, drf, mode="greedy", max_batch=8, max_k=8, prompt_len=24, max_new=Nnew, seed=9)
+        states = [SequenceState(request_id=i, target_len=Nnew) for i in range(b)]
+        eng.generate(states, k)
+    finally:
+        lib.sb_set_draft_loop(0)
     assert eng.stats.kernels_per_iteration <= 3 + 1 + 20  # prepare/accept/commit + ONE draft launch + verify
     log = eng.stats.accepted
     live = log >= 0
