@@ -708,8 +708,9 @@ def run_ours(args):
     tf_path = ROOT / "profiles" / "verify_traffic.json"
     if tf_path.exists():
         tfd = json.loads(tf_path.read_text())
-        if tfd.get("b") == b and tfd.get("k") == k and str(tfd.get("workload", "")).startswith(TARGET + " "):
-            traffic = tfd["dram_bytes_read_plus_write"]
+        for e in tfd.get("entries", [tfd]):
+            if e.get("b") == b and e.get("k") == k and str(e.get("workload", "")).startswith(TARGET + " "):
+                traffic = e["dram_bytes_read_plus_write"]
 
     # ---- CPU baseline (rank 0, N=1 only): the reference arm's method on a smaller sample
     cpu = None

@@ -876,12 +876,17 @@ int gemm_tc_autotune(const void* x, const void* w, float* y, int M, int N, int K
   struct Cand {
     int cps, sp, wt, tn;
   };
-  Cand cands[40];
+  Cand cands[48];
   int nc = 0;
   // token tiles: the default, and for wide M the 128 / 192 tiles (more CTAs per wave)
-  int tns[3] = {0, 0, 0}, ntn = 1;
+  int tns[4] = {0, 0, 0, 0}, ntn = 1;
   if (M > 128 && tn > 128) tns[ntn++] = 128;
   if (M > 192 && tn > 192) tns[ntn++] = 192;
+  {  // balanced tiles (e.g. 288 = 2 x 144, not 256 + 32): no mostly-empty remainder tile re-streaming weights
+    const int nt = (M + TC_MAX_TN - 1) / TC_MAX_TN;
+    const int tb = ((M + nt - 1) / nt + 15) / 16 * 16;
+    if (nt > 1 && tb < tn && tb != 128 && tb != 192) tns[ntn++] = tb;
+  }
   for (int ti = 0; ti < ntn; ++ti) {
     const int tn_c = tns[ti] ? tns[ti] : tn;
     const int tiles_c = ((N + TC_BM - 1) / TC_BM) * ((M + tn_c - 1) / tn_c);
