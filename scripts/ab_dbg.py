@@ -10,10 +10,12 @@ flags = [int(a) for a in sys.argv[1:]] or [0, 8]
 dev = torch.device("cuda:0")
 tgt = Decoder(CONFIGS["llama-2-7b"], dtype="bf16", device=dev, init="device", max_pos=320)
 drf = Decoder(CONFIGS["llama-68m"], dtype="bf16", device=dev, seed=1, init="device", max_pos=320)
-eng = SpecEngine(tgt, drf, mode="injected", acceptance=example_trace(), max_batch=32, max_k=8, prompt_len=128,
-                 max_new=128)
+cells = [tuple(int(x) for x in c.split(",")) for c in os.environ.get("CELLS", "").split()] or \
+    [(1, 8), (2, 7), (4, 7), (8, 3), (16, 8), (32, 8)]
+eng = SpecEngine(tgt, drf, mode="injected", acceptance=example_trace(), max_batch=max(32, max(b for b, _ in cells)),
+                 max_k=8, prompt_len=128, max_new=128)
 lib = N.load()
-for b, k in [(1, 8), (2, 7), (4, 7), (8, 3), (16, 8), (32, 8)]:
+for b, k in cells:
     row = []
     for f in flags:
         lib.sb_debug_gemm_pdl(0, 0, f)
