@@ -885,7 +885,7 @@ int gemm_tc_autotune(const void* x, const void* w, float* y, int M, int N, int K
   {  // balanced tiles (e.g. 288 = 2 x 144, not 256 + 32): no mostly-empty remainder tile re-streaming weights
     const int nt = (M + TC_MAX_TN - 1) / TC_MAX_TN;
     const int tb = ((M + nt - 1) / nt + 15) / 16 * 16;
-    if (nt > 1 && tb < tn && tb != 128 && tb != 192) tns[ntn++] = tb;
+    if (nt == 2 && tb < tn && tb != 128 && tb != 192) tns[ntn++] = tb;  // (measured: T=288 7.8 -> 7.2 ms)
   }
   for (int ti = 0; ti < ntn; ++ti) {
     const int tn_c = tns[ti] ? tns[ti] : tn;
