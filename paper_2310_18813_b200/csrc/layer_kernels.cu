@@ -623,8 +623,10 @@ int attention_tc_init() {
   if (e == cudaSuccess)                                                                                           \
     e = cudaFuncSetAttribute(attention_tc_kernel<H, S, true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
                              (int)TcAttnSmem<H, S>::bytes)
+    SB_ATTN_ATTR(128, 2);
     SB_ATTN_ATTR(128, 3);
     SB_ATTN_ATTR(128, 4);
+    SB_ATTN_ATTR(64, 2);
     SB_ATTN_ATTR(64, 3);
     SB_ATTN_ATTR(64, 4);
     if (e == cudaSuccess) e = attn_simt_attr<__nv_bfloat16, 64>();
@@ -657,7 +659,14 @@ static int launch_attn_grid(const AttnArgs& A0, int hd, int n_seq, int z, cudaSt
     g_attn_stages = e ? atoi(e) : 4;  // measured: 4 and 6 tie, 3-5% over 3 at b = 2..4
   }
   const int ctas = A.nkv * n_seq * z;
-  const int stages = ctas <= num_sms() ? g_attn_stages : 3;
+  static int multi = -1;  // ring depth beyond two CTAs per SM (env SB_ATTN_STAGES_MULTI)
+  if (multi < 0) {
+    const char* e = getenv("SB_ATTN_STAGES_MULTI");
+    multi = e ? atoi(e) : 2;
+  }
+  // deepest ring that keeps the grid in one wave: 4 stages at <= 1 CTA per SM, 3 (2 per SM), then 2
+  // (3 per SM; measured: b=64,k=2 verify 6.72 -> 6.23 ms, b=32,k=2 4.61 -> 4.40 ms)
+  const int stages = ctas <= num_sms() ? g_attn_stages : ctas <= 2 * num_sms() ? 3 : multi;
   {  // normally done by gemm_tc_init outside capture; relaxed so a first call inside a capture is legal
     cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
     cudaThreadExchangeStreamCaptureMode(&mode);
@@ -675,8 +684,8 @@ static int launch_attn_grid(const AttnArgs& A0, int hd, int n_seq, int z, cudaSt
        : spl ? go(attention_tc_kernel<H, S, false, true>, TcAttnSmem<H, S>::bytes) \
              : go(attention_tc_kernel<H, S, false, false>, TcAttnSmem<H, S>::bytes))
   cudaError_t e;
-  if (hd == 128) e = stages >= 4 ? SB_ATTN_GO(128, 4) : SB_ATTN_GO(128, 3);
-  else e = stages >= 4 ? SB_ATTN_GO(64, 4) : SB_ATTN_GO(64, 3);
+  if (hd == 128) e = stages >= 4 ? SB_ATTN_GO(128, 4) : stages == 3 ? SB_ATTN_GO(128, 3) : SB_ATTN_GO(128, 2);
+  else e = stages >= 4 ? SB_ATTN_GO(64, 4) : stages == 3 ? SB_ATTN_GO(64, 3) : SB_ATTN_GO(64, 2);
 #undef SB_ATTN_GO
   if (e != cudaSuccess) return (int)e;
   ++g_kernel_count;

@@ -44,11 +44,19 @@ def main():
     report = {}
     raws = {}
     for b, k in cells:
-        plain = eng.time_verify(b, k, ctx=192, reps=20)
+        plain = eng.time_draft_step(b, ctx=192, reps=20) if "--draft" in sys.argv else eng.time_verify(b, k, ctx=192, reps=20)
         _stage_context(eng, b, k, 192)
         lib.sb_debug_cta_trace(N.ptr(buf))
-        fn = lambda: eng.target.forward(eng.kv_t, eng.v_ids, eng.slots, eng.v_pos, b, k + 1, eng.t_logits,
-                                        N.LOGITS_ALL, eng.workspace)
+        if "--draft" in sys.argv:  # one draft decode step (b sequences x 1 token, greedy sink) instead
+            sink = N.SbTokenSink(None, 0, eng.ds_ids.data_ptr(), None, None, 0)
+
+            def fn():
+                st = torch.cuda.current_stream(eng.dev).cuda_stream
+                eng.draft.forward_greedy(eng.kv_d, eng.ds_ids, eng.slots, eng.ds_pos, b, 1, None, N.LOGITS_LAST,
+                                         eng.workspace, sink, st)
+        else:
+            fn = lambda: eng.target.forward(eng.kv_t, eng.v_ids, eng.slots, eng.v_pos, b, k + 1, eng.t_logits,
+                                            N.LOGITS_ALL, eng.workspace)
         g = _capture_graph(fn, eng.stream)
         lib.sb_debug_cta_trace(None)
         with torch.cuda.stream(eng.stream):
@@ -79,7 +87,8 @@ def main():
             kind = int(r[0, 1])
             ent, dep, first, main, ext = (r[:, c] for c in range(4, 9))
             layer, j = divmod(i, 5)
-            name = f"L{layer}.{NAMES[j]}" if layer < tgt.cfg.n_layers else "lm_head"
+            nl = drf.cfg.n_layers if "--draft" in sys.argv else tgt.cfg.n_layers
+            name = f"L{layer}.{NAMES[j]}" if layer < nl else "lm_head"
             row = dict(id=i, name=name, kind=kind, ctas=len(r), sms=len(set(r[:, 2].tolist())),
                        entry_first=float(ent.min()), entry_last=float(ent.max()), dep_first=float(dep.min()),
                        dep_med=float(np.median(dep)), first_med=float(np.median(first)),
@@ -95,7 +104,7 @@ def main():
         print(f"{'launch':10s} {'ctas':>5s} {'sms':>4s} {'entry0':>8s} {'entryN':>8s} {'dep0':>8s} {'gap':>6s} "
               f"{'first':>8s} {'mainMed':>8s} {'mainN':>8s} {'exitMed':>8s} {'exitN':>8s} {'epiMed':>6s} {'epiMax':>6s}")
         for r in rows:
-            if r["id"] < 10 or r["id"] >= len(ids) - 6 or r["id"] // 5 == 16:
+            if "--draft" in sys.argv or r["id"] < 10 or r["id"] >= len(ids) - 6 or r["id"] // 5 == 16:
                 g_ = "" if r["gap_dep"] is None else f"{r['gap_dep']:6.2f}"
                 print(f"{r['name']:10s} {r['ctas']:5d} {r['sms']:4d} {r['entry_first']:8.2f} {r['entry_last']:8.2f} "
                       f"{r['dep_first']:8.2f} {g_:>6s} {r['first_med']:8.2f} {r['main_med']:8.2f} {r['main_last']:8.2f} "
@@ -105,7 +114,7 @@ def main():
             if r["name"] == "lm_head":
                 continue
             layer = r["id"] // 5
-            if 2 <= layer < tgt.cfg.n_layers - 2:
+            if ("--draft" in sys.argv and layer < drf.cfg.n_layers) or 2 <= layer < tgt.cfg.n_layers - 2:
                 a = agg.setdefault(NAMES[r["id"] % 5], [])
                 a.append((r["gap_dep"], r["dep_first"] - r["entry_first"], r["main_last"] - r["dep_first"],
                           r["exit_last"] - r["main_last"], r["epi_med"], r["exit_last"] - r["dep_first"]))

@@ -34,14 +34,21 @@ for b, k in cells:
             continue  # (the verify lm_head rows = T as well; skip: one launch)
         orig = get(rows, n, kk)
         best, best_t = orig, cur
-        for cps in (1, 2):
-            for sp in (1, 2, 4, 8):
-                if (cps, sp, 1, orig[3]) == orig:
-                    continue
-                N.call("sb_gemm_tune_set", rows, n, kk, cps, sp, 1, orig[3])
-                t = tv(b, k)
-                if t < best_t - 0.005:
-                    best, best_t = (cps, sp, 1, orig[3]), t
+        cands = [(cps, sp, 1, orig[3]) for cps in (1, 2) for sp in (1, 2, 4, 8)]
+        if rows >= 96:  # two weight tiles per CTA share the token stage (half the L2 token traffic per MAC)
+            nt = -(-rows // 256)
+            bal = (-(-rows // nt) + 15) // 16 * 16
+            for tn in sorted({0, 128, 192, bal if nt > 1 else 0}):
+                if tn == 0 or tn < min(256, (rows + 15) // 16 * 16):
+                    cands += [(1, 1, 2, tn), (1, 1, 1, tn), (2, 1, 1, tn)]
+        for c in dict.fromkeys(cands):
+            if c == orig:
+                continue
+            if N.load().sb_gemm_tune_set(rows, n, kk, *c) != 0:
+                continue
+            t = tv(b, k)
+            if t < best_t - 0.005:
+                best, best_t = c, t
         N.call("sb_gemm_tune_set", rows, n, kk, *best)
         cur = best_t
         out.append(f"  {name}: {orig} -> {best}: {cur:.3f} ms")
