@@ -158,7 +158,8 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
 template <int E_>
 __device__ __forceinline__ void tc_emit_row(const TcParams& p, int lane, int j, int jr, int acc, int tn, int m0,
                                             int n0a, int tile_a, float (&x)[4], float sc, uint64_t* res_bar,
-                                            const float* rb) {
+                                            const float* rb, bool has_pre = false,
+                                            float4 pre = make_float4(0.f, 0.f, 0.f, 0.f)) {
   const int m = m0 + j;
   if (m >= p.M) return;  // (warp-uniform) padding token
   const int n = n0a + 4 * lane;
@@ -197,7 +198,9 @@ __device__ __forceinline__ void tc_emit_row(const TcParams& p, int lane, int j, 
     }
   } else {  // EPI_RESID_ADD: new residual, its bf16 copy scaled by the consumer's gain, norm partial
     float4 pr = make_float4(0.f, 0.f, 0.f, 0.f);
-    if (p.res_bytes) {
+    if (has_pre) {  // loaded by the caller with the rest of its batch
+      pr = pre;
+    } else if (p.res_bytes) {
       mbar_wait(res_bar, 0);
       pr = *reinterpret_cast<const float4*>(rb + ((size_t)acc * tn + jr) * TC_BM + 4 * lane);
     } else if (nv) {
@@ -456,12 +459,29 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 for (int j = 0; j < 16; ++j) sb[(16 + j) * TC_BM + row] = __uint_as_float(r1[j]);
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");
-            for (int jl = ew; jl < cn; jl += 4) {
+            // EPI_RESID_ADD without the smem prefetch (large tiles): the warp's residual rows of the
+            // chunk are loaded together (one round trip per chunk: prefill o / down epilogue 53 -> 27 us)
+            constexpr bool RL = E_ == EPI_RESID_ADD;
+            float4 res8[TC_EPI_CH / 4];
+            if (RL && !p.res_bytes) {
+              const int n = n0 + acc * TC_BM + 4 * lane;
+#pragma unroll
+              for (int i = 0; i < TC_EPI_CH / 4; ++i) {
+                const int m = m0 + j0 + ew + 4 * i;
+                res8[i] = (ew + 4 * i < cn && m < p.M && n < p.N)
+                              ? __ldcg(reinterpret_cast<const float4*>((const float*)p.y + (size_t)m * p.N + n))
+                              : make_float4(0.f, 0.f, 0.f, 0.f);
+              }
+            }
+#pragma unroll
+            for (int i = 0; i < TC_EPI_CH / 4; ++i) {
+              const int jl = ew + 4 * i;
+              if (jl >= cn) break;
               const int j = j0 + jl;
               const float4 a = *reinterpret_cast<const float4*>(sb + jl * TC_BM + 4 * lane);
               float x[4] = {a.x, a.y, a.z, a.w};
               tc_emit_row<E_>(p, lane, j, j, acc, tn, m0, n0 + acc * TC_BM, tile_n * wt + acc, x,
-                              scale ? inv_s[j] : 1.f, res_bar, res_rows);
+                              scale ? inv_s[j] : 1.f, res_bar, res_rows, RL && !p.res_bytes, res8[i]);
             }
           }
         }
@@ -560,21 +580,38 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const uint32_t red_addr = smem_u32(red);
       const bool scale = p.ns_part != nullptr;
       const int jlo = split * tn / p.splits, jhi = (split + 1) * tn / p.splits;
-      for (int j = jlo + ew; j < jhi; j += 4) {
-        float4 t[8];
+      for (int jb = jlo + ew; jb < jhi; jb += 16) {  // groups of 4 tokens per warp
+        float4 res4[4];  // residual rows of the group (no smem prefetch: large tiles), loads in flight together
+        if (E_ == EPI_RESID_ADD && !p.res_bytes) {
+          const int n = n0 + 4 * lane;
 #pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (q < p.splits) t[q] = ld_dsmem_v4_nc(red_addr + (uint32_t)((j * TC_BM + 4 * lane) * 4), q);
-        float x[4] = {0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-        for (int q = 0; q < 8; ++q)
-          if (q < p.splits) {
-            x[0] += t[q].x;
-            x[1] += t[q].y;
-            x[2] += t[q].z;
-            x[3] += t[q].w;
+          for (int i = 0; i < 4; ++i) {
+            const int m = m0 + jb + 4 * i;
+            res4[i] = (jb + 4 * i < jhi && m < p.M && n < p.N)
+                          ? __ldcg(reinterpret_cast<const float4*>((const float*)p.y + (size_t)m * p.N + n))
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
           }
-        tc_emit_row<E_>(p, lane, j, j - jlo, 0, tn, m0, n0, tile_n, x, scale ? inv_s[j] : 1.f, res_bar, res_rows);
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int j = jb + 4 * i;
+          if (j >= jhi) break;
+          float4 t[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (q < p.splits) t[q] = ld_dsmem_v4_nc(red_addr + (uint32_t)((j * TC_BM + 4 * lane) * 4), q);
+          float x[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (q < p.splits) {
+              x[0] += t[q].x;
+              x[1] += t[q].y;
+              x[2] += t[q].z;
+              x[3] += t[q].w;
+            }
+          tc_emit_row<E_>(p, lane, j, j - jlo, 0, tn, m0, n0, tile_n, x, scale ? inv_s[j] : 1.f, res_bar, res_rows,
+                          E_ == EPI_RESID_ADD && !p.res_bytes, res4[i]);
+        }
       }
       }
     } else if (warp >= 2) {

@@ -44,10 +44,18 @@ def main():
     report = {}
     raws = {}
     for b, k in cells:
-        plain = eng.time_draft_step(b, ctx=192, reps=20) if "--draft" in sys.argv else eng.time_verify(b, k, ctx=192, reps=20)
-        _stage_context(eng, b, k, 192)
+        plain = (eng.time_draft_step(b, ctx=192, reps=20) if "--draft" in sys.argv else
+                 0.0 if "--prefill" in sys.argv else eng.time_verify(b, k, ctx=192, reps=20))
+        if "--prefill" not in sys.argv:
+            _stage_context(eng, b, k, 192)
         lib.sb_debug_cta_trace(N.ptr(buf))
-        if "--draft" in sys.argv:  # one draft decode step (b sequences x 1 token, greedy sink) instead
+        if "--prefill" in sys.argv:  # a prefill chunk: b prompts of k tokens (positions 0..k-1)
+            i32 = dict(device=dev, dtype=torch.int32)
+            pids = torch.randint(0, 32000, (b * k,), **i32)
+            ppos = torch.arange(k, **i32).repeat(b)
+            pws = torch.zeros(tgt.workspace_bytes(b * k), device=dev, dtype=torch.uint8)
+            fn = lambda: eng.target.forward(eng.kv_t, pids, eng.slots, ppos, b, k, None, N.LOGITS_NONE, pws)
+        elif "--draft" in sys.argv:  # one draft decode step (b sequences x 1 token, greedy sink) instead
             sink = N.SbTokenSink(None, 0, eng.ds_ids.data_ptr(), None, None, 0)
 
             def fn():
