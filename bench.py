@@ -479,10 +479,13 @@ def run_trace(args):
             rep = serve_wallclock(workload, ServerConfig(policy=pol, max_batch=16), eng, time_scale=args.trace_scale)
             lat[pol.label].append(rep.avg_latency / args.trace_scale)  # back to trace seconds
             batches[pol.label].append(float(np.mean([r.served_batch_size for r in rep.records])))
-    # continuous batching: retire / admit every iteration, k from the LUT per iteration
+    # continuous batching: retire / admit every iteration, k from the LUT per iteration;
+    # against the formed-batch best fixed k and fixed-3
+    fixed_mean = {k: float(np.mean(v)) for k, v in lat.items() if k.startswith("fixed")}
+    k_best = int(min(fixed_mean, key=fixed_mean.get).split("-")[1])
     workload = gen_phased(PhaseSchedule(phases=phases), np.random.default_rng([0, 6]), gen_len=NEW)
     cont = {}
-    for pol in [AdaptivePolicy(lut), FixedPolicy(3)]:
+    for pol in [AdaptivePolicy(lut)] + [FixedPolicy(kk) for kk in sorted({3, k_best})]:
         rep, extra = serve_continuous(workload, eng, pol, time_scale=args.trace_scale, max_batch=16)
         cont[pol.label] = {"latency_s": round(rep.avg_latency / args.trace_scale, 4),
                            "mean_live_batch": round(extra["mean_live_batch"], 2), "mean_k": round(extra["mean_k"], 2),

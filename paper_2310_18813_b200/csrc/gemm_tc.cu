@@ -592,6 +592,31 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                           : make_float4(0.f, 0.f, 0.f, 0.f);
           }
         }
+        if (p.splits <= 2) {
+          // two ranks: the group's 4 x 2 partial rows load together (one DSMEM round trip per group)
+          float4 t2[4][2];
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const int j = jb + 4 * i;
+              if (j < jhi && q < p.splits) t2[i][q] = ld_dsmem_v4_nc(red_addr + (uint32_t)((j * TC_BM + 4 * lane) * 4), q);
+            }
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const int j = jb + 4 * i;
+            if (j >= jhi) break;
+            float x[4] = {t2[i][0].x, t2[i][0].y, t2[i][0].z, t2[i][0].w};
+            if (p.splits > 1) {
+              x[0] += t2[i][1].x;
+              x[1] += t2[i][1].y;
+              x[2] += t2[i][1].z;
+              x[3] += t2[i][1].w;
+            }
+            tc_emit_row<E_>(p, lane, j, j - jlo, 0, tn, m0, n0, tile_n, x, scale ? inv_s[j] : 1.f, res_bar,
+                            res_rows, E_ == EPI_RESID_ADD && !p.res_bytes, res4[i]);
+          }
+        } else {
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
           const int j = jb + 4 * i;
@@ -611,6 +636,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             }
           tc_emit_row<E_>(p, lane, j, j - jlo, 0, tn, m0, n0, tile_n, x, scale ? inv_s[j] : 1.f, res_bar, res_rows,
                           E_ == EPI_RESID_ADD && !p.res_bytes, res4[i]);
+        }
         }
       }
       }

@@ -21,6 +21,7 @@
 
 #include "common.cuh"
 #include "kernels.cuh"
+#include "tc_ptx.cuh"
 
 namespace sb {
 
@@ -157,6 +158,258 @@ __device__ int block_inverse_cdf(const float* a, const float* b, int mode, int V
   const int r = pick;
   __syncthreads();
   return r;
+}
+
+// ------------------------------------------------------- cluster-parallel rows
+// A vocabulary row (32000-50272 floats) on ONE 256-thread CTA was a serial latency chain: 70-113 us
+// per softmax / sample (ncu, stochastic iteration at b=1, k=8: 1.06 ms of 4.15).  Here a cluster of
+// RC CTAs owns one row, each CTA a contiguous slice: block reductions, then the RC partials are read
+// over DSMEM in rank order (every CTA gets the identical max / sum / total), and the inverse CDF's
+// exact fixed-point prefix crosses CTAs through the same exchange.
+constexpr int RC = 8;
+
+__device__ __forceinline__ void row_slice(int V, int r, int& lo, int& hi) {
+  const int per = ((V + RC - 1) / RC + 3) & ~3;
+  lo = min(V, r * per);
+  hi = min(V, lo + per);
+}
+__device__ __forceinline__ uint32_t dsmem_addr(const void* local, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(smem_u32(local)), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ float dsmem_f32(const float* local, int rank) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];" : "=f"(v) : "r"(dsmem_addr(local, rank)) : "memory");
+  return v;
+}
+__device__ __forceinline__ int dsmem_i32(const int* local, int rank) {
+  int v;
+  asm volatile("ld.shared::cluster.s32 %0, [%1];" : "=r"(v) : "r"(dsmem_addr(local, rank)) : "memory");
+  return v;
+}
+__device__ __forceinline__ u128 dsmem_u128(const u128* local, int rank) {
+  unsigned long long lo, hi;
+  const uint32_t a = dsmem_addr(local, rank);
+  asm volatile("ld.shared::cluster.v2.u64 {%0, %1}, [%2];" : "=l"(lo), "=l"(hi) : "r"(a) : "memory");
+  return ((u128)hi << 64) | lo;
+}
+
+struct RowSmem {
+  float mx, sum;
+  float amv;
+  int ami;
+  u128 tot[2];  // fixed-point slice totals (two inverse-CDF rounds)
+  int pick;
+};
+
+// Cluster softmax of row x into p (this CTA's slice [lo, hi)): p = expf(x - max) * (1 / sum).
+__device__ void cluster_softmax_slice(const float* x, float* p, int lo, int hi, RowSmem& rs) {
+  float m = -INFINITY;
+  for (int v = lo + threadIdx.x; v < hi; v += blockDim.x) m = fmaxf(m, x[v]);
+  m = block_reduce(m, true);
+  if (threadIdx.x == 0) rs.mx = m;
+  cluster_sync_all();
+  m = -INFINITY;
+#pragma unroll
+  for (int r = 0; r < RC; ++r) m = fmaxf(m, dsmem_f32(&rs.mx, r));
+  float sl = 0.f;
+  for (int v = lo + threadIdx.x; v < hi; v += blockDim.x) sl += expf(x[v] - m);
+  sl = block_reduce(sl, false);
+  if (threadIdx.x == 0) rs.sum = sl;
+  cluster_sync_all();
+  float s = 0.f;
+#pragma unroll
+  for (int r = 0; r < RC; ++r) s += dsmem_f32(&rs.sum, r);
+  const float inv = 1.f / s;
+  for (int v = lo + threadIdx.x; v < hi; v += blockDim.x) p[v] = expf(x[v] - m) * inv;
+  __syncthreads();
+}
+
+// Cluster argmax of row x (ties -> lowest index); every CTA returns the row's winner.
+__device__ ArgMax cluster_argmax_row(const float* x, int lo, int hi, RowSmem& rs) {
+  ArgMax a = block_argmax_row(x + lo, hi - lo);
+  if (threadIdx.x == 0) {
+    rs.amv = a.v;
+    rs.ami = a.i == INT_MAX ? INT_MAX : a.i + lo;
+  }
+  cluster_sync_all();
+  ArgMax best{-INFINITY, INT_MAX};
+#pragma unroll
+  for (int r = 0; r < RC; ++r) best = argmax_merge(best, ArgMax{dsmem_f32(&rs.amv, r), dsmem_i32(&rs.ami, r)});
+  return best;
+}
+
+// Canonical inverse CDF of the row (see block_inverse_cdf) over the cluster: the pick if it lies in
+// this CTA's slice, else -1; *total_zero tells every CTA whether all weights were 0.
+__device__ int cluster_inverse_cdf(const float* a, const float* b, int mode, int lo, int hi, float u, int round,
+                                   RowSmem& rs, bool* total_zero) {
+  __shared__ u128 wsum[32];
+  const int nt = blockDim.x, t = threadIdx.x, lane = t & 31, w = t >> 5;
+  const int len = hi - lo, n = (len + nt - 1) / nt;
+  const int v0 = lo + min(len, t * n), v1 = lo + min(len, t * n + n);
+  u128 mine = 0;
+  for (int v = v0; v < v1; ++v) mine += fix80(mode ? fmaxf(a[v] - b[v], 0.f) : a[v]);
+  u128 inc = mine;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const u128 o = shfl_up_u128(inc, d);
+    if (lane >= d) inc += o;
+  }
+  if (t == 0) rs.pick = -1;
+  if (lane == 31) wsum[w] = inc;
+  __syncthreads();
+  if (t == 0) {
+    u128 run = 0;
+    for (int i = 0; i < (nt >> 5); ++i) {
+      const u128 x = wsum[i];
+      wsum[i] = run;
+      run += x;
+    }
+    rs.tot[round] = run;
+  }
+  cluster_sync_all();
+  const int crank = (int)cluster_rank();
+  u128 total = 0, off = 0;
+#pragma unroll
+  for (int r = 0; r < RC; ++r) {
+    const u128 x = dsmem_u128(&rs.tot[round], r);
+    if (r < crank) off += x;
+    total += x;
+  }
+  *total_zero = total == 0;
+  if (total != 0) {
+    const u128 excl = off + wsum[w] + inc - mine;
+    const u128 target = (u128)(uint64_t)(u * 4294967296.0f) * total;
+    if (mine != 0 && (excl << 32) <= target && ((excl + mine) << 32) > target) {
+      u128 run = excl;
+      for (int v = v0; v < v1; ++v) {
+        run += fix80(mode ? fmaxf(a[v] - b[v], 0.f) : a[v]);
+        if ((run << 32) > target) {
+          rs.pick = v;
+          break;
+        }
+      }
+    }
+  }
+  __syncthreads();
+  return rs.pick;
+}
+
+// grid (RC, rows), cluster (RC, 1, 1)
+__global__ void softmax_rows_cluster_kernel(const float* logits, int V, float* probs) {
+  griddep_wait();
+  griddep_launch();
+  __shared__ RowSmem rs;
+  int lo, hi;
+  row_slice(V, (int)cluster_rank(), lo, hi);
+  cluster_softmax_slice(logits + (size_t)blockIdx.y * V, probs + (size_t)blockIdx.y * V, lo, hi, rs);
+  cluster_sync_all();  // peers have read this CTA's partials
+}
+
+__global__ void select_cluster_kernel(const float* logits, int V, int mode, const float* __restrict__ u, int u_stride,
+                                      float* probs, long long probs_stride, int32_t* out_tok, int out_stride,
+                                      int32_t* next_ids, int32_t* next_pos, const int32_t* base_pos, int pos_offset) {
+  griddep_wait();
+  griddep_launch();
+  __shared__ RowSmem rs;
+  const int r = blockIdx.y;
+  int lo, hi;
+  row_slice(V, (int)cluster_rank(), lo, hi);
+  const float* row = logits + (size_t)r * V;
+  int tok = -1;
+  bool mine;
+  if (mode == SB_SELECT_ARGMAX) {
+    tok = cluster_argmax_row(row, lo, hi, rs).i;
+    if (probs) cluster_softmax_slice(row, probs + (size_t)r * probs_stride, lo, hi, rs);
+    mine = cluster_rank() == 0;
+  } else {
+    float* p = probs + (size_t)r * probs_stride;
+    cluster_softmax_slice(row, p, lo, hi, rs);
+    bool zero;
+    tok = cluster_inverse_cdf(p, nullptr, 0, lo, hi, u[(size_t)r * u_stride], 0, rs, &zero);
+    mine = tok >= 0;
+  }
+  if (mine && threadIdx.x == 0) {
+    if (out_tok) out_tok[(size_t)r * out_stride] = tok;
+    if (next_ids) next_ids[r] = tok;
+    if (next_pos) next_pos[r] = base_pos[r] + pos_offset;
+  }
+  cluster_sync_all();
+}
+
+// Stochastic acceptance (mode SB_ACCEPT_STOCHASTIC) with the residual / bonus draw over the cluster.
+__global__ void accept_stochastic_cluster_kernel(int k, int V, const float* __restrict__ p_probs,
+                                                 const float* __restrict__ q_probs, const int32_t* __restrict__ draft_tok,
+                                                 int draft_stride, const float* __restrict__ u_acc,
+                                                 const float* __restrict__ u_res, int u_stride,
+                                                 const int32_t* __restrict__ produced,
+                                                 const int32_t* __restrict__ target_len, int32_t* accepted_len,
+                                                 int32_t* advanced, int32_t* out_tok) {
+  griddep_wait();
+  griddep_launch();
+  __shared__ RowSmem rs;
+  __shared__ int sh_l;
+  const int s = blockIdx.y;
+  const int32_t* d = draft_tok + (size_t)s * draft_stride;
+  if (threadIdx.x < 32) {  // lane j tests draft j (k <= 32); the first rejection ends the run
+    const int j = threadIdx.x;
+    bool rej = false;
+    if (j < k) {
+      const int tok = d[j];
+      const float pj = p_probs[((size_t)s * (k + 1) + j) * V + tok];
+      const float qj = q_probs[((size_t)s * k + j) * V + tok];
+      const float uq = u_acc[(size_t)s * u_stride + j] * qj;
+      rej = !(uq < pj);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, rej);
+    if (j == 0) sh_l = m ? __ffs(m) - 1 : k;
+  }
+  __syncthreads();
+  const int l = sh_l;
+  int lo, hi;
+  row_slice(V, (int)cluster_rank(), lo, hi);
+  const float* p = p_probs + ((size_t)s * (k + 1) + l) * V;
+  const float u = u_res[(size_t)s * u_stride];
+  bool zero = false;
+  int next;
+  if (l < k) {
+    next = cluster_inverse_cdf(p, q_probs + ((size_t)s * k + l) * V, 1, lo, hi, u, 0, rs, &zero);
+    if (zero) next = cluster_inverse_cdf(p, nullptr, 0, lo, hi, u, 1, rs, &zero);
+  } else {
+    next = cluster_inverse_cdf(p, nullptr, 0, lo, hi, u, 0, rs, &zero);
+  }
+  int32_t* o = out_tok + (size_t)s * (k + 1);
+  if (threadIdx.x == 0 && cluster_rank() == 0) {
+    const int rem = target_len[s] - produced[s];
+    accepted_len[s] = l;
+    advanced[s] = rem <= 0 ? 0 : min(l + 1, rem);
+    for (int j = 0; j < l; ++j) o[j] = d[j];
+    for (int j = l + 1; j <= k; ++j) o[j] = -1;
+  }
+  if (threadIdx.x == 0 && next >= 0) o[l] = next;
+  cluster_sync_all();
+}
+
+template <typename... KArgs, typename... Args>
+static int launch_rows_cluster(void (*kern)(KArgs...), int rows, cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(RC, rows, 1);
+  cfg.blockDim = dim3(256, 1, 1);
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = RC;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = g_pdl ? 2 : 1;
+  cudaError_t e = cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...);
+  if (e != cudaSuccess) return (int)e;
+  ++g_kernel_count;
+  return 0;
 }
 
 __global__ void argmax_rows_kernel(const float* __restrict__ logits, int V, int32_t* __restrict__ out) {
@@ -365,7 +618,7 @@ int sb_argmax_rows(const float* logits, int32_t rows, int32_t vocab, int32_t* ou
 
 int sb_softmax_rows(const float* logits, int32_t rows, int32_t vocab, float* probs, void* stream) {
   if (rows <= 0) return 0;
-  return launch_k(softmax_rows_kernel, dim3(rows), dim3(256), 0, (cudaStream_t)stream, logits, vocab, probs);
+  return launch_rows_cluster(softmax_rows_cluster_kernel, rows, (cudaStream_t)stream, logits, vocab, probs);
 }
 
 int sb_select_tokens(const float* logits, int32_t rows, int32_t vocab, int32_t mode, const float* u, int32_t u_stride,
@@ -375,8 +628,9 @@ int sb_select_tokens(const float* logits, int32_t rows, int32_t vocab, int32_t m
   if (mode == SB_SELECT_SAMPLE && (probs_out == nullptr || u == nullptr)) return SB_EINVAL;
   if (next_pos && !base_pos) return SB_EINVAL;
   if (vocab >= 65536) return SB_EUNSUPPORTED;  // fixed-point totals stay below 2^96
-  return launch_k(select_kernel, dim3(rows), dim3(256), 0, (cudaStream_t)stream, logits, vocab, mode, u, u_stride, probs_out, probs_stride,
-                                                        out_tok, out_stride, next_ids, next_pos, base_pos, pos_offset);
+  return launch_rows_cluster(select_cluster_kernel, rows, (cudaStream_t)stream, logits, vocab, mode, u, u_stride,
+                             probs_out, (long long)probs_stride, out_tok, out_stride, next_ids, next_pos, base_pos,
+                             pos_offset);
 }
 
 int sb_accept(int32_t mode, int32_t b, int32_t k, int32_t vocab, const int32_t* target_tok, const float* p_probs,
@@ -389,6 +643,10 @@ int sb_accept(int32_t mode, int32_t b, int32_t k, int32_t vocab, const int32_t* 
   if (mode == SB_ACCEPT_INJECTED && !l_inj) return SB_EINVAL;
   if (mode < 0 || mode > 2) return SB_EINVAL;
   if (vocab >= 65536) return SB_EUNSUPPORTED;  // fixed-point totals stay below 2^96
+  if (mode == SB_ACCEPT_STOCHASTIC)
+    return launch_rows_cluster(accept_stochastic_cluster_kernel, b, (cudaStream_t)stream, k, vocab, p_probs, q_probs,
+                               draft_tok, draft_stride, u_acc, u_res, u_stride, produced, target_len, accepted_len,
+                               advanced, out_tok);
   return launch_k(accept_kernel, dim3(b), dim3(256), 0, (cudaStream_t)stream, mode, k, vocab, target_tok, p_probs, q_probs, draft_tok,
                                                      draft_stride, u_acc, u_res, u_stride, l_inj, produced,
                                                      target_len, accepted_len, advanced, out_tok);

@@ -15,6 +15,8 @@ cells = [tuple(int(x) for x in c.split(",")) for c in os.environ.get("CELLS", ""
 eng = SpecEngine(tgt, drf, mode="injected", acceptance=example_trace(), max_batch=max(32, max(b for b, _ in cells)),
                  max_k=8, prompt_len=128, max_new=128)
 lib = N.load()
+if os.environ.get("ATTN_SPLITS"):
+    lib.sb_set_attention_splits(int(os.environ["ATTN_SPLITS"]))
 for b, k in cells:
     row = []
     for f in flags:

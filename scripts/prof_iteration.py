@@ -19,7 +19,9 @@ k = int(os.environ.get("PK", "3"))
 dev = torch.device("cuda:0")
 tgt = Decoder(CONFIGS["llama-2-7b"], dtype="bf16", device=dev, seed=0, init="device", max_pos=320)
 drf = Decoder(CONFIGS["llama-68m"], dtype="bf16", device=dev, seed=1, init="device", max_pos=320)
-eng = SpecEngine(tgt, drf, mode="injected", acceptance=example_trace(), max_batch=8, max_k=8, prompt_len=128,
+PMODE = os.environ.get("PMODE", "injected")  # injected | greedy | stochastic
+eng = SpecEngine(tgt, drf, mode=PMODE, acceptance=example_trace() if PMODE == "injected" else None, max_batch=8,
+                 max_k=8, prompt_len=128,
                  max_new=128, seed=0)
 _stage_context(eng, b, k, 192)
 g = eng._graph(b, k)
