@@ -162,8 +162,9 @@ class SpecEngine:
             Ts = {b * (k + 1) for b in range(1, B + 1) for k in range(K + 1)} | set(range(1, 2 * B + 1))
             if prompt_len > 1:  # prefill chunks of nb prompts (measured: qkv 6.4 -> 5.2 ms at T=1016)
                 Ts |= {nb * (prompt_len - 1) for nb in range(1, min(B, self.pf_chunk) + 1)}
-            # (the draft keeps the heuristic: its isolated-GEMM winners measured slower in-graph)
             self.tuning["target"] = target.autotune(Ts)
+            if draft is not None:  # draft decode steps: b tokens (2b in step 1); measured 1-2% over the heuristic
+                self.tuning["draft"] = draft.autotune({n for b in range(1, B + 1) for n in (b, 2 * b)})
 
     # ------------------------------------------------------------- prompts
     def _default_prompt(self, request_id: int) -> np.ndarray:
