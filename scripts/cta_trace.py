@@ -80,12 +80,14 @@ def main():
         raw = buf[8:8 + 8 * n].view(n, 8).cpu().numpy().astype(np.int64)
         # columns: id, kind, smid, block, t_entry, t_dep, t_first, t_main, t_exit (us from the first entry)
         t0 = raw[:, 2].min()
-        rec = np.zeros((n, 9))
+        rec = np.zeros((n, 9))  # (+ column 9: sub-phase stamp)
         rec[:, 0] = raw[:, 0] & 0xffffffff
         rec[:, 1] = (raw[:, 0] >> 32) & 0xff
         rec[:, 2] = raw[:, 0] >> 40
         rec[:, 3] = raw[:, 1]
         rec[:, 4:9] = (raw[:, 2:7] - t0) / 1e3
+        sub = np.where(raw[:, 7] > 0, (raw[:, 7] - t0) / 1e3, np.nan)  # kernel sub-phase stamp (if any)
+        rec = np.concatenate([rec, sub[:, None]], axis=1)
         raws[f"b{b}k{k}"] = rec
         ids = sorted(set(rec[:, 0].astype(int).tolist()))
         rows = []
