@@ -142,6 +142,16 @@ typedef struct sb_decoder {
   const void* const* b_o;         /* [hidden] */
   const void* const* b_fc1;       /* [ffn] */
   const void* const* b_fc2;       /* [hidden] */
+  /* OPT, bf16: LayerNorm fused into the consuming GEMMs (all NULL = separate LayerNorm kernels).  For a
+     consumer with weight W [N, K] behind LayerNorm (gamma, beta): c1 = W gamma, c2 = W beta (fp32 [N]),
+     and W . LN(x) = rstd * W . (x * gamma) - mean * rstd * c1 + c2, with the residual's producer writing
+     xb = bf16(x * gamma) and per-tile sums of x and x^2 (mean, rstd in the consumer's epilogue). */
+  const float* const* ln_qkv_c1;  /* [n_layers] -> [qkv rows] */
+  const float* const* ln_qkv_c2;
+  const float* const* ln_fc1_c1;  /* [n_layers] -> [ffn] */
+  const float* const* ln_fc1_c2;
+  const float* ln_lm_c1;          /* [vocab] */
+  const float* ln_lm_c2;
 } sb_decoder_t;
 
 /* KV cache: k/v base pointers of layout [n_layers][slots][n_kv_heads][ctx_max][head_dim]. */

@@ -28,6 +28,7 @@ struct FwdWorkspace {
   int* amax_idx;
   void* xb;       // bf16 copy of the residual (fused-RMSNorm GEMM input)
   float* npart;   // sum-of-squares partials [P_max][T]
+  float* npart1;  // sum partials [P_max][T] (OPT fused LayerNorm)
   float* tp_part;     // TP: fp32 partial residual update, all-reduced in place [T, H]
   float* tp_logits;   // TP: local vocab slice of the logits [T, vocab_local]
   float* tp_gather;   // TP: all-gathered slices [world][T][vocab_local]
@@ -75,6 +76,7 @@ static size_t carve(const sb_decoder_t* m, int T, char* base, FwdWorkspace* w) {
   o->amax_idx = (int*)take(vt * 4);
   o->xb = take((size_t)T * m->hidden * 2);
   o->npart = (float*)take((size_t)((m->hidden + 127) / 128) * 8 * T * 4);
+  o->npart1 = m->arch == SB_ARCH_OPT ? (float*)take((size_t)((m->hidden + 127) / 128) * 8 * T * 4) : nullptr;
   const int tpw = m->tp ? m->tp->world : 0;
   o->tp_part = tpw ? (float*)take((size_t)T * m->hidden * 4) : nullptr;
   o->tp_logits = tpw ? (float*)take((size_t)T * m->vocab * 4) : nullptr;
@@ -349,6 +351,90 @@ static int forward_fused_norm(const sb_decoder_t* m, const sb_kvcache_t* kv, con
 // (fc1 -> relu -> fc2), final LayerNorm, lm_head tied to the embedding (the
 // host passes the same pointer).  RoPE tables are identity for OPT, so the
 // shared attention kernels apply no rotation.
+// OPT with every LayerNorm fused into the GEMMs around it (bf16; Decoder._build_ln_fusion): the
+// residual's producers (embedding, o, fc2) write xb = bf16(x * gamma_next) and per-tile sums of x and x^2;
+// the consumers (qkv, fc1, lm_head) scale by rstd and add - mean * rstd * (W gamma) + W beta per row.
+// Removes the three LayerNorm kernels per layer pair of the unfused forward (measured: see DESIGN).
+static int forward_opt_fused(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* ids, const int32_t* slot,
+                             const int32_t* pos, int n_seq, int q_len, float* logits, int logits_mode,
+                             const sb_token_sink_t* sink, const FwdWorkspace& w, cudaStream_t st) {
+  const int T = n_seq * q_len;
+  const int nq = m->n_heads, nkv = m->n_kv_heads, hd = m->head_dim, H = m->hidden;
+  const int qkv_n = (nq + 2 * nkv) * hd;
+  const size_t layer_kv = (size_t)kv->slots * nkv * kv->ctx_max * hd * 2;
+  const float inv_h = 1.0f / (float)H;
+  auto next_gain = [&](int l) -> const void* { return l + 1 < m->n_layers ? m->attn_norm[l + 1] : m->final_norm; };
+  SB_TRY(launch_embed_norm(m->embed, ids, pos, w.resid, w.xb, w.npart, T, H, m->vocab, st, m->attn_norm[0],
+                           m->pos_embed, m->pos_offset, w.npart1));
+  prof_mark("embed", st);
+  int P = 1;
+  auto consumer = [&](GemmArgs& g, const float* c1, const float* c2) {
+    g.ns_part = w.npart;
+    g.ns_P = P;
+    g.ns_stride = T;
+    g.ns_eps = m->rms_eps;
+    g.ns_inv_h = inv_h;
+    g.ln_s1 = w.npart1;
+    g.ln_c1 = c1;
+    g.ln_c2 = c2;
+  };
+  for (int l = 0; l < m->n_layers; ++l) {
+    char* kc = (char*)kv->k + l * layer_kv;
+    char* vc = (char*)kv->v + l * layer_kv;
+    GemmArgs g{SB_BF16, w.xb, m->w_qkv[l], w.qkv, T, qkv_n, H, H, EPI_STORE, w.gemm_ws, w.gemm_ws_bytes};
+    g.bias = m->b_qkv[l];
+    consumer(g, m->ln_qkv_c1[l], m->ln_qkv_c2[l]);
+    SB_TRY(gemm_tc(g, st));
+    prof_mark("qkv", st);
+    int rc_fa = g_attn_impl == 0 ? launch_attention_tc(w.qkv, kc, vc, w.attn, slot, pos, m->rope_cos, m->rope_sin,
+                                                        n_seq, q_len, nq, nkv, hd, kv->ctx_max, m->max_pos, st,
+                                                        &w.att_split, m->w_o[l], (size_t)H * nq * hd * 2)
+                                 : SB_EUNSUPPORTED;
+    if (rc_fa != 0 && rc_fa != SB_EUNSUPPORTED) return rc_fa;
+    if (rc_fa == SB_EUNSUPPORTED) {
+      SB_TRY(launch_rope_append(SB_BF16, w.qkv, w.qr, kc, vc, slot, pos, m->rope_cos, m->rope_sin, T, q_len, nq, nkv,
+                                hd, kv->ctx_max, m->max_pos, st));
+      SB_TRY(launch_attention_any(SB_BF16, w.qr, kc, vc, w.attn, slot, pos, n_seq, q_len, nq, nkv, hd, kv->ctx_max, st));
+    }
+    prof_mark("attn", st);
+    GemmArgs o{SB_BF16, w.attn, m->w_o[l], w.resid, T, H, nq * hd, nq * hd, EPI_RESID_ADD, w.gemm_ws, w.gemm_ws_bytes};
+    o.bias = m->b_o[l];
+    o.out_part = w.npart;
+    o.out_part1 = w.npart1;
+    o.out_xb = w.xb;
+    o.out_gain = m->mlp_norm[l];
+    SB_TRY(gemm_tc(o, st));
+    P = gemm_tc_norm_partials(o);
+    prof_mark("o", st);
+    GemmArgs f1{SB_BF16, w.xb, m->w_gu[l], w.act, T, m->ffn, H, H, EPI_STORE, w.gemm_ws, w.gemm_ws_bytes};
+    f1.bias = m->b_fc1[l];
+    f1.relu = 1;
+    consumer(f1, m->ln_fc1_c1[l], m->ln_fc1_c2[l]);
+    SB_TRY(gemm_tc(f1, st));
+    prof_mark("fc1", st);
+    GemmArgs f2{SB_BF16, w.act, m->w_down[l], w.resid, T, H, m->ffn, m->ffn, EPI_RESID_ADD, w.gemm_ws,
+                w.gemm_ws_bytes};
+    f2.bias = m->b_fc2[l];
+    f2.out_part = w.npart;
+    f2.out_part1 = w.npart1;
+    f2.out_xb = w.xb;
+    f2.out_gain = next_gain(l);
+    SB_TRY(gemm_tc(f2, st));
+    P = gemm_tc_norm_partials(f2);
+    prof_mark("fc2", st);
+  }
+  if (logits_mode == SB_LOGITS_NONE) return 0;
+  const bool last = logits_mode == SB_LOGITS_LAST;
+  const int rows = last ? n_seq : T;
+  const int step = last ? q_len : 1, off = last ? q_len - 1 : 0;
+  GemmArgs g{SB_BF16, (const char*)w.xb + (size_t)off * H * 2, m->lm_head, logits, rows, m->vocab, H, step * H,
+             EPI_STORE_F32, w.gemm_ws, w.gemm_ws_bytes};
+  consumer(g, m->ln_lm_c1, m->ln_lm_c2);
+  g.ns_row_step = step;
+  g.ns_row_off = off;
+  return lm_head(m, g, logits, sink, w, rows, st);
+}
+
 static int forward_opt(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* ids, const int32_t* slot,
                        const int32_t* pos, int n_seq, int q_len, float* logits, int logits_mode,
                        const sb_token_sink_t* sink, const FwdWorkspace& w, cudaStream_t st) {
@@ -356,6 +442,9 @@ static int forward_opt(const sb_decoder_t* m, const sb_kvcache_t* kv, const int3
   if (!m->pos_embed || !m->b_qkv || !m->b_o || !m->b_fc1 || !m->b_fc2 || !m->attn_norm_b || !m->mlp_norm_b ||
       !m->final_norm_b)
     return SB_EINVAL;
+  if (m->dtype == SB_BF16 && g_fuse_norm && g_backend_override != GEMM_SIMT && m->ln_qkv_c1 && m->ln_qkv_c2 &&
+      m->ln_fc1_c1 && m->ln_fc1_c2 && m->ln_lm_c1 && m->ln_lm_c2 && w.npart1 && m->hidden % 16 == 0)
+    return forward_opt_fused(m, kv, ids, slot, pos, n_seq, q_len, logits, logits_mode, sink, w, st);
   const int T = n_seq * q_len;
   const int dt = m->dtype;
   const size_t es = dt == SB_BF16 ? 2 : 4;

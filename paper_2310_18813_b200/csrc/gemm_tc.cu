@@ -72,6 +72,10 @@ struct TcParams {
   int launch_late;  // 1: trigger dependents at the end of the epilogue instead of after the last load
   int dbg;          // experiments (sb_debug_gemm_pdl): bit 0 skip the epilogue stores, bit 3 plain stores,
                     // bit 4 scalar (per-element) epilogue
+  const float* ln_s1;  // fused LayerNorm (GemmArgs::ln_*, out_part1)
+  const float* ln_c1;
+  const float* ln_c2;
+  float* out_part1;
   int vec;          // row epilogue (N % 16 == 0, 16-byte aligned outputs, power-of-two splits)
   int res_bytes;    // EPI_RESID_ADD: bytes of residual rows prefetched into shared memory (0 = loaded per row)
 };
@@ -159,7 +163,7 @@ template <int E_>
 __device__ __forceinline__ void tc_emit_row(const TcParams& p, int lane, int j, int jr, int acc, int tn, int m0,
                                             int n0a, int tile_a, float (&x)[4], float sc, uint64_t* res_bar,
                                             const float* rb, bool has_pre = false,
-                                            float4 pre = make_float4(0.f, 0.f, 0.f, 0.f)) {
+                                            float4 pre = make_float4(0.f, 0.f, 0.f, 0.f), float musc = 0.f) {
   const int m = m0 + j;
   if (m >= p.M) return;  // (warp-uniform) padding token
   const int n = n0a + 4 * lane;
@@ -167,6 +171,14 @@ __device__ __forceinline__ void tc_emit_row(const TcParams& p, int lane, int j, 
   const size_t o = (size_t)m * p.N + n;
 #pragma unroll
   for (int i = 0; i < 4; ++i) x[i] *= sc;
+  if (p.ln_c1 && nv) {  // fused LayerNorm: - mean * rstd * (W gamma) + W beta
+    const float4 c1 = *reinterpret_cast<const float4*>(p.ln_c1 + n);
+    const float4 c2 = *reinterpret_cast<const float4*>(p.ln_c2 + n);
+    x[0] += c2.x - musc * c1.x;
+    x[1] += c2.y - musc * c1.y;
+    x[2] += c2.z - musc * c1.z;
+    x[3] += c2.w - musc * c1.w;
+  }
   if (p.bias && nv) {
     const uint2 bb = *reinterpret_cast<const uint2*>(p.bias + n);
     x[0] += __bfloat162float(__ushort_as_bfloat16((unsigned short)(bb.x & 0xffff)));
@@ -223,6 +235,10 @@ __device__ __forceinline__ void tc_emit_row(const TcParams& p, int lane, int j, 
       const float sq = warp_sum(nv ? ((a0 * a0 + a1 * a1) + a2 * a2) + a3 * a3 : 0.f);
       if (lane == 0 && tile_a < p.n_tiles_n) st_o(p, p.out_part + (size_t)tile_a * p.M + m, sq);
     }
+    if (p.out_part1) {  // (LayerNorm consumers also need the sum)
+      const float s1 = warp_sum(nv ? ((a0 + a1) + a2) + a3 : 0.f);
+      if (lane == 0 && tile_a < p.n_tiles_n) st_o(p, p.out_part1 + (size_t)tile_a * p.M + m, s1);
+    }
   }
 }
 
@@ -258,8 +274,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
   uint64_t* tmem_full = empty + p.stages;
   uint64_t* res_bar = tmem_full + 1;  // prefetched residual rows landed (row epilogue)
   uint32_t* tmem_slot = (uint32_t*)(res_bar + 1);
-  float* inv_s = (float*)(tmem_slot + 4);  // [tn] per-token 1/rms (fused RMSNorm)
+  float* inv_s = (float*)(tmem_slot + 4);  // [tn] per-token 1/rms (fused RMSNorm) / rstd (fused LayerNorm)
   float* nsum = inv_s + tn;                 // [4][tn] per-token partial sums of squares (fused RMSNorm)
+  float* musc = nsum + 4 * tn;              // [tn] fused LayerNorm: mean * rstd
+  float* nsum1 = musc + tn;                 // [4][tn] fused LayerNorm: partial sums of x
   float* red = (float*)smem;               // split-K partial tile [tn][128] (reuses the drained ring)
   float* sq = p.splits > 1 ? red + tn * TC_BM : red + 8 * tn;  // norm squares staging
 
@@ -415,12 +433,36 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
           }
         }
         nsum[part * tn + j] = acc;
+        if (p.ln_s1) {  // fused LayerNorm: the sums of x the same way
+          float a1 = 0.f;
+          if (m < p.M) {
+            const float* src = p.ln_s1 + (size_t)m * p.ns_row_step + p.ns_row_off;
+            for (int q = q0; q < q1; q += 8) {
+              float t8[8];
+#pragma unroll
+              for (int i = 0; i < 8; ++i) t8[i] = q + i < q1 ? __ldcg(src + (size_t)(q + i) * p.ns_stride) : 0.f;
+#pragma unroll
+              for (int i = 0; i < 8; ++i) a1 += t8[i];
+            }
+          }
+          nsum1[part * tn + j] = a1;
+        }
       }
       asm volatile("bar.sync 2, 128;" ::: "memory");
       for (int j = et; j < tn; j += 128) {
         float tot = nsum[j];
         for (int part = 1; part < tpj; ++part) tot += nsum[part * tn + j];
-        inv_s[j] = rsqrtf(tot * p.ns_inv_h + p.ns_eps);
+        if (p.ln_s1) {  // LayerNorm: mean = S1 / H, var = S2 / H - mean^2, rstd = rsqrt(var + eps)
+          float t1 = nsum1[j];
+          for (int part = 1; part < tpj; ++part) t1 += nsum1[part * tn + j];
+          const float mean = t1 * p.ns_inv_h;
+          const float var = fmaxf(tot * p.ns_inv_h - mean * mean, 0.f);
+          const float rstd = rsqrtf(var + p.ns_eps);
+          inv_s[j] = rstd;
+          musc[j] = mean * rstd;
+        } else {
+          inv_s[j] = rsqrtf(tot * p.ns_inv_h + p.ns_eps);
+        }
       }
       asm volatile("bar.sync 2, 128;" ::: "memory");
     }
@@ -481,7 +523,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               const float4 a = *reinterpret_cast<const float4*>(sb + jl * TC_BM + 4 * lane);
               float x[4] = {a.x, a.y, a.z, a.w};
               tc_emit_row<E_>(p, lane, j, j, acc, tn, m0, n0 + acc * TC_BM, tile_n * wt + acc, x,
-                              scale ? inv_s[j] : 1.f, res_bar, res_rows, RL && !p.res_bytes, res8[i]);
+                              scale ? inv_s[j] : 1.f, res_bar, res_rows, RL && !p.res_bytes, res8[i],
+                              p.ln_s1 ? musc[j] : 0.f);
             }
           }
         }
@@ -614,7 +657,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               x[3] += t2[i][1].w;
             }
             tc_emit_row<E_>(p, lane, j, j - jlo, 0, tn, m0, n0, tile_n, x, scale ? inv_s[j] : 1.f, res_bar,
-                            res_rows, E_ == EPI_RESID_ADD && !p.res_bytes, res4[i]);
+                            res_rows, E_ == EPI_RESID_ADD && !p.res_bytes, res4[i], p.ln_s1 ? musc[j] : 0.f);
           }
         } else {
 #pragma unroll
@@ -635,7 +678,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               x[3] += t[q].w;
             }
           tc_emit_row<E_>(p, lane, j, j - jlo, 0, tn, m0, n0, tile_n, x, scale ? inv_s[j] : 1.f, res_bar, res_rows,
-                          E_ == EPI_RESID_ADD && !p.res_bytes, res4[i]);
+                          E_ == EPI_RESID_ADD && !p.res_bytes, res4[i], p.ln_s1 ? musc[j] : 0.f);
         }
         }
       }
@@ -824,7 +867,7 @@ static void tc_plan_smem(TcPlan& q) {
   const size_t stage = (size_t)(TC_BM * q.wt + q.tn) * TC_BK * 2;
   const size_t ring = (size_t)q.stages * stage;
   const size_t scratch = tc_scratch_bytes(q.tn, q.splits, q.vec, split_rows_max(q.splits));
-  q.smem = 1024 + tc_res_offset((uint32_t)ring, (uint32_t)scratch) + q.res_bytes + 256 + 16 + (size_t)q.tn * 4 * 5;
+  q.smem = 1024 + tc_res_offset((uint32_t)ring, (uint32_t)scratch) + q.res_bytes + 256 + 16 + (size_t)q.tn * 4 * 10;
 }
 
 // Split-K policy for the HBM-bound regime: enough CTAs that every SM streams
@@ -1119,6 +1162,12 @@ int gemm_tc(const GemmArgs& a, cudaStream_t st) {
   p.pre_max = g_gemm_pre_max;
   p.launch_late = g_gemm_launch_late;
   p.dbg = g_gemm_dbg;
+  p.ln_s1 = a.ln_s1;
+  p.ln_c1 = a.ln_c1;
+  p.ln_c2 = a.ln_c2;
+  p.out_part1 = a.out_part1;
+  if ((a.ln_s1 || a.ln_c1 || a.out_part1) && !q.vec) return SB_EUNSUPPORTED;  // row epilogue only
+  if (a.ln_s1 && (!a.ln_c1 || !a.ln_c2 || !a.ns_part)) return SB_EINVAL;
   p.vec = q.vec;
   p.res_bytes = q.res_bytes;
   p.trace = g_cta_trace;

@@ -44,6 +44,12 @@ struct GemmArgs {
   // OPT: per-output-row bias (model dtype, [N]) added to the fp32 accumulator, then ReLU (store epilogues)
   const void* bias = nullptr;
   int relu = 0;
+  // fused LayerNorm (OPT): consumer -- ln_s1 = sums of x partials (layout of ns_part), output row n gets
+  // rstd * acc - mean * rstd * ln_c1[n] + ln_c2[n]; producer (EPI_RESID_ADD) -- out_part1 = sums of x
+  const float* ln_s1 = nullptr;
+  const float* ln_c1 = nullptr;
+  const float* ln_c2 = nullptr;
+  float* out_part1 = nullptr;
 };
 
 extern int g_backend_override;  // sb_set_gemm_backend (ablation / tests)
@@ -70,7 +76,8 @@ int launch_embed(int dtype, const void* table, const int32_t* ids, const int32_t
 int launch_layernorm(int dtype, const float* x, const void* g, const void* b, void* y, int rows, int hidden, float eps,
                      int row_step, int row_off, cudaStream_t st);
 int launch_embed_norm(const void* table, const int32_t* ids, const int32_t* pos, float* h, void* xb, float* part,
-                      int n_tok, int hidden, int vocab, cudaStream_t st, const void* gain);
+                      int n_tok, int hidden, int vocab, cudaStream_t st, const void* gain, const void* pos_table = nullptr,
+                      int pos_offset = 0, float* part1 = nullptr);
 int launch_rmsnorm(int dtype, const float* x, const void* g, void* y, int rows, int hidden, float eps, int row_step,
                    int row_off, cudaStream_t st);
 int launch_rope_append(int dtype, const void* qkv, void* q_out, void* kc, void* vc, const int32_t* tok_slot,

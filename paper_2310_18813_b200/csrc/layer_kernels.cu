@@ -59,36 +59,53 @@ __global__ void __launch_bounds__(256) embed_norm_kernel(const __nv_bfloat16* __
                                                          const int32_t* __restrict__ pos, float* __restrict__ h,
                                                          __nv_bfloat16* __restrict__ xb, float* __restrict__ part,
                                                          int hidden, int vocab,
-                                                         const __nv_bfloat16* __restrict__ gain) {
+                                                         const __nv_bfloat16* __restrict__ gain,
+                                                         const __nv_bfloat16* __restrict__ pos_table, int pos_offset,
+                                                         float* __restrict__ part1) {
   griddep_wait();
   griddep_launch();
   const int t = blockIdx.x;
   const int id = ids[t];
   const bool pad = (pos != nullptr && pos[t] < 0) || id < 0 || id >= vocab;
   const __nv_bfloat16* row = table + (size_t)(pad ? 0 : id) * hidden;
-  float ss = 0.f;
+  // OPT: learned absolute positions (row p + offset); part1: the row's sum (fused LayerNorm consumers)
+  const __nv_bfloat16* prow = (pos_table && !pad) ? pos_table + (size_t)(pos[t] + pos_offset) * hidden : nullptr;
+  float ss = 0.f, s1 = 0.f;
   for (int i = threadIdx.x; i < hidden; i += blockDim.x) {
     float v = pad ? 0.f : __bfloat162float(row[i]);
+    if (prow) v += __bfloat162float(prow[i]);
     h[(size_t)t * hidden + i] = v;
     xb[(size_t)t * hidden + i] = __float2bfloat16_rn(gain ? v * __bfloat162float(gain[i]) : v);
     ss += v * v;
+    s1 += v;
   }
-  __shared__ float red[8];
+  __shared__ float red[8], red1[8];
   ss = warp_sum(ss);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = ss;
+  s1 = warp_sum(s1);
+  if ((threadIdx.x & 31) == 0) {
+    red[threadIdx.x >> 5] = ss;
+    red1[threadIdx.x >> 5] = s1;
+  }
   __syncthreads();
   if (threadIdx.x == 0) {
-    float tot = 0.f;
-    for (int w = 0; w < 8; ++w) tot += red[w];
+    float tot = 0.f, tot1 = 0.f;
+    for (int w = 0; w < 8; ++w) {
+      tot += red[w];
+      tot1 += red1[w];
+    }
     part[t] = tot;
+    if (part1) part1[t] = tot1;
   }
 }
 
 int launch_embed_norm(const void* table, const int32_t* ids, const int32_t* pos, float* h, void* xb, float* part,
-                      int n_tok, int hidden, int vocab, cudaStream_t st, const void* gain) {
+                      int n_tok, int hidden, int vocab, cudaStream_t st, const void* gain, const void* pos_table,
+                      int pos_offset, float* part1) {
   if (n_tok <= 0) return 0;
+  if (pos_table && !pos) return SB_EINVAL;
   return launch_k(embed_norm_kernel, dim3(n_tok), dim3(256), 0, st, (const __nv_bfloat16*)table, ids, pos, h,
-                  (__nv_bfloat16*)xb, part, hidden, vocab, (const __nv_bfloat16*)gain);
+                  (__nv_bfloat16*)xb, part, hidden, vocab, (const __nv_bfloat16*)gain,
+                  (const __nv_bfloat16*)pos_table, pos_offset, part1);
 }
 
 // ---------------------------------------------------------------- RMSNorm

@@ -270,7 +270,29 @@ class Decoder:
                 setattr(s, k, C.cast(self._arrays[k], C.POINTER(C.c_void_p)))
             s.pos_offset, s.pos_embed = cfg.pos_offset, self.pos_embed.data_ptr()
             s.final_norm_b = self.final_norm_b.data_ptr()
+            if self.sb_dtype == N.SB_BF16 and self.device.type == "cuda":
+                self._build_ln_fusion(s)
         self.struct = s
+
+    def _build_ln_fusion(self, s) -> None:
+        """OPT bf16: LayerNorm fused into its consumer GEMMs (csrc/forward.cu forward_opt): for weight W
+        behind LayerNorm (gamma, beta), c1 = W gamma and c2 = W beta (fp32, from the bf16 weights the
+        kernels use), so W . LN(x) = rstd * W . (x * gamma) - mean * rstd * c1 + c2."""
+        L = self.cfg.n_layers
+
+        def wv(w, v):
+            return (w.float() @ v.float()).contiguous()
+
+        self._ln = {"qkv_c1": [wv(l["w_qkv"], l["attn_norm"]) for l in self.layers],
+                    "qkv_c2": [wv(l["w_qkv"], l["attn_norm_b"]) for l in self.layers],
+                    "fc1_c1": [wv(l["w_gu"], l["mlp_norm"]) for l in self.layers],
+                    "fc1_c2": [wv(l["w_gu"], l["mlp_norm_b"]) for l in self.layers],
+                    "lm_c1": wv(self.lm_head, self.final_norm), "lm_c2": wv(self.lm_head, self.final_norm_b)}
+        for k in ("qkv_c1", "qkv_c2", "fc1_c1", "fc1_c2"):
+            a = (C.c_void_p * L)(*[t.data_ptr() for t in self._ln[k]])
+            self._arrays["ln_" + k] = a
+            setattr(s, "ln_" + k, C.cast(a, C.POINTER(C.c_void_p)))
+        s.ln_lm_c1, s.ln_lm_c2 = self._ln["lm_c1"].data_ptr(), self._ln["lm_c2"].data_ptr()
 
     def gemm_shapes(self) -> dict:
         """(N, K, weight tensor) of the GEMMs one forward runs (layer 0 stands for all)."""
