@@ -54,7 +54,7 @@ __device__ __forceinline__ void cta_trace_write(unsigned long long* buf, int id,
   o[4] = t[2];
   o[5] = t[3];
   o[6] = now;
-  o[7] = 0;
+  o[7] = kind == 1 ? t[4] : 0;
 }
 
 // Launch helper: cudaLaunchKernelEx with the PDL attribute (and optional cluster).

@@ -95,7 +95,9 @@ __host__ __device__ inline uint32_t tc_res_offset(uint32_t ring_bytes, uint32_t 
   return ((ring_bytes > scratch_bytes ? ring_bytes : scratch_bytes) + 127) & ~127u;
 }
 
-__device__ __forceinline__ float silu_f(float g) { return g / (1.f + __expf(-g)); }
+// (approximate division: the IEEE one costs a slow-path check + convergence barrier per element in the
+// row epilogue; the product is rounded to bf16)
+__device__ __forceinline__ float silu_f(float g) { return __fdividef(g, 1.f + __expf(-g)); }
 
 // Epilogue stores are streaming (st.global.cs): with the weight stream saturating HBM, default
 // write-back stores took ~2 us per 16-token chunk (measured: scripts/epi_micro.py, 2.40 -> 0.90 us at
@@ -159,10 +161,36 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
 // (Measured alternatives, slower in the forward: per-element stores -- one 2-4 byte store per row and
 // token, ~2 us per 16 tokens under the weight stream; bulk (TMA engine) copies of rows formatted in
 // shared memory -- 3.15 vs 3.01 ms verify at b=8, k=3.)
+// Per-row constants of the row epilogue (lane l: rows n..n+3), loaded once per tile instead of once
+// per token: a load after the previous token's stores could not be hoisted above them.
+struct EmitRow {
+  float4 c1, c2, bias, gain;
+};
+__device__ __forceinline__ float4 bf16x4_to_f4(uint2 v) {
+  return make_float4(__bfloat162float(__ushort_as_bfloat16((unsigned short)(v.x & 0xffff))),
+                     __bfloat162float(__ushort_as_bfloat16((unsigned short)(v.x >> 16))),
+                     __bfloat162float(__ushort_as_bfloat16((unsigned short)(v.y & 0xffff))),
+                     __bfloat162float(__ushort_as_bfloat16((unsigned short)(v.y >> 16))));
+}
+__device__ __forceinline__ EmitRow load_emit_row(const TcParams& p, int n0a, int lane) {
+  const int n = n0a + 4 * lane;
+  EmitRow r;
+  r.c1 = r.c2 = r.bias = make_float4(0.f, 0.f, 0.f, 0.f);
+  r.gain = make_float4(1.f, 1.f, 1.f, 1.f);
+  if (n < p.N) {
+    if (p.ln_c1) {
+      r.c1 = *reinterpret_cast<const float4*>(p.ln_c1 + n);
+      r.c2 = *reinterpret_cast<const float4*>(p.ln_c2 + n);
+    }
+    if (p.bias) r.bias = bf16x4_to_f4(*reinterpret_cast<const uint2*>(p.bias + n));
+    if (p.out_gain) r.gain = bf16x4_to_f4(*reinterpret_cast<const uint2*>(p.out_gain + n));
+  }
+  return r;
+}
 template <int E_>
-__device__ __forceinline__ void tc_emit_row(const TcParams& p, int lane, int j, int jr, int acc, int tn, int m0,
-                                            int n0a, int tile_a, float (&x)[4], float sc, uint64_t* res_bar,
-                                            const float* rb, bool has_pre = false,
+__device__ __forceinline__ void tc_emit_row(const TcParams& p, const EmitRow& er, int lane, int j, int jr, int acc,
+                                            int tn, int m0, int n0a, int tile_a, float (&x)[4], float sc,
+                                            uint64_t* res_bar, const float* rb, bool has_pre = false,
                                             float4 pre = make_float4(0.f, 0.f, 0.f, 0.f), float musc = 0.f) {
   const int m = m0 + j;
   if (m >= p.M) return;  // (warp-uniform) padding token
@@ -171,20 +199,17 @@ __device__ __forceinline__ void tc_emit_row(const TcParams& p, int lane, int j, 
   const size_t o = (size_t)m * p.N + n;
 #pragma unroll
   for (int i = 0; i < 4; ++i) x[i] *= sc;
-  if (p.ln_c1 && nv) {  // fused LayerNorm: - mean * rstd * (W gamma) + W beta
-    const float4 c1 = *reinterpret_cast<const float4*>(p.ln_c1 + n);
-    const float4 c2 = *reinterpret_cast<const float4*>(p.ln_c2 + n);
-    x[0] += c2.x - musc * c1.x;
-    x[1] += c2.y - musc * c1.y;
-    x[2] += c2.z - musc * c1.z;
-    x[3] += c2.w - musc * c1.w;
+  if (p.ln_c1) {  // fused LayerNorm: - mean * rstd * (W gamma) + W beta
+    x[0] += er.c2.x - musc * er.c1.x;
+    x[1] += er.c2.y - musc * er.c1.y;
+    x[2] += er.c2.z - musc * er.c1.z;
+    x[3] += er.c2.w - musc * er.c1.w;
   }
-  if (p.bias && nv) {
-    const uint2 bb = *reinterpret_cast<const uint2*>(p.bias + n);
-    x[0] += __bfloat162float(__ushort_as_bfloat16((unsigned short)(bb.x & 0xffff)));
-    x[1] += __bfloat162float(__ushort_as_bfloat16((unsigned short)(bb.x >> 16)));
-    x[2] += __bfloat162float(__ushort_as_bfloat16((unsigned short)(bb.y & 0xffff)));
-    x[3] += __bfloat162float(__ushort_as_bfloat16((unsigned short)(bb.y >> 16)));
+  if (p.bias) {
+    x[0] += er.bias.x;
+    x[1] += er.bias.y;
+    x[2] += er.bias.z;
+    x[3] += er.bias.w;
   }
   if (E_ != EPI_RESID_ADD && p.relu)
 #pragma unroll
@@ -221,14 +246,7 @@ __device__ __forceinline__ void tc_emit_row(const TcParams& p, int lane, int j, 
     const float a0 = pr.x + x[0], a1 = pr.y + x[1], a2 = pr.z + x[2], a3 = pr.w + x[3];
     if (nv) __stcs(reinterpret_cast<float4*>((float*)p.y + o), make_float4(a0, a1, a2, a3));
     if (p.out_xb && nv) {
-      float g[4] = {1.f, 1.f, 1.f, 1.f};
-      if (p.out_gain) {
-        const uint2 gg = *reinterpret_cast<const uint2*>(p.out_gain + n);
-        g[0] = __bfloat162float(__ushort_as_bfloat16((unsigned short)(gg.x & 0xffff)));
-        g[1] = __bfloat162float(__ushort_as_bfloat16((unsigned short)(gg.x >> 16)));
-        g[2] = __bfloat162float(__ushort_as_bfloat16((unsigned short)(gg.y & 0xffff)));
-        g[3] = __bfloat162float(__ushort_as_bfloat16((unsigned short)(gg.y >> 16)));
-      }
+      const float g[4] = {er.gain.x, er.gain.y, er.gain.z, er.gain.w};
       __stcs(reinterpret_cast<uint2*>(p.out_xb + o), make_uint2(pack_bf16x2(a0 * g[0], a1 * g[1]), pack_bf16x2(a2 * g[2], a3 * g[3])));
     }
     if (p.out_part) {
@@ -250,10 +268,11 @@ __host__ __device__ __forceinline__ int split_rows_max(int splits) { return 2 * 
 // grid = (n_tiles_n * splits, m_tiles), cluster = (splits, 1, 1): the `splits`
 // CTAs of a cluster share one 128 x tn output tile and split its K range.
 template <int E_, int V_>
-__global__ void __launch_bounds__(TC_THREADS, 1)
+__global__ void __launch_bounds__(TC_THREADS, 2)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap map_w, const __grid_constant__ CUtensorMap map_x, TcParams p) {
   extern __shared__ uint8_t smem_raw[];
-  __shared__ unsigned long long tr_t[4];
+  __shared__ unsigned long long tr_t[5];
+  if (p.trace && threadIdx.x == 0) tr_t[4] = 0;
   if (p.trace && threadIdx.x == 0) tr_t[0] = gtime();
   // 1024-aligned base by pointer arithmetic on smem_raw (keeps the shared address space visible to the
   // compiler: STS / LDS instead of generic ST / LD for the epilogue staging)
@@ -486,6 +505,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
         const int ew = warp - 2;
         int ci = 0;
         for (int acc = 0; acc < wt; ++acc) {
+          const EmitRow er = load_emit_row(p, n0 + acc * TC_BM, lane);
           for (int j0 = 0; j0 < tn; j0 += TC_EPI_CH, ++ci) {
             float* sb = red + (ci & 1) * TC_EPI_CH * TC_BM;
             const int cn = min(TC_EPI_CH, tn - j0);  // 16 or 32 (tn % 16 == 0)
@@ -501,18 +521,34 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 for (int j = 0; j < 16; ++j) sb[(16 + j) * TC_BM + row] = __uint_as_float(r1[j]);
             }
             asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (p.trace && et == 0 && ci == 0) tr_t[4] = gtime();
+            if (p.dbg & 2) continue;  // experiment: TMEM -> shared staging only, no emit
             // EPI_RESID_ADD without the smem prefetch (large tiles): the warp's residual rows of the
             // chunk are loaded together (one round trip per chunk: prefill o / down epilogue 53 -> 27 us)
+            // All of the warp's staged rows (and residual rows) are loaded before its first store:
+            // the token emits are then independent chains the scheduler interleaves.
             constexpr bool RL = E_ == EPI_RESID_ADD;
-            float4 res8[TC_EPI_CH / 4];
-            if (RL && !p.res_bytes) {
-              const int n = n0 + acc * TC_BM + 4 * lane;
+            const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+            float4 a8[TC_EPI_CH / 4], res8[TC_EPI_CH / 4];
+            if (!RL)  // (the residual epilogue keeps its staged reads per token: register budget at 2 CTAs/SM)
 #pragma unroll
               for (int i = 0; i < TC_EPI_CH / 4; ++i) {
-                const int m = m0 + j0 + ew + 4 * i;
-                res8[i] = (ew + 4 * i < cn && m < p.M && n < p.N)
-                              ? __ldcg(reinterpret_cast<const float4*>((const float*)p.y + (size_t)m * p.N + n))
-                              : make_float4(0.f, 0.f, 0.f, 0.f);
+                const int jl = ew + 4 * i;
+                a8[i] = jl < cn ? *reinterpret_cast<const float4*>(sb + jl * TC_BM + 4 * lane) : z4;
+              }
+            if (RL) {
+              const int n = n0 + acc * TC_BM + 4 * lane;
+              if (p.res_bytes) mbar_wait(res_bar, 0);
+#pragma unroll
+              for (int i = 0; i < TC_EPI_CH / 4; ++i) {
+                const int jl = ew + 4 * i;
+                const int m = m0 + j0 + jl;
+                if (p.res_bytes)
+                  res8[i] = jl < cn ? *reinterpret_cast<const float4*>(res_rows + ((size_t)acc * tn + j0 + jl) * TC_BM + 4 * lane) : z4;
+                else
+                  res8[i] = (jl < cn && m < p.M && n < p.N)
+                                ? __ldcg(reinterpret_cast<const float4*>((const float*)p.y + (size_t)m * p.N + n))
+                                : z4;
               }
             }
 #pragma unroll
@@ -520,10 +556,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               const int jl = ew + 4 * i;
               if (jl >= cn) break;
               const int j = j0 + jl;
-              const float4 a = *reinterpret_cast<const float4*>(sb + jl * TC_BM + 4 * lane);
+              const float4 a = RL ? *reinterpret_cast<const float4*>(sb + jl * TC_BM + 4 * lane) : a8[i];
               float x[4] = {a.x, a.y, a.z, a.w};
-              tc_emit_row<E_>(p, lane, j, j, acc, tn, m0, n0 + acc * TC_BM, tile_n * wt + acc, x,
-                              scale ? inv_s[j] : 1.f, res_bar, res_rows, RL && !p.res_bytes, res8[i],
+              tc_emit_row<E_>(p, er, lane, j, j, acc, tn, m0, n0 + acc * TC_BM, tile_n * wt + acc, x,
+                              scale ? inv_s[j] : 1.f, res_bar, res_rows, RL, RL ? res8[i] : z4,
                               p.ln_s1 ? musc[j] : 0.f);
             }
           }
@@ -623,9 +659,11 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
       const uint32_t red_addr = smem_u32(red);
       const bool scale = p.ns_part != nullptr;
       const int jlo = split * tn / p.splits, jhi = (split + 1) * tn / p.splits;
+      const EmitRow er = load_emit_row(p, n0, lane);
+      constexpr bool RL = E_ == EPI_RESID_ADD;
       for (int jb = jlo + ew; jb < jhi; jb += 16) {  // groups of 4 tokens per warp
         float4 res4[4];  // residual rows of the group (no smem prefetch: large tiles), loads in flight together
-        if (E_ == EPI_RESID_ADD && !p.res_bytes) {
+        if (RL && !p.res_bytes) {
           const int n = n0 + 4 * lane;
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
@@ -656,8 +694,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               x[2] += t2[i][1].z;
               x[3] += t2[i][1].w;
             }
-            tc_emit_row<E_>(p, lane, j, j - jlo, 0, tn, m0, n0, tile_n, x, scale ? inv_s[j] : 1.f, res_bar,
-                            res_rows, E_ == EPI_RESID_ADD && !p.res_bytes, res4[i], p.ln_s1 ? musc[j] : 0.f);
+            tc_emit_row<E_>(p, er, lane, j, j - jlo, 0, tn, m0, n0, tile_n, x, scale ? inv_s[j] : 1.f, res_bar,
+                            res_rows, RL && !p.res_bytes, res4[i], p.ln_s1 ? musc[j] : 0.f);
           }
         } else {
 #pragma unroll
@@ -677,8 +715,8 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
               x[2] += t[q].z;
               x[3] += t[q].w;
             }
-          tc_emit_row<E_>(p, lane, j, j - jlo, 0, tn, m0, n0, tile_n, x, scale ? inv_s[j] : 1.f, res_bar, res_rows,
-                          E_ == EPI_RESID_ADD && !p.res_bytes, res4[i], p.ln_s1 ? musc[j] : 0.f);
+          tc_emit_row<E_>(p, er, lane, j, j - jlo, 0, tn, m0, n0, tile_n, x, scale ? inv_s[j] : 1.f, res_bar, res_rows,
+                          RL && !p.res_bytes, res4[i], p.ln_s1 ? musc[j] : 0.f);
         }
         }
       }
