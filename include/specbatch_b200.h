@@ -337,7 +337,8 @@ int sb_kv_compact(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* 
  * GEMM entry used by tests/benches: Y[M,N] = X[M,K] W[N,K]^T, fp32 accumulate.
  * epi: 0 store dtype, 1 store fp32, 2 fp32 residual +=, 3 silu(gate)*up on
  * interleaved (gate, up) rows -> [M, N/2].  backend: 0 auto, 1 SIMT (FFMA),
- * 2 tcgen05 (bf16 only; SB_EUNSUPPORTED otherwise).  The workspace must be
+ * 2 tcgen05 (bf16 only; SB_EUNSUPPORTED otherwise), 3 the small-token mma.sync kernel of the draft step
+ * (bf16, M <= 16, K = 256 x {1,2,3,4,6,8,12}, epi 0/2/3; SB_EUNSUPPORTED otherwise).  The workspace must be
  * zero-initialised once (stream-K tile counters self-reset).
  */
 int sb_gemm(int32_t dtype, const void* x, const void* w, void* y, int32_t M, int32_t N, int32_t K,
@@ -367,6 +368,9 @@ int sb_debug_cta_trace(void* buf);
 int sb_debug_gemm_pdl(int32_t pre_max, int32_t launch_late, int32_t flags);
 /* RMSNorm fused into the GEMM epilogues on the bf16 path (default on); 0 = separate norm kernels. */
 int sb_set_fuse_norm(int32_t enabled);
+/* Decode-sized GEMMs of small models (<= 16 tokens, <= 8M weights: the draft step) on the mma.sync small-token
+   kernel (default 1); 0 = every bf16 GEMM on the tcgen05 kernel (A/B, tests). */
+int sb_set_small_gemm(int32_t enabled);
 /* Diagnostics: eager forward with an event after every kernel; per-stage summed ms as "tag=ms;..." in buf. */
 int sb_profile_forward(const sb_decoder_t* m, const sb_kvcache_t* kv, const int32_t* tok_ids,
                        const int32_t* tok_slot, const int32_t* tok_pos, int32_t n_seq, int32_t q_len,

@@ -26,7 +26,7 @@ LOGITS_ALL, LOGITS_LAST, LOGITS_NONE = 0, 1, 2
 ACCEPT_GREEDY, ACCEPT_STOCHASTIC, ACCEPT_INJECTED = 0, 1, 2
 SELECT_ARGMAX, SELECT_SAMPLE = 0, 1
 EPI_STORE, EPI_STORE_F32, EPI_RESID_ADD, EPI_SILU_MUL = 0, 1, 2, 3
-GEMM_AUTO, GEMM_SIMT, GEMM_TC = 0, 1, 2
+GEMM_AUTO, GEMM_SIMT, GEMM_TC, GEMM_SMALL = 0, 1, 2, 3
 
 _P = C.c_void_p
 _I = C.c_int32
@@ -79,6 +79,7 @@ _SIGS = {
     "sb_set_gemm_backend": (C.c_int, [_I]),
     "sb_set_pdl": (C.c_int, [_I]),
     "sb_set_fuse_norm": (C.c_int, [_I]),
+    "sb_set_small_gemm": (C.c_int, [_I]),
     "sb_debug_skip": (C.c_int, [_I]),
     "sb_debug_cta_trace": (C.c_int, [_P]),
     "sb_debug_gemm_pdl": (C.c_int, [_I, _I, _I]),

@@ -253,6 +253,10 @@ static int forward_fused_norm(const sb_decoder_t* m, const sb_kvcache_t* kv, con
   const float inv_h = 1.0f / (float)H;
   // gain of the consumer of the residual after layer l's down_proj (next layer's attn_norm, or final_norm)
   auto next_gain = [&](int l) -> const void* { return l + 1 < m->n_layers ? m->attn_norm[l + 1] : m->final_norm; };
+  // decode-sized GEMMs of a small model (the draft step): the mma.sync small-token kernel; else tcgen05
+  auto small = [&](const GemmArgs& a) { return (size_t)a.N * a.K <= ((size_t)8 << 20) && gemm_small_ok(a); };
+  auto run = [&](const GemmArgs& a) { return small(a) ? gemm_small(a, st) : gemm_tc(a, st); };
+  auto parts = [&](const GemmArgs& a) { return small(a) ? gemm_small_norm_partials(a) : gemm_tc_norm_partials(a); };
   SB_TRY(launch_embed_norm(m->embed, ids, pos, w.resid, w.xb, w.npart, T, H, vocab_full(m), st, next_gain(-1)));
   prof_mark("embed", st);
   int P = 1;
@@ -265,7 +269,7 @@ static int forward_fused_norm(const sb_decoder_t* m, const sb_kvcache_t* kv, con
     g.ns_stride = T;
     g.ns_eps = m->rms_eps;
     g.ns_inv_h = inv_h;
-    if (!(g_skip & 2)) SB_TRY(gemm_tc(g, st));
+    if (!(g_skip & 2)) SB_TRY(run(g));
     prof_mark("qkv", st);
     int rc_fa = (g_skip & 1) ? 0 : g_attn_impl == 0 ? launch_attention_tc(w.qkv, kc, vc, w.attn, slot, pos, m->rope_cos, m->rope_sin,
                                                         n_seq, q_len, nq, nkv, hd, kv->ctx_max, m->max_pos, st, &w.att_split,
@@ -299,8 +303,8 @@ static int forward_fused_norm(const sb_decoder_t* m, const sb_kvcache_t* kv, con
       o.out_part = w.npart;
       o.out_xb = w.xb;
       o.out_gain = m->mlp_norm[l];
-      if (!(g_skip & 4)) SB_TRY(gemm_tc(o, st));
-      P = gemm_tc_norm_partials(o);
+      if (!(g_skip & 4)) SB_TRY(run(o));
+      P = parts(o);
       prof_mark("o", st);
     }
     GemmArgs gu{SB_BF16, w.xb, m->w_gu[l], w.act, T, 2 * m->ffn, H, H, EPI_SILU_MUL, w.gemm_ws, w.gemm_ws_bytes};
@@ -309,7 +313,7 @@ static int forward_fused_norm(const sb_decoder_t* m, const sb_kvcache_t* kv, con
     gu.ns_stride = T;
     gu.ns_eps = m->rms_eps;
     gu.ns_inv_h = inv_h;
-    if (!(g_skip & 8)) SB_TRY(gemm_tc(gu, st));
+    if (!(g_skip & 8)) SB_TRY(run(gu));
     prof_mark("gu", st);
     if (m->tp) {  // row-parallel down_proj
       GemmArgs dn{SB_BF16, w.act, m->w_down[l], w.tp_part, T, H, m->ffn, m->ffn, EPI_STORE, w.gemm_ws,
@@ -324,8 +328,8 @@ static int forward_fused_norm(const sb_decoder_t* m, const sb_kvcache_t* kv, con
       dn.out_part = w.npart;
       dn.out_xb = w.xb;
       dn.out_gain = next_gain(l);
-      if (!(g_skip & 16)) SB_TRY(gemm_tc(dn, st));
-      P = gemm_tc_norm_partials(dn);
+      if (!(g_skip & 16)) SB_TRY(run(dn));
+      P = parts(dn);
       prof_mark("down", st);
     }
   }
@@ -752,6 +756,11 @@ int sb_debug_gemm_pdl(int32_t pre_max, int32_t launch_late, int32_t flags) {
 int sb_debug_cta_trace(void* buf) {
   sb::g_cta_trace = (unsigned long long*)buf;
   sb::g_cta_trace_seq = 0;
+  return 0;
+}
+
+int sb_set_small_gemm(int32_t enabled) {
+  g_small_gemm = enabled ? 1 : 0;
   return 0;
 }
 

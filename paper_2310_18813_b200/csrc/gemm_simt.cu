@@ -110,6 +110,7 @@ int gemm(const GemmArgs& a, int backend, cudaStream_t st) {
   if (backend == GEMM_AUTO) backend = g_backend_override;
   if (backend == GEMM_SIMT) return gemm_simt(a, st);
   if (backend == GEMM_TC) return gemm_tc(a, st);
+  if (backend == GEMM_SMALL) return gemm_small(a, st);  // (tests: the draft-step kernel on its own)
   if (a.dtype == SB_BF16 && gemm_tc_supported(a)) return gemm_tc(a, st);
   return gemm_simt(a, st);
 }

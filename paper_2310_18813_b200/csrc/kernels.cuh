@@ -17,7 +17,7 @@ enum GemmEpi : int {
   EPI_ARGMAX = 4,     // optional fp32 y [M, N] + per-128-row-tile argmax partials (aux_val/aux_idx [N/128][M])
 };
 
-enum GemmBackend : int { GEMM_AUTO = 0, GEMM_SIMT = 1, GEMM_TC = 2 };
+enum GemmBackend : int { GEMM_AUTO = 0, GEMM_SIMT = 1, GEMM_TC = 2, GEMM_SMALL = 3 };
 
 struct GemmArgs {
   int dtype;
@@ -60,6 +60,11 @@ int gemm_tc(const GemmArgs& a, cudaStream_t st);  // tcgen05 (bf16 only); SB_EUN
 bool gemm_tc_supported(const GemmArgs& a);
 int gemm_tc_init();
 int gemm_tc_norm_partials(const GemmArgs& a);  // rows of out_part this GEMM writes
+// small-token GEMM (gemm_small.cu: T <= 16, mma.sync, 16-32 weight rows per CTA); SB_EUNSUPPORTED outside its envelope
+extern int g_small_gemm;  // sb_set_small_gemm
+bool gemm_small_ok(const GemmArgs& a);
+int gemm_small(const GemmArgs& a, cudaStream_t st);
+int gemm_small_norm_partials(const GemmArgs& a);  // rows of out_part it writes (one per 16 weight rows)
 int gemm_tc_tune(int cps, int stages, int splits);
 int gemm_tc_autotune(const void* x, const void* w, float* y, int M, int N, int K, cudaStream_t st, int* cps_out,
                      int* splits_out, float* us_out);

@@ -380,3 +380,35 @@ def test_gemm_tuned_token_tile(cuda_dev, M, N_, K, cps, splits, wt, tn):
         lib.sb_gemm_autotune_clear()
     err = (y - ref).abs().max().item()
     assert err <= 1e-4 * ref.abs().max().item() + 1e-5, err
+
+
+@pytest.mark.parametrize("M,N_,K", [(1, 2304, 768), (8, 768, 3072), (13, 6144, 768), (16, 512, 512), (5, 768, 768),
+                                   (9, 6144, 768)])
+def test_gemm_small_token_kernel(cuda_dev, M, N_, K):
+    """The draft step's small-token mma.sync GEMM (backend 3) against the fp32 product: bf16 store,
+    residual add and silu(gate)*up, both token count classes (1 or 2 n-tiles of 8 tokens), 16- and
+    32-row CTAs (gate/up at N=6144)."""
+    g = torch.Generator(device=cuda_dev).manual_seed(M * 31 + N_ + K)
+    x = (torch.randn(M, K, generator=g, device=cuda_dev) * 0.5).to(torch.bfloat16)
+    w = (torch.randn(N_, K, generator=g, device=cuda_dev) * 0.02).to(torch.bfloat16)
+    ref = x.float() @ w.float().T
+    base = torch.randn(M, N_, generator=g, device=cuda_dev)
+    y = base.clone()
+    N.call("sb_gemm", N.SB_BF16, x.data_ptr(), w.data_ptr(), y.data_ptr(), M, N_, K, N.EPI_RESID_ADD, N.GEMM_SMALL,
+           None, 0, _st())
+    torch.cuda.synchronize()
+    assert (y - (base + ref)).abs().max().item() <= 1e-4 * ref.abs().max().item() + 1e-5
+    yb = torch.zeros(M, N_, device=cuda_dev, dtype=torch.bfloat16)
+    N.call("sb_gemm", N.SB_BF16, x.data_ptr(), w.data_ptr(), yb.data_ptr(), M, N_, K, N.EPI_STORE, N.GEMM_SMALL,
+           None, 0, _st())
+    torch.cuda.synchronize()
+    assert (yb.float() - ref).abs().max().item() <= 1e-2 * ref.abs().max().item()
+    ya = torch.zeros(M, N_ // 2, device=cuda_dev, dtype=torch.bfloat16)
+    N.call("sb_gemm", N.SB_BF16, x.data_ptr(), w.data_ptr(), ya.data_ptr(), M, N_, K, N.EPI_SILU_MUL, N.GEMM_SMALL,
+           None, 0, _st())
+    torch.cuda.synchronize()
+    want = torch.nn.functional.silu(ref[:, 0::2]) * ref[:, 1::2]
+    assert (ya.float() - want).abs().max().item() <= 1e-2 * want.abs().max().item() + 1e-4
+    # outside the envelope: refused, not silently wrong
+    assert N.load().sb_gemm(N.SB_BF16, x.data_ptr(), w.data_ptr(), y.data_ptr(), M, N_, K, N.EPI_STORE_F32,
+                            N.GEMM_SMALL, None, 0, _st()) == N.SB_EUNSUPPORTED
