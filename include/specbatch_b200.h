@@ -152,6 +152,10 @@ typedef struct sb_decoder {
   const float* const* ln_fc1_c2;
   const float* ln_lm_c1;          /* [vocab] */
   const float* ln_lm_c2;
+  /* 1 = a draft model: its decode-sized bf16 GEMMs (<= 16 tokens, <= 8M weights) may take the small-token
+     kernel (sb_set_small_gemm).  0 (targets) keeps one GEMM kernel family across token counts, so a greedy
+     verify of k+1 tokens computes what k+1 single-token decodes would. */
+  int32_t role;
 } sb_decoder_t;
 
 /* KV cache: k/v base pointers of layout [n_layers][slots][n_kv_heads][ctx_max][head_dim]. */

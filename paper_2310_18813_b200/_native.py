@@ -56,7 +56,7 @@ class SbDecoder(C.Structure):
         ("arch", _I), ("pos_offset", _I), ("pos_embed", _P), ("final_norm_b", _P), ("attn_norm_b", _PP),
         ("mlp_norm_b", _PP), ("b_qkv", _PP), ("b_o", _PP), ("b_fc1", _PP), ("b_fc2", _PP),
         ("ln_qkv_c1", _PP), ("ln_qkv_c2", _PP), ("ln_fc1_c1", _PP), ("ln_fc1_c2", _PP), ("ln_lm_c1", _P),
-        ("ln_lm_c2", _P),
+        ("ln_lm_c2", _P), ("role", _I),
     ]
 
 

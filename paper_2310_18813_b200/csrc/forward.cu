@@ -254,7 +254,7 @@ static int forward_fused_norm(const sb_decoder_t* m, const sb_kvcache_t* kv, con
   // gain of the consumer of the residual after layer l's down_proj (next layer's attn_norm, or final_norm)
   auto next_gain = [&](int l) -> const void* { return l + 1 < m->n_layers ? m->attn_norm[l + 1] : m->final_norm; };
   // decode-sized GEMMs of a small model (the draft step): the mma.sync small-token kernel; else tcgen05
-  auto small = [&](const GemmArgs& a) { return (size_t)a.N * a.K <= ((size_t)8 << 20) && gemm_small_ok(a); };
+  auto small = [&](const GemmArgs& a) { return m->role == 1 && (size_t)a.N * a.K <= ((size_t)8 << 20) && gemm_small_ok(a); };
   auto run = [&](const GemmArgs& a) { return small(a) ? gemm_small(a, st) : gemm_tc(a, st); };
   auto parts = [&](const GemmArgs& a) { return small(a) ? gemm_small_norm_partials(a) : gemm_tc_norm_partials(a); };
   SB_TRY(launch_embed_norm(m->embed, ids, pos, w.resid, w.xb, w.npart, T, H, vocab_full(m), st, next_gain(-1)));

@@ -73,6 +73,8 @@ class SpecEngine:
         N.load()
         N.init_device()
         self.target, self.draft = target, draft
+        if draft is not None and draft is not target:
+            draft.struct.role = 1  # decode-sized draft GEMMs on the small-token kernel (sb_decoder_t.role)
         self.mode = mode
         self.mode_id = _MODES[mode]
         self.acceptance = acceptance

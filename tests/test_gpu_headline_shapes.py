@@ -42,11 +42,17 @@ def _rel(got, want):
     return float(np.abs(got - want).max() / np.abs(want).max())
 
 
+@pytest.mark.parametrize("role", [0, 1])
 @pytest.mark.parametrize("dtype", ["fp32", "bf16"])
 @pytest.mark.parametrize("shape", list(SHAPES))
-def test_headline_shape_logits_match_oracle(cuda_dev, shape, dtype):
+def test_headline_shape_logits_match_oracle(cuda_dev, shape, dtype, role):
+    """role 1 (draft): the 68M model's windows of <= 16 tokens run on the small-token GEMM (gemm_small.cu),
+    its fused-RMSNorm partials feeding / fed by the tcgen05 GEMMs of the prefill and the lm_head."""
+    if role and (shape != "llama-68m" or dtype != "bf16"):
+        pytest.skip("the small-token GEMM serves bf16 draft models")
     cfg = SHAPES[shape]
     dec = Decoder(cfg, dtype=dtype, device=cuda_dev, seed=21, init="host", max_pos=MAXPOS)
+    dec.struct.role = role
     assert any((lay["attn_norm"].float() - 1).abs().max() > 0.05 for lay in dec.layers)
     big = cfg.hidden >= 8192
     ref = model_ref.LlamaRef(dec.masters, cfg.n_heads, cfg.n_kv_heads, cfg.rms_eps, max_pos=MAXPOS,
