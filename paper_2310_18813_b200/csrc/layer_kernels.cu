@@ -625,6 +625,11 @@ __global__ void __launch_bounds__(128) attention_tc_kernel(AttnArgs A) {
   }
 }
 
+// A decode grid of at most one CTA per SM reserves this much shared memory per CTA, so that no two of its
+// CTAs share an SM (launched early under PDL, beside the qkv GEMM's CTAs, they were otherwise packed three
+// to an SM: 96 CTAs on 32 SMs for the draft step).
+constexpr size_t kAttnSpreadBytes = 120 * 1024;
+static int g_attn_spread = -1;
 // Opt every ring variant in to its dynamic shared memory once (outside graph capture).
 int attention_tc_init() {
   static int rc = -1;
@@ -633,7 +638,7 @@ int attention_tc_init() {
 #define SB_ATTN_ATTR(H, S)                                                                                        \
   if (e == cudaSuccess)                                                                                           \
     e = cudaFuncSetAttribute(attention_tc_kernel<H, S, false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, \
-                             (int)TcAttnSmem<H, S>::bytes);                                                        \
+                             (int)(TcAttnSmem<H, S>::bytes > kAttnSpreadBytes ? TcAttnSmem<H, S>::bytes : kAttnSpreadBytes)); \
   if (e == cudaSuccess)                                                                                           \
     e = cudaFuncSetAttribute(attention_tc_kernel<H, S, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,  \
                              (int)TcAttnSmem<H, S>::bytes);                                                        \
@@ -691,8 +696,13 @@ static int launch_attn_grid(const AttnArgs& A0, int hd, int n_seq, int z, cudaSt
     cudaThreadExchangeStreamCaptureMode(&mode);
     if (rc) return rc;
   }
+  if (g_attn_spread < 0) {
+    const char* e = getenv("SB_ATTN_SPREAD");
+    g_attn_spread = e ? atoi(e) : 1;
+  }
+  const bool spread = g_attn_spread && ctas <= num_sms() && A.qr == nullptr && z == 1;
   auto go = [&](void (*kern)(AttnArgs), size_t bytes) {
-    cfg.dynamicSmemBytes = bytes;
+    cfg.dynamicSmemBytes = spread && bytes < kAttnSpreadBytes ? kAttnSpreadBytes : bytes;
     return cudaLaunchKernelEx(&cfg, kern, A);
   };
   const bool blk = A.qr != nullptr, spl = z > 1 && !blk;
