@@ -377,9 +377,9 @@ def run_trace(args):
     from paper_2310_18813_b200.cost_model import OptimalityParams, optimal_speculation_continuous, \
         save_calibration, save_step_samples
     from paper_2310_18813_b200.decoder import CONFIGS, Decoder
-    from paper_2310_18813_b200.policy import AdaptivePolicy, FixedPolicy, build_lut, save_lut
+    from paper_2310_18813_b200.policy import AdaptivePolicy, DensePolicy, FixedPolicy, build_lut, save_lut
     from paper_2310_18813_b200.presets import example_trace
-    from paper_2310_18813_b200.profiler import calibrate, table_lut
+    from paper_2310_18813_b200.profiler import calibrate, dense_tables, measure_cost_table, table_lut
     from paper_2310_18813_b200.serving import serve_continuous
     from paper_2310_18813_b200.simulator import ServerConfig, serve_wallclock
     from paper_2310_18813_b200.spec_engine import SpecEngine
@@ -416,6 +416,11 @@ def run_trace(args):
     save_lut(lut, out / "lut_measured.csv", seed=0, calibration="measured on this B200 (build_lut mode=measured)")
     lut_table, _cells = table_lut(verify_ms, draft_ms, trace, s_grid=K_GRID, profiled_sizes=sizes,
                                   sample_size=200, rng=np.random.default_rng([0, 2]), gen_len=NEW)
+    # dense tables: every live size 1..16 measured (the reference rule resolves 9..15 to min(s_8, s_16))
+    dense_sizes = range(1, 17)
+    vms_all, dms_all = measure_cost_table(eng, dense_sizes, k_grid=K_GRID, ctx=ctx, reps=10)
+    tab_formed, tab_cont, _ = dense_tables(vms_all, dms_all, trace, dense_sizes, s_grid=K_GRID, sample_size=200,
+                                           rng=np.random.default_rng([0, 3]), gen_len=NEW)
     delta_root = {str(b): round(optimal_speculation_continuous(OptimalityParams.from_model(model, fit, b), 1, 8,
                                                                tol=1e-6), 3) for b in sizes}
     ref = _ref_harness()
@@ -426,7 +431,11 @@ def run_trace(args):
                "draft_step_ms": {str(b): round(v, 4) for b, v in draft_ms.items()},
                "delta_root_s": delta_root,
                "lut_measured": {str(b): v for b, v in lut.entries.items()},
-               "lut_table_simulated": {str(b): v for b, v in lut_table.entries.items()}}
+               "lut_table_simulated": {str(b): v for b, v in lut_table.entries.items()},
+               "dense_formed_table": {str(b): v for b, v in tab_formed.items()},
+               "dense_continuous_table": {str(b): v for b, v in tab_cont.items()},
+               "verify_ms_dense": {f"{b},{s}": round(v, 4) for (b, s), v in sorted(vms_all.items())},
+               "draft_step_ms_dense": {str(b): round(v, 4) for b, v in dms_all.items()}}
     if ref is not None:
         rh, rsim, rpol, rcm = ref
         rmodel, rfit = rcm.load_calibration(out / "calibration.json")
@@ -462,7 +471,7 @@ def run_trace(args):
     # ---- wall-clock replay on the GPU engine, every policy, several arrival seeds
     phases = tuple((50.0, TrafficConfig(mean_interval=0.2 if i % 2 == 0 else 1.0, cv=1.0, count=1000))
                    for i in range(6))
-    policies = [AdaptivePolicy(lut)] + [FixedPolicy(k) for k in range(1, 9)]
+    policies = [AdaptivePolicy(lut), DensePolicy(tab_formed)] + [FixedPolicy(k) for k in range(1, 9)]
     t_cap = time.perf_counter()
     for bb in range(1, 17):  # capture every (b, k) iteration graph up front: no capture inside a replay
         for kk in range(0, 9):
@@ -479,17 +488,31 @@ def run_trace(args):
             rep = serve_wallclock(workload, ServerConfig(policy=pol, max_batch=16), eng, time_scale=args.trace_scale)
             lat[pol.label].append(rep.avg_latency / args.trace_scale)  # back to trace seconds
             batches[pol.label].append(float(np.mean([r.served_batch_size for r in rep.records])))
-    # continuous batching: retire / admit every iteration, k from the LUT per iteration;
-    # against the formed-batch best fixed k and fixed-3
-    fixed_mean = {k: float(np.mean(v)) for k, v in lat.items() if k.startswith("fixed")}
-    k_best = int(min(fixed_mean, key=fixed_mean.get).split("-")[1])
-    workload = gen_phased(PhaseSchedule(phases=phases), np.random.default_rng([0, 6]), gen_len=NEW)
-    cont = {}
-    for pol in [AdaptivePolicy(lut)] + [FixedPolicy(kk) for kk in sorted({3, k_best})]:
-        rep, extra = serve_continuous(workload, eng, pol, time_scale=args.trace_scale, max_batch=16)
-        cont[pol.label] = {"latency_s": round(rep.avg_latency / args.trace_scale, 4),
-                           "mean_live_batch": round(extra["mean_live_batch"], 2), "mean_k": round(extra["mean_k"], 2),
-                           "riding_prefill_rows": extra["ridden_rows"], "separate_prefill_rows": extra["prefill_rows"]}
+    # continuous batching: retire / admit every iteration, k re-chosen per iteration:
+    # the formed-batch LUT (reference lookup rule), the dense continuous table, and every fixed k
+    cont_pols = [AdaptivePolicy(lut), DensePolicy(tab_cont, "adaptive-cont")] + [FixedPolicy(kk) for kk in range(1, 9)]
+    cont = {pol.label: {"latency_s_per_seed": [], "mean_live_batch": [], "mean_k": [], "riding_prefill_rows": [],
+                        "separate_prefill_rows": []} for pol in cont_pols}
+    for seed in range(args.trace_seeds):
+        workload = gen_phased(PhaseSchedule(phases=phases), np.random.default_rng([seed, 6]), gen_len=NEW)
+        for pol in cont_pols:
+            rep, extra = serve_continuous(workload, eng, pol, time_scale=args.trace_scale, max_batch=16)
+            c = cont[pol.label]
+            c["latency_s_per_seed"].append(round(rep.avg_latency / args.trace_scale, 4))
+            c["mean_live_batch"].append(round(extra["mean_live_batch"], 2))
+            c["mean_k"].append(round(extra["mean_k"], 2))
+            c["riding_prefill_rows"].append(extra["ridden_rows"])
+            c["separate_prefill_rows"].append(extra["prefill_rows"])
+    for c in cont.values():
+        c["latency_s"] = round(float(np.mean(c["latency_s_per_seed"])), 4)
+    cfixed = {k: v["latency_s"] for k, v in cont.items() if k.startswith("fixed")}
+    cbest = min(cfixed, key=cfixed.get)
+    cont_summary = {"best_fixed": cbest,
+                    **{f"{a}_vs_best_fixed": round(cont[a]["latency_s"] / cfixed[cbest], 4)
+                       for a in ("adaptive", "adaptive-cont")},
+                    **{f"{a}_vs_best_fixed_per_seed": [round(x / y, 4) for x, y in zip(
+                        cont[a]["latency_s_per_seed"], cont[cbest]["latency_s_per_seed"])]
+                       for a in ("adaptive", "adaptive-cont")}}
     t_run = time.perf_counter() - t_run
     mean = {k: float(np.mean(v)) for k, v in lat.items()}
     fixed = {k: v for k, v in mean.items() if k.startswith("fixed")}
@@ -498,6 +521,8 @@ def run_trace(args):
     per_seed_ratio = [a / f for a, f in zip(lat[ad], lat[best])]
     per_seed_best = [min(fixed, key=lambda k: lat[k][i]) for i in range(args.trace_seeds)]
     per_seed_ratio_own_best = [lat[ad][i] / lat[per_seed_best[i]][i] for i in range(args.trace_seeds)]
+    dn = "adaptive-dense"
+    dense_ratio = [a / f for a, f in zip(lat[dn], lat[best])]
     line = {"metric": "mean request latency, phased Poisson trace (adaptive k)", "value": mean[ad], "unit": "s",
             "n_gpus": 1, "higher_is_better": False, "impl": "ours", "dtype": "bf16",
             "data": "synthetic (random-init weights, injected example_trace acceptance)",
@@ -513,6 +538,9 @@ def run_trace(args):
             "adaptive_vs_best_fixed_per_seed": [round(x, 4) for x in per_seed_ratio],
             "adaptive_vs_per_seed_best_fixed": [round(x, 4) for x in per_seed_ratio_own_best],
             "per_seed_best_fixed": per_seed_best,
+            "adaptive_dense_vs_best_fixed_latency": mean[dn] / fixed[best],
+            "adaptive_dense_vs_best_fixed_per_seed": [round(x, 4) for x in dense_ratio],
+            "continuous_summary": cont_summary,
             "wall_s": round(t_run, 1), "continuous_batching": cont, "graph_capture_s": round(t_cap, 1),
             "f1_closure": closure}
     (out / "result.json").write_text(json.dumps(line, indent=1) + "\n")
