@@ -132,3 +132,39 @@ def test_headline_shape_fp32_greedy_spec_matches_oracle(cuda_dev, shape, draft):
     live = eng.stats.accepted >= 0
     print(f"{shape} + {draft}: accepted {int(eng.stats.accepted[live].sum())} of {k * int(live.sum())} drafts, "
           f"{ties} tie divergences")
+
+
+@pytest.mark.parametrize("b", [1, 8, 16])
+def test_draft_greedy_token_matches_oracle(cuda_dev, b):
+    """The draft step's greedy token (role 1, bf16 LLaMA-68M with non-unit gains: small-token layer
+    GEMMs, tcgen05 lm_head with the argmax fused, argmax_partials) equals the bf16-emulating fp64
+    oracle's argmax wherever the oracle's top-2 gap exceeds bf16 noise."""
+    cfg = CONFIGS["llama-68m"]
+    dec = Decoder(cfg, dtype="bf16", device=cuda_dev, seed=31, init="host", max_pos=MAXPOS)
+    dec.struct.role = 1
+    ref = model_ref.LlamaRef(dec.masters, cfg.n_heads, cfg.n_kv_heads, cfg.rms_eps, max_pos=MAXPOS,
+                             theta=cfg.rope_theta, dtype=torch.float64, bf16_emulation=True)
+    dec.masters = None
+    rng = np.random.default_rng(11 + b)
+    P = 20
+    kv = dec.new_kv(b, MAXPOS)
+    ws = torch.zeros(dec.workspace_bytes(b * P), device=cuda_dev, dtype=torch.uint8)
+    slots = torch.arange(b, dtype=torch.int32, device=cuda_dev)
+    ids = rng.integers(0, cfg.vocab, size=(b, P)).astype(np.int32)
+    dec.forward(kv, torch.as_tensor(ids[:, :-1].reshape(-1), device=cuda_dev), slots,
+                torch.arange(P - 1, dtype=torch.int32, device=cuda_dev).repeat(b), b, P - 1, None, N.LOGITS_NONE, ws)
+    out = torch.full((b,), -1, dtype=torch.int32, device=cuda_dev)
+    sink = N.SbTokenSink(out.data_ptr(), 1, None, None, None, 0)
+    dec.forward_greedy(kv, torch.as_tensor(ids[:, -1].copy(), device=cuda_dev), slots,
+                       torch.full((b,), P - 1, dtype=torch.int32, device=cuda_dev), b, 1, None, N.LOGITS_LAST, ws,
+                       sink)
+    torch.cuda.synchronize()
+    toks = out.cpu().numpy()
+    checked = 0
+    for s in range(b):
+        want = ref.forward(list(ids[s]), list(range(P)), ref.new_cache())[-1]
+        top2 = np.sort(want)[-2:]
+        if top2[1] - top2[0] > 2e-2 * np.abs(want).max():
+            assert toks[s] == int(want.argmax()), (s, toks[s], int(want.argmax()))
+            checked += 1
+    assert checked >= max(1, b // 2), checked
