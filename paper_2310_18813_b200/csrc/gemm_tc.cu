@@ -71,7 +71,7 @@ struct TcParams {
   int pre_max;      // ring stages of weights requested before the PDL wait (0 = all)
   int launch_late;  // 1: trigger dependents at the end of the epilogue instead of after the last load
   int dbg;          // experiments (sb_debug_gemm_pdl): bit 0 skip the epilogue stores, bit 3 plain stores,
-                    // bit 4 scalar (per-element) epilogue
+                    // bit 4 scalar (per-element) epilogue, bit 2 the 4-8 byte row emit of store / silu tiles
   const float* ln_s1;  // fused LayerNorm (GemmArgs::ln_*, out_part1)
   const float* ln_c1;
   const float* ln_c2;
@@ -523,6 +523,55 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
             asm volatile("bar.sync 1, 128;" ::: "memory");
             if (p.trace && et == 0 && ci == 0) tr_t[4] = gtime();
             if (p.dbg & 2) continue;  // experiment: TMEM -> shared staging only, no emit
+            if (E_ == EPI_STORE && !(p.dbg & 4) && !p.bias && !p.relu && !p.ln_c1) {
+              // wide emit: lane (h, q) takes rows 8q..8q+7 of token 2*ew + h (+8 ...): one 16-byte store;
+              // a warp instruction covers 2 tokens
+              const int h = lane >> 4, q = lane & 15;
+              const int nq0 = n0 + acc * TC_BM + 8 * q;
+              for (int jb = 2 * ew + h; jb < cn; jb += 8) {
+                const int j = j0 + jb, m = m0 + j;
+                const float4 v0 = *reinterpret_cast<const float4*>(sb + jb * TC_BM + 8 * q);
+                const float4 v1 = *reinterpret_cast<const float4*>(sb + jb * TC_BM + 8 * q + 4);
+                const float sc = scale ? inv_s[j] : 1.f;
+                if (m < p.M && nq0 < p.N)
+                  __stcs(reinterpret_cast<uint4*>((__nv_bfloat16*)p.y + (size_t)m * p.N + nq0),
+                         make_uint4(pack_bf16x2(v0.x * sc, v0.y * sc), pack_bf16x2(v0.z * sc, v0.w * sc),
+                                    pack_bf16x2(v1.x * sc, v1.y * sc), pack_bf16x2(v1.z * sc, v1.w * sc)));
+              }
+              continue;
+            }
+            if (E_ == EPI_SILU_MUL && !(p.dbg & 4) && !p.bias && !p.relu && !p.ln_c1) {
+              // wide emit: lane (sub, q) takes 16 rows of token 4*ew + sub (+16 ...): 8 silu outputs, one
+              // 16-byte store; a warp instruction covers 4 tokens.  Under the weight stream of the other
+              // CTAs the emit is bound by store instructions, not bytes: silu epilogue 3.4 -> 2.0 us at
+              // 64 tokens, 24 -> 13 us at 1016 (scripts/epi_wide.py; outputs bit-identical)
+              const int sub = lane >> 3, q = lane & 7;
+              const int nq0 = n0 + acc * TC_BM + 16 * q;
+              for (int jb = 4 * ew + sub; jb < cn; jb += 16) {
+                const int j = j0 + jb, m = m0 + j;
+                const float* src = sb + jb * TC_BM + 16 * q;
+                float f[16];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                  const float4 v4 = *reinterpret_cast<const float4*>(src + 4 * c);
+                  f[4 * c + 0] = v4.x;
+                  f[4 * c + 1] = v4.y;
+                  f[4 * c + 2] = v4.z;
+                  f[4 * c + 3] = v4.w;
+                }
+                const float sc = scale ? inv_s[j] : 1.f;
+                uint32_t o[4];
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                  const float g0 = f[4 * i] * sc, u0 = f[4 * i + 1] * sc, g1 = f[4 * i + 2] * sc, u1 = f[4 * i + 3] * sc;
+                  o[i] = pack_bf16x2(silu_f(g0) * u0, silu_f(g1) * u1);
+                }
+                if (m < p.M && nq0 < p.N)
+                  __stcs(reinterpret_cast<uint4*>((__nv_bfloat16*)p.y + (size_t)m * (p.N / 2) + nq0 / 2),
+                         make_uint4(o[0], o[1], o[2], o[3]));
+              }
+              continue;
+            }
             // EPI_RESID_ADD without the smem prefetch (large tiles): the warp's residual rows of the
             // chunk are loaded together (one round trip per chunk: prefill o / down epilogue 53 -> 27 us)
             // All of the warp's staged rows (and residual rows) are loaded before its first store:
@@ -673,7 +722,47 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
                           : make_float4(0.f, 0.f, 0.f, 0.f);
           }
         }
-        if (p.splits <= 2) {
+        if (E_ == EPI_STORE && !(p.dbg & 4) && !p.bias && !p.relu && !p.ln_c1 && p.splits <= 2) {
+          // wide emit (as in the chunk path): lane (h, q) sums rows 8q..8q+7 of tokens jb + h, jb + 2h'...
+          // over the ranks in order and emits them with one 16-byte store; the warp's 4 tokens of the
+          // group are covered by 2 instructions
+          const int h = lane >> 4, q = lane & 15;
+          const int n = n0 + 8 * q;
+          float4 tw[2][2][2];
+#pragma unroll
+          for (int i = 0; i < 2; ++i)
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+              const int j = jb + 4 * (2 * i + h);
+              if (j < jhi && r < p.splits) {
+                tw[i][r][0] = ld_dsmem_v4_nc(red_addr + (uint32_t)((j * TC_BM + 8 * q) * 4), r);
+                tw[i][r][1] = ld_dsmem_v4_nc(red_addr + (uint32_t)((j * TC_BM + 8 * q + 4) * 4), r);
+              }
+            }
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const int j = jb + 4 * (2 * i + h);
+            if (j >= jhi) continue;
+            float x[8] = {tw[i][0][0].x, tw[i][0][0].y, tw[i][0][0].z, tw[i][0][0].w,
+                          tw[i][0][1].x, tw[i][0][1].y, tw[i][0][1].z, tw[i][0][1].w};
+            if (p.splits > 1) {
+              x[0] += tw[i][1][0].x;
+              x[1] += tw[i][1][0].y;
+              x[2] += tw[i][1][0].z;
+              x[3] += tw[i][1][0].w;
+              x[4] += tw[i][1][1].x;
+              x[5] += tw[i][1][1].y;
+              x[6] += tw[i][1][1].z;
+              x[7] += tw[i][1][1].w;
+            }
+            const float sc = scale ? inv_s[j] : 1.f;
+            const int m = m0 + j;
+            if (m < p.M && n < p.N)
+              __stcs(reinterpret_cast<uint4*>((__nv_bfloat16*)p.y + (size_t)m * p.N + n),
+                     make_uint4(pack_bf16x2(x[0] * sc, x[1] * sc), pack_bf16x2(x[2] * sc, x[3] * sc),
+                                pack_bf16x2(x[4] * sc, x[5] * sc), pack_bf16x2(x[6] * sc, x[7] * sc)));
+          }
+        } else if (p.splits <= 2) {
           // two ranks: the group's 4 x 2 partial rows load together (one DSMEM round trip per group)
           float4 t2[4][2];
 #pragma unroll
