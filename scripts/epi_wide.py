@@ -1,4 +1,4 @@
-"""gate/up (silu) GEMM epilogue: 4-byte row emit (dbg 0) vs wide 16-byte emit (dbg 4) vs staging only
+"""gate/up (silu), qkv (store) and down (residual add) GEMM epilogues: 4-byte row emit (dbg 0) vs wide 16-byte emit (dbg 4) vs staging only
 (dbg 2): per-CTA trace medians (us) and bit-identity of the outputs."""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
@@ -10,13 +10,14 @@ lib = N.load()
 lib.sb_init()
 buf = torch.zeros(8 + 8 * 100000, dtype=torch.int64, device=dev)
 st = torch.cuda.current_stream().cuda_stream
-for Nw, K, EPI, cols in ((22016, 4096, N.EPI_SILU_MUL, 11008), (12288, 4096, N.EPI_STORE, 12288)):
+for Nw, K, EPI, cols in ((22016, 4096, N.EPI_SILU_MUL, 11008), (12288, 4096, N.EPI_STORE, 12288),
+                        (4096, 11008, N.EPI_RESID_ADD, 4096)):
   w = (torch.randn(Nw, K, device=dev) * 0.02).to(torch.bfloat16)
   for M in (9, 16, 32, 64, 128, 192, 288, 1016):
       x = torch.randn(M, K, device=dev).to(torch.bfloat16)
       outs = {}
       for dbg in (0, 4, 2):
-          y = torch.zeros(M, cols, device=dev, dtype=torch.bfloat16)
+          y = torch.zeros(M, cols, device=dev, dtype=torch.float32 if EPI == N.EPI_RESID_ADD else torch.bfloat16)
           lib.sb_debug_gemm_pdl(0, 0, dbg)
           for _ in range(3):
               N.call("sb_gemm", N.SB_BF16, x.data_ptr(), w.data_ptr(), y.data_ptr(), M, Nw, K, EPI, N.GEMM_TC, None, 0, st)
