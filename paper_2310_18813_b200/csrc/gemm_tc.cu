@@ -775,21 +775,9 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
       const int jlo = split * tn / p.splits, jhi = (split + 1) * tn / p.splits;
       const EmitRow er = load_emit_row(p, n0, lane);
       constexpr bool RL = E_ == EPI_RESID_ADD;
-      // wide residual emit (as in the chunk path): lane (h, q) owns rows 8q..8q+7 of its tokens
-      const bool wide_resid = RL && !(p.dbg & 4) && !p.bias && !p.relu && !p.ln_c1 && !p.out_part1;
-      float gn[8] = {1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f};
-      if (wide_resid) {
-        const int n = n0 + 8 * (lane & 15);
-        if (p.out_gain && n < p.N) {
-          const uint4 g4 = *reinterpret_cast<const uint4*>(p.out_gain + n);
-          const float4 ga = bf16x4_to_f4(make_uint2(g4.x, g4.y)), gb = bf16x4_to_f4(make_uint2(g4.z, g4.w));
-          gn[0] = ga.x, gn[1] = ga.y, gn[2] = ga.z, gn[3] = ga.w, gn[4] = gb.x, gn[5] = gb.y, gn[6] = gb.z, gn[7] = gb.w;
-        }
-        if (p.res_bytes) mbar_wait(res_bar, 0);
-      }
       for (int jb = jlo + ew; jb < jhi; jb += 16) {  // groups of 4 tokens per warp
         float4 res4[4];  // residual rows of the group (no smem prefetch: large tiles), loads in flight together
-        if (RL && !p.res_bytes && !wide_resid) {
+        if (RL && !p.res_bytes) {
           const int n = n0 + 4 * lane;
 #pragma unroll
           for (int i = 0; i < 4; ++i) {
@@ -838,70 +826,6 @@ __global__ void __launch_bounds__(TC_THREADS, 2)
               __stcs(reinterpret_cast<uint4*>((__nv_bfloat16*)p.y + (size_t)m * p.N + n),
                      make_uint4(pack_bf16x2(x[0] * sc, x[1] * sc), pack_bf16x2(x[2] * sc, x[3] * sc),
                                 pack_bf16x2(x[4] * sc, x[5] * sc), pack_bf16x2(x[6] * sc, x[7] * sc)));
-          }
-        } else if (wide_resid) {
-          // the warp's 4 tokens of the group in 2 instructions (halves h = 0 / 1); each lane sums its
-          // 8 rows over the ranks in order, adds the residual and emits 16-byte stores
-          const int h = lane >> 4, q = lane & 15;
-          const int n = n0 + 8 * q;
-          const bool nv = n < p.N;
-#pragma unroll
-          for (int i = 0; i < 2; ++i) {
-            const int j = jb + 4 * (2 * i + h), m = m0 + j;
-            const bool jv = j < jhi, ok = jv && m < p.M && nv;
-            float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
-            if (jv && p.res_bytes) {
-              const float* rr = res_rows + (size_t)(j - jlo) * TC_BM + 8 * q;
-              r0 = *reinterpret_cast<const float4*>(rr);
-              r1 = *reinterpret_cast<const float4*>(rr + 4);
-            } else if (ok) {
-              const float* rr = (const float*)p.y + (size_t)m * p.N + n;
-              r0 = __ldcg(reinterpret_cast<const float4*>(rr));
-              r1 = __ldcg(reinterpret_cast<const float4*>(rr + 4));
-            }
-            float x[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-            for (int r0_ = 0; r0_ < 8; r0_ += 4) {  // 4 ranks' loads in flight, summed in rank order
-              float4 t0[4], t1[4];
-#pragma unroll
-              for (int r = 0; r < 4; ++r)
-                if (r0_ + r < p.splits && jv) {
-                  t0[r] = ld_dsmem_v4_nc(red_addr + (uint32_t)((j * TC_BM + 8 * q) * 4), r0_ + r);
-                  t1[r] = ld_dsmem_v4_nc(red_addr + (uint32_t)((j * TC_BM + 8 * q + 4) * 4), r0_ + r);
-                }
-#pragma unroll
-              for (int r = 0; r < 4; ++r)
-                if (r0_ + r < p.splits && jv) {
-                  x[0] += t0[r].x;
-                  x[1] += t0[r].y;
-                  x[2] += t0[r].z;
-                  x[3] += t0[r].w;
-                  x[4] += t1[r].x;
-                  x[5] += t1[r].y;
-                  x[6] += t1[r].z;
-                  x[7] += t1[r].w;
-                }
-            }
-            const float sc = (scale && jv) ? inv_s[j] : 1.f;
-            const float a[8] = {r0.x + x[0] * sc, r0.y + x[1] * sc, r0.z + x[2] * sc, r0.w + x[3] * sc,
-                                r1.x + x[4] * sc, r1.y + x[5] * sc, r1.z + x[6] * sc, r1.w + x[7] * sc};
-            if (ok) {
-              float* yo = (float*)p.y + (size_t)m * p.N + n;
-              __stcs(reinterpret_cast<float4*>(yo), make_float4(a[0], a[1], a[2], a[3]));
-              __stcs(reinterpret_cast<float4*>(yo + 4), make_float4(a[4], a[5], a[6], a[7]));
-              if (p.out_xb)
-                __stcs(reinterpret_cast<uint4*>(p.out_xb + (size_t)m * p.N + n),
-                       make_uint4(pack_bf16x2(a[0] * gn[0], a[1] * gn[1]), pack_bf16x2(a[2] * gn[2], a[3] * gn[3]),
-                                  pack_bf16x2(a[4] * gn[4], a[5] * gn[5]), pack_bf16x2(a[6] * gn[6], a[7] * gn[7])));
-            }
-            if (p.out_part) {
-              float sq = ok ? (((a[0] * a[0] + a[1] * a[1]) + a[2] * a[2]) + a[3] * a[3]) +
-                                  (((a[4] * a[4] + a[5] * a[5]) + a[6] * a[6]) + a[7] * a[7])
-                            : 0.f;
-#pragma unroll
-              for (int o = 1; o < 16; o <<= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
-              if (q == 0 && jv && m < p.M && tile_n < p.n_tiles_n) st_o(p, p.out_part + (size_t)tile_n * p.M + m, sq);
-            }
           }
         } else if (p.splits <= 2) {
           // two ranks: the group's 4 x 2 partial rows load together (one DSMEM round trip per group)
