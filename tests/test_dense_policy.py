@@ -63,3 +63,28 @@ def test_dense_policy_drives_the_simulator():
                          example_trace(), np.random.default_rng(0))
     assert rep.policy == "adaptive-dense"
     assert all(r.used_s == 4 for r in rep.records)
+
+
+def test_measure_cost_table_calls_engine_per_cell():
+    from paper_2310_18813_b200.profiler import measure_cost_table
+
+    class FakeEngine:
+        prompt_len, max_new = 128, 128
+
+        def __init__(self):
+            self.calls = []
+
+        def time_verify(self, b, k, ctx, reps):
+            self.calls.append(("v", b, k, ctx))
+            return 2.7 + 0.01 * b * (k + 1)
+
+        def time_draft_step(self, b, ctx, reps):
+            self.calls.append(("d", b, ctx))
+            return 0.05 + 0.001 * b
+
+    eng = FakeEngine()
+    vm, dm = measure_cost_table(eng, range(1, 4), k_grid=range(3))
+    assert sorted(vm) == [(b, k) for b in range(1, 4) for k in range(3)]
+    assert sorted(dm) == [1, 2, 3]
+    assert vm[(2, 1)] == pytest.approx(2.74) and dm[3] == pytest.approx(0.053)
+    assert all(c[-1] == 192 for c in eng.calls)  # default context: prompt + half the generation
