@@ -450,16 +450,31 @@ __global__ void select_kernel(const float* logits, int V, int mode, const float*
 
 // Finalize of the lm_head-fused argmax: one warp per row merges the per-tile
 // (value, index) partials (ties -> lowest index, identical to a full argmax).
+// One CTA of 256 threads per row: every tile partial is loaded in one round trip (250 tiles for a
+// 32000-entry vocabulary), reduced per warp, then across the 8 warps.  argmax_merge is a total order
+// (larger value, then lower index), so the result does not depend on the reduction order.
 __global__ void argmax_partials_kernel(const float* __restrict__ val, const int* __restrict__ idx, int n_tiles, int rows,
                                        int32_t* out_tok, int out_stride, int32_t* next_ids, int32_t* next_pos,
                                        const int32_t* base_pos, int pos_offset) {
+  __shared__ float wv[8];
+  __shared__ int wi[8];
   griddep_wait();
   griddep_launch();
-  const int r = blockIdx.x, lane = threadIdx.x;
+  const int r = blockIdx.x, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   ArgMax a{-INFINITY, INT_MAX};
-  for (int t = lane; t < n_tiles; t += 32) a = argmax_merge(a, ArgMax{val[(size_t)t * rows + r], idx[(size_t)t * rows + r]});
+  for (int t = threadIdx.x; t < n_tiles; t += blockDim.x)
+    a = argmax_merge(a, ArgMax{val[(size_t)t * rows + r], idx[(size_t)t * rows + r]});
   a = warp_argmax(a);
   if (lane == 0) {
+    wv[warp] = a.v;
+    wi[warp] = a.i;
+  }
+  __syncthreads();
+  if (warp == 0) {
+    a = lane < (int)(blockDim.x >> 5) ? ArgMax{wv[lane], wi[lane]} : ArgMax{-INFINITY, INT_MAX};
+    a = warp_argmax(a);
+  }
+  if (threadIdx.x == 0) {
     if (out_tok) out_tok[(size_t)r * out_stride] = a.i;
     if (next_ids) next_ids[r] = a.i;
     if (next_pos) next_pos[r] = base_pos[r] + pos_offset;
@@ -470,7 +485,7 @@ int launch_argmax_partials(const float* val, const int* idx, int n_tiles, int ro
                            int32_t* next_ids, int32_t* next_pos, const int32_t* base_pos, int pos_offset,
                            cudaStream_t st) {
   if (rows <= 0) return 0;
-  return launch_k(argmax_partials_kernel, dim3(rows), dim3(32), 0, st, val, idx, n_tiles, rows, out_tok, out_stride,
+  return launch_k(argmax_partials_kernel, dim3(rows), dim3(256), 0, st, val, idx, n_tiles, rows, out_tok, out_stride,
                   next_ids, next_pos, base_pos, pos_offset);
 }
 
