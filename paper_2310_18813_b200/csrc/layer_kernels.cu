@@ -71,13 +71,49 @@ __global__ void __launch_bounds__(256) embed_norm_kernel(const __nv_bfloat16* __
   // OPT: learned absolute positions (row p + offset); part1: the row's sum (fused LayerNorm consumers)
   const __nv_bfloat16* prow = (pos_table && !pad) ? pos_table + (size_t)(pos[t] + pos_offset) * hidden : nullptr;
   float ss = 0.f, s1 = 0.f;
-  for (int i = threadIdx.x; i < hidden; i += blockDim.x) {
-    float v = pad ? 0.f : __bfloat162float(row[i]);
-    if (prow) v += __bfloat162float(prow[i]);
-    h[(size_t)t * hidden + i] = v;
-    xb[(size_t)t * hidden + i] = __float2bfloat16_rn(gain ? v * __bfloat162float(gain[i]) : v);
-    ss += v * v;
-    s1 += v;
+  if ((hidden & 7) == 0) {
+    // 8 elements per thread: one 16-byte load per source row, 16-byte stores (one round trip)
+    for (int i = threadIdx.x * 8; i < hidden; i += blockDim.x * 8) {
+      float v[8];
+      const uint4 r4 = pad ? make_uint4(0u, 0u, 0u, 0u) : *reinterpret_cast<const uint4*>(row + i);
+      const __nv_bfloat16* rb = reinterpret_cast<const __nv_bfloat16*>(&r4);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) v[e] = __bfloat162float(rb[e]);
+      if (prow) {
+        const uint4 p4 = *reinterpret_cast<const uint4*>(prow + i);
+        const __nv_bfloat16* pb = reinterpret_cast<const __nv_bfloat16*>(&p4);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) v[e] += __bfloat162float(pb[e]);
+      }
+      float g[8] = {1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f, 1.f};
+      if (gain) {
+        const uint4 g4 = *reinterpret_cast<const uint4*>(gain + i);
+        const __nv_bfloat16* gb = reinterpret_cast<const __nv_bfloat16*>(&g4);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) g[e] = __bfloat162float(gb[e]);
+      }
+      float4* hd = reinterpret_cast<float4*>(h + (size_t)t * hidden + i);
+      hd[0] = make_float4(v[0], v[1], v[2], v[3]);
+      hd[1] = make_float4(v[4], v[5], v[6], v[7]);
+      uint4 o;
+      __nv_bfloat16* ob = reinterpret_cast<__nv_bfloat16*>(&o);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        ob[e] = __float2bfloat16_rn(gain ? v[e] * g[e] : v[e]);
+        ss += v[e] * v[e];
+        s1 += v[e];
+      }
+      *reinterpret_cast<uint4*>(xb + (size_t)t * hidden + i) = o;
+    }
+  } else {
+    for (int i = threadIdx.x; i < hidden; i += blockDim.x) {
+      float v = pad ? 0.f : __bfloat162float(row[i]);
+      if (prow) v += __bfloat162float(prow[i]);
+      h[(size_t)t * hidden + i] = v;
+      xb[(size_t)t * hidden + i] = __float2bfloat16_rn(gain ? v * __bfloat162float(gain[i]) : v);
+      ss += v * v;
+      s1 += v;
+    }
   }
   __shared__ float red[8], red1[8];
   ss = warp_sum(ss);
